@@ -1,0 +1,558 @@
+"""grafem-b200: B200-native per-timestep hot path of the remeshing-free graph-based FEM fracture method.
+
+Python mirror of the reference's C++ simulator API (namespace grafem, /root/reference/proj/include/grafem)
+over the C ABI of libgrafem_b200.so (include/grafem_b200.h). Names, argument meaning and error types follow
+the reference: TetMesh / make_box_mesh / make_mesh / load_tetgen, MaterialParams.from_youngs, SolverConfig,
+BoundaryCondition + Schedule3, Collider, Simulation.{dynamic_step, damage_pass, state, ...}, and the
+FormatError / GeometryError / SolveError exceptions.
+
+All compute runs in hand-written sm_100a CUDA kernels. There is no CPU fallback: importing works anywhere
+(the library is plain C ABI), but creating a Simulation without a Blackwell GPU raises CudaError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "FormatError", "GeometryError", "SolveError", "CudaError", "TetMesh", "make_box_mesh", "make_mesh",
+    "load_tetgen", "MaterialParams", "SolverConfig", "Schedule3", "BoundaryCondition", "Collider", "Simulation",
+    "StepStats", "SimState", "cg_solve_csr", "library_path", "STABLE_NEO_HOOKEAN", "STVK",
+]
+
+STABLE_NEO_HOOKEAN, STVK = 0, 1
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "_lib", "libgrafem_b200.so")
+
+F64P = C.POINTER(C.c_double)
+I32P = C.POINTER(C.c_int32)
+U8P = C.POINTER(C.c_uint8)
+
+
+class GrafemError(RuntimeError):
+    pass
+
+
+class FormatError(GrafemError):
+    """grafem::FormatError (types.hpp:17-20)"""
+
+
+class GeometryError(GrafemError):
+    """grafem::GeometryError (types.hpp:22-25)"""
+
+
+class SolveError(GrafemError):
+    """grafem::SolveError (types.hpp:27-29)"""
+
+
+class CudaError(GrafemError):
+    """No usable sm_100 device / CUDA runtime failure (no CPU fallback exists)."""
+
+
+_ERRORS = {1: FormatError, 2: GeometryError, 3: SolveError, 4: CudaError, 5: GrafemError}
+
+
+# ---------------------------------------------------------------- C ABI structs (grafem_b200.h)
+class _Material(C.Structure):
+    _fields_ = [("youngs", C.c_double), ("poisson", C.c_double), ("density", C.c_double), ("mu", C.c_double),
+                ("lambda_", C.c_double), ("sigma_thres", C.c_double), ("r_d", C.c_double),
+                ("damp_mass_coeff", C.c_double), ("damp_stiff_coeff", C.c_double),
+                ("energy_model", C.c_int32), ("_pad", C.c_int32)]
+
+
+class _SolverConfig(C.Structure):
+    _fields_ = [("dt", C.c_double), ("newton_tol", C.c_double), ("newton_max_iters", C.c_int32),
+                ("cg_max_iters", C.c_int32), ("cg_tol", C.c_double), ("ls_backtrack", C.c_double),
+                ("ls_sufficient_decrease", C.c_double), ("ls_max_halvings", C.c_int32),
+                ("dynamic_full_newton", C.c_int32), ("gravity", C.c_double * 3),
+                ("collision_substeps", C.c_int32), ("_pad", C.c_int32)]
+
+
+class _Bc(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n_nodes", C.c_int32), ("nodes", I32P), ("n_keys", C.c_int32),
+                ("_pad", C.c_int32), ("key_times", F64P), ("key_values", F64P),
+                ("axis_point", C.c_double * 3), ("axis_dir", C.c_double * 3)]
+
+
+class _Collider(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n_keys", C.c_int32), ("key_times", F64P), ("key_values", F64P),
+                ("radius", C.c_double), ("point", C.c_double * 3), ("normal", C.c_double * 3),
+                ("stiffness", C.c_double), ("restitution", C.c_double), ("friction", C.c_double)]
+
+
+class StepStats(C.Structure):
+    """grafem::StepStats (solver.hpp:49-55)"""
+    _fields_ = [("newton_iterations", C.c_int32), ("cg_iterations", C.c_int32), ("newly_broken", C.c_int32),
+                ("_pad", C.c_int32), ("residual", C.c_double), ("load", C.c_double)]
+
+
+class _CgResult(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("negative_curvature", C.c_int32),
+                ("_pad", C.c_int32), ("relative_residual", C.c_double)]
+
+
+class KernelTime(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("total_ms", C.c_double), ("bytes", C.c_double)]
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _LIB
+
+
+def lib():
+    """Load libgrafem_b200.so. Fails loudly when the extension has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            raise ImportError(f"{_LIB} is missing: build it with `python -m paper_2103_14870_b200.build` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(_LIB)
+        L.gf_last_error.restype = C.c_char_p
+        L.gf_version.restype = C.c_char_p
+        L.gf_mesh_make_box.argtypes = [F64P, I32P, F64P, C.c_double, C.c_uint64, C.POINTER(C.c_void_p)]
+        L.gf_mesh_mean_face_area.restype = C.c_double
+        L.gf_mesh_pattern_nnz.restype = C.c_int64
+        L.gf_mesh_pattern.restype = C.c_uint64
+        L.gf_mesh_nonlocal_table.restype = C.c_int64
+        L.gf_mesh_nonlocal_table.argtypes = [C.c_void_p, C.c_double, I32P, I32P, F64P]
+        L.gf_sim_pattern_hash.restype = C.c_uint64
+        L.gf_sim_last_collider_load.restype = C.c_double
+        L.gf_host_alloc.restype = C.c_void_p
+        L.gf_host_alloc.argtypes = [C.c_size_t]
+        L.gf_host_free.argtypes = [C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise _ERRORS.get(rc, GrafemError)(lib().gf_last_error().decode())
+
+
+def _f64(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(F64P)
+
+
+def _i32(a):
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    return a, a.ctypes.data_as(I32P)
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+# ---------------------------------------------------------------- mesh (mesh.hpp, primitives.hpp)
+class TetMesh:
+    """TetMesh (mesh.hpp:15-43): rest positions, tets, canonical edges, rest quantities (host setup)."""
+
+    def __init__(self, handle):
+        self._h = handle
+        n, t, e = C.c_int32(), C.c_int32(), C.c_int32()
+        lib().gf_mesh_counts(self._h, C.byref(n), C.byref(t), C.byref(e))
+        self._counts = (n.value, t.value, e.value)
+        self._arrays = None
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.gf_mesh_destroy(self._h)
+            self._h = None
+
+    def num_nodes(self):
+        return self._counts[0]
+
+    def num_tets(self):
+        return self._counts[1]
+
+    def num_edges(self):
+        return self._counts[2]
+
+    def num_dofs(self):
+        return 3 * self._counts[0]
+
+    def _get(self):
+        if self._arrays is None:
+            N, T, E = self._counts
+            a = dict(rest_positions=np.zeros((N, 3)), tets=np.zeros((T, 4), np.int32),
+                     edges=np.zeros((E, 2), np.int32), tet_edges=np.zeros((T, 6), np.int32),
+                     rest_volumes=np.zeros(T), rest_shape_inverse=np.zeros((T, 3, 3)),
+                     rest_centroids=np.zeros((T, 3)), rest_edge_lengths=np.zeros(E))
+            lib().gf_mesh_get(self._h, *[_p(a[k], t) for k, t in [
+                ("rest_positions", F64P), ("tets", I32P), ("edges", I32P), ("tet_edges", I32P),
+                ("rest_volumes", F64P), ("rest_shape_inverse", F64P), ("rest_centroids", F64P),
+                ("rest_edge_lengths", F64P)]])
+            self._arrays = a
+        return self._arrays
+
+    def __getattr__(self, name):
+        if name in ("rest_positions", "tets", "edges", "tet_edges", "rest_volumes", "rest_shape_inverse",
+                    "rest_centroids", "rest_edge_lengths"):
+            return self._get()[name]
+        raise AttributeError(name)
+
+    def total_volume(self):
+        return float(self.rest_volumes.sum())
+
+    def mean_face_area(self):
+        return lib().gf_mesh_mean_face_area(self._h)
+
+    def pattern(self):
+        """Scalar CSR of make_system_pattern (fem.cpp:140-149): (row_ptr, cols, structure_hash)."""
+        nnz = lib().gf_mesh_pattern_nnz(self._h)
+        rp = np.zeros(self.num_dofs() + 1, np.int32)
+        cols = np.zeros(nnz, np.int32)
+        h = lib().gf_mesh_pattern(self._h, _p(rp, I32P), _p(cols, I32P))
+        return rp, cols, int(h)
+
+    def nonlocal_table(self, r_d: float):
+        """build_nonlocal_table (fracture.cpp:32-54) as CSR (ptr, ids, weights)."""
+        n = lib().gf_mesh_nonlocal_table(self._h, r_d, None, None, None)
+        ptr = np.zeros(self.num_tets() + 1, np.int32)
+        ids = np.zeros(n, np.int32)
+        w = np.zeros(n)
+        lib().gf_mesh_nonlocal_table(self._h, r_d, _p(ptr, I32P), _p(ids, I32P), _p(w, F64P))
+        return ptr, ids, w
+
+
+def make_box_mesh(size, cells, origin=(0.0, 0.0, 0.0), jitter: float = 0.0, seed: int = 0) -> TetMesh:
+    """make_box_mesh (primitives.hpp:12-13) + optional seeded interior-node jitter (cell units)."""
+    h = C.c_void_p()
+    _, ps = _f64(size)
+    c, pc = _i32(cells)
+    _, po = _f64(origin)
+    s = np.asarray(size, np.float64)
+    o = np.asarray(origin, np.float64)
+    _check(lib().gf_mesh_make_box(s.ctypes.data_as(F64P), pc, o.ctypes.data_as(F64P), C.c_double(jitter),
+                                  C.c_uint64(seed), C.byref(h)))
+    return TetMesh(h)
+
+
+def make_mesh(nodes, tets) -> TetMesh:
+    """make_mesh (mesh.hpp:55-56)"""
+    h = C.c_void_p()
+    nodes, pn = _f64(nodes)
+    tets, pt = _i32(tets)
+    _check(lib().gf_mesh_create(pn, C.c_int32(len(nodes)), pt, C.c_int32(len(tets)), C.byref(h)))
+    return TetMesh(h)
+
+
+def load_tetgen(node_text: str, ele_text: str) -> TetMesh:
+    """load_tetgen (mesh.hpp:59)"""
+    h = C.c_void_p()
+    _check(lib().gf_mesh_load_tetgen(node_text.encode(), ele_text.encode(), C.byref(h)))
+    return TetMesh(h)
+
+
+# ---------------------------------------------------------------- parameters
+class MaterialParams:
+    """MaterialParams (material.hpp:14-31)."""
+
+    def __init__(self, raw: _Material):
+        self._raw = raw
+
+    @staticmethod
+    def from_youngs(youngs, poisson, density, sigma_thres, r_d=0.0, model=STABLE_NEO_HOOKEAN):
+        m = _Material()
+        _check(lib().gf_material_from_youngs(C.c_double(youngs), C.c_double(poisson), C.c_double(density),
+                                             C.c_double(sigma_thres), C.c_double(r_d), C.c_int32(model), C.byref(m)))
+        return MaterialParams(m)
+
+    def __getattr__(self, k):
+        raw = self.__dict__["_raw"]
+        return getattr(raw, "lambda_" if k == "lambda_" or k == "lam" else k)
+
+    def __setattr__(self, k, v):
+        if k == "_raw":
+            object.__setattr__(self, k, v)
+        else:
+            setattr(self._raw, k, v)
+
+
+class SolverConfig:
+    """SolverConfig (solver.hpp:15-31)."""
+
+    def __init__(self, **kw):
+        self._raw = _SolverConfig()
+        lib().gf_solver_config_default(C.byref(self._raw))
+        for k, v in kw.items():
+            setattr(self, k, v)
+
+    def __getattr__(self, k):
+        return getattr(self.__dict__["_raw"], k)
+
+    def __setattr__(self, k, v):
+        if k == "_raw":
+            object.__setattr__(self, k, v)
+        elif k == "gravity":
+            self._raw.gravity[:] = [float(x) for x in v]
+        else:
+            setattr(self._raw, k, v)
+
+
+@dataclass
+class Schedule3:
+    """Piecewise-linear vector schedule (collision.hpp:10-18)."""
+    times: Sequence[float] = ()
+    values: Sequence[Sequence[float]] = ()
+
+    @staticmethod
+    def constant(v):
+        return Schedule3([0.0], [list(v)])
+
+
+@dataclass
+class BoundaryCondition:
+    """BoundaryCondition (solver.hpp:35-47). kind 'translate' (translation schedule) or 'rotate'."""
+    nodes: Sequence[int]
+    kind: str = "translate"
+    name: str = ""
+    translation: Schedule3 = field(default_factory=lambda: Schedule3.constant((0.0, 0.0, 0.0)))
+    axis_point: Sequence[float] = (0.0, 0.0, 0.0)
+    axis_dir: Sequence[float] = (1.0, 0.0, 0.0)
+    angle: Schedule3 = field(default_factory=Schedule3)
+
+
+@dataclass
+class Collider:
+    """Collider (collision.hpp:20-34). kind 'sphere' (centre schedule) or 'halfspace'."""
+    kind: str = "sphere"
+    center: Schedule3 = field(default_factory=Schedule3)
+    radius: float = 0.0
+    point: Sequence[float] = (0.0, 0.0, 0.0)
+    normal: Sequence[float] = (0.0, 0.0, 1.0)
+    stiffness: float = 1e6
+    restitution: float = 0.0
+    friction: float = 0.0
+
+
+@dataclass
+class SimState:
+    """SimState (fem.hpp:15-28), host copy."""
+    displacements: np.ndarray
+    velocities: np.ndarray
+    edge_damage: np.ndarray
+    element_chi: np.ndarray
+    time: float
+
+    def broken_edge_count(self):
+        return int(self.edge_damage.sum())
+
+
+def _sched_arrays(s: Schedule3):
+    t = np.ascontiguousarray(s.times, np.float64).reshape(-1)
+    v = np.ascontiguousarray(s.values, np.float64).reshape(-1, 3) if len(t) else np.zeros((0, 3))
+    return t, np.ascontiguousarray(v)
+
+
+# ---------------------------------------------------------------- simulation (solver.hpp:60-118)
+class Simulation:
+    def __init__(self, mesh: TetMesh, material: MaterialParams, config: SolverConfig,
+                 bcs: Sequence[BoundaryCondition] = (), colliders: Sequence[Collider] = ()):
+        keep = []
+        B = (_Bc * max(1, len(bcs)))()
+        for i, bc in enumerate(bcs):
+            nodes = np.ascontiguousarray(bc.nodes, np.int32)
+            sched = bc.translation if bc.kind == "translate" else bc.angle
+            t, v = _sched_arrays(sched)
+            keep += [nodes, t, v]
+            B[i].kind = 0 if bc.kind == "translate" else 1
+            B[i].n_nodes = len(nodes)
+            B[i].nodes = nodes.ctypes.data_as(I32P)
+            B[i].n_keys = len(t)
+            B[i].key_times = t.ctypes.data_as(F64P)
+            B[i].key_values = v.ctypes.data_as(F64P)
+            B[i].axis_point[:] = [float(x) for x in bc.axis_point]
+            B[i].axis_dir[:] = [float(x) for x in bc.axis_dir]
+        K = (_Collider * max(1, len(colliders)))()
+        for i, c in enumerate(colliders):
+            t, v = _sched_arrays(c.center)
+            keep += [t, v]
+            K[i].kind = 0 if c.kind == "sphere" else 1
+            K[i].n_keys = len(t)
+            K[i].key_times = t.ctypes.data_as(F64P)
+            K[i].key_values = v.ctypes.data_as(F64P)
+            K[i].radius = c.radius
+            K[i].point[:] = [float(x) for x in c.point]
+            K[i].normal[:] = [float(x) for x in c.normal]
+            K[i].stiffness, K[i].restitution, K[i].friction = c.stiffness, c.restitution, c.friction
+        h = C.c_void_p()
+        _check(lib().gf_sim_create(mesh._h, C.byref(material._raw), C.byref(config._raw), B, C.c_int32(len(bcs)),
+                                   K, C.c_int32(len(colliders)), C.byref(h)))
+        self._h = h
+        self._mesh = mesh
+        self.material = material
+        self.config = config
+        self.N, self.T, self.E = mesh.num_nodes(), mesh.num_tets(), mesh.num_edges()
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.gf_sim_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def mesh(self):
+        return self._mesh
+
+    def dynamic_step(self) -> StepStats:
+        st = StepStats()
+        _check(lib().gf_sim_dynamic_step(self._h, C.byref(st)))
+        return st
+
+    def damage_pass(self) -> np.ndarray:
+        ids = np.zeros(self.E, np.int32)
+        n = C.c_int64()
+        _check(lib().gf_sim_damage_pass(self._h, _p(ids, I32P), C.c_int64(self.E), C.byref(n)))
+        return ids[: n.value].copy()
+
+    def state(self) -> SimState:
+        u, v = np.zeros((self.N, 3)), np.zeros((self.N, 3))
+        z, chi, t = np.zeros(self.E, np.uint8), np.zeros(self.T), C.c_double()
+        _check(lib().gf_sim_get_state(self._h, _p(u, F64P), _p(v, F64P), _p(z, U8P), _p(chi, F64P), C.byref(t)))
+        return SimState(u, v, z, chi, t.value)
+
+    def set_state(self, displacements=None, velocities=None, edge_damage=None, element_chi=None, time=None):
+        args, keep = [], []
+        for a, dt, t in ((displacements, np.float64, F64P), (velocities, np.float64, F64P),
+                         (edge_damage, np.uint8, U8P), (element_chi, np.float64, F64P)):
+            if a is None:
+                args.append(None)
+            else:
+                a = np.ascontiguousarray(a, dt)
+                keep.append(a)
+                args.append(a.ctypes.data_as(t))
+        tt = C.c_double(time) if time is not None else None
+        _check(lib().gf_sim_set_state(self._h, *args, C.byref(tt) if tt is not None else None))
+
+    def get_state_into(self, u=None, v=None, zeta=None, chi=None):
+        """Zero-copy variant for pinned buffers (raw pointers or numpy arrays)."""
+        def ptr(a, t):
+            if a is None:
+                return None
+            return C.cast(a, t) if isinstance(a, int) else a.ctypes.data_as(t)
+        _check(lib().gf_sim_get_state(self._h, ptr(u, F64P), ptr(v, F64P), ptr(zeta, U8P), ptr(chi, F64P), None))
+
+    def set_state_from(self, u=None, v=None):
+        def ptr(a):
+            if a is None:
+                return None
+            return C.cast(a, F64P) if isinstance(a, int) else a.ctypes.data_as(F64P)
+        _check(lib().gf_sim_set_state(self._h, ptr(u), ptr(v), None, None, None))
+
+    def set_external_forces(self, f3n=None):
+        if f3n is None:
+            _check(lib().gf_sim_set_external_forces(self._h, None))
+        else:
+            f, pf = _f64(np.asarray(f3n).reshape(-1))
+            _check(lib().gf_sim_set_external_forces(self._h, pf))
+
+    def pattern_hash(self) -> int:
+        return int(lib().gf_sim_pattern_hash(self._h))
+
+    def dof_count(self) -> int:
+        return int(lib().gf_sim_dof_count(self._h))
+
+    def broken_fraction(self) -> float:
+        n = C.c_int64()
+        _check(lib().gf_sim_broken_edge_count(self._h, C.byref(n)))
+        return n.value / self.E if self.E else 0.0
+
+    def last_collider_load(self) -> float:
+        return lib().gf_sim_last_collider_load(self._h)
+
+    def mass(self) -> np.ndarray:
+        m = np.zeros(3 * self.N)
+        _check(lib().gf_sim_mass(self._h, _p(m, F64P)))
+        return m
+
+    def reaction_load(self, nodes, axis) -> float:
+        n, pn = _i32(nodes)
+        a = (C.c_double * 3)(*[float(x) for x in axis])
+        out = C.c_double()
+        _check(lib().gf_sim_reaction_load(self._h, pn, C.c_int32(len(n)), a, C.byref(out)))
+        return out.value
+
+    def energies(self):
+        s, k = C.c_double(), C.c_double()
+        _check(lib().gf_sim_energies(self._h, C.byref(s), C.byref(k)))
+        return s.value, k.value
+
+    # parity / microbench hooks
+    def eval_forces(self) -> np.ndarray:
+        f = np.zeros(3 * self.N)
+        _check(lib().gf_sim_eval_forces(self._h, _p(f, F64P)))
+        return f
+
+    def eval_stiffness(self) -> np.ndarray:
+        vals = np.zeros(lib().gf_mesh_pattern_nnz(self._mesh._h))
+        _check(lib().gf_sim_eval_stiffness(self._h, _p(vals, F64P)))
+        return vals
+
+    def eval_cauchy(self) -> np.ndarray:
+        s = np.zeros((self.T, 6))
+        _check(lib().gf_sim_eval_cauchy(self._h, _p(s, F64P)))
+        return s
+
+    def eval_screening(self):
+        scr, sf, deg = np.zeros(self.E), np.zeros((self.T, 6)), np.zeros(self.T, np.uint8)
+        _check(lib().gf_sim_eval_screening(self._h, _p(scr, F64P), _p(sf, F64P), _p(deg, U8P)))
+        return scr, sf, deg
+
+    def last_system(self):
+        vals = np.zeros(lib().gf_mesh_pattern_nnz(self._mesh._h))
+        rhs = np.zeros(3 * self.N)
+        _check(lib().gf_sim_last_system(self._h, _p(vals, F64P), _p(rhs, F64P)))
+        return vals, rhs
+
+    def spmv(self, x) -> np.ndarray:
+        x, px = _f64(x)
+        y = np.zeros(3 * self.N)
+        _check(lib().gf_sim_spmv(self._h, px, _p(y, F64P)))
+        return y
+
+    # runtime utilities
+    def set_profiling(self, on: bool):
+        _check(lib().gf_sim_set_profiling(self._h, C.c_int32(int(on))))
+
+    def kernel_times(self):
+        arr = (KernelTime * 64)()
+        n = C.c_int32()
+        _check(lib().gf_sim_kernel_times(self._h, arr, C.c_int32(64), C.byref(n)))
+        return {arr[i].name.decode(): dict(launches=arr[i].launches, total_ms=arr[i].total_ms, bytes=arr[i].bytes)
+                for i in range(n.value)}
+
+    def reset_kernel_times(self):
+        _check(lib().gf_sim_reset_kernel_times(self._h))
+
+    def synchronize(self):
+        _check(lib().gf_sim_synchronize(self._h))
+
+
+def cg_solve_csr(row_ptr, cols, vals, b, x0, tol, max_iters):
+    """cg_solve (sparse.cpp:129-188) on the GPU for a scalar CSR; returns (x, result dict)."""
+    rp, prp = _i32(row_ptr)
+    cl, pcl = _i32(cols)
+    v, pv = _f64(vals)
+    b, pb = _f64(b)
+    x = np.array(x0, dtype=np.float64, copy=True)
+    r = _CgResult()
+    _check(lib().gf_cg_solve_csr(C.c_int32(len(rp) - 1), prp, pcl, pv, pb, _p(x, F64P), C.c_double(tol),
+                                 C.c_int32(max_iters), C.byref(r)))
+    return x, dict(iterations=r.iterations, converged=bool(r.converged),
+                   negative_curvature=bool(r.negative_curvature), relative_residual=r.relative_residual)
+
+
+def device_info():
+    sm, ma, mi = C.c_int32(), C.c_int32(), C.c_int32()
+    name = C.create_string_buffer(128)
+    _check(lib().gf_device_info(C.byref(sm), C.byref(ma), C.byref(mi), name, C.c_int32(128)))
+    return dict(sm_count=sm.value, cc=(ma.value, mi.value), name=name.value.decode())

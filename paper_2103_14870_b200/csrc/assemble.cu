@@ -1,0 +1,351 @@
+// assemble.cu — force + tangent-stiffness assembly fused with the implicit-Euler system build.
+//
+// Replaces assemble_forces (fem.cpp:96-108), element_stiffness/assemble_stiffness (fem.cpp:110-169),
+// the K*v SpMV, rhs and scaling/mass shift of dynamic_step (solver.cpp:275-289) and the Dirichlet
+// projection (sparse.cpp:98-120) with ONE pass:
+//
+//   one warp per node row i; lane l takes the l-th tet incident to i (ascending tet id, the reference's
+//   scatter order) and evaluates that tet's force on i and the four 3x3 Hessian blocks K(i, j) of row i
+//   from the compact closed form (equal to the reference's 12 directional derivatives of
+//   pk1 to ~1e-16):
+//     NH   K_ij = s[c1 (g_i.g_j) I + c2 (F g_i)(F g_j)^T + lambda (cof g_i)(cof g_j)^T - lambda(J-a)[F(g_i x g_j)]_x]
+//     StVK K_ij = s[(g_i^T S g_j) I + mu (F g_j)(F g_i)^T + mu (g_i.g_j) F F^T + lambda (F g_i)(F g_j)^T]
+//   with g = shape gradients from B^-1 and s = chi*V. Blocks go to shared memory; lane c then sums the
+//   contributions that land in column block c of the row (precomputed slot bytes: no search, no atomics,
+//   deterministic), and finishes the row in registers: K v, A = (dt beta + dt^2) K + (1 + dt alpha) M,
+//   Dirichlet projection, rhs, Jacobi inverse diagonal, CG initial guess. The matrix is written exactly
+//   once, coalesced (consecutive lanes = consecutive 72 B blocks of the row).
+#include "device_math.cuh"
+
+namespace gfb {
+namespace {
+
+constexpr int kWarps = 4;
+constexpr int kMaxDeg = 64;  // columns per node row handled by one warp (2 per lane)
+
+struct ElemOut {
+  double f[3];
+  double H[4][9];
+};
+
+// contribution of tet e to node-row i (local index li): force on i and K(li, lj), lj = 0..3
+template <bool kBlocks>
+__device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, int e, int li, double scale,
+                                            ElemOut& o) {
+  const int4 t = __ldg(d.tets + e);
+  const int id[4] = {t.x, t.y, t.z, t.w};
+  double u[4][3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) u[k][a] = __ldg(d.u + 3 * (size_t)id[k] + a);
+  double B[9], du[9], F[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) B[q] = __ldg(d.binv + 9 * (size_t)e + q);
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) du[3 * r + c] = u[c + 1][r] - u[0][r];
+  def_grad(du, B, F);
+  double g[4][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    g[1][a] = B[a];
+    g[2][a] = B[3 + a];
+    g[3][a] = B[6 + a];
+    g[0][a] = -((B[a] + B[3 + a]) + B[6 + a]);
+  }
+  double P[9];
+  const double J = pk1(F, m, P);
+  double gi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) gi[a] = g[li][a];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) o.f[a] = -scale * ((P[3 * a] * gi[0] + P[3 * a + 1] * gi[1]) + P[3 * a + 2] * gi[2]);
+  if (!kBlocks) return;
+
+  double ai[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) ai[a] = F[3 * a] * gi[0] + F[3 * a + 1] * gi[1] + F[3 * a + 2] * gi[2];
+  if (m.model == 1) {
+    double E[9], S[9], FFt[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        E[3 * r + c] = 0.5 * ((F[r] * F[c] + F[3 + r] * F[3 + c] + F[6 + r] * F[6 + c]) - (r == c ? 1.0 : 0.0));
+        FFt[3 * r + c] = F[3 * r] * F[3 * c] + F[3 * r + 1] * F[3 * c + 1] + F[3 * r + 2] * F[3 * c + 2];
+      }
+    const double lt = m.lambda * (E[0] + E[4] + E[8]);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) S[q] = 2.0 * m.mu * E[q] + ((q % 4 == 0) ? lt : 0.0);
+    double Sgi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) Sgi[a] = S[3 * a] * gi[0] + S[3 * a + 1] * gi[1] + S[3 * a + 2] * gi[2];
+#pragma unroll
+    for (int lj = 0; lj < 4; ++lj) {
+      double aj[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) aj[a] = F[3 * a] * g[lj][0] + F[3 * a + 1] * g[lj][1] + F[3 * a + 2] * g[lj][2];
+      const double gij = gi[0] * g[lj][0] + gi[1] * g[lj][1] + gi[2] * g[lj][2];
+      const double gSg = Sgi[0] * g[lj][0] + Sgi[1] * g[lj][1] + Sgi[2] * g[lj][2];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double v = (r == c ? gSg : 0.0) + m.mu * aj[r] * ai[c] + m.mu * gij * FFt[3 * r + c] +
+                           m.lambda * ai[r] * aj[c];
+          o.H[lj][3 * r + c] = scale * v;
+        }
+    }
+  } else {
+    double C[9];
+    cofactor(F, C);
+    const double ic = sqnorm9(F);
+    const double ip1 = ic + 1.0;
+    const double c1 = m.mu * (1.0 - 1.0 / ip1);
+    const double c2 = 2.0 * m.mu / (ip1 * ip1);
+    const double c4 = m.lambda * (J - m.alpha_nh);
+    double bi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) bi[a] = C[3 * a] * gi[0] + C[3 * a + 1] * gi[1] + C[3 * a + 2] * gi[2];
+#pragma unroll
+    for (int lj = 0; lj < 4; ++lj) {
+      const double* gj = g[lj];
+      double aj[3], bj[3], cr[3], w[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        aj[a] = F[3 * a] * gj[0] + F[3 * a + 1] * gj[1] + F[3 * a + 2] * gj[2];
+        bj[a] = C[3 * a] * gj[0] + C[3 * a + 1] * gj[1] + C[3 * a + 2] * gj[2];
+      }
+      cr[0] = gi[1] * gj[2] - gi[2] * gj[1];
+      cr[1] = gi[2] * gj[0] - gi[0] * gj[2];
+      cr[2] = gi[0] * gj[1] - gi[1] * gj[0];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) w[a] = F[3 * a] * cr[0] + F[3 * a + 1] * cr[1] + F[3 * a + 2] * cr[2];
+      const double gij = gi[0] * gj[0] + gi[1] * gj[1] + gi[2] * gj[2];
+      const double hj[9] = {0.0, w[2], -w[1], -w[2], 0.0, w[0], w[1], -w[0], 0.0};
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double v = (r == c ? c1 * gij : 0.0) + c2 * ai[r] * aj[c] + m.lambda * bi[r] * bj[c] + c4 * hj[3 * r + c];
+          o.H[lj][3 * r + c] = scale * v;
+        }
+    }
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(32 * kWarps) k_assemble(DevData d, MatDev m, StepCoeffs sc) {
+  constexpr bool kBlocks = kMode != kAssembleForcesOnly;
+  __shared__ double s_blk[kBlocks ? kWarps : 1][32][36];
+  __shared__ double s_frc[kWarps][32][3];
+  __shared__ uint32_t s_slot[kWarps][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kWarps + w;
+  if (i >= d.nn) return;
+  const int p0 = __ldg(d.nt_ptr + i), p1 = __ldg(d.nt_ptr + i + 1);
+  const int row0 = __ldg(d.brow + i), deg = __ldg(d.brow + i + 1) - row0;
+
+  double acc[2][9];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[h][q] = 0.0;
+  double fsum = 0.0;  // lanes 0..2: force component
+
+  for (int chunk = p0; chunk < p1; chunk += 32) {
+    const int q = chunk + lane;
+    uint32_t slot = 0xffffffffu;
+    ElemOut eo;
+    eo.f[0] = eo.f[1] = eo.f[2] = 0.0;
+    if (q < p1) {
+      const int e = __ldg(d.nt_tet + q);
+      slot = __ldg(d.nt_slot + q);
+      const int4 t = __ldg(d.tets + e);
+      const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
+      const double scale = d.chi[e] * __ldg(d.vol + e);
+      if (scale != 0.0) {  // fem.cpp:51 / fem.cpp:114 early-out
+        element_row<kBlocks>(d, m, e, li, scale, eo);
+      } else if (kBlocks) {
+#pragma unroll
+        for (int lj = 0; lj < 4; ++lj)
+#pragma unroll
+          for (int r = 0; r < 9; ++r) eo.H[lj][r] = 0.0;
+      }
+      if (kBlocks) {
+#pragma unroll
+        for (int lj = 0; lj < 4; ++lj)
+#pragma unroll
+          for (int r = 0; r < 9; ++r) s_blk[w][lane][9 * lj + r] = eo.H[lj][r];
+      }
+    }
+    s_slot[w][lane] = slot;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) s_frc[w][lane][a] = eo.f[a];
+    __syncwarp();
+    const int n = min(32, p1 - chunk);
+    if (lane < 3)
+      for (int l = 0; l < n; ++l) fsum += s_frc[w][l][lane];  // ascending tet order (fem.cpp:104-106)
+    if (kBlocks) {
+      for (int l = 0; l < n; ++l) {
+        const uint32_t s = s_slot[w][l];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int pos = (int)((s >> (8 * k)) & 0xffu);
+          if (pos == lane) {
+#pragma unroll
+            for (int r = 0; r < 9; ++r) acc[0][r] += s_blk[w][l][9 * k + r];
+          } else if (pos == lane + 32) {
+#pragma unroll
+            for (int r = 0; r < 9; ++r) acc[1][r] += s_blk[w][l][9 * k + r];
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  const bool fixed_i = __ldg(d.node_bc + i) >= 0;
+  double kv[3] = {0.0, 0.0, 0.0}, corr[3] = {0.0, 0.0, 0.0};
+  if (kBlocks) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c >= deg) break;
+      const int blk = row0 + c;
+      double* out = d.bval + 9 * (size_t)blk;
+      if (kMode == kAssembleRawK) {
+#pragma unroll
+        for (int r = 0; r < 9; ++r) out[r] = acc[h][r];
+        continue;
+      }
+      const int j = __ldg(d.bcol + blk);
+      double vj[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) vj[a] = d.v[3 * (size_t)j + a];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) kv[a] += acc[h][3 * a] * vj[0] + acc[h][3 * a + 1] * vj[1] + acc[h][3 * a + 2] * vj[2];
+      double A[9];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) A[r] = sc.kscale * acc[h][r];
+      if (j == i) {
+        const double md = sc.mscale * __ldg(d.mass + i);
+        A[0] += md;
+        A[4] += md;
+        A[8] += md;
+      }
+      if (fixed_i) {  // project_dirichlet: fixed row zeroed, unit diagonal
+#pragma unroll
+        for (int r = 0; r < 9; ++r) A[r] = (j == i && r % 4 == 0) ? 1.0 : 0.0;
+      } else if (__ldg(d.node_bc + j) >= 0) {  // fixed column: move A_ij * dv_j to the rhs, zero it
+        double fj[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) fj[a] = d.fv[3 * (size_t)j + a];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) corr[a] += A[3 * a] * fj[0] + A[3 * a + 1] * fj[1] + A[3 * a + 2] * fj[2];
+#pragma unroll
+        for (int r = 0; r < 9; ++r) A[r] = 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < 9; ++r) out[r] = A[r];
+      if (j == i) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double dd = A[4 * a];
+          d.dinv[3 * (size_t)i + a] = (fabs(dd) > 1e-300) ? 1.0 / dd : 1.0;  // sparse.cpp:133-136
+        }
+      }
+    }
+  }
+  if (kMode == kAssembleSystem) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      kv[a] = warp_sum(kv[a]);
+      corr[a] = warp_sum(corr[a]);
+    }
+  }
+  if (lane < 3) {
+    const int a = lane;
+    const size_t dof = 3 * (size_t)i + a;
+    if (d.fint_out) d.fint_out[dof] = fsum;
+    if (kMode == kAssembleSystem) {
+      if (fixed_i) {
+        d.rhs[dof] = d.fv[dof];
+        d.x[dof] = d.fv[dof];
+      } else {
+        const double mv = __ldg(d.mass + i) * d.v[dof];
+        double r = sc.rhs_fint_scale * ((d.fext[dof] + d.fcoll[dof]) + fsum);
+        r -= sc.rhs_mv_scale * mv;
+        r -= sc.rhs_kv_scale * kv[a];
+        r -= corr[a];
+        d.rhs[dof] = r;
+        d.x[dof] = 0.0;
+      }
+    }
+  }
+}
+
+// per-tet strain energy chi*V*Psi(F) (fem.cpp:190-199), block partial sums (deterministic order)
+__global__ void __launch_bounds__(256) k_energy(DevData d, MatDev m, double* partials) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d.nt; e += gridDim.x * blockDim.x) {
+    const double scale = d.chi[e] * d.vol[e];
+    if (scale == 0.0) continue;
+    const int4 t = d.tets[e];
+    const int id[4] = {t.x, t.y, t.z, t.w};
+    double du[9], B[9], F[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) B[q] = d.binv[9 * (size_t)e + q];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int r = 0; r < 3; ++r) du[3 * r + c] = d.u[3 * (size_t)id[c + 1] + r] - d.u[3 * (size_t)id[0] + r];
+    def_grad(du, B, F);
+    double psi;
+    if (m.model == 1) {
+      double Cm[9];
+      for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) Cm[3 * r + c] = F[r] * F[c] + F[3 + r] * F[3 + c] + F[6 + r] * F[6 + c];
+      const double ic = Cm[0] + Cm[4] + Cm[8];
+      double iic = 0.0;
+      for (int q = 0; q < 9; ++q) iic += Cm[q] * Cm[q];
+      psi = 0.125 * m.lambda * (ic - 3.0) * (ic - 3.0) + 0.25 * m.mu * (iic - 2.0 * ic + 3.0);
+    } else {
+      const double ic = sqnorm9(F);
+      const double j = det3(F);
+      psi = 0.5 * m.mu * (ic - 3.0) + 0.5 * m.lambda * (j - m.alpha_nh) * (j - m.alpha_nh) - 0.5 * m.mu * log(ic + 1.0);
+    }
+    acc += scale * psi;
+  }
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = s[0];
+}
+
+}  // namespace
+
+void launch_assemble(const DevData& d, const MatDev& m, const StepCoeffs& c, int mode, cudaStream_t s) {
+  const int grid = (d.nn + kWarps - 1) / kWarps;
+  if (mode == kAssembleSystem) k_assemble<kAssembleSystem><<<grid, 32 * kWarps, 0, s>>>(d, m, c);
+  else if (mode == kAssembleRawK) k_assemble<kAssembleRawK><<<grid, 32 * kWarps, 0, s>>>(d, m, c);
+  else k_assemble<kAssembleForcesOnly><<<grid, 32 * kWarps, 0, s>>>(d, m, c);
+}
+
+void launch_energy(const DevData& d, const MatDev& m, double* partials, int nblocks, cudaStream_t s) {
+  k_energy<<<nblocks, 256, 0, s>>>(d, m, partials);
+}
+
+}  // namespace gfb

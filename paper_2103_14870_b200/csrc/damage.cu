@@ -1,0 +1,211 @@
+// damage.cu — per-timestep damage pass (Simulation::damage_pass, solver.cpp:90-103) on the GPU.
+//
+// BUILT WITH -fmad=false: every kernel here must reproduce the CPU oracle bit-for-bit (edge labels,
+// newly-broken sets and chi are bit-exact from an identical state; north_star).
+//
+//  k_tet_stress  thread/tet: F, P, Cauchy six-vector sigma_c (per_tet_cauchy, solver.cpp:79-88), edge
+//                transform T (build_T, fracture.cpp:16-28), local edge stresses sigma_f = T sigma_c
+//                (fracture.cpp:74), degenerate flag; for r_d = 0 also the screened value T*(0 + 1*sigma_c)
+//                reduced straight into the per-edge max (fracture.cpp:80-87) by an order-free atomic max.
+//  k_nonlocal    thread/tet (r_d > 0): avg = sum_w w*sigma_c[o] in table order (fracture.cpp:75-76),
+//                screened = T*avg (fracture.cpp:77), atomic max into the edges.
+//  k_relabel     thread/edge: decode the max (-inf -> 0, fracture.cpp:88-89), signed >= threshold relabel
+//                of intact edges (update_damage, fracture.cpp:93-104), warp-ballot + one atomic per warp
+//                compaction of the newly-broken ids (ascending order restored on read-back), key reset.
+//  k_chi         thread/tet: compute_chi (fracture.cpp:127-157) incl. fragment_components
+//                (fracture.cpp:106-125), degenerate -> 0, chi = min(chi_old, value) (solver.cpp:97-101).
+#include "device_math.cuh"
+
+namespace gfb {
+namespace {
+
+constexpr int kTpb = 256;
+
+__device__ __forceinline__ void load_tet_positions(const DevData& d, int4 t, double x[4][3], double du[9]) {
+  const int id[4] = {t.x, t.y, t.z, t.w};
+  double u[4][3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      u[k][a] = __ldg(d.u + 3 * (size_t)id[k] + a);
+      x[k][a] = __ldg(d.X + 3 * (size_t)id[k] + a) + u[k][a];
+    }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) du[3 * r + c] = u[c + 1][r] - u[0][r];
+}
+
+__device__ __forceinline__ void tet_rest_lengths(const DevData& d, int e, int te[6], double rl[6]) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    te[k] = __ldg(d.tet_edges + 6 * (size_t)e + k);
+    rl[k] = __ldg(d.rest_len + te[k]);
+  }
+}
+
+__device__ __forceinline__ void scatter_max(const DevData& d, const int te[6], const double scr[6]) {
+#pragma unroll
+  for (int k = 0; k < 6; ++k) atomicMax(d.scr_key + te[k], dkey(scr[k]));
+}
+
+__global__ void __launch_bounds__(kTpb) k_tet_stress(DevData d, MatDev m, int local_screen) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.nt) return;
+  const int4 t = __ldg(d.tets + e);
+  double x[4][3], du[9], B[9], F[9], P[9], c6[6];
+  load_tet_positions(d, t, x, du);
+#pragma unroll
+  for (int q = 0; q < 9; ++q) B[q] = __ldg(d.binv + 9 * (size_t)e + q);
+  def_grad(du, B, F);
+  const double J = pk1(F, m, P);
+  cauchy6(F, P, J, c6);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) d.sigc[6 * (size_t)e + k] = c6[k];
+
+  int te[6];
+  double rl[6], T[6][6], sf[6];
+  tet_rest_lengths(d, e, te, rl);
+  const bool ok = build_T(x, rl, T);
+  d.deg[e] = ok ? 0 : 1;
+  if (!ok) {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) d.sigf[6 * (size_t)e + k] = 0.0;  // tet_edge_stress stays Zero
+    return;
+  }
+  matvec6(T, c6, sf);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) d.sigf[6 * (size_t)e + k] = sf[k];
+  if (local_screen) {  // r_d = 0: table {(e, 1.0)} -> avg = 0 + 1.0 * sigma_c
+    double avg[6], scr[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) avg[k] = 0.0 + 1.0 * c6[k];
+    matvec6(T, avg, scr);
+    scatter_max(d, te, scr);
+  }
+}
+
+__global__ void __launch_bounds__(kTpb) k_nonlocal(DevData d) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.nt) return;
+  if (d.deg[e]) return;
+  const int4 t = __ldg(d.tets + e);
+  double x[4][3], du[9];
+  load_tet_positions(d, t, x, du);
+  int te[6];
+  double rl[6], T[6][6];
+  tet_rest_lengths(d, e, te, rl);
+  build_T(x, rl, T);  // non-degenerate (checked by k_tet_stress with identical arithmetic)
+  double avg[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const int64_t q1 = __ldg(d.nl_ptr + e + 1);
+  for (int64_t q = __ldg(d.nl_ptr + e); q < q1; ++q) {
+    const double w = __ldg(d.nl_w + q);
+    const double* so = d.sigc + 6 * (size_t)__ldg(d.nl_ids + q);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) avg[k] = avg[k] + w * __ldg(so + k);
+  }
+  double scr[6];
+  matvec6(T, avg, scr);
+  scatter_max(d, te, scr);
+}
+
+__global__ void __launch_bounds__(kTpb) k_relabel(DevData d, double thres, int relabel, int keep_values) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool broke = false;
+  if (i < d.ne) {
+    const unsigned long long key = d.scr_key[i];
+    const double s = (key == kKeyNegInf) ? 0.0 : dkey_inv(key);
+    if (keep_values) d.screening[i] = s;
+    d.scr_key[i] = kKeyNegInf;
+    if (relabel && !d.zeta[i] && s >= thres) {
+      d.zeta[i] = 1;
+      broke = true;
+    }
+  }
+  const unsigned mask = __ballot_sync(0xffffffffu, broke);
+  if (mask == 0) return;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == 0) base = atomicAdd(d.newly_count, __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (broke) d.newly[base + __popc(mask & ((1u << lane) - 1u))] = i;
+}
+
+__global__ void __launch_bounds__(kTpb) k_chi(DevData d, MatDev m) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.nt) return;
+  int te[6];
+  bool dmg[6];
+  int intact = 0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    te[k] = __ldg(d.tet_edges + 6 * (size_t)e + k);
+    dmg[k] = d.zeta[te[k]] != 0;
+    intact += dmg[k] ? 0 : 1;
+  }
+  double value;
+  if (d.deg[e]) {
+    value = 0.0;
+  } else if (intact == 6) {
+    value = 1.0;
+  } else if (intact == 0) {
+    value = 0.0;
+  } else {
+    constexpr int le[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+    int label[4] = {0, 1, 2, 3};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      if (dmg[k]) continue;
+      int a = le[k][0], b = le[k][1];
+      while (label[a] != a) a = label[a];
+      while (label[b] != b) b = label[b];
+      if (a != b) label[a > b ? a : b] = a < b ? a : b;
+    }
+    int comps = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int r = i;
+      while (label[r] != r) r = label[r];
+      comps += (r == i) ? 1 : 0;
+    }
+    if (comps >= 2) {
+      value = 0.0;
+    } else {
+      double surviving = 0.0, total = 0.0;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const double s = fabs(d.sigf[6 * (size_t)e + k]);
+        total += s;
+        if (!dmg[k]) surviving += s;
+      }
+      value = (total < m.chi_eps) ? (double)intact / 6.0 : surviving / total;
+    }
+  }
+  const double old = d.chi[e];
+  const double nv = std_min(old, value);
+  if (__double_as_longlong(nv) != __double_as_longlong(old)) d.chi[e] = nv;
+}
+
+__global__ void k_reset_keys(unsigned long long* k, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) k[i] = kKeyNegInf;
+}
+
+inline int nblk(int64_t n) { return (int)((n + kTpb - 1) / kTpb); }
+
+}  // namespace
+
+void launch_tet_stress(const DevData& d, const MatDev& m, bool local_screen, cudaStream_t s) {
+  k_tet_stress<<<nblk(d.nt), kTpb, 0, s>>>(d, m, local_screen ? 1 : 0);
+}
+void launch_nonlocal(const DevData& d, cudaStream_t s) { k_nonlocal<<<nblk(d.nt), kTpb, 0, s>>>(d); }
+void launch_relabel(const DevData& d, double thres, bool relabel, bool keep_values, cudaStream_t s) {
+  k_relabel<<<nblk(d.ne), kTpb, 0, s>>>(d, thres, relabel ? 1 : 0, keep_values ? 1 : 0);
+}
+void launch_chi(const DevData& d, const MatDev& m, cudaStream_t s) { k_chi<<<nblk(d.nt), kTpb, 0, s>>>(d, m); }
+void launch_reset_keys(const DevData& d, cudaStream_t s) {
+  k_reset_keys<<<nblk(d.ne), kTpb, 0, s>>>(d.scr_key, d.ne);
+}
+
+}  // namespace gfb

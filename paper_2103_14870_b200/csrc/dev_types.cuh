@@ -1,0 +1,151 @@
+// dev_types.cuh — HBM-resident data of one Simulation (plain device pointers) and kernel launchers.
+//
+// Layout: node vectors interleaved xyz (dof = 3*node+axis, 24 B contiguous per node so a
+// gather is one sector); per-tet records AoS (B^-1 72 B, sigma 48 B) so scattered per-tet gathers are
+// contiguous; the system matrix is a node-block CSR (BSR 3x3, row-major blocks, 72 B per block).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace gfb {
+
+struct MatDev {
+  double mu, lambda, alpha_nh;  // alpha_nh = 1 + mu/lambda - mu/(4 lambda) (material.cpp:65-67)
+  double sigma_thres, chi_eps;  // chi_eps = 1e-12 * sigma_thres (fracture.cpp:132)
+  int32_t model;                // 0 stable neo-hookean, 1 stvk
+};
+
+struct StepCoeffs {  // per-step scalars of solver.cpp:279-289
+  double dt;
+  double rhs_fint_scale;  // dt
+  double rhs_mv_scale;    // dt*alpha
+  double rhs_kv_scale;    // dt*beta + dt*dt
+  double kscale;          // dt*beta + dt*dt
+  double mscale;          // 1 + dt*alpha
+};
+
+// one entry per boundary condition, evaluated by the host each step (solver.cpp:22-29)
+struct BcStep {
+  int32_t kind;    // 0 translate, 1 rotate
+  int32_t _pad;
+  double d0[3], d1[3];   // translate: u(t), u(t+dt)
+  double R0[9], R1[9];   // rotate: rotation matrices at t, t+dt (row-major)
+  double axis_point[3];
+};
+
+struct ColliderDev {
+  int32_t kind;  // 0 sphere, 1 halfspace
+  int32_t _pad;
+  double center[3], cvel[3];  // sphere centre / centre rate at the probe time
+  double radius;
+  double point[3], normal[3];
+  double stiffness, restitution, friction;
+};
+
+struct DevData {
+  int32_t nn, nt, ne, nb;  // nodes, tets, edges, node blocks (BSR nnz)
+  // mesh (read-only)
+  const double* X;          // 3nn
+  const int4* tets;         // nt
+  const double* binv;       // 9nt row-major AoS
+  const double* vol;        // nt
+  const int32_t* tet_edges; // 6nt AoS
+  const double* rest_len;   // ne
+  const int32_t* et_ptr;    // ne+1 (edge -> tets, ascending)
+  const int32_t* et_ids;
+  const double* mass;       // nn (lumped node mass; all three dofs equal)
+  const int32_t* node_bc;   // nn: bc index or -1
+  // node -> tet incidence (ascending tet) with packed column slots
+  const int32_t* nt_ptr;
+  const int32_t* nt_tet;
+  const uint32_t* nt_slot;
+  // BSR pattern
+  const int32_t* brow;      // nn+1
+  const int32_t* bcol;      // nb
+  const int32_t* bdiag;     // nn
+  // non-local table (r_d > 0)
+  const int64_t* nl_ptr;
+  const int32_t* nl_ids;
+  const double* nl_w;
+  // state
+  double* u;                // 3nn
+  double* v;                // 3nn
+  uint8_t* zeta;            // ne
+  double* chi;              // nt
+  // damage scratch
+  double* sigc;             // 6nt
+  double* sigf;             // 6nt
+  uint8_t* deg;             // nt
+  unsigned long long* scr_key;  // ne ordered-key max accumulator
+  double* screening;        // ne (parity hooks only)
+  int32_t* newly;           // ne
+  int32_t* newly_count;     // 1
+  // system
+  double* bval;             // 9nb
+  double* rhs;              // 3nn
+  double* dinv;             // 3nn
+  double* x;                // 3nn  (dv)
+  double* fext;             // 3nn static part: m g + user load
+  double* fcoll;            // 3nn collision part of the current step
+  double* fv;               // 3nn fixed-dof prescribed dv (valid on BC nodes)
+  double* utgt;             // 3nn pinned u(t+dt) (valid on BC nodes)
+  double* vtgt;             // 3nn pinned v(t+dt)
+  double* fint_out;         // 3nn optional (parity hook)
+  double* absdiag;          // 3nn |diag| with fixed dofs zeroed (CG shift ladder)
+  // CG work
+  double* r;
+  double* z;
+  double* p0;
+  double* p1;
+  double* Ap;
+  double* partials;         // per-block reduction slots
+  double* cg_out;           // [iterations, converged, negcurv, relres]
+  // misc
+  const BcStep* bcstep;
+  const ColliderDev* colliders;
+  int32_t n_colliders;
+  double* coll_partials;
+};
+
+// ---- launchers (damage.cu, compiled with -fmad=false) ----
+void launch_tet_stress(const DevData& d, const MatDev& m, bool local_screen, cudaStream_t s);
+void launch_nonlocal(const DevData& d, cudaStream_t s);
+void launch_relabel(const DevData& d, double sigma_thres, bool relabel, bool keep_values, cudaStream_t s);
+void launch_chi(const DevData& d, const MatDev& m, cudaStream_t s);
+void launch_reset_keys(const DevData& d, cudaStream_t s);
+// ---- assemble.cu ----
+enum AssembleMode { kAssembleSystem = 0, kAssembleRawK = 1, kAssembleForcesOnly = 2 };
+void launch_assemble(const DevData& d, const MatDev& m, const StepCoeffs& c, int mode, cudaStream_t s);
+void launch_energy(const DevData& d, const MatDev& m, double* out_partials, int nblocks, cudaStream_t s);
+// ---- cg.cu ----
+struct CgLaunch {
+  int32_t nrows;          // block rows (B=3: nodes) or scalar rows (B=1)
+  const int32_t* row_ptr;
+  const int32_t* cols;
+  const double* vals;
+  const double* b;
+  double* x;
+  const double* dinv;     // may be null: computed from the diagonal
+  double* r; double* z; double* p0; double* p1; double* Ap;
+  double* partials;
+  double* out;            // [iterations, converged, negative_curvature, relative_residual]
+  double tol;
+  int32_t max_iters;
+};
+int cg_grid_size(int block_size);
+void launch_pcg3(const CgLaunch& a, cudaStream_t s);
+void launch_pcg1(const CgLaunch& a, cudaStream_t s);
+void launch_spmv3(const CgLaunch& a, const double* xin, double* y, cudaStream_t s);
+// ---- misc.cu ----
+void launch_bc_targets(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, double dt, cudaStream_t s);
+int collide_blocks(const DevData& d);
+void launch_collide(const DevData& d, int substep, double tau, double dt, int nsub, cudaStream_t s);
+void launch_collide_load(const DevData& d, int nsub, double* out, cudaStream_t s);
+void launch_integrate(const DevData& d, double dt, cudaStream_t s);
+void launch_shift_diag(const DevData& d, double shift, cudaStream_t s);
+void launch_absdiag(const DevData& d, cudaStream_t s);
+void launch_bsr_dinv(const DevData& d, cudaStream_t s);
+void launch_fill(double* p, double v, int64_t n, cudaStream_t s);
+
+}  // namespace gfb

@@ -1,0 +1,713 @@
+// sim.cu — host orchestration of the B200 Simulation (solver.cpp:31-333 restated B200-first).
+//
+// Per dynamic_step (solver.cpp:219-333) the host issues, on one stream and with no intermediate sync:
+//   damage    k_tet_stress [+ k_nonlocal] -> k_relabel -> k_chi              (solver.cpp:225, 90-103)
+//   f_ext     [k_collide x substeps -> k_collide_load]                        (solver.cpp:229-250)
+//   BCs       k_bc_targets                                                    (solver.cpp:255-262)
+//   system    k_assemble (forces, K, K v, rhs, A, projection, D^-1, x0)       (solver.cpp:275-295)
+//   solve     k_pcg (one cooperative kernel for the whole CG)                 (solver.cpp:105-136)
+//   update    k_integrate (v += dv, u += dt v, pin)                           (solver.cpp:296-328)
+// and reads back one 48-byte stats record (CG result, newly-broken count, collider load); the
+// reference's retry/shift ladder (solver.cpp:110-135) runs only when that record says the CG failed.
+#include "sim.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+namespace gfb {
+
+#define GF_CUDA(x)                                                                          \
+  do {                                                                                      \
+    const cudaError_t _e = (x);                                                             \
+    if (_e != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+void launch_reset_x(const DevData& d, cudaStream_t s);
+
+// ---------------------------------------------------------------- schedules / BCs (host, per step)
+void Schedule::eval(double time, double out[3]) const {  // Schedule3::eval (collision.cpp:8-18)
+  if (t.empty()) {
+    out[0] = out[1] = out[2] = 0.0;
+    return;
+  }
+  if (time <= t.front()) {
+    for (int a = 0; a < 3; ++a) out[a] = v[a];
+    return;
+  }
+  if (time >= t.back()) {
+    for (int a = 0; a < 3; ++a) out[a] = v[3 * (t.size() - 1) + a];
+    return;
+  }
+  const size_t hi = (size_t)(std::upper_bound(t.begin(), t.end(), time) - t.begin()), lo = hi - 1;
+  const double span = t[hi] - t[lo];
+  const double w = span > 0.0 ? (time - t[lo]) / span : 0.0;
+  for (int a = 0; a < 3; ++a) out[a] = (1.0 - w) * v[3 * lo + a] + w * v[3 * hi + a];
+}
+
+void Schedule::rate(double time, double out[3]) const {  // Schedule3::rate (collision.cpp:20-30)
+  out[0] = out[1] = out[2] = 0.0;
+  if (t.size() < 2 || time < t.front() || time > t.back()) return;
+  size_t hi = (size_t)(std::upper_bound(t.begin(), t.end(), time) - t.begin());
+  if (hi == 0) hi = 1;
+  if (hi >= t.size()) hi = t.size() - 1;
+  const size_t lo = hi - 1;
+  const double span = t[hi] - t[lo];
+  if (!(span > 0.0)) return;
+  for (int a = 0; a < 3; ++a) out[a] = (v[3 * hi + a] - v[3 * lo + a]) / span;
+}
+
+// BoundaryCondition::displacement_at (solver.cpp:22-29): translate -> d; rotate -> R of AngleAxis
+void HostBc::displacement_params(double time, double d[3], double R[9]) const {
+  if (kind == 0) {
+    sched.eval(time, d);
+    return;
+  }
+  double ang[3];
+  sched.eval(time, ang);
+  const double nn = (axis_dir[0] * axis_dir[0] + axis_dir[1] * axis_dir[1]) + axis_dir[2] * axis_dir[2];
+  double ax[3] = {axis_dir[0], axis_dir[1], axis_dir[2]};
+  if (nn > 0.0) {
+    const double l = std::sqrt(nn);
+    for (int a = 0; a < 3; ++a) ax[a] = axis_dir[a] / l;
+  }
+  const double s = std::sin(ang[0]), c = std::cos(ang[0]);
+  const double sa[3] = {s * ax[0], s * ax[1], s * ax[2]};
+  const double ca[3] = {(1.0 - c) * ax[0], (1.0 - c) * ax[1], (1.0 - c) * ax[2]};
+  double tmp = ca[0] * ax[1];
+  R[1] = tmp - sa[2];
+  R[3] = tmp + sa[2];
+  tmp = ca[0] * ax[2];
+  R[2] = tmp + sa[1];
+  R[6] = tmp - sa[1];
+  tmp = ca[1] * ax[2];
+  R[5] = tmp - sa[0];
+  R[7] = tmp + sa[0];
+  for (int a = 0; a < 3; ++a) R[4 * a] = ca[a] * ax[a] + c;
+}
+
+// ---------------------------------------------------------------- construction (solver.cpp:31-60)
+void* Simulation::dalloc(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 8;
+  GF_CUDA(cudaMalloc(&p, bytes));
+  allocs_.push_back(p);
+  return p;
+}
+
+Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_solver_config& cfg,
+                       const gf_boundary_condition* bcs, int32_t n_bcs, const gf_collider* cols, int32_t n_cols)
+    : mesh_(mesh), mat_(mat), cfg_(cfg) {
+  // validation in the reference's order (material.cpp:37-43, solver.cpp:10-20, collision.cpp:32-40, 46-56)
+  if (!(mat.youngs > 0.0)) throw FormatError("youngs modulus must be positive");
+  if (!(mat.poisson >= 0.0 && mat.poisson < 0.5)) throw FormatError("poisson ratio must be in [0, 0.5)");
+  if (!(mat.density > 0.0)) throw FormatError("density must be positive");
+  if (!(mat.sigma_thres > 0.0)) throw FormatError("sigma_thres must be positive");
+  if (!(mat.r_d >= 0.0)) throw FormatError("r_d must be non-negative");
+  if (!(cfg.dt > 0.0)) throw FormatError("dt must be positive");
+  if (!(cfg.cg_tol > 0.0)) throw FormatError("cg_tol must be positive");
+  if (cfg.newton_max_iters <= 0 || cfg.cg_max_iters <= 0) throw FormatError("iteration limits must be positive");
+  if (!(cfg.ls_backtrack > 0.0 && cfg.ls_backtrack < 1.0))
+    throw FormatError("line-search backtrack factor must be in (0, 1)");
+  if (!(cfg.ls_sufficient_decrease > 0.0 && cfg.ls_sufficient_decrease < 1.0))
+    throw FormatError("line-search sufficient-decrease constant must be in (0, 1)");
+  if (cfg.collision_substeps < 1) throw FormatError("collision_substeps must be >= 1");
+  if (cfg.dynamic_full_newton) throw FormatError("dynamic_full_newton is outside the B200 hot path");
+  for (int c = 0; c < n_cols; ++c) {
+    const gf_collider& k = cols[c];
+    const double nn = std::sqrt((k.normal[0] * k.normal[0] + k.normal[1] * k.normal[1]) + k.normal[2] * k.normal[2]);
+    if (k.kind == 0 && !(k.radius > 0.0)) throw FormatError("sphere radius must be positive");
+    if (k.kind == 1 && std::abs(nn - 1.0) > 1e-9) throw FormatError("halfspace normal must be unit length");
+    if (!(k.stiffness > 0.0)) throw FormatError("collider stiffness must be positive");
+    if (k.restitution < 0.0 || k.restitution > 1.0) throw FormatError("restitution must be in [0, 1]");
+    if (k.friction < 0.0) throw FormatError("friction must be non-negative");
+  }
+  if (n_cols > 8) throw FormatError("at most 8 colliders are supported by the device collision kernel");
+  std::vector<int32_t> node_bc(mesh_.nn, -1);
+  for (int b = 0; b < n_bcs; ++b) {
+    const std::string name = "bc" + std::to_string(b);
+    if (bcs[b].n_nodes <= 0) throw FormatError("boundary condition '" + name + "' selects no nodes");
+    for (int q = 0; q < bcs[b].n_nodes; ++q) {
+      const int32_t n = bcs[b].nodes[q];
+      if (n < 0 || n >= mesh_.nn) throw FormatError("boundary condition '" + name + "' references node out of range");
+      if (node_bc[n] >= 0) throw FormatError("node " + std::to_string(n) + " appears in two boundary conditions");
+      node_bc[n] = b;
+    }
+    HostBc hb;
+    hb.kind = bcs[b].kind;
+    hb.nodes.assign(bcs[b].nodes, bcs[b].nodes + bcs[b].n_nodes);
+    hb.sched.t.assign(bcs[b].key_times, bcs[b].key_times + bcs[b].n_keys);
+    hb.sched.v.assign(bcs[b].key_values, bcs[b].key_values + 3 * bcs[b].n_keys);
+    for (int a = 0; a < 3; ++a) {
+      hb.axis_point[a] = bcs[b].axis_point[a];
+      hb.axis_dir[a] = bcs[b].axis_dir[a];
+    }
+    bcs_.push_back(std::move(hb));
+  }
+  for (int c = 0; c < n_cols; ++c) {
+    HostCollider hc;
+    hc.kind = cols[c].kind;
+    hc.center.t.assign(cols[c].key_times, cols[c].key_times + cols[c].n_keys);
+    hc.center.v.assign(cols[c].key_values, cols[c].key_values + 3 * cols[c].n_keys);
+    hc.radius = cols[c].radius;
+    for (int a = 0; a < 3; ++a) {
+      hc.point[a] = cols[c].point[a];
+      hc.normal[a] = cols[c].normal[a];
+    }
+    hc.stiffness = cols[c].stiffness;
+    hc.restitution = cols[c].restitution;
+    hc.friction = cols[c].friction;
+    cols_.push_back(hc);
+  }
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    throw CudaError("no CUDA device: the B200 hot path has no CPU fallback");
+  }
+  int dev = 0, major = 0;
+  GF_CUDA(cudaGetDevice(&dev));
+  GF_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major < 10) throw CudaError("device is not sm_100 class (Blackwell); this build targets sm_100a only");
+
+  // host setup: pattern, incidence, table, mass (fem.cpp:140-179, fracture.cpp:32-54)
+  pat_ = make_node_pattern(mesh_);
+  if (pat_.max_degree > 64) throw GeometryError("node valence above 64 is not supported by the assembly kernel");
+  const NodeTets ntets = make_node_tets(mesh_, pat_);
+  hash_ = pat_.structure_hash(mesh_.nn);
+  mass_.assign(mesh_.nn, 0.0);
+  for (int32_t e = 0; e < mesh_.nt; ++e) {  // lumped_mass (fem.cpp:171-179), ascending tet order
+    const double q = mat.density * mesh_.vol[e] / 4.0;
+    for (int k = 0; k < 4; ++k) mass_[mesh_.tets[4 * (size_t)e + k]] += q;
+  }
+  md_.mu = mat.mu;
+  md_.lambda = mat.lambda;
+  md_.alpha_nh = 1.0 + mat.mu / mat.lambda - mat.mu / (4.0 * mat.lambda);
+  md_.sigma_thres = mat.sigma_thres;
+  md_.chi_eps = 1e-12 * mat.sigma_thres;
+  md_.model = mat.energy_model;
+
+  GF_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  const int32_t nn = mesh_.nn, nt = mesh_.nt, ne = mesh_.ne, nb = (int32_t)pat_.cols.size();
+  auto up = [&](const void* src, size_t bytes) {
+    void* p = dalloc(bytes);
+    if (bytes) GF_CUDA(cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, stream_));
+    return p;
+  };
+  d_.nn = nn; d_.nt = nt; d_.ne = ne; d_.nb = nb;
+  d_.X = (const double*)up(mesh_.X.data(), 8 * mesh_.X.size());
+  d_.tets = (const int4*)up(mesh_.tets.data(), 4 * mesh_.tets.size());
+  d_.binv = (const double*)up(mesh_.binv.data(), 8 * mesh_.binv.size());
+  d_.vol = (const double*)up(mesh_.vol.data(), 8 * mesh_.vol.size());
+  d_.tet_edges = (const int32_t*)up(mesh_.tet_edges.data(), 4 * mesh_.tet_edges.size());
+  d_.rest_len = (const double*)up(mesh_.rest_len.data(), 8 * mesh_.rest_len.size());
+  d_.et_ptr = (const int32_t*)up(mesh_.et_ptr.data(), 4 * mesh_.et_ptr.size());
+  d_.et_ids = (const int32_t*)up(mesh_.et_ids.data(), 4 * mesh_.et_ids.size());
+  d_.mass = (const double*)up(mass_.data(), 8 * mass_.size());
+  d_.node_bc = (const int32_t*)up(node_bc.data(), 4 * node_bc.size());
+  d_.nt_ptr = (const int32_t*)up(ntets.ptr.data(), 4 * ntets.ptr.size());
+  d_.nt_tet = (const int32_t*)up(ntets.tet.data(), 4 * ntets.tet.size());
+  d_.nt_slot = (const uint32_t*)up(ntets.slot.data(), 4 * ntets.slot.size());
+  d_.brow = (const int32_t*)up(pat_.row_ptr.data(), 4 * pat_.row_ptr.size());
+  d_.bcol = (const int32_t*)up(pat_.cols.data(), 4 * pat_.cols.size());
+  d_.bdiag = (const int32_t*)up(pat_.diag.data(), 4 * pat_.diag.size());
+  if (mat.r_d > 0.0) {
+    const NonlocalTable tb = make_nonlocal_table(mesh_, mat.r_d);
+    nl_entries_ = (int64_t)tb.ids.size();
+    d_.nl_ptr = (const int64_t*)up(tb.ptr.data(), 8 * tb.ptr.size());
+    d_.nl_ids = (const int32_t*)up(tb.ids.data(), 4 * tb.ids.size());
+    d_.nl_w = (const double*)up(tb.w.data(), 8 * tb.w.size());
+    GF_CUDA(cudaStreamSynchronize(stream_));  // tb goes out of scope
+  } else {
+    nl_entries_ = nt;
+  }
+  const size_t nd = 3 * (size_t)nn;
+  auto zeros = [&](size_t bytes) {
+    void* p = dalloc(bytes);
+    GF_CUDA(cudaMemsetAsync(p, 0, bytes, stream_));
+    return p;
+  };
+  d_.u = (double*)zeros(8 * nd);
+  d_.v = (double*)zeros(8 * nd);
+  d_.zeta = (uint8_t*)zeros(ne);
+  d_.chi = (double*)dalloc(8 * (size_t)nt);
+  launch_fill(d_.chi, 1.0, nt, stream_);  // SimState::rest (fem.cpp:7-14)
+  d_.sigc = (double*)zeros(48 * (size_t)nt);
+  d_.sigf = (double*)zeros(48 * (size_t)nt);
+  d_.deg = (uint8_t*)zeros(nt);
+  d_.scr_key = (unsigned long long*)dalloc(8 * (size_t)ne);
+  d_.screening = (double*)zeros(8 * (size_t)ne);
+  d_.newly = (int32_t*)zeros(4 * (size_t)ne);
+  d_.newly_count = (int32_t*)zeros(8);
+  d_.bval = (double*)zeros(72 * (size_t)nb);
+  d_.rhs = (double*)zeros(8 * nd);
+  d_.dinv = (double*)zeros(8 * nd);
+  d_.x = (double*)zeros(8 * nd);
+  d_.fext = (double*)zeros(8 * nd);
+  d_.fcoll = (double*)zeros(8 * nd);
+  d_.fv = (double*)zeros(8 * nd);
+  d_.utgt = (double*)zeros(8 * nd);
+  d_.vtgt = (double*)zeros(8 * nd);
+  d_.absdiag = (double*)zeros(8 * nd);
+  d_.r = (double*)zeros(8 * nd);
+  d_.z = (double*)zeros(8 * nd);
+  d_.p0 = (double*)zeros(8 * nd);
+  d_.p1 = (double*)zeros(8 * nd);
+  d_.Ap = (double*)zeros(8 * nd);
+  d_.partials = (double*)zeros(8 * 2 * 3 * (size_t)std::max(cg_grid_size(3), cg_grid_size(1)));
+  d_.cg_out = (double*)zeros(8 * 8);
+  d_.n_colliders = (int32_t)cols_.size();
+  const int nsub = cfg.collision_substeps;
+  if (!cols_.empty()) {
+    d_cols_ = (ColliderDev*)dalloc(sizeof(ColliderDev) * cols_.size() * nsub);
+    d_.colliders = d_cols_;
+    d_.coll_partials = (double*)zeros(8 * (size_t)nsub * cols_.size() * 3 * collide_blocks(d_));
+    GF_CUDA(cudaMallocHost(&h_cols_, sizeof(ColliderDev) * cols_.size() * nsub));
+  }
+  d_load_ = (double*)zeros(8);
+  d_energy_partials_ = (double*)zeros(8 * 1024);
+  if (!bcs_.empty()) {
+    d_bcstep_ = (BcStep*)dalloc(sizeof(BcStep) * bcs_.size());
+    d_.bcstep = d_bcstep_;
+    GF_CUDA(cudaMallocHost(&h_bcstep_, sizeof(BcStep) * bcs_.size()));
+  }
+  std::vector<int32_t> fixed;
+  for (int32_t i = 0; i < nn; ++i)
+    if (node_bc[i] >= 0) fixed.push_back(i);
+  n_fixed_ = (int32_t)fixed.size();
+  d_fixed_nodes_ = (int32_t*)up(fixed.data(), 4 * fixed.size());
+  GF_CUDA(cudaMallocHost(&h_stats_, 8 * 8));
+  // static external force: m g (solver.cpp:230-231)
+  std::vector<double> fext(nd);
+  for (int32_t i = 0; i < nn; ++i)
+    for (int a = 0; a < 3; ++a) fext[3 * (size_t)i + a] = mass_[i] * cfg.gravity[a];
+  GF_CUDA(cudaMemcpyAsync(d_.fext, fext.data(), 8 * nd, cudaMemcpyHostToDevice, stream_));
+  launch_reset_keys(d_, stream_);
+
+  cg_.nrows = nn;
+  cg_.row_ptr = d_.brow;
+  cg_.cols = d_.bcol;
+  cg_.vals = d_.bval;
+  cg_.b = d_.rhs;
+  cg_.x = d_.x;
+  cg_.dinv = d_.dinv;
+  cg_.r = d_.r; cg_.z = d_.z; cg_.p0 = d_.p0; cg_.p1 = d_.p1; cg_.Ap = d_.Ap;
+  cg_.partials = d_.partials;
+  cg_.out = d_.cg_out;
+  cg_.tol = cfg.cg_tol;
+  GF_CUDA(cudaStreamSynchronize(stream_));
+  GF_CUDA(cudaGetLastError());
+}
+
+Simulation::~Simulation() {
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& p : pending_) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : event_pool_) cudaEventDestroy(e);
+  for (void* p : allocs_) cudaFree(p);
+  if (h_bcstep_) cudaFreeHost(h_bcstep_);
+  if (h_cols_) cudaFreeHost(h_cols_);
+  if (h_stats_) cudaFreeHost(h_stats_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+// ---------------------------------------------------------------- launch bookkeeping / profiling
+template <class F>
+void Simulation::launch(const char* name, double bytes, F&& f) {
+  if (!profiling_) {
+    f();
+    GF_CUDA(cudaGetLastError());
+    return;
+  }
+  auto take = [&]() {
+    cudaEvent_t e;
+    if (!event_pool_.empty()) {
+      e = event_pool_.back();
+      event_pool_.pop_back();
+    } else {
+      GF_CUDA(cudaEventCreate(&e));
+    }
+    return e;
+  };
+  Pending p{name, take(), take(), bytes};
+  GF_CUDA(cudaEventRecord(p.a, stream_));
+  f();
+  GF_CUDA(cudaGetLastError());
+  GF_CUDA(cudaEventRecord(p.b, stream_));
+  pending_.push_back(p);
+}
+
+void Simulation::flush_events() {
+  for (auto& p : pending_) {
+    float ms = 0.f;
+    GF_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    auto& k = ktimes_[p.name];
+    std::strncpy(k.name, p.name.c_str(), sizeof(k.name) - 1);
+    k.launches += 1;
+    k.total_ms += ms;
+    k.bytes += p.bytes;
+    event_pool_.push_back(p.a);
+    event_pool_.push_back(p.b);
+  }
+  pending_.clear();
+}
+
+void Simulation::synchronize() {
+  GF_CUDA(cudaStreamSynchronize(stream_));
+  flush_events();
+}
+
+std::vector<gf_kernel_time> Simulation::kernel_times() {
+  synchronize();
+  std::vector<gf_kernel_time> out;
+  for (auto& kv : ktimes_) out.push_back(kv.second);
+  return out;
+}
+
+// ---------------------------------------------------------------- damage pass (solver.cpp:90-103)
+void Simulation::run_damage(bool relabel, bool keep_values, bool chi) {
+  const double N = mesh_.nn, T = mesh_.nt, E = mesh_.ne;
+  const bool local = mat_.r_d <= 0.0;
+  launch("tet_stress", 48 * N + (16 + 72 + 24 + 48 + 48 + 1) * T + 8 * E + (local ? 16 * E : 0),
+         [&] { launch_tet_stress(d_, md_, local, stream_); });
+  if (!local)
+    launch("nonlocal", 48 * N + (16 + 24 + 1 + 8 + 48) * T + 12.0 * nl_entries_ + 24 * E,
+           [&] { launch_nonlocal(d_, stream_); });
+  GF_CUDA(cudaMemsetAsync(d_.newly_count, 0, 4, stream_));
+  launch("relabel", 18 * E, [&] { launch_relabel(d_, mat_.sigma_thres, relabel, keep_values, stream_); });
+  if (chi) launch("chi", (24 + 1 + 48 + 16) * T + E, [&] { launch_chi(d_, md_, stream_); });
+}
+
+std::vector<int32_t> Simulation::damage_pass() {
+  run_damage(true, false, true);
+  int32_t n = 0;
+  GF_CUDA(cudaMemcpyAsync(&n, d_.newly_count, 4, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  std::vector<int32_t> ids(n);
+  if (n) GF_CUDA(cudaMemcpy(ids.data(), d_.newly, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+  std::sort(ids.begin(), ids.end());  // update_damage returns ascending ids (fracture.hpp:48-50)
+  return ids;
+}
+
+// ---------------------------------------------------------------- dynamic step (solver.cpp:219-333)
+void Simulation::upload_bc_step(double t, double dt) {
+  for (size_t b = 0; b < bcs_.size(); ++b) {
+    BcStep& s = h_bcstep_[b];
+    std::memset(&s, 0, sizeof s);
+    s.kind = bcs_[b].kind;
+    bcs_[b].displacement_params(t, s.d0, s.R0);
+    bcs_[b].displacement_params(t + dt, s.d1, s.R1);
+    for (int a = 0; a < 3; ++a) s.axis_point[a] = bcs_[b].axis_point[a];
+  }
+  GF_CUDA(cudaMemcpyAsync(d_bcstep_, h_bcstep_, sizeof(BcStep) * bcs_.size(), cudaMemcpyHostToDevice, stream_));
+}
+
+double Simulation::run_cg(int max_iters) {
+  cg_.max_iters = max_iters;
+  const double N = mesh_.nn, NB = pat_.cols.size();
+  // bytes are filled in after the run from the iteration count (see dynamic_step)
+  launch("pcg", 0.0 * (N + NB), [&] { launch_pcg3(cg_, stream_); });
+  GF_CUDA(cudaMemcpyAsync(h_stats_, d_.cg_out, 32, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  return h_stats_[0];
+}
+
+gf_step_stats Simulation::dynamic_step() {
+  gf_step_stats st{};
+  const double t = time_, dt = cfg_.dt;
+  run_damage(true, false, true);
+
+  const int nsub = cfg_.collision_substeps;
+  if (!cols_.empty()) {
+    const size_t nc = cols_.size();
+    for (int s = 0; s < nsub; ++s) {
+      const double tau = dt * (double)s / (double)nsub;
+      for (size_t c = 0; c < nc; ++c) {
+        ColliderDev& k = h_cols_[s * nc + c];
+        std::memset(&k, 0, sizeof k);
+        k.kind = cols_[c].kind;
+        if (k.kind == 0) {
+          cols_[c].center.eval(t + tau, k.center);
+          cols_[c].center.rate(t + tau, k.cvel);
+        }
+        k.radius = cols_[c].radius;
+        for (int a = 0; a < 3; ++a) {
+          k.point[a] = cols_[c].point[a];
+          k.normal[a] = cols_[c].normal[a];
+        }
+        k.stiffness = cols_[c].stiffness;
+        k.restitution = cols_[c].restitution;
+        k.friction = cols_[c].friction;
+      }
+    }
+    GF_CUDA(cudaMemcpyAsync(d_cols_, h_cols_, sizeof(ColliderDev) * nc * nsub, cudaMemcpyHostToDevice, stream_));
+    for (int s = 0; s < nsub; ++s) {
+      const double tau = dt * (double)s / (double)nsub;
+      launch("collide", 96.0 * mesh_.nn, [&] { launch_collide(d_, s, tau, dt, nsub, stream_); });
+    }
+    launch("collide_load", 0.0, [&] { launch_collide_load(d_, nsub, d_load_, stream_); });
+  }
+  if (!bcs_.empty()) {
+    upload_bc_step(t, dt);
+    launch("bc_targets", 96.0 * n_fixed_, [&] { launch_bc_targets(d_, n_fixed_, d_fixed_nodes_, dt, stream_); });
+  }
+  StepCoeffs c;
+  c.dt = dt;
+  c.rhs_fint_scale = dt;
+  c.rhs_mv_scale = dt * mat_.damp_mass_coeff;
+  c.rhs_kv_scale = dt * mat_.damp_stiff_coeff + dt * dt;
+  c.kscale = dt * mat_.damp_stiff_coeff + dt * dt;
+  c.mscale = 1.0 + dt * mat_.damp_mass_coeff;
+  const double N = mesh_.nn, T = mesh_.nt, NB = pat_.cols.size();
+  d_.fint_out = nullptr;
+  launch("assemble", (24 + 4 + 4 + 24 + 8 + 4 + 24 + 24 + 24) * N + (16 + 72 + 8 + 8 + 16 + 16) * T +
+                         (72 + 4) * NB + (24 + 24 + 24) * N,
+         [&] { launch_assemble(d_, md_, c, kAssembleSystem, stream_); });
+
+  // solve_linear (solver.cpp:105-136): first attempt, 4x retry, then cumulative diagonal shifts
+  cg_.max_iters = cfg_.cg_max_iters;
+  launch("pcg", 0.0, [&] { launch_pcg3(cg_, stream_); });
+  GF_CUDA(cudaMemcpyAsync(h_stats_, d_.cg_out, 32, cudaMemcpyDeviceToHost, stream_));
+  GF_CUDA(cudaMemcpyAsync(h_stats_ + 4, d_load_, 8, cudaMemcpyDeviceToHost, stream_));
+  GF_CUDA(cudaMemcpyAsync(h_stats_ + 5, d_.newly_count, 4, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  const double cg_bytes_per_iter = (72 + 4) * NB + 4 * (N + 1) + 240 * N;
+  auto account = [&](double iters) {
+    if (profiling_) ktimes_["pcg"].bytes += iters * cg_bytes_per_iter + 200 * N;
+  };
+  int32_t newly = 0;
+  std::memcpy(&newly, h_stats_ + 5, 4);
+  st.newly_broken = newly;
+  last_load_ = cols_.empty() ? 0.0 : h_stats_[4];
+  st.load = last_load_;
+  st.cg_iterations = (int32_t)h_stats_[0];
+  account(h_stats_[0]);
+  bool ok = h_stats_[1] != 0.0;
+  if (!ok) {
+    st.cg_iterations += (int32_t)run_cg(4 * cfg_.cg_max_iters);
+    account(h_stats_[0]);
+    ok = h_stats_[1] != 0.0;
+  }
+  if (!ok) {
+    launch("absdiag", 0.0, [&] { launch_absdiag(d_, stream_); });
+    double shift = 1e-8;
+    for (int attempt = 0; attempt < 8 && !ok; ++attempt) {
+      launch("shift_diag", 0.0, [&] { launch_shift_diag(d_, shift, stream_); });
+      launch("bsr_dinv", 0.0, [&] { launch_bsr_dinv(d_, stream_); });
+      launch("reset_x", 0.0, [&] { launch_reset_x(d_, stream_); });
+      st.cg_iterations += (int32_t)run_cg(cfg_.cg_max_iters);
+      account(h_stats_[0]);
+      ok = h_stats_[1] != 0.0;
+      shift *= 10.0;
+    }
+    if (!ok) {
+      std::ostringstream msg;
+      msg << "linear solve failed: relative residual " << h_stats_[3] << " after " << (int)h_stats_[0]
+          << " iterations" << (h_stats_[2] != 0.0 ? " (negative curvature)" : "");
+      throw SolveError(msg.str());
+    }
+  }
+  launch("integrate", 24.0 * 5 * N, [&] { launch_integrate(d_, dt, stream_); });
+  time_ = t + dt;
+  st.residual = 0.0;
+  return st;
+}
+
+// ---------------------------------------------------------------- state access
+void Simulation::get_state(double* u, double* v, uint8_t* zeta, double* chi, double* time) {
+  const size_t nd = 3 * (size_t)mesh_.nn;
+  if (u) GF_CUDA(cudaMemcpyAsync(u, d_.u, 8 * nd, cudaMemcpyDeviceToHost, stream_));
+  if (v) GF_CUDA(cudaMemcpyAsync(v, d_.v, 8 * nd, cudaMemcpyDeviceToHost, stream_));
+  if (zeta) GF_CUDA(cudaMemcpyAsync(zeta, d_.zeta, mesh_.ne, cudaMemcpyDeviceToHost, stream_));
+  if (chi) GF_CUDA(cudaMemcpyAsync(chi, d_.chi, 8 * (size_t)mesh_.nt, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  if (time) *time = time_;
+}
+
+void Simulation::set_state(const double* u, const double* v, const uint8_t* zeta, const double* chi,
+                           const double* time) {
+  const size_t nd = 3 * (size_t)mesh_.nn;
+  if (u) GF_CUDA(cudaMemcpyAsync(d_.u, u, 8 * nd, cudaMemcpyHostToDevice, stream_));
+  if (v) GF_CUDA(cudaMemcpyAsync(d_.v, v, 8 * nd, cudaMemcpyHostToDevice, stream_));
+  if (zeta) GF_CUDA(cudaMemcpyAsync(d_.zeta, zeta, mesh_.ne, cudaMemcpyHostToDevice, stream_));
+  if (chi) GF_CUDA(cudaMemcpyAsync(d_.chi, chi, 8 * (size_t)mesh_.nt, cudaMemcpyHostToDevice, stream_));
+  if (time) time_ = *time;
+  synchronize();
+}
+
+void Simulation::set_external_forces(const double* f3n) {
+  const size_t nd = 3 * (size_t)mesh_.nn;
+  std::vector<double> fext(nd);
+  for (int32_t i = 0; i < mesh_.nn; ++i)
+    for (int a = 0; a < 3; ++a) {
+      const size_t k = 3 * (size_t)i + a;
+      fext[k] = mass_[i] * cfg_.gravity[a];
+      if (f3n) fext[k] += f3n[k];
+    }
+  GF_CUDA(cudaMemcpyAsync(d_.fext, fext.data(), 8 * nd, cudaMemcpyHostToDevice, stream_));
+  synchronize();
+}
+
+int64_t Simulation::broken_edge_count() {
+  std::vector<uint8_t> z(mesh_.ne);
+  get_state(nullptr, nullptr, z.data(), nullptr, nullptr);
+  int64_t n = 0;
+  for (uint8_t b : z) n += b;
+  return n;
+}
+
+void Simulation::mass(double* m3n) const {
+  for (int32_t i = 0; i < mesh_.nn; ++i)
+    for (int a = 0; a < 3; ++a) m3n[3 * (size_t)i + a] = mass_[i];
+}
+
+// ---------------------------------------------------------------- parity / microbench hooks
+void Simulation::eval_forces(double* f3n) {
+  const size_t nd = 3 * (size_t)mesh_.nn;
+  StepCoeffs c{};
+  d_.fint_out = d_.r;  // scratch
+  launch("forces", 0.0, [&] { launch_assemble(d_, md_, c, kAssembleForcesOnly, stream_); });
+  d_.fint_out = nullptr;
+  GF_CUDA(cudaMemcpyAsync(f3n, d_.r, 8 * nd, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+}
+
+void Simulation::bsr_to_csr(const std::vector<double>& bval, double* vals) const {
+  for (int32_t i = 0; i < mesh_.nn; ++i) {
+    const int32_t r0 = pat_.row_ptr[i], deg = pat_.row_ptr[i + 1] - r0;
+    for (int a = 0; a < 3; ++a) {
+      const size_t start = 9 * (size_t)r0 + 3 * (size_t)a * deg;
+      for (int32_t q = 0; q < deg; ++q)
+        for (int b = 0; b < 3; ++b) vals[start + 3 * q + b] = bval[9 * (size_t)(r0 + q) + 3 * a + b];
+    }
+  }
+}
+
+void Simulation::eval_stiffness(double* vals) {
+  StepCoeffs c{};
+  launch("stiffness", 0.0, [&] { launch_assemble(d_, md_, c, kAssembleRawK, stream_); });
+  std::vector<double> b(9 * pat_.cols.size());
+  GF_CUDA(cudaMemcpyAsync(b.data(), d_.bval, 8 * b.size(), cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  bsr_to_csr(b, vals);
+}
+
+void Simulation::last_system(double* vals, double* rhs) {
+  std::vector<double> b(9 * pat_.cols.size());
+  GF_CUDA(cudaMemcpyAsync(b.data(), d_.bval, 8 * b.size(), cudaMemcpyDeviceToHost, stream_));
+  if (rhs) GF_CUDA(cudaMemcpyAsync(rhs, d_.rhs, 24 * (size_t)mesh_.nn, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  if (vals) bsr_to_csr(b, vals);
+}
+
+void Simulation::eval_cauchy(double* sigma6) {
+  launch("tet_stress", 0.0, [&] { launch_tet_stress(d_, md_, false, stream_); });
+  GF_CUDA(cudaMemcpyAsync(sigma6, d_.sigc, 48 * (size_t)mesh_.nt, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+}
+
+void Simulation::eval_screening(double* screening, double* sigma_f6, uint8_t* degenerate) {
+  run_damage(false, true, false);
+  if (screening) GF_CUDA(cudaMemcpyAsync(screening, d_.screening, 8 * (size_t)mesh_.ne, cudaMemcpyDeviceToHost, stream_));
+  if (sigma_f6) GF_CUDA(cudaMemcpyAsync(sigma_f6, d_.sigf, 48 * (size_t)mesh_.nt, cudaMemcpyDeviceToHost, stream_));
+  if (degenerate) GF_CUDA(cudaMemcpyAsync(degenerate, d_.deg, mesh_.nt, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+}
+
+void Simulation::spmv(const double* x, double* y) {
+  const size_t nd = 3 * (size_t)mesh_.nn;
+  GF_CUDA(cudaMemcpyAsync(d_.z, x, 8 * nd, cudaMemcpyHostToDevice, stream_));
+  launch("spmv", 0.0, [&] { launch_spmv3(cg_, d_.z, d_.Ap, stream_); });
+  GF_CUDA(cudaMemcpyAsync(y, d_.Ap, 8 * nd, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+}
+
+double Simulation::reaction_load(const int32_t* nodes, int32_t n, const double axis[3]) {  // solver.cpp:335-340
+  std::vector<double> f(3 * (size_t)mesh_.nn);
+  eval_forces(f.data());
+  double tot[3] = {0, 0, 0};
+  for (int32_t q = 0; q < n; ++q)
+    for (int a = 0; a < 3; ++a) tot[a] += f[3 * (size_t)nodes[q] + a];
+  return -((tot[0] * axis[0] + tot[1] * axis[1]) + tot[2] * axis[2]);
+}
+
+void Simulation::energies(double* strain, double* kinetic) {
+  const int nblocks = 1024;
+  launch("energy", 0.0, [&] { launch_energy(d_, md_, d_energy_partials_, nblocks, stream_); });
+  std::vector<double> part(nblocks), v(3 * (size_t)mesh_.nn);
+  GF_CUDA(cudaMemcpyAsync(part.data(), d_energy_partials_, 8 * nblocks, cudaMemcpyDeviceToHost, stream_));
+  GF_CUDA(cudaMemcpyAsync(v.data(), d_.v, 8 * v.size(), cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  double s = 0.0;
+  for (double p : part) s += p;
+  double k = 0.0;  // kinetic_energy (fem.cpp:201-206)
+  for (int32_t i = 0; i < mesh_.nn; ++i) {
+    const double* vi = &v[3 * (size_t)i];
+    k += 0.5 * mass_[i] * ((vi[0] * vi[0] + vi[1] * vi[1]) + vi[2] * vi[2]);
+  }
+  if (strain) *strain = s;
+  if (kinetic) *kinetic = k;
+}
+
+}  // namespace gfb
+
+namespace gfb {
+// cg_solve on a caller-provided scalar CSR (sparse.cpp:129-188): the same cooperative kernel, B = 1
+void cg_solve_csr(int32_t n, const int32_t* row_ptr, const int32_t* cols, const double* vals, const double* b,
+                  double* x, double tol, int32_t max_iters, gf_cg_result* res) {
+  cudaStream_t s;
+  GF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const int64_t nnz = row_ptr[n];
+  std::vector<void*> bufs;
+  auto alloc = [&](size_t bytes) {
+    void* p = nullptr;
+    GF_CUDA(cudaMalloc(&p, bytes ? bytes : 8));
+    bufs.push_back(p);
+    return p;
+  };
+  auto cleanup = [&]() {
+    for (void* p : bufs) cudaFree(p);
+    cudaStreamDestroy(s);
+  };
+  try {
+    CgLaunch a{};
+    a.nrows = n;
+    a.row_ptr = (const int32_t*)alloc(4 * (size_t)(n + 1));
+    a.cols = (const int32_t*)alloc(4 * (size_t)nnz);
+    a.vals = (const double*)alloc(8 * (size_t)nnz);
+    a.b = (const double*)alloc(8 * (size_t)n);
+    a.x = (double*)alloc(8 * (size_t)n);
+    a.dinv = (const double*)alloc(8 * (size_t)n);
+    a.r = (double*)alloc(8 * (size_t)n);
+    a.z = (double*)alloc(8 * (size_t)n);
+    a.p0 = (double*)alloc(8 * (size_t)n);
+    a.p1 = (double*)alloc(8 * (size_t)n);
+    a.Ap = (double*)alloc(8 * (size_t)n);
+    a.partials = (double*)alloc(8 * 2 * 3 * (size_t)cg_grid_size(1));
+    a.out = (double*)alloc(8 * 4);
+    a.tol = tol;
+    a.max_iters = max_iters;
+    GF_CUDA(cudaMemcpyAsync((void*)a.row_ptr, row_ptr, 4 * (size_t)(n + 1), cudaMemcpyHostToDevice, s));
+    GF_CUDA(cudaMemcpyAsync((void*)a.cols, cols, 4 * (size_t)nnz, cudaMemcpyHostToDevice, s));
+    GF_CUDA(cudaMemcpyAsync((void*)a.vals, vals, 8 * (size_t)nnz, cudaMemcpyHostToDevice, s));
+    GF_CUDA(cudaMemcpyAsync((void*)a.b, b, 8 * (size_t)n, cudaMemcpyHostToDevice, s));
+    GF_CUDA(cudaMemcpyAsync(a.x, x, 8 * (size_t)n, cudaMemcpyHostToDevice, s));
+    launch_pcg1(a, s);
+    double out[4];
+    GF_CUDA(cudaMemcpyAsync(out, a.out, 32, cudaMemcpyDeviceToHost, s));
+    GF_CUDA(cudaMemcpyAsync(x, a.x, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
+    GF_CUDA(cudaStreamSynchronize(s));
+    res->iterations = (int32_t)out[0];
+    res->converged = out[1] != 0.0;
+    res->negative_curvature = out[2] != 0.0;
+    res->relative_residual = out[3];
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+}  // namespace gfb

@@ -1,0 +1,117 @@
+// sim.hpp — B200 Simulation: the reference's grafem::Simulation (solver.hpp:60-118) with all per-step
+// state HBM-resident and every hot phase on the GPU (damage.cu, assemble.cu, cg.cu, misc.cu).
+#pragma once
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/grafem_b200.h"
+#include "dev_types.cuh"
+#include "host_mesh.hpp"
+
+namespace gfb {
+
+struct Schedule {  // Schedule3 (collision.hpp:10-18)
+  std::vector<double> t;
+  std::vector<double> v;  // 3 per key
+  void eval(double time, double out[3]) const;
+  void rate(double time, double out[3]) const;
+};
+
+struct HostBc {
+  int kind = 0;
+  std::vector<int32_t> nodes;
+  Schedule sched;
+  double axis_point[3] = {0, 0, 0}, axis_dir[3] = {1, 0, 0};
+  void displacement_params(double time, double d[3], double R[9]) const;
+};
+
+struct HostCollider {
+  int kind = 0;
+  Schedule center;
+  double radius = 0, point[3] = {0, 0, 0}, normal[3] = {0, 0, 1}, stiffness = 1e6, restitution = 0, friction = 0;
+};
+
+class Simulation {
+ public:
+  Simulation(const HostMesh& mesh, const gf_material& mat, const gf_solver_config& cfg,
+             const gf_boundary_condition* bcs, int32_t n_bcs, const gf_collider* cols, int32_t n_cols);
+  ~Simulation();
+  Simulation(const Simulation&) = delete;
+  Simulation& operator=(const Simulation&) = delete;
+
+  gf_step_stats dynamic_step();
+  std::vector<int32_t> damage_pass();
+  void get_state(double* u, double* v, uint8_t* zeta, double* chi, double* time);
+  void set_state(const double* u, const double* v, const uint8_t* zeta, const double* chi, const double* time);
+  void set_external_forces(const double* f3n);
+  uint64_t pattern_hash() const { return hash_; }
+  int32_t dof_count() const { return 3 * mesh_.nn; }
+  int64_t broken_edge_count();
+  double last_collider_load() const { return last_load_; }
+  void mass(double* m3n) const;
+  double reaction_load(const int32_t* nodes, int32_t n, const double axis[3]);
+  void energies(double* strain, double* kinetic);
+
+  void eval_forces(double* f3n);
+  void eval_stiffness(double* vals);
+  void eval_cauchy(double* sigma6);
+  void eval_screening(double* screening, double* sigma_f6, uint8_t* degenerate);
+  void last_system(double* vals, double* rhs);
+  void spmv(const double* x, double* y);
+
+  void set_profiling(bool on) { profiling_ = on; }
+  std::vector<gf_kernel_time> kernel_times();
+  void reset_kernel_times() { ktimes_.clear(); }
+  void synchronize();
+
+ private:
+  template <class F>
+  void launch(const char* name, double bytes, F&& f);
+  void flush_events();
+  void* dalloc(size_t bytes);
+  void upload_bc_step(double t, double dt);
+  void run_damage(bool relabel, bool keep_values, bool chi);
+  void bsr_to_csr(const std::vector<double>& bval, double* vals) const;
+  double run_cg(int max_iters);
+
+  HostMesh mesh_;
+  NodePattern pat_;
+  gf_material mat_;
+  gf_solver_config cfg_;
+  MatDev md_{};
+  std::vector<HostBc> bcs_;
+  std::vector<HostCollider> cols_;
+  std::vector<double> mass_;  // per node
+  std::vector<double> fuser_;
+  uint64_t hash_ = 0;
+  int64_t nl_entries_ = 0;
+  double time_ = 0.0, last_load_ = 0.0;
+  int32_t n_fixed_ = 0;
+
+  cudaStream_t stream_ = nullptr;
+  DevData d_{};
+  CgLaunch cg_{};
+  std::vector<void*> allocs_;
+  int32_t* d_fixed_nodes_ = nullptr;
+  BcStep* d_bcstep_ = nullptr;
+  ColliderDev* d_cols_ = nullptr;
+  double* d_load_ = nullptr;
+  double* d_energy_partials_ = nullptr;
+  // pinned staging
+  BcStep* h_bcstep_ = nullptr;
+  ColliderDev* h_cols_ = nullptr;
+  double* h_stats_ = nullptr;  // [cg_out(4), load, newly_count]
+  // profiling
+  bool profiling_ = false;
+  struct Pending { std::string name; cudaEvent_t a, b; double bytes; };
+  std::vector<Pending> pending_;
+  std::vector<cudaEvent_t> event_pool_;
+  std::map<std::string, gf_kernel_time> ktimes_;
+};
+
+void cg_solve_csr(int32_t n, const int32_t* row_ptr, const int32_t* cols, const double* vals, const double* b,
+                  double* x, double tol, int32_t max_iters, gf_cg_result* res);
+
+}  // namespace gfb

@@ -1,0 +1,354 @@
+"""GPU parity: the CUDA hot path (through the C ABI) against the CPU oracle on identical seeded inputs.
+
+Bars (north_star): damage labels / newly-broken sets / chi / Cauchy stresses / screening values bit-exact
+from an identical state; forces and matrix entries within 1e-9 relative (fp64); trajectories within 1e-6
+relative in node positions."""
+import numpy as np
+import pytest
+
+import paper_2103_14870_b200 as g
+from paper_2103_14870_b200 import configs as cf
+from oracle import oracle as o
+from oracle.scenario import build_oracle
+
+pytestmark = pytest.mark.gpu
+
+FORCE_TOL = 1e-9
+TRAJ_TOL = 1e-6
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64) if a.dtype == np.float64 else a
+
+
+def same_bits_or_zero(a, b):
+    """bit-exact up to the sign of zero (-0.0 == +0.0 compare equal in the reference's tests too)."""
+    a, b = np.asarray(a), np.asarray(b)
+    return np.array_equal(bits(a), bits(b)) or (np.array_equal(a, b) and np.array_equal(np.isnan(a), np.isnan(b)))
+
+
+def pair(s, rng=None, disp=0.05, damage=0.0, chi_random=False):
+    gs, gm = cf.build_gpu(s)
+    os_, om = build_oracle(s)
+    st = os_.get_state()
+    if rng is not None:
+        u = rng.uniform(-disp * cf.H, disp * cf.H, st["u"].shape)
+        v = rng.uniform(-0.01, 0.01, st["v"].shape)
+        z = (rng.uniform(0, 1, st["zeta"].shape) < damage).astype(np.uint8)
+        chi = rng.uniform(0.0, 1.0, st["chi"].shape) if chi_random else np.ones_like(st["chi"])
+        os_.set_state(u=u, v=v, zeta=z, chi=chi)
+        gs.set_state(u, v, z, chi)
+    return gs, os_, gm, om
+
+
+SMALL = [cf.scaled("c1", (4, 4, 12)), cf.scaled("c2", (6, 6, 6)), cf.scaled("c3", (8, 8, 7))]
+
+
+@pytest.mark.parametrize("s", SMALL, ids=lambda s: s.name)
+@pytest.mark.parametrize("model", [0, 1])
+def test_cauchy_bit_exact(s, model):
+    s.model = model
+    rng = np.random.default_rng(11)
+    gs, os_, gm, om = pair(s, rng, disp=0.2)
+    u = os_.get_state()["u"]
+    ref = om.per_tet_cauchy(os_.mat, u)
+    got = gs.eval_cauchy()
+    assert same_bits_or_zero(got, ref)
+
+
+@pytest.mark.parametrize("s", SMALL, ids=lambda s: s.name)
+def test_screening_bit_exact(s):
+    rng = np.random.default_rng(12)
+    gs, os_, gm, om = pair(s, rng, disp=0.2)
+    st = os_.get_state()
+    sig = om.per_tet_cauchy(os_.mat, st["u"])
+    ref_scr, ref_sf, ref_deg = om.nonlocal_screen(st["u"], sig, s.r_d)
+    scr, sf, deg = gs.eval_screening()
+    assert np.array_equal(deg, ref_deg)
+    assert same_bits_or_zero(sf, ref_sf)
+    assert same_bits_or_zero(scr, ref_scr)
+
+
+def test_degenerate_tets_flagged_identically():
+    s = cf.scaled("c1", (3, 3, 3))
+    gs, os_, gm, om = pair(s)
+    st = os_.get_state()
+    X = om.arrays()["rest"]
+    u = st["u"].copy()
+    u[5] = X[6] - X[5]  # collapse node 5 onto node 6: tets using edge (5,6) degenerate
+    os_.set_state(u=u)
+    gs.set_state(u)
+    sig = om.per_tet_cauchy(os_.mat, u)
+    ref = om.nonlocal_screen(u, sig, 0.0)
+    got = gs.eval_screening()
+    assert ref[2].sum() > 0
+    assert np.array_equal(got[2], ref[2]) and same_bits_or_zero(got[0], ref[0])
+
+
+@pytest.mark.parametrize("s", SMALL, ids=lambda s: s.name)
+@pytest.mark.parametrize("damage", [0.0, 0.1, 0.5])
+def test_damage_pass_bit_exact(s, damage):
+    # thresholds chosen so that a good fraction of edges break in this pass
+    rng = np.random.default_rng(13 + int(100 * damage))
+    gs, os_, gm, om = pair(s, rng, disp=0.3, damage=damage, chi_random=True)
+    ref_new = os_.damage_pass()
+    got_new = gs.damage_pass()
+    ost, gst = os_.get_state(), gs.state()
+    assert np.array_equal(got_new, ref_new)
+    assert np.array_equal(gst.edge_damage, ost["zeta"])
+    assert same_bits_or_zero(gst.element_chi, ost["chi"])
+
+
+def test_damage_pass_breaks_edges_at_low_threshold():
+    s = cf.scaled("c3", (8, 8, 7))
+    s.sigma_thres = 50.0
+    rng = np.random.default_rng(21)
+    gs, os_, gm, om = pair(s, rng, disp=0.3)
+    ref_new = os_.damage_pass()
+    got_new = gs.damage_pass()
+    assert len(ref_new) > 10
+    assert np.array_equal(got_new, ref_new)
+    assert same_bits_or_zero(gs.state().element_chi, os_.get_state()["chi"])
+
+
+def rel_err(a, b):
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.mark.parametrize("s", SMALL, ids=lambda s: s.name)
+@pytest.mark.parametrize("model", [0, 1])
+def test_forces_and_stiffness_within_1e9(s, model):
+    s.model = model
+    rng = np.random.default_rng(14)
+    gs, os_, gm, om = pair(s, rng, disp=0.2, chi_random=True)
+    st = os_.get_state()
+    f_ref = om.assemble_forces(os_.mat, st["u"], st["chi"])
+    assert rel_err(gs.eval_forces(), f_ref) < FORCE_TOL
+    k_ref = om.assemble_stiffness(os_.mat, st["u"], st["chi"])
+    assert rel_err(gs.eval_stiffness(), k_ref) < FORCE_TOL
+
+
+@pytest.mark.parametrize("s", SMALL, ids=lambda s: s.name)
+def test_system_matrix_and_rhs_within_1e9(s):
+    rng = np.random.default_rng(15)
+    gs, os_, gm, om = pair(s, rng, disp=0.01)
+    os_.dynamic_step()
+    gs.dynamic_step()
+    a_ref, r_ref = os_.last_system()
+    a_got, r_got = gs.last_system()
+    assert rel_err(a_got, a_ref) < FORCE_TOL
+    assert rel_err(r_got, r_ref) < FORCE_TOL
+
+
+def test_pattern_hash_matches():
+    s = cf.scaled("c3", (8, 8, 7))
+    gs, os_, gm, om = pair(s)
+    assert gs.pattern_hash() == os_.pattern_hash() == om.pattern()[2]
+
+
+# ---------------------------------------------------------------- CG (test_sparse.cpp KATs on the device)
+def dense_csr(A):
+    n = A.shape[0]
+    return np.arange(0, n * n + 1, n, dtype=np.int32), np.tile(np.arange(n, dtype=np.int32), n), A.reshape(-1)
+
+
+def test_cg_kats():
+    n = 10
+    x, r = g.cg_solve_csr(np.arange(n + 1), np.arange(n), np.ones(n), np.linspace(1, 2, n), np.zeros(n), 1e-12, 100)
+    assert r["converged"] and r["iterations"] == 1 and np.linalg.norm(x - np.linspace(1, 2, n)) < 1e-12
+    n = 17
+    d = 1.0 + np.arange(n)
+    b = np.sin(np.arange(n) + 1.0)
+    x, r = g.cg_solve_csr(np.arange(n + 1), np.arange(n), d, b, np.zeros(n), 1e-14, n + 1)
+    assert r["converged"] and r["iterations"] <= n and np.abs(x - b / d).max() < 1e-12
+    rng = np.random.default_rng(3)
+    n = 50
+    M = rng.uniform(-1, 1, (n, n))
+    A = M @ M.T + 5 * np.eye(n)
+    b = rng.uniform(-1, 1, n)
+    x, r = g.cg_solve_csr(*dense_csr(A), b, np.zeros(n), 1e-12, 10 * n)
+    ex = np.linalg.solve(A, b)
+    assert r["converged"] and np.linalg.norm(x - ex) / np.linalg.norm(ex) < 1e-8
+    x, r = g.cg_solve_csr(*dense_csr(np.array([[1.0, 0.0], [0.0, -1.0]])), np.array([0.0, 1.0]), np.zeros(2), 1e-10, 10)
+    assert not r["converged"] and r["negative_curvature"]
+    x, r = g.cg_solve_csr(*dense_csr(A), np.zeros(n), np.ones(n), 1e-12, 10)
+    assert r["converged"] and np.all(x == 0.0)
+
+
+def test_cg_monotone_a_norm():
+    rng = np.random.default_rng(5)
+    n = 30
+    M = rng.uniform(-1, 1, (n, n))
+    A = M @ M.T + 2 * np.eye(n)
+    b = rng.uniform(-1, 1, n)
+    ex = np.linalg.solve(A, b)
+    prev = np.inf
+    for it in range(1, 26):
+        x, _ = g.cg_solve_csr(*dense_csr(A), b, np.zeros(n), 0.0, it)
+        e = x - ex
+        an = e @ A @ e
+        assert an <= prev * (1 + 1e-9) + 1e-30
+        prev = an
+
+
+def test_spmv_matches_oracle_multiply():
+    s = cf.scaled("c2", (5, 5, 5))
+    rng = np.random.default_rng(16)
+    gs, os_, gm, om = pair(s, rng, disp=0.01)
+    os_.dynamic_step()
+    gs.dynamic_step()
+    a_ref, _ = os_.last_system()
+    rp, cols, _ = om.pattern()
+    x = rng.uniform(-1, 1, 3 * om.num_nodes)
+    assert rel_err(gs.spmv(x), o.spmv_csr(rp, cols, a_ref, x)) < FORCE_TOL
+
+
+# ---------------------------------------------------------------- dynamics KATs (test_solver.cpp) on the GPU
+def _sim(mesh_fn, mat, cfg, bcs=()):
+    return g.Simulation(mesh_fn(), mat, cfg, bcs)
+
+
+def test_gpu_rest_stays_rest():  # test_solver.cpp:89-98
+    m = g.make_box_mesh((0.1, 0.1, 0.1), (2, 2, 2))
+    s = g.Simulation(m, g.MaterialParams.from_youngs(1e6, 0.3, 1000, 1e9, 0, g.STVK), g.SolverConfig(dt=1e-3))
+    s.dynamic_step()
+    s.dynamic_step()
+    st = s.state()
+    assert np.all(st.displacements == 0) and np.all(st.velocities == 0)
+
+
+def test_gpu_free_fall():  # test_solver.cpp:100-113
+    m = g.make_box_mesh((0.1, 0.1, 0.1), (2, 2, 2))
+    gv = np.array([0.3, -9.81, 0.2])
+    s = g.Simulation(m, g.MaterialParams.from_youngs(1e6, 0.3, 1000, 1e9, 0, g.STVK),
+                     g.SolverConfig(dt=1e-4, gravity=gv, cg_tol=1e-13, cg_max_iters=20000))
+    for _ in range(25):
+        s.dynamic_step()
+    v = s.state().velocities
+    expect = 25 * 1e-4 * gv
+    assert np.all(np.linalg.norm(v - expect, axis=1) <= 1e-12 * np.linalg.norm(expect))
+
+
+def test_gpu_ballistic_broken_tet():  # test_solver.cpp:115-138
+    m = g.make_mesh([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 1, 1]], [[0, 1, 2, 3], [1, 2, 3, 4]])
+    gv = np.array([0, -9.81, 0])
+    X = m.rest_positions
+    s = g.Simulation(m, g.MaterialParams.from_youngs(1e6, 0.3, 1000, 1e9, 0, g.STVK),
+                     g.SolverConfig(dt=1e-4, gravity=gv, cg_tol=1e-13, cg_max_iters=20000),
+                     [g.BoundaryCondition(nodes=np.nonzero(X[:, 0] <= 1e-9)[0])])
+    st = s.state()
+    z = st.edge_damage.copy()
+    z[m.tet_edges[1]] = 1
+    chi = st.element_chi.copy()
+    chi[1] = 0.0
+    s.set_state(edge_damage=z, element_chi=chi)
+    for _ in range(20):
+        s.dynamic_step()
+    st = s.state()
+    ev = 20 * 1e-4 * gv
+    assert np.linalg.norm(st.velocities[4] - ev) <= 1e-9 * np.linalg.norm(ev)
+    eu = 0.5 * 20 * 21 * 1e-8 * gv
+    assert np.linalg.norm(st.displacements[4] - eu) <= 1e-9 * np.linalg.norm(eu)
+
+
+def test_gpu_bc_nodes_exact():  # test_solver.cpp:140-155
+    m = g.make_box_mesh((0.2, 0.1, 0.1), (4, 2, 2))
+    X = m.rest_positions
+    nodes = np.nonzero(X[:, 0] <= 1e-9)[0]
+    bc = g.BoundaryCondition(nodes=nodes, translation=g.Schedule3([0.0, 1.0], [[0, 0, 0], [0.01, 0.02, -0.005]]))
+    s = g.Simulation(m, g.MaterialParams.from_youngs(1e6, 0.3, 1000, 1e9, 0, g.STVK), g.SolverConfig(dt=1e-3), [bc])
+    for _ in range(10):
+        s.dynamic_step()
+    st = s.state()
+    w = (st.time - 0.0) / 1.0
+    want = np.array([(1 - w) * 0.0 + w * v for v in (0.01, 0.02, -0.005)])
+    assert np.all(st.displacements[nodes] == want)
+
+
+def test_gpu_energy_never_grows():  # test_solver.cpp:175-202 (bound restated, see test_oracle_kat)
+    m = g.make_box_mesh((0.1, 0.05, 0.05), (4, 2, 2))
+    p = g.MaterialParams.from_youngs(1e6, 0.3, 1000, 1e9, 0, g.STVK)
+    X = m.rest_positions
+    s = g.Simulation(m, p, g.SolverConfig(dt=2e-5, cg_tol=1e-12), [g.BoundaryCondition(nodes=np.nonzero(X[:, 0] <= 1e-9)[0])])
+    u = np.zeros_like(X)
+    u[:, 0] = 1e-4 * X[:, 0]
+    s.set_state(displacements=u)
+    e0 = prev = sum(s.energies())
+    for _ in range(100):
+        s.dynamic_step()
+        e = sum(s.energies())
+        assert e <= prev * (1 + 1e-9)
+        prev = e
+    assert prev / e0 == pytest.approx(0.9078, abs=0.005)
+
+
+def test_gpu_collider_load_matches_oracle():
+    s = cf.scaled("c4", (4, 4, 4))
+    gs, os_, gm, om = pair(s)
+    for _ in range(3):
+        gs.dynamic_step()
+        os_.dynamic_step()
+    assert gs.last_collider_load() == pytest.approx(os_.last_collider_load(), rel=1e-9)
+    assert rel_err(gs.state().displacements, os_.get_state()["u"]) < 1e-9
+
+
+# ---------------------------------------------------------------- trajectories
+def run_pair(s, steps, resync_tol=1e-6):
+    """Step both paths; labels must agree (if a label differs, its screening value must sit within
+    resync_tol of the threshold — a legitimate roundoff flip — and the GPU is re-seeded from the oracle:
+    the 'label-sync' mode of SURVEY §7 hard part 7). Returns max relative position error and #resyncs."""
+    gs, os_, gm, om = pair(s)
+    X = om.arrays()["rest"]
+    scale = np.abs(X).max()
+    worst, resyncs, broken = 0.0, 0, 0
+    for _ in range(steps):
+        os_.dynamic_step()
+        gs.dynamic_step()
+        ost, gst = os_.get_state(), gs.state()
+        if not np.array_equal(gst.edge_damage, ost["zeta"]):
+            diff = np.nonzero(gst.edge_damage != ost["zeta"])[0]
+            resyncs += 1
+            assert resyncs <= 3, f"labels diverged at {len(diff)} edges"
+            gs.set_state(ost["u"], ost["v"], ost["zeta"], ost["chi"])
+            continue
+        worst = max(worst, np.abs(gst.displacements - ost["u"]).max() / scale)
+        broken = int(ost["zeta"].sum())
+    return worst, resyncs, broken
+
+
+def test_trajectory_c1_scaled():
+    s = cf.scaled("c1", (4, 4, 16), steps=60)
+    s.point_load = (s.point_load[0], (0.0, -500.0 / 8, 0.0))  # same bending stress as the 8x8 section
+    worst, resyncs, _ = run_pair(s, s.steps)
+    assert worst < TRAJ_TOL
+
+
+def test_trajectory_c3_scaled_with_fracture():
+    s = cf.scaled("c3", (10, 10, 9), steps=60)
+    worst, resyncs, broken = run_pair(s, s.steps)
+    assert broken > 0
+    assert worst < TRAJ_TOL
+
+
+@pytest.mark.slow
+def test_trajectory_c1_full_200_steps():
+    s = cf.get("c1")
+    worst, resyncs, broken = run_pair(s, s.steps)
+    assert worst < TRAJ_TOL
+
+
+@pytest.mark.slow
+def test_damage_pass_bit_exact_c3_full_size():
+    """Headline config (622,080 tets, r_d = 2h, ~200 neighbours per tet): labels, newly-broken set and chi
+    bit-exact from an identical (seeded, loaded) state."""
+    s = cf.get("c3")
+    s.sigma_thres = 2000.0
+    rng = np.random.default_rng(22)
+    gs, os_, gm, om = pair(s, rng, disp=0.05, damage=0.02)
+    ref_new = os_.damage_pass()
+    got_new = gs.damage_pass()
+    assert len(ref_new) > 0
+    assert np.array_equal(got_new, ref_new)
+    assert np.array_equal(gs.state().edge_damage, os_.get_state()["zeta"])
+    assert same_bits_or_zero(gs.state().element_chi, os_.get_state()["chi"])
