@@ -1,0 +1,278 @@
+#!/usr/bin/env python
+"""bench.py — element-steps/sec of the grafem per-timestep hot path (force + damage + CG) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl reference]
+
+Workload: BASELINE.json configs[2] ("tearing slab", 48x48x45 cells = 622,080 tets, non-local damage over
+r_d = 2h, NH, dt = 1e-3, CG tol 1e-8) — the ~620k-tet configuration the metric is quoted on. A step is one
+Simulation::dynamic_step (damage pass + force/stiffness assembly + implicit-Euler PCG solve + update).
+N > 1 (torchrun): N independent replicas, one per GPU ("replicas only", weak scaling); rank 0 prints.
+
+value  = whole-job element-steps/s from CUDA events on the simulation stream (inputs HBM-resident), max
+         over ranks;
+e2e    = the same metric through the public C ABI with host buffers: every step uploads the caller's state
+         (u, v) from pinned memory and reads the step's result (u, v, edge labels, chi) back;
+roofline / gpu_launches from per-kernel CUDA events recorded inside the timed region;
+cpu_baseline = the CPU oracle (port of the reference's OpenMP path) on this host, rank 0, bounded sample.
+--impl reference times that CPU path alone on the same config/metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "element-steps/sec (force+damage+CG) at 620k tets"
+UNIT = "element-steps/s"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class Dist:
+    def __init__(self, world, backend):
+        self.world = world
+        self.pg = None
+        if world > 1:
+            import torch.distributed as td
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            td.init_process_group(backend)
+            self.td = td
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        dev = "cuda" if self.td.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.td.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md recipe)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        if not sm:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows if len(r) >= 9 for n, v in zip(names, r[5:9]) if v == "Active"})
+        smax = max(float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit())
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": reasons, "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------- CPU baseline (oracle)
+def run_cpu(s, steps, budget_s):
+    """Times the CPU oracle (reference's algorithm + OpenMP layout) on a bounded sample of the workload."""
+    from oracle import oracle as o
+    from oracle.scenario import build_oracle
+    sim, mesh = build_oracle(s)
+    sim.dynamic_step()  # one untimed step (first-touch)
+    done, t0 = 0, time.perf_counter()
+    while done < steps:
+        sim.dynamic_step()
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    el = time.perf_counter() - t0
+    return dict(value=s.num_tets * done / el, unit=UNIT, cores=o.num_threads(), kind="port",
+                sample=f"{done} dynamic_step(s) of {s.name} after 1 untimed step ({el:.1f} s, "
+                       f"OMP threads={o.num_threads()}); oracle/grafem_oracle.cpp -O3 -fopenmp")
+
+
+def config_dict(s, scaling_note):
+    return {"workload": s.name, "tets": s.num_tets, "cells": list(s.cells), "r_d_m": s.r_d, "dt": s.dt,
+            "cg_tol": s.cg_tol, "material": "stable_neo_hookean" if s.model == 0 else "stvk",
+            "l2": "inputs larger than L2: BSR system matrix (~122 MB) + non-local table (~1.5 GB) streamed per step",
+            "parallelism": scaling_note}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-steps", type=int, default=4)
+    ap.add_argument("--cpu-budget", type=float, default=25.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+
+    from paper_2103_14870_b200 import configs as cf
+    s = cf.get(args.config)
+    n = max(world, args.gpus)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        budget = 150.0
+        r = run_cpu(s, args.steps, budget)
+        line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": n, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * s.num_tets / r["value"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded jittered box mesh)",
+                "config": config_dict(s, "cpu"), "impl": "reference", "cpu_baseline": r,
+                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import paper_2103_14870_b200 as g
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local)
+    g.set_device(local)
+    dist = Dist(world, "nccl")
+    sim, mesh = cf.build_gpu(s)
+    N, T, E = mesh.num_nodes(), mesh.num_tets(), mesh.num_edges()
+
+    for _ in range(args.warmup):
+        sim.dynamic_step()
+    sim.synchronize()
+    # ---------------- timed region (device, CUDA events on the simulation stream)
+    sim.reset_kernel_times()
+    sim.set_profiling(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    dist.barrier()
+    sim.synchronize()
+    sim.timer_record(0)
+    cg_iters, newly = 0, 0
+    for _ in range(args.steps):
+        st = sim.dynamic_step()
+        cg_iters += st.cg_iterations
+        newly += st.newly_broken
+    sim.timer_record(1)
+    ms = sim.timer_elapsed_ms(0, 1)
+    sim.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    sim.set_profiling(False)
+    kt = sim.kernel_times()
+    ms_max = dist.max(ms)
+    value = n * T * args.steps / (ms_max / 1e3)
+    launches = int(sum(v["launches"] for v in kt.values()))
+
+    # roofline of the dominant kernel
+    dom = max(kt.items(), key=lambda kv: kv[1]["total_ms"])
+    dname, d = dom
+    avg_ms = d["total_ms"] / max(1, d["launches"])
+    bytes_per_launch = d["bytes"] / max(1, d["launches"])
+    achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak_hbm()
+    traffic = ncu_traffic(dname)
+    roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+                "share_of_step": d["total_ms"] / ms,
+                "kernels": {k: {"launches": v["launches"], "avg_ms": v["total_ms"] / max(1, v["launches"]),
+                                "share": v["total_ms"] / ms,
+                                "GBps": (v["bytes"] / v["total_ms"] / 1e6) if v["total_ms"] > 0 and v["bytes"] > 0 else None}
+                            for k, v in sorted(kt.items(), key=lambda kv: -kv[1]["total_ms"])}}
+
+    # ---------------- e2e: public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        nd = 3 * N
+        pu, pv = g.host_alloc(8 * nd), g.host_alloc(8 * nd)
+        pz, pc = g.host_alloc(E), g.host_alloc(8 * T)
+        sim.get_state_into(pu, pv, pz, pc)
+        e_steps = max(1, args.steps // 2)
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            sim.set_state_from(pu, pv)              # H2D: caller-owned state (u, v)
+            sim.dynamic_step()
+            sim.get_state_into(pu, pv, pz, pc)      # D2H: the step's result (u, v, labels, chi)
+        el = dist.max(time.perf_counter() - t0)
+        e2e = {"value": n * T * e_steps / el, "unit": UNIT, "h2d_bytes_per_step": 16 * nd,
+               "d2h_bytes_per_step": 16 * nd + E + 8 * T, "steps": e_steps, "timing": "host wall clock, max over ranks"}
+        for p in (pu, pv, pz, pc):
+            g.host_free(p)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = run_cpu(s, args.cpu_steps, args.cpu_budget)
+    dist.close()
+    if rank != 0:
+        return
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded jittered box mesh, BASELINE configs[2] shapes)",
+            "config": config_dict(s, f"replicas x{n}" if n > 1 else "single GPU"),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk, "cg_iterations_per_step": cg_iters / args.steps, "newly_broken_in_region": newly}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -183,6 +183,12 @@ int gf_sim_set_profiling(gf_sim* s, int32_t enable);
 int gf_sim_kernel_times(gf_sim* s, gf_kernel_time* out, int32_t cap, int32_t* n);
 int gf_sim_reset_kernel_times(gf_sim* s);
 int gf_sim_synchronize(gf_sim* s);
+/* CUDA events on the simulation's stream (device-side timing of whole steps): record slot 0..7, then read
+ * the elapsed milliseconds between two recorded slots (synchronizes) */
+int gf_sim_timer_record(gf_sim* s, int32_t slot);
+int gf_sim_timer_elapsed(gf_sim* s, int32_t slot_a, int32_t slot_b, double* ms);
+/* select the CUDA device for subsequently created simulations (one process per GPU) */
+int gf_set_device(int32_t device);
 int gf_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor, char* name, int32_t name_cap);
 
 #ifdef __cplusplus

@@ -536,6 +536,14 @@ class Simulation:
     def synchronize(self):
         _check(lib().gf_sim_synchronize(self._h))
 
+    def timer_record(self, slot: int):
+        _check(lib().gf_sim_timer_record(self._h, C.c_int32(slot)))
+
+    def timer_elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_double()
+        _check(lib().gf_sim_timer_elapsed(self._h, C.c_int32(a), C.c_int32(b), C.byref(ms)))
+        return ms.value
+
 
 def cg_solve_csr(row_ptr, cols, vals, b, x0, tol, max_iters):
     """cg_solve (sparse.cpp:129-188) on the GPU for a scalar CSR; returns (x, result dict)."""
@@ -549,6 +557,22 @@ def cg_solve_csr(row_ptr, cols, vals, b, x0, tol, max_iters):
                                  C.c_int32(max_iters), C.byref(r)))
     return x, dict(iterations=r.iterations, converged=bool(r.converged),
                    negative_curvature=bool(r.negative_curvature), relative_residual=r.relative_residual)
+
+
+def set_device(device: int):
+    _check(lib().gf_set_device(C.c_int32(device)))
+
+
+def host_alloc(nbytes: int) -> int:
+    """Pinned host memory (cudaMallocHost) as a raw pointer; free with host_free."""
+    p = lib().gf_host_alloc(C.c_size_t(nbytes))
+    if not p:
+        raise CudaError("gf_host_alloc failed")
+    return p
+
+
+def host_free(p: int):
+    lib().gf_host_free(C.c_void_p(p))
 
 
 def device_info():

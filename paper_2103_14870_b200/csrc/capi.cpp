@@ -246,6 +246,21 @@ int gf_sim_reset_kernel_times(gf_sim* s) {
 int gf_sim_synchronize(gf_sim* s) {
   return guard([&] { s->s->synchronize(); });
 }
+int gf_sim_timer_record(gf_sim* s, int32_t slot) {
+  return guard([&] { s->s->timer_record(slot); });
+}
+int gf_sim_timer_elapsed(gf_sim* s, int32_t a, int32_t b, double* ms) {
+  return guard([&] { *ms = s->s->timer_elapsed(a, b); });
+}
+int gf_set_device(int32_t device) {
+  return guard([&] {
+    const cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw CudaError(std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    }
+  });
+}
 int gf_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor, char* name, int32_t name_cap) {
   return guard([&] {
     int dev = 0;

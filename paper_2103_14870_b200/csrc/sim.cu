@@ -307,6 +307,8 @@ Simulation::~Simulation() {
     cudaEventDestroy(p.b);
   }
   for (auto e : event_pool_) cudaEventDestroy(e);
+  for (auto e : timers_)
+    if (e) cudaEventDestroy(e);
   for (void* p : allocs_) cudaFree(p);
   if (h_bcstep_) cudaFreeHost(h_bcstep_);
   if (h_cols_) cudaFreeHost(h_cols_);
@@ -358,6 +360,20 @@ void Simulation::flush_events() {
 void Simulation::synchronize() {
   GF_CUDA(cudaStreamSynchronize(stream_));
   flush_events();
+}
+
+void Simulation::timer_record(int slot) {
+  if (slot < 0 || slot >= 8) throw FormatError("timer slot must be in [0, 8)");
+  if (!timers_[slot]) GF_CUDA(cudaEventCreate(&timers_[slot]));
+  GF_CUDA(cudaEventRecord(timers_[slot], stream_));
+}
+
+double Simulation::timer_elapsed(int a, int b) {
+  if (a < 0 || a >= 8 || b < 0 || b >= 8 || !timers_[a] || !timers_[b]) throw FormatError("timer slot not recorded");
+  GF_CUDA(cudaEventSynchronize(timers_[b]));
+  float ms = 0.f;
+  GF_CUDA(cudaEventElapsedTime(&ms, timers_[a], timers_[b]));
+  return ms;
 }
 
 std::vector<gf_kernel_time> Simulation::kernel_times() {

@@ -65,6 +65,8 @@ class Simulation {
   std::vector<gf_kernel_time> kernel_times();
   void reset_kernel_times() { ktimes_.clear(); }
   void synchronize();
+  void timer_record(int slot);
+  double timer_elapsed(int a, int b);
 
  private:
   template <class F>
@@ -109,6 +111,7 @@ class Simulation {
   std::vector<Pending> pending_;
   std::vector<cudaEvent_t> event_pool_;
   std::map<std::string, gf_kernel_time> ktimes_;
+  cudaEvent_t timers_[8] = {};
 };
 
 void cg_solve_csr(int32_t n, const int32_t* row_ptr, const int32_t* cols, const double* vals, const double* b,
