@@ -25,6 +25,7 @@ CU_SOURCES = {  # file -> extra flags
     "misc.cu": ["-fmad=false"],
     "assemble.cu": [],
     "cg.cu": [],
+    "cg_sell.cu": [],
     "sim.cu": [],
 }
 CPP_SOURCES = ["host_mesh.cpp", "capi.cpp"]

@@ -10,65 +10,54 @@
 //   pk1 to ~1e-16):
 //     NH   K_ij = s[c1 (g_i.g_j) I + c2 (F g_i)(F g_j)^T + lambda (cof g_i)(cof g_j)^T - lambda(J-a)[F(g_i x g_j)]_x]
 //     StVK K_ij = s[(g_i^T S g_j) I + mu (F g_j)(F g_i)^T + mu (g_i.g_j) F F^T + lambda (F g_i)(F g_j)^T]
-//   with g = shape gradients from B^-1 and s = chi*V. Blocks go to shared memory; lane c then sums the
-//   contributions that land in column block c of the row (precomputed slot bytes: no search, no atomics,
-//   deterministic), and finishes the row in registers: K v, A = (dt beta + dt^2) K + (1 + dt alpha) M,
-//   Dirichlet projection, rhs, Jacobi inverse diagonal, CG initial guess. The matrix is written exactly
-//   once, coalesced (consecutive lanes = consecutive 72 B blocks of the row).
+//   with g = shape gradients from B^-1 and s = chi*V. Blocks go to shared memory; the row's outputs are then
+//   reduced over precomputed contribution lists (no search, no atomics, deterministic ascending-tet order)
+//   and finished in registers: K v, A = (dt beta + dt^2) K + (1 + dt alpha) M, Dirichlet projection, rhs,
+//   Jacobi inverse diagonal, CG initial guess. The matrix is written exactly once, in SELL-32 order.
 #include "device_math.cuh"
 
 namespace gfb {
 namespace {
 
 constexpr int kWarps = 4;
-constexpr int kMaxDeg = 64;  // columns per node row handled by one warp (2 per lane)
+constexpr int kMaxValence = 32;  // tets per node handled by one warp (validated at setup)
+constexpr int kMaxDeg = 32;      // column blocks per node row (validated at setup)
 
-struct ElemOut {
-  double f[3];
-  double H[4][9];
-};
-
-// contribution of tet e to node-row i (local index li): force on i and K(li, lj), lj = 0..3
+// contribution of tet e to node-row i (local index li): force on i (returned) and the four blocks K(li, lj),
+// written straight to shared memory (blk[9*lj + r]) so they never occupy registers together
 template <bool kBlocks>
 __device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, int e, int li, double scale,
-                                            ElemOut& o) {
+                                            double f[3], double* blk) {
   const int4 t = __ldg(d.tets + e);
   const int id[4] = {t.x, t.y, t.z, t.w};
-  double u[4][3];
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-#pragma unroll
-    for (int a = 0; a < 3; ++a) u[k][a] = __ldg(d.u + 3 * (size_t)id[k] + a);
   double B[9], du[9], F[9];
 #pragma unroll
   for (int q = 0; q < 9; ++q) B[q] = __ldg(d.binv + 9 * (size_t)e + q);
+  {
+    double u0[3];
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
+    for (int a = 0; a < 3; ++a) u0[a] = __ldg(d.u + 3 * (size_t)id[0] + a);
 #pragma unroll
-    for (int r = 0; r < 3; ++r) du[3 * r + c] = u[c + 1][r] - u[0][r];
-  def_grad(du, B, F);
-  double g[4][3];
+    for (int c = 0; c < 3; ++c)
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    g[1][a] = B[a];
-    g[2][a] = B[3 + a];
-    g[3][a] = B[6 + a];
-    g[0][a] = -((B[a] + B[3 + a]) + B[6 + a]);
+      for (int r = 0; r < 3; ++r) du[3 * r + c] = __ldg(d.u + 3 * (size_t)id[c + 1] + r) - u0[r];
   }
-  double P[9];
-  const double J = pk1(F, m, P);
+  def_grad(du, B, F);
   double gi[3];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) gi[a] = g[li][a];
+  for (int a = 0; a < 3; ++a)
+    gi[a] = (li == 0) ? -((B[a] + B[3 + a]) + B[6 + a]) : B[3 * (li - 1) + a];
+  double P[9];
+  const double J = pk1(F, m, P);
 #pragma unroll
-  for (int a = 0; a < 3; ++a) o.f[a] = -scale * ((P[3 * a] * gi[0] + P[3 * a + 1] * gi[1]) + P[3 * a + 2] * gi[2]);
+  for (int a = 0; a < 3; ++a) f[a] = -scale * ((P[3 * a] * gi[0] + P[3 * a + 1] * gi[1]) + P[3 * a + 2] * gi[2]);
   if (!kBlocks) return;
 
   double ai[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) ai[a] = F[3 * a] * gi[0] + F[3 * a + 1] * gi[1] + F[3 * a + 2] * gi[2];
   if (m.model == 1) {
-    double E[9], S[9], FFt[9];
+    double E[9], FFt[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -77,41 +66,44 @@ __device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, i
         FFt[3 * r + c] = F[3 * r] * F[3 * c] + F[3 * r + 1] * F[3 * c + 1] + F[3 * r + 2] * F[3 * c + 2];
       }
     const double lt = m.lambda * (E[0] + E[4] + E[8]);
-#pragma unroll
-    for (int q = 0; q < 9; ++q) S[q] = 2.0 * m.mu * E[q] + ((q % 4 == 0) ? lt : 0.0);
     double Sgi[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) Sgi[a] = S[3 * a] * gi[0] + S[3 * a + 1] * gi[1] + S[3 * a + 2] * gi[2];
-#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      Sgi[a] = 2.0 * m.mu * (E[3 * a] * gi[0] + E[3 * a + 1] * gi[1] + E[3 * a + 2] * gi[2]) + lt * gi[a];
+#pragma unroll 1
     for (int lj = 0; lj < 4; ++lj) {
+      double gj[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) gj[a] = (lj == 0) ? -((B[a] + B[3 + a]) + B[6 + a]) : B[3 * (lj - 1) + a];
       double aj[3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) aj[a] = F[3 * a] * g[lj][0] + F[3 * a + 1] * g[lj][1] + F[3 * a + 2] * g[lj][2];
-      const double gij = gi[0] * g[lj][0] + gi[1] * g[lj][1] + gi[2] * g[lj][2];
-      const double gSg = Sgi[0] * g[lj][0] + Sgi[1] * g[lj][1] + Sgi[2] * g[lj][2];
+      for (int a = 0; a < 3; ++a) aj[a] = F[3 * a] * gj[0] + F[3 * a + 1] * gj[1] + F[3 * a + 2] * gj[2];
+      const double gij = gi[0] * gj[0] + gi[1] * gj[1] + gi[2] * gj[2];
+      const double gSg = Sgi[0] * gj[0] + Sgi[1] * gj[1] + Sgi[2] * gj[2];
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double v = (r == c ? gSg : 0.0) + m.mu * aj[r] * ai[c] + m.mu * gij * FFt[3 * r + c] +
                            m.lambda * ai[r] * aj[c];
-          o.H[lj][3 * r + c] = scale * v;
+          blk[9 * lj + 3 * r + c] = scale * v;
         }
     }
   } else {
     double C[9];
     cofactor(F, C);
-    const double ic = sqnorm9(F);
-    const double ip1 = ic + 1.0;
+    const double ip1 = sqnorm9(F) + 1.0;
     const double c1 = m.mu * (1.0 - 1.0 / ip1);
     const double c2 = 2.0 * m.mu / (ip1 * ip1);
     const double c4 = m.lambda * (J - m.alpha_nh);
     double bi[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) bi[a] = C[3 * a] * gi[0] + C[3 * a + 1] * gi[1] + C[3 * a + 2] * gi[2];
-#pragma unroll
+#pragma unroll 1
     for (int lj = 0; lj < 4; ++lj) {
-      const double* gj = g[lj];
+      double gj[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) gj[a] = (lj == 0) ? -((B[a] + B[3 + a]) + B[6 + a]) : B[3 * (lj - 1) + a];
       double aj[3], bj[3], cr[3], w[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
@@ -130,7 +122,7 @@ __device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, i
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double v = (r == c ? c1 * gij : 0.0) + c2 * ai[r] * aj[c] + m.lambda * bi[r] * bj[c] + c4 * hj[3 * r + c];
-          o.H[lj][3 * r + c] = scale * v;
+          blk[9 * lj + 3 * r + c] = scale * v;
         }
     }
   }
@@ -142,125 +134,100 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// One warp per node row i:
+//  1. lane l < valence(i) evaluates the l-th incident tet (ascending id): force on i -> s_frc, blocks -> s_blk
+//  2. the row's 9*deg outputs (column c, entry q) are spread over the 32 lanes; each sums its precomputed
+//     contribution list (ascending tet order, deterministic) from s_blk into s_row
+//  3. lane c finishes column block c: K v, A = kscale K + mscale M, Dirichlet projection, SELL-32 store
 template <int kMode>
-__global__ void __launch_bounds__(32 * kWarps) k_assemble(DevData d, MatDev m, StepCoeffs sc) {
+__global__ void __launch_bounds__(32 * kWarps, 4) k_assemble(DevData d, MatDev m, StepCoeffs sc) {
   constexpr bool kBlocks = kMode != kAssembleForcesOnly;
-  __shared__ double s_blk[kBlocks ? kWarps : 1][32][36];
+  __shared__ double s_blk[kBlocks ? kWarps : 1][32 * 36];
+  __shared__ double s_row[kBlocks ? kWarps : 1][kMaxDeg * 9];
   __shared__ double s_frc[kWarps][32][3];
-  __shared__ uint32_t s_slot[kWarps][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kWarps + w;
   if (i >= d.nn) return;
-  const int p0 = __ldg(d.nt_ptr + i), p1 = __ldg(d.nt_ptr + i + 1);
+  const int p0 = __ldg(d.nt_ptr + i), np = __ldg(d.nt_ptr + i + 1) - p0;
   const int row0 = __ldg(d.brow + i), deg = __ldg(d.brow + i + 1) - row0;
 
-  double acc[2][9];
+  double f[3] = {0.0, 0.0, 0.0};
+  if (lane < np) {
+    const int e = __ldg(d.nt_tet + p0 + lane);
+    const int4 t = __ldg(d.tets + e);
+    const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
+    const double scale = d.chi[e] * __ldg(d.vol + e);
+    double* blk = kBlocks ? &s_blk[w][36 * lane] : nullptr;
+    if (scale != 0.0) {  // fem.cpp:51 / fem.cpp:114 early-out
+      element_row<kBlocks>(d, m, e, li, scale, f, blk);
+    } else if (kBlocks) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc[h][q] = 0.0;
-  double fsum = 0.0;  // lanes 0..2: force component
-
-  for (int chunk = p0; chunk < p1; chunk += 32) {
-    const int q = chunk + lane;
-    uint32_t slot = 0xffffffffu;
-    ElemOut eo;
-    eo.f[0] = eo.f[1] = eo.f[2] = 0.0;
-    if (q < p1) {
-      const int e = __ldg(d.nt_tet + q);
-      slot = __ldg(d.nt_slot + q);
-      const int4 t = __ldg(d.tets + e);
-      const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
-      const double scale = d.chi[e] * __ldg(d.vol + e);
-      if (scale != 0.0) {  // fem.cpp:51 / fem.cpp:114 early-out
-        element_row<kBlocks>(d, m, e, li, scale, eo);
-      } else if (kBlocks) {
-#pragma unroll
-        for (int lj = 0; lj < 4; ++lj)
-#pragma unroll
-          for (int r = 0; r < 9; ++r) eo.H[lj][r] = 0.0;
-      }
-      if (kBlocks) {
-#pragma unroll
-        for (int lj = 0; lj < 4; ++lj)
-#pragma unroll
-          for (int r = 0; r < 9; ++r) s_blk[w][lane][9 * lj + r] = eo.H[lj][r];
-      }
+      for (int r = 0; r < 36; ++r) blk[r] = 0.0;
     }
-    s_slot[w][lane] = slot;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) s_frc[w][lane][a] = eo.f[a];
-    __syncwarp();
-    const int n = min(32, p1 - chunk);
-    if (lane < 3)
-      for (int l = 0; l < n; ++l) fsum += s_frc[w][l][lane];  // ascending tet order (fem.cpp:104-106)
-    if (kBlocks) {
-      for (int l = 0; l < n; ++l) {
-        const uint32_t s = s_slot[w][l];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int pos = (int)((s >> (8 * k)) & 0xffu);
-          if (pos == lane) {
-#pragma unroll
-            for (int r = 0; r < 9; ++r) acc[0][r] += s_blk[w][l][9 * k + r];
-          } else if (pos == lane + 32) {
-#pragma unroll
-            for (int r = 0; r < 9; ++r) acc[1][r] += s_blk[w][l][9 * k + r];
-          }
-        }
-      }
-    }
-    __syncwarp();
   }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) s_frc[w][lane][a] = f[a];
+  __syncwarp();
+  double fsum = 0.0;  // lanes 0..2: force component, ascending tet order (fem.cpp:104-106)
+  if (lane < 3)
+    for (int l = 0; l < np; ++l) fsum += s_frc[w][l][lane];
 
   const bool fixed_i = __ldg(d.node_bc + i) >= 0;
   double kv[3] = {0.0, 0.0, 0.0}, corr[3] = {0.0, 0.0, 0.0};
   if (kBlocks) {
+    for (int o = lane; o < 9 * deg; o += 32) {
+      const int c = o / 9, q = o - 9 * c;
+      const int it0 = __ldg(d.contrib_ptr + row0 + c), it1 = __ldg(d.contrib_ptr + row0 + c + 1);
+      double sum = 0.0;
+      for (int it = it0; it < it1; ++it) sum += s_blk[w][9 * (int)__ldg(d.contrib_item + it) + q];
+      s_row[w][o] = sum;
+    }
+    __syncwarp();
+    const int c = lane;
+    if (c < deg) {
+      double K[9];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = lane + 32 * h;
-      if (c >= deg) break;
-      const int blk = row0 + c;
-      double* out = d.bval + 9 * (size_t)blk;
+      for (int r = 0; r < 9; ++r) K[r] = s_row[w][9 * c + r];
+      double* out = d.bval + sell_addr(d.sell_ptr, i, c, 0);  // entry r at out[32 * r]
       if (kMode == kAssembleRawK) {
 #pragma unroll
-        for (int r = 0; r < 9; ++r) out[r] = acc[h][r];
-        continue;
-      }
-      const int j = __ldg(d.bcol + blk);
-      double vj[3];
+        for (int r = 0; r < 9; ++r) out[32 * r] = K[r];
+      } else {
+        const int j = __ldg(d.bcol + row0 + c);
+        double vj[3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) vj[a] = d.v[3 * (size_t)j + a];
+        for (int a = 0; a < 3; ++a) vj[a] = d.v[3 * (size_t)j + a];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) kv[a] += acc[h][3 * a] * vj[0] + acc[h][3 * a + 1] * vj[1] + acc[h][3 * a + 2] * vj[2];
-      double A[9];
+        for (int a = 0; a < 3; ++a) kv[a] = K[3 * a] * vj[0] + K[3 * a + 1] * vj[1] + K[3 * a + 2] * vj[2];
+        double A[9];
 #pragma unroll
-      for (int r = 0; r < 9; ++r) A[r] = sc.kscale * acc[h][r];
-      if (j == i) {
-        const double md = sc.mscale * __ldg(d.mass + i);
-        A[0] += md;
-        A[4] += md;
-        A[8] += md;
-      }
-      if (fixed_i) {  // project_dirichlet: fixed row zeroed, unit diagonal
+        for (int r = 0; r < 9; ++r) A[r] = sc.kscale * K[r];
+        if (j == i) {
+          const double md = sc.mscale * __ldg(d.mass + i);
+          A[0] += md;
+          A[4] += md;
+          A[8] += md;
+        }
+        if (fixed_i) {  // project_dirichlet: fixed row zeroed, unit diagonal
 #pragma unroll
-        for (int r = 0; r < 9; ++r) A[r] = (j == i && r % 4 == 0) ? 1.0 : 0.0;
-      } else if (__ldg(d.node_bc + j) >= 0) {  // fixed column: move A_ij * dv_j to the rhs, zero it
-        double fj[3];
+          for (int r = 0; r < 9; ++r) A[r] = (j == i && r % 4 == 0) ? 1.0 : 0.0;
+        } else if (__ldg(d.node_bc + j) >= 0) {  // fixed column: move A_ij * dv_j to the rhs, zero it
+          double fj[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) fj[a] = d.fv[3 * (size_t)j + a];
+          for (int a = 0; a < 3; ++a) fj[a] = d.fv[3 * (size_t)j + a];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) corr[a] += A[3 * a] * fj[0] + A[3 * a + 1] * fj[1] + A[3 * a + 2] * fj[2];
+          for (int a = 0; a < 3; ++a) corr[a] = A[3 * a] * fj[0] + A[3 * a + 1] * fj[1] + A[3 * a + 2] * fj[2];
 #pragma unroll
-        for (int r = 0; r < 9; ++r) A[r] = 0.0;
-      }
+          for (int r = 0; r < 9; ++r) A[r] = 0.0;
+        }
 #pragma unroll
-      for (int r = 0; r < 9; ++r) out[r] = A[r];
-      if (j == i) {
+        for (int r = 0; r < 9; ++r) out[32 * r] = A[r];
+        if (j == i) {
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const double dd = A[4 * a];
-          d.dinv[3 * (size_t)i + a] = (fabs(dd) > 1e-300) ? 1.0 / dd : 1.0;  // sparse.cpp:133-136
+          for (int a = 0; a < 3; ++a) {
+            const double dd = A[4 * a];
+            d.dinv[3 * (size_t)i + a] = (fabs(dd) > 1e-300) ? 1.0 / dd : 1.0;  // sparse.cpp:133-136
+          }
         }
       }
     }

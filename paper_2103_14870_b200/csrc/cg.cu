@@ -20,18 +20,45 @@
 
 namespace cg = cooperative_groups;
 
+
 namespace gfb {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 1024;  // one CTA per SM: fewer grid-barrier arrivals (148 vs 592)
 constexpr int kMaxRed = 3;
+
+// Grid barrier for a co-resident (cooperatively launched) grid: one release-atomic arrival per CTA on a
+// counter, the last arrival resets it and publishes a new generation; the others spin on an acquire load.
+// Data written before the barrier by other CTAs is read afterwards with ld.global.cg (L2), never from L1.
+struct GridBarrier {
+  unsigned* count;
+  unsigned* gen;
+  __device__ __forceinline__ void sync() const {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned g, arrived;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+      __threadfence();
+      asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(count) : "memory");
+      if (arrived == gridDim.x - 1) {
+        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(count), "r"(0u) : "memory");
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
+      } else {
+        unsigned cur;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(gen) : "memory");
+        } while (cur == g);
+      }
+    }
+    __syncthreads();
+  }
+};
 
 // block-reduce NV values, publish per-block partials, grid barrier, then every block sums all partials in
 // the same order. Two alternating partial buffers make the re-use race-free (see header).
-template <int NV>
-__device__ __forceinline__ void grid_reduce(double (&v)[NV], double* partials, int& parity, cg::grid_group& grid) {
+template <int NV, class Grid>
+__device__ __forceinline__ void grid_reduce(double (&v)[NV], double* partials, int& parity, Grid& grid) {
   __shared__ double s_red[kThreads / 32][kMaxRed];
-  __shared__ double s_out[kMaxRed];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
@@ -48,17 +75,16 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* partials, i
     slot[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = x;
   }
   grid.sync();
-  if (w < NV) {
+  // every warp sums all block partials itself, in the same fixed order: identical bits everywhere and no
+  // second intra-block barrier on the critical path
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
     double x = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) x += slot[(size_t)w * gridDim.x + b];
+    for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(slot + (size_t)q * gridDim.x + b);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) s_out[w] = x;
+    v[q] = x;
   }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < NV; ++q) v[q] = s_out[q];
-  __syncthreads();
   parity ^= 1;
 }
 
@@ -76,8 +102,8 @@ struct Gather {  // p_j = fused ? fma(beta, p_old_j, z_j) : src_j
 // y = A * P over all block rows owned by this half-warp; returns the owner's partial P_row . y_row.
 // If `write_p`, the row owner stores P_row to `pout` (the fused p update).
 template <int B>
-__device__ __forceinline__ double spmv_phase(const CgLaunch& a, const Gather<B>& P, double* y, double* pout,
-                                             bool write_p) {
+__device__ __forceinline__ double spmv_csr(const CgLaunch& a, const Gather<B>& P, double* y, double* pout,
+                                           bool write_p) {
   const int sub = threadIdx.x & 15;
   const int half = (threadIdx.x >> 4) & 1;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -123,6 +149,82 @@ __device__ __forceinline__ double spmv_phase(const CgLaunch& a, const Gather<B>&
   }
   return dotp;
 }
+
+// SELL-32 node-block SpMV: one warp per 32-row slice, one lane per block row; every slot load (column id,
+// 9 block entries) is a coalesced 128/256 B warp access; the 3 gathered p_j values are 24 contiguous bytes.
+__device__ __forceinline__ double spmv_sell3(const CgLaunch& a, const Gather<3>& P, double* y, double* pout,
+                                             bool write_p) {
+  const int lane = threadIdx.x & 31;
+  // each CTA owns one contiguous, equal run of slices (balanced over SMs, neighbouring rows stay on one SM so
+  // the gathered p_j hit the same L1); warps of the CTA stride through the run
+  int s_begin, s_end, s_step;
+  if (a.mapping == 2) {
+    const int per = (a.nslices + gridDim.x - 1) / gridDim.x;
+    s_begin = blockIdx.x * per + (threadIdx.x >> 5);
+    s_end = min(a.nslices, (blockIdx.x + 1) * per);
+    s_step = blockDim.x >> 5;
+  } else if (a.mapping == 1) {
+    s_begin = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    s_end = a.nslices;
+    s_step = (gridDim.x * blockDim.x) >> 5;
+  } else {
+    s_begin = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    s_end = a.nslices;
+    s_step = (gridDim.x * blockDim.x) >> 5;
+  }
+  double dotp = 0.0;
+  for (int sl = s_begin; sl < s_end; sl += s_step) {
+    const int row = sl * 32 + lane;
+    const int k0 = __ldg(a.row_ptr + sl), k1 = __ldg(a.row_ptr + sl + 1);
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+#pragma unroll 2
+    for (int k = k0; k < k1; ++k) {
+      const size_t j = (size_t)__ldg(a.cols + (size_t)k * 32 + lane);
+      const double* v = a.vals + (size_t)k * 288 + lane;
+      const double p0 = P(3 * j), p1 = P(3 * j + 1), p2 = P(3 * j + 2);
+      acc0 = __fma_rn(__ldg(v + 0), p0, acc0);
+      acc0 = __fma_rn(__ldg(v + 32), p1, acc0);
+      acc0 = __fma_rn(__ldg(v + 64), p2, acc0);
+      acc1 = __fma_rn(__ldg(v + 96), p0, acc1);
+      acc1 = __fma_rn(__ldg(v + 128), p1, acc1);
+      acc1 = __fma_rn(__ldg(v + 160), p2, acc1);
+      acc2 = __fma_rn(__ldg(v + 192), p0, acc2);
+      acc2 = __fma_rn(__ldg(v + 224), p1, acc2);
+      acc2 = __fma_rn(__ldg(v + 256), p2, acc2);
+    }
+    if (row < a.nrows) {
+      const double acc[3] = {acc0, acc1, acc2};
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const size_t dof = 3 * (size_t)row + r;
+        const double pr = P(dof);
+        y[dof] = acc[r];
+        if (write_p) pout[dof] = pr;
+        dotp = __fma_rn(pr, acc[r], dotp);
+      }
+    }
+  }
+  return dotp;
+}
+
+template <int B>
+__device__ __forceinline__ double spmv_phase(const CgLaunch& a, const Gather<B>& P, double* y, double* pout,
+                                             bool write_p) {
+  if constexpr (B == 3) return spmv_sell3(a, P, y, pout, write_p);
+  else return spmv_csr<B>(a, P, y, pout, write_p);
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// optional phase trace (GF_CG_TRACE): block b in {0, last} thread 0 stamps %globaltimer at 5 points/iteration
+#define CG_STAMP(k, point)                                                                              \
+  do {                                                                                                  \
+    if (a.trace && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && (k) < 200)   \
+      a.trace[((blockIdx.x == 0 ? 0 : 1) * 200 + (k)) * 5 + (point)] = gtimer();                     \
+  } while (0)
 
 template <int B>
 __global__ void __launch_bounds__(kThreads) k_pcg(CgLaunch a) {
@@ -175,14 +277,22 @@ __global__ void __launch_bounds__(kThreads) k_pcg(CgLaunch a) {
     bool done = false;
     for (int it = 0; it < a.max_iters; ++it) {
       const bool fused = it > 0;
+      CG_STAMP(it, 0);
       Gather<B> gp{pcur, a.z, beta, fused};
       double pap[1] = {spmv_phase<B>(a, gp, a.Ap, pnext, fused)};
+      CG_STAMP(it, 1);
+      if (a.trace && it == 10) {
+        __syncthreads();
+        if (threadIdx.x == 0) a.trace[3000 + blockIdx.x] = gtimer();
+        if (threadIdx.x == 0 && blockIdx.x == 0) a.trace[4000] = gtimer();
+      }
       if (fused) {
         double* t = pcur;
         pcur = pnext;
         pnext = t;
       }
       grid_reduce<1>(pap, a.partials, parity, grid);
+      CG_STAMP(it, 2);
       if (pap[0] <= 0.0) {  // sparse.cpp:160-168
         negcurv = pap[0] < 0.0;
         iterations = it;
@@ -203,7 +313,13 @@ __global__ void __launch_bounds__(kThreads) k_pcg(CgLaunch a) {
         red2[0] = __fma_rn(ri, ri, red2[0]);
         red2[1] = __fma_rn(ri, zi, red2[1]);
       }
+      CG_STAMP(it, 3);
+      if (a.trace && it == 10) {  // per-block end of phase A/B at iteration 10 (diagnostics)
+        __syncthreads();
+        if (threadIdx.x == 0) a.trace[2000 + blockIdx.x] = gtimer();
+      }
       grid_reduce<2>(red2, a.partials, parity, grid);
+      CG_STAMP(it, 4);
       rr = red2[0];
       iterations = it + 1;
       const double rnorm = sqrt(rr);
@@ -271,4 +387,61 @@ void launch_spmv3(const CgLaunch& a, const double* xin, double* y, cudaStream_t 
   k_spmv<3><<<grid_for<3>(), kThreads, 0, s>>>(a, xin, y);
 }
 
+}  // namespace gfb
+
+// ---------------------------------------------------------------- diagnostics: grid-barrier microbenchmark
+namespace gfb {
+namespace {
+__global__ void k_bar_cg(int iters, double* sink) {
+  cg::grid_group grid = cg::this_grid();
+  double acc = 0.0;
+  for (int i = 0; i < iters; ++i) {
+    acc += (double)threadIdx.x;
+    grid.sync();
+  }
+  if (acc < 0) sink[0] = acc;
+}
+__global__ void k_bar_custom(int iters, double* sink, unsigned* bar) {
+  const GridBarrier grid{bar, bar + 1};
+  double acc = 0.0;
+  for (int i = 0; i < iters; ++i) {
+    acc += (double)threadIdx.x;
+    grid.sync();
+  }
+  if (acc < 0) sink[0] = acc;
+}
+}  // namespace
+
+double barrier_bench(int variant, int iters, int blocks, int threads) {
+  double* sink = nullptr;
+  unsigned* bar = nullptr;
+  cudaMalloc(&sink, 64);
+  cudaMalloc(&bar, 64);
+  cudaMemset(bar, 0, 64);
+  void* args_cg[] = {&iters, &sink};
+  void* args_cu[] = {&iters, &sink, &bar};
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto run = [&]() {
+    return variant == 0 ? cudaLaunchCooperativeKernel((const void*)k_bar_cg, blocks, threads, args_cg, 0, 0)
+                        : cudaLaunchCooperativeKernel((const void*)k_bar_custom, blocks, threads, args_cu, 0, 0);
+  };
+  run();
+  cudaEventRecord(a);
+  const cudaError_t e = run();
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaFree(sink);
+  cudaFree(bar);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return -1.0;
+  }
+  return 1e3 * ms / iters;
+}
 }  // namespace gfb

@@ -90,6 +90,22 @@ __global__ void __launch_bounds__(kTpb) k_nonlocal(DevData d) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.nt) return;
   if (d.deg[e]) return;
+  // avg = sum_q w_q * sigma_c[o_q], strictly in table order (fracture.cpp:75-76); coalesced sliced-ELL reads
+  double avg[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const int64_t base = __ldg(d.nl_sptr + (e >> 5)) * 32 + (e & 31);
+  const int len = __ldg(d.nl_len + e);
+  for (int j = 0; j < len; ++j) {
+    const int64_t q = base + 32 * (int64_t)j;
+    const double w = __ldg(d.nl_w + q);
+    const double2* so = reinterpret_cast<const double2*>(d.sigc + 6 * (size_t)__ldg(d.nl_ids + q));
+    const double2 s01 = __ldg(so), s23 = __ldg(so + 1), s45 = __ldg(so + 2);
+    avg[0] = avg[0] + w * s01.x;
+    avg[1] = avg[1] + w * s01.y;
+    avg[2] = avg[2] + w * s23.x;
+    avg[3] = avg[3] + w * s23.y;
+    avg[4] = avg[4] + w * s45.x;
+    avg[5] = avg[5] + w * s45.y;
+  }
   const int4 t = __ldg(d.tets + e);
   double x[4][3], du[9];
   load_tet_positions(d, t, x, du);
@@ -97,14 +113,6 @@ __global__ void __launch_bounds__(kTpb) k_nonlocal(DevData d) {
   double rl[6], T[6][6];
   tet_rest_lengths(d, e, te, rl);
   build_T(x, rl, T);  // non-degenerate (checked by k_tet_stress with identical arithmetic)
-  double avg[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  const int64_t q1 = __ldg(d.nl_ptr + e + 1);
-  for (int64_t q = __ldg(d.nl_ptr + e); q < q1; ++q) {
-    const double w = __ldg(d.nl_w + q);
-    const double* so = d.sigc + 6 * (size_t)__ldg(d.nl_ids + q);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) avg[k] = avg[k] + w * __ldg(so + k);
-  }
   double scr[6];
   matvec6(T, avg, scr);
   scatter_max(d, te, scr);

@@ -10,6 +10,10 @@
 
 namespace gfb {
 
+__host__ __device__ __forceinline__ size_t sell_addr(const int32_t* sell_ptr, int i, int c, int q) {
+  return ((size_t)(sell_ptr[i >> 5] + c) * 9 + q) * 32 + (i & 31);
+}
+
 struct MatDev {
   double mu, lambda, alpha_nh;  // alpha_nh = 1 + mu/lambda - mu/(4 lambda) (material.cpp:65-67)
   double sigma_thres, chi_eps;  // chi_eps = 1e-12 * sigma_thres (fracture.cpp:132)
@@ -60,12 +64,23 @@ struct DevData {
   const int32_t* nt_ptr;
   const int32_t* nt_tet;
   const uint32_t* nt_slot;
-  // BSR pattern
+  // per block (CSR order) the contributions (pair l, local node k) as items l*4+k, ascending tet order
+  const int32_t* contrib_ptr;  // nb+1
+  const uint8_t* contrib_item;
+  // node-block pattern (CSR view: column ids per row, ascending)
   const int32_t* brow;      // nn+1
   const int32_t* bcol;      // nb
-  const int32_t* bdiag;     // nn
-  // non-local table (r_d > 0)
-  const int64_t* nl_ptr;
+  const int32_t* bdiag;     // nn: position of the diagonal block within the row
+  // SELL-32 storage of the system matrix values: slices of 32 consecutive node rows; slice s owns slots
+  // sell_ptr[s]..sell_ptr[s+1] (max row degree of the slice); entry q of block (row i, slot c) lives at
+  // ((sell_ptr[i/32] + c) * 9 + q) * 32 + i%32, so a warp owning a slice reads every slot coalesced.
+  const int32_t* sell_ptr;  // nslices+1
+  const int32_t* sell_col;  // 32 * total slots (padding slots point at the row itself, zero values)
+  int32_t nslices;
+  // non-local table (r_d > 0), sliced-ELL over 32 consecutive tets: entry j of tet e (slice s = e/32) is at
+  // (nl_sptr[s] + j) * 32 + e%32, j < nl_len[e]; table order (ascending neighbour id) is preserved per tet
+  const int64_t* nl_sptr;
+  const int32_t* nl_len;
   const int32_t* nl_ids;
   const double* nl_w;
   // state
@@ -82,7 +97,7 @@ struct DevData {
   int32_t* newly;           // ne
   int32_t* newly_count;     // 1
   // system
-  double* bval;             // 9nb
+  double* bval;             // 9 * 32 * total slots (SELL-32 layout above)
   double* rhs;              // 3nn
   double* dinv;             // 3nn
   double* x;                // 3nn  (dv)
@@ -121,8 +136,8 @@ void launch_energy(const DevData& d, const MatDev& m, double* out_partials, int 
 // ---- cg.cu ----
 struct CgLaunch {
   int32_t nrows;          // block rows (B=3: nodes) or scalar rows (B=1)
-  const int32_t* row_ptr;
-  const int32_t* cols;
+  const int32_t* row_ptr; // B=1: scalar CSR; B=3: SELL-32 slice pointer
+  const int32_t* cols;    // B=1: CSR columns; B=3: SELL-32 slot columns
   const double* vals;
   const double* b;
   double* x;
@@ -132,11 +147,18 @@ struct CgLaunch {
   double* out;            // [iterations, converged, negative_curvature, relative_residual]
   double tol;
   int32_t max_iters;
+  int32_t nslices;        // B=3: number of 32-row SELL slices
+  unsigned* barrier;      // 2 zero-initialised words: grid-barrier counter + generation
+  int32_t mapping;        // SpMV slice->warp mapping (tuning knob, GF_CG_MAP)
+  unsigned long long* trace;  // optional per-phase %globaltimer stamps (GF_CG_TRACE), 2*200*5 entries
 };
 int cg_grid_size(int block_size);
 void launch_pcg3(const CgLaunch& a, cudaStream_t s);
 void launch_pcg1(const CgLaunch& a, cudaStream_t s);
 void launch_spmv3(const CgLaunch& a, const double* xin, double* y, cudaStream_t s);
+// ---- cg_sell.cu (production solver on the SELL-32 matrix) ----
+int pcg_sell_grid();
+void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_part, cudaStream_t s);
 // ---- misc.cu ----
 void launch_bc_targets(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, double dt, cudaStream_t s);
 int collide_blocks(const DevData& d);

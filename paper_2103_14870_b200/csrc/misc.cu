@@ -179,26 +179,26 @@ __global__ void k_absdiag(DevData d) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d.nn) return;
   const bool fixed = d.node_bc[i] >= 0;
-  const double* A = d.bval + 9 * (size_t)d.bdiag[i];
+  const double* A = d.bval + sell_addr(d.sell_ptr, i, d.bdiag[i], 0);
 #pragma unroll
-  for (int a = 0; a < 3; ++a) d.absdiag[3 * (size_t)i + a] = fixed ? 0.0 : fabs(A[4 * a]);
+  for (int a = 0; a < 3; ++a) d.absdiag[3 * (size_t)i + a] = fixed ? 0.0 : fabs(A[32 * 4 * a]);
 }
 
 __global__ void k_shift_diag(DevData d, double shift) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d.nn) return;
-  double* A = d.bval + 9 * (size_t)d.bdiag[i];
+  double* A = d.bval + sell_addr(d.sell_ptr, i, d.bdiag[i], 0);
 #pragma unroll
-  for (int a = 0; a < 3; ++a) A[4 * a] += shift * d.absdiag[3 * (size_t)i + a];
+  for (int a = 0; a < 3; ++a) A[32 * 4 * a] += shift * d.absdiag[3 * (size_t)i + a];
 }
 
 __global__ void k_bsr_dinv(DevData d) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d.nn) return;
-  const double* A = d.bval + 9 * (size_t)d.bdiag[i];
+  const double* A = d.bval + sell_addr(d.sell_ptr, i, d.bdiag[i], 0);
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const double dd = A[4 * a];
+    const double dd = A[32 * 4 * a];
     d.dinv[3 * (size_t)i + a] = (fabs(dd) > 1e-300) ? 1.0 / dd : 1.0;
   }
 }

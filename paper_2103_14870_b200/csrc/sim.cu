@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -173,8 +174,9 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
 
   // host setup: pattern, incidence, table, mass (fem.cpp:140-179, fracture.cpp:32-54)
   pat_ = make_node_pattern(mesh_);
-  if (pat_.max_degree > 64) throw GeometryError("node valence above 64 is not supported by the assembly kernel");
+  if (pat_.max_degree > 32) throw GeometryError("node rows with more than 32 neighbour blocks are not supported by the assembly kernel");
   const NodeTets ntets = make_node_tets(mesh_, pat_);
+  if (ntets.max_valence > 32) throw GeometryError("nodes shared by more than 32 tets are not supported by the assembly kernel");
   hash_ = pat_.structure_hash(mesh_.nn);
   mass_.assign(mesh_.nn, 0.0);
   for (int32_t e = 0; e < mesh_.nt; ++e) {  // lumped_mass (fem.cpp:171-179), ascending tet order
@@ -209,16 +211,76 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   d_.nt_ptr = (const int32_t*)up(ntets.ptr.data(), 4 * ntets.ptr.size());
   d_.nt_tet = (const int32_t*)up(ntets.tet.data(), 4 * ntets.tet.size());
   d_.nt_slot = (const uint32_t*)up(ntets.slot.data(), 4 * ntets.slot.size());
+  {  // contribution lists of the assembly reduction (assemble.cu): per block, items l*4+k, ascending l
+    std::vector<int32_t> cnt(pat_.cols.size() + 1, 0);
+    for (int32_t i = 0; i < nn; ++i)
+      for (int32_t q = ntets.ptr[i]; q < ntets.ptr[i + 1]; ++q)
+        for (int k = 0; k < 4; ++k) cnt[pat_.row_ptr[i] + ((ntets.slot[q] >> (8 * k)) & 0xff) + 1]++;
+    for (size_t b = 0; b < pat_.cols.size(); ++b) cnt[b + 1] += cnt[b];
+    std::vector<uint8_t> items(cnt.back());
+    std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
+    for (int32_t i = 0; i < nn; ++i)
+      for (int32_t q = ntets.ptr[i]; q < ntets.ptr[i + 1]; ++q)
+        for (int k = 0; k < 4; ++k)
+          items[cur[pat_.row_ptr[i] + ((ntets.slot[q] >> (8 * k)) & 0xff)]++] = (uint8_t)(4 * (q - ntets.ptr[i]) + k);
+    d_.contrib_ptr = (const int32_t*)up(cnt.data(), 4 * cnt.size());
+    d_.contrib_item = (const uint8_t*)up(items.data(), items.size());
+    GF_CUDA(cudaStreamSynchronize(stream_));
+  }
   d_.brow = (const int32_t*)up(pat_.row_ptr.data(), 4 * pat_.row_ptr.size());
   d_.bcol = (const int32_t*)up(pat_.cols.data(), 4 * pat_.cols.size());
-  d_.bdiag = (const int32_t*)up(pat_.diag.data(), 4 * pat_.diag.size());
+  {
+    std::vector<int32_t> dpos(nn);
+    for (int32_t i = 0; i < nn; ++i) dpos[i] = pat_.diag[i] - pat_.row_ptr[i];
+    d_.bdiag = (const int32_t*)up(dpos.data(), 4 * dpos.size());
+    // SELL-32 slices (dev_types.cuh): slots per slice = max degree of its 32 rows
+    const int32_t ns = (nn + 31) / 32;
+    sell_ptr_.assign(ns + 1, 0);
+    for (int32_t sl = 0; sl < ns; ++sl) {
+      int32_t mx = 0;
+      for (int32_t i = 32 * sl; i < std::min(nn, 32 * sl + 32); ++i) mx = std::max(mx, pat_.row_ptr[i + 1] - pat_.row_ptr[i]);
+      sell_ptr_[sl + 1] = sell_ptr_[sl] + mx;
+    }
+    std::vector<int32_t> scol(32 * (size_t)sell_ptr_[ns]);
+    for (int32_t sl = 0; sl < ns; ++sl)
+      for (int32_t k = sell_ptr_[sl]; k < sell_ptr_[sl + 1]; ++k)
+        for (int32_t l = 0; l < 32; ++l) {
+          const int32_t i = 32 * sl + l, c = k - sell_ptr_[sl];
+          int32_t col = 0;
+          if (i < nn) col = (c < pat_.row_ptr[i + 1] - pat_.row_ptr[i]) ? pat_.cols[pat_.row_ptr[i] + c] : i;
+          scol[32 * (size_t)k + l] = col;
+        }
+    d_.sell_ptr = (const int32_t*)up(sell_ptr_.data(), 4 * sell_ptr_.size());
+    d_.sell_col = (const int32_t*)up(scol.data(), 4 * scol.size());
+    d_.nslices = ns;
+    sell_slots_ = sell_ptr_[ns];
+  }
   if (mat.r_d > 0.0) {
     const NonlocalTable tb = make_nonlocal_table(mesh_, mat.r_d);
     nl_entries_ = (int64_t)tb.ids.size();
-    d_.nl_ptr = (const int64_t*)up(tb.ptr.data(), 8 * tb.ptr.size());
-    d_.nl_ids = (const int32_t*)up(tb.ids.data(), 4 * tb.ids.size());
-    d_.nl_w = (const double*)up(tb.w.data(), 8 * tb.w.size());
-    GF_CUDA(cudaStreamSynchronize(stream_));  // tb goes out of scope
+    const int32_t ns = (nt + 31) / 32;
+    std::vector<int64_t> sptr(ns + 1, 0);
+    std::vector<int32_t> len(nt);
+    for (int32_t e = 0; e < nt; ++e) len[e] = (int32_t)(tb.ptr[e + 1] - tb.ptr[e]);
+    for (int32_t sl = 0; sl < ns; ++sl) {
+      int32_t mx = 0;
+      for (int32_t e = 32 * sl; e < std::min(nt, 32 * sl + 32); ++e) mx = std::max(mx, len[e]);
+      sptr[sl + 1] = sptr[sl] + mx;
+    }
+    std::vector<int32_t> ids(32 * (size_t)sptr[ns], 0);
+    std::vector<double> w(32 * (size_t)sptr[ns], 0.0);
+    for (int32_t e = 0; e < nt; ++e) {
+      const int64_t b = sptr[e >> 5] * 32 + (e & 31);
+      for (int32_t j = 0; j < len[e]; ++j) {
+        ids[b + 32 * (int64_t)j] = tb.ids[tb.ptr[e] + j];
+        w[b + 32 * (int64_t)j] = tb.w[tb.ptr[e] + j];
+      }
+    }
+    d_.nl_sptr = (const int64_t*)up(sptr.data(), 8 * sptr.size());
+    d_.nl_len = (const int32_t*)up(len.data(), 4 * len.size());
+    d_.nl_ids = (const int32_t*)up(ids.data(), 4 * ids.size());
+    d_.nl_w = (const double*)up(w.data(), 8 * w.size());
+    GF_CUDA(cudaStreamSynchronize(stream_));  // host staging goes out of scope
   } else {
     nl_entries_ = nt;
   }
@@ -240,7 +302,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   d_.screening = (double*)zeros(8 * (size_t)ne);
   d_.newly = (int32_t*)zeros(4 * (size_t)ne);
   d_.newly_count = (int32_t*)zeros(8);
-  d_.bval = (double*)zeros(72 * (size_t)nb);
+  d_.bval = (double*)zeros(8 * 9 * 32 * (size_t)sell_slots_);  // padding slots stay zero
   d_.rhs = (double*)zeros(8 * nd);
   d_.dinv = (double*)zeros(8 * nd);
   d_.x = (double*)zeros(8 * nd);
@@ -286,8 +348,9 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   launch_reset_keys(d_, stream_);
 
   cg_.nrows = nn;
-  cg_.row_ptr = d_.brow;
-  cg_.cols = d_.bcol;
+  cg_.row_ptr = d_.sell_ptr;
+  cg_.cols = d_.sell_col;
+  cg_.nslices = d_.nslices;
   cg_.vals = d_.bval;
   cg_.b = d_.rhs;
   cg_.x = d_.x;
@@ -295,6 +358,12 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   cg_.r = d_.r; cg_.z = d_.z; cg_.p0 = d_.p0; cg_.p1 = d_.p1; cg_.Ap = d_.Ap;
   cg_.partials = d_.partials;
   cg_.out = d_.cg_out;
+  cg_.barrier = (unsigned*)zeros(64);
+  if (const char* e = std::getenv("GF_CG_MAP")) cg_.mapping = std::atoi(e);
+  if (const char* e = std::getenv("GF_CG_KERNEL")) cg_kernel_ = std::atoi(e);
+  d_ctr_ = (unsigned long long*)zeros(64);
+  d_slice_part_ = (double*)zeros(8 * 2 * 3 * (size_t)d_.nslices);
+  if (std::getenv("GF_CG_TRACE")) cg_.trace = (unsigned long long*)zeros(8 * 5000);
   cg_.tol = cfg.cg_tol;
   GF_CUDA(cudaStreamSynchronize(stream_));
   GF_CUDA(cudaGetLastError());
@@ -362,6 +431,12 @@ void Simulation::synchronize() {
   flush_events();
 }
 
+void Simulation::cg_trace(unsigned long long* out) {
+  if (!cg_.trace) throw FormatError("CG trace disabled (set GF_CG_TRACE before creating the simulation)");
+  GF_CUDA(cudaMemcpyAsync(out, cg_.trace, 8 * 5000, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+}
+
 void Simulation::timer_record(int slot) {
   if (slot < 0 || slot >= 8) throw FormatError("timer slot must be in [0, 8)");
   if (!timers_[slot]) GF_CUDA(cudaEventCreate(&timers_[slot]));
@@ -421,11 +496,16 @@ void Simulation::upload_bc_step(double t, double dt) {
   GF_CUDA(cudaMemcpyAsync(d_bcstep_, h_bcstep_, sizeof(BcStep) * bcs_.size(), cudaMemcpyHostToDevice, stream_));
 }
 
+void Simulation::launch_cg() {
+  if (cg_kernel_ == 0) launch_pcg_sell(cg_, d_ctr_, d_slice_part_, stream_);
+  else launch_pcg3(cg_, stream_);
+}
+
 double Simulation::run_cg(int max_iters) {
   cg_.max_iters = max_iters;
   const double N = mesh_.nn, NB = pat_.cols.size();
   // bytes are filled in after the run from the iteration count (see dynamic_step)
-  launch("pcg", 0.0 * (N + NB), [&] { launch_pcg3(cg_, stream_); });
+  launch("pcg", 0.0 * (N + NB), [&] { launch_cg(); });
   GF_CUDA(cudaMemcpyAsync(h_stats_, d_.cg_out, 32, cudaMemcpyDeviceToHost, stream_));
   synchronize();
   return h_stats_[0];
@@ -485,12 +565,12 @@ gf_step_stats Simulation::dynamic_step() {
 
   // solve_linear (solver.cpp:105-136): first attempt, 4x retry, then cumulative diagonal shifts
   cg_.max_iters = cfg_.cg_max_iters;
-  launch("pcg", 0.0, [&] { launch_pcg3(cg_, stream_); });
+  launch("pcg", 0.0, [&] { launch_cg(); });
   GF_CUDA(cudaMemcpyAsync(h_stats_, d_.cg_out, 32, cudaMemcpyDeviceToHost, stream_));
   GF_CUDA(cudaMemcpyAsync(h_stats_ + 4, d_load_, 8, cudaMemcpyDeviceToHost, stream_));
   GF_CUDA(cudaMemcpyAsync(h_stats_ + 5, d_.newly_count, 4, cudaMemcpyDeviceToHost, stream_));
   synchronize();
-  const double cg_bytes_per_iter = (72 + 4) * NB + 4 * (N + 1) + 240 * N;
+  const double cg_bytes_per_iter = (72 + 4) * NB + 4 * (N + 1) + 240 * N;  // algorithmic (no SELL padding)
   auto account = [&](double iters) {
     if (profiling_) ktimes_["pcg"].bytes += iters * cg_bytes_per_iter + 200 * N;
   };
@@ -597,7 +677,7 @@ void Simulation::bsr_to_csr(const std::vector<double>& bval, double* vals) const
     for (int a = 0; a < 3; ++a) {
       const size_t start = 9 * (size_t)r0 + 3 * (size_t)a * deg;
       for (int32_t q = 0; q < deg; ++q)
-        for (int b = 0; b < 3; ++b) vals[start + 3 * q + b] = bval[9 * (size_t)(r0 + q) + 3 * a + b];
+        for (int b = 0; b < 3; ++b) vals[start + 3 * q + b] = bval[sell_addr(sell_ptr_.data(), i, q, 3 * a + b)];
     }
   }
 }
@@ -605,14 +685,14 @@ void Simulation::bsr_to_csr(const std::vector<double>& bval, double* vals) const
 void Simulation::eval_stiffness(double* vals) {
   StepCoeffs c{};
   launch("stiffness", 0.0, [&] { launch_assemble(d_, md_, c, kAssembleRawK, stream_); });
-  std::vector<double> b(9 * pat_.cols.size());
+  std::vector<double> b(9 * 32 * (size_t)sell_slots_);
   GF_CUDA(cudaMemcpyAsync(b.data(), d_.bval, 8 * b.size(), cudaMemcpyDeviceToHost, stream_));
   synchronize();
   bsr_to_csr(b, vals);
 }
 
 void Simulation::last_system(double* vals, double* rhs) {
-  std::vector<double> b(9 * pat_.cols.size());
+  std::vector<double> b(9 * 32 * (size_t)sell_slots_);
   GF_CUDA(cudaMemcpyAsync(b.data(), d_.bval, 8 * b.size(), cudaMemcpyDeviceToHost, stream_));
   if (rhs) GF_CUDA(cudaMemcpyAsync(rhs, d_.rhs, 24 * (size_t)mesh_.nn, cudaMemcpyDeviceToHost, stream_));
   synchronize();
@@ -704,6 +784,8 @@ void cg_solve_csr(int32_t n, const int32_t* row_ptr, const int32_t* cols, const 
     a.Ap = (double*)alloc(8 * (size_t)n);
     a.partials = (double*)alloc(8 * 2 * 3 * (size_t)cg_grid_size(1));
     a.out = (double*)alloc(8 * 4);
+    a.barrier = (unsigned*)alloc(64);
+    GF_CUDA(cudaMemsetAsync(a.barrier, 0, 64, s));
     a.tol = tol;
     a.max_iters = max_iters;
     GF_CUDA(cudaMemcpyAsync((void*)a.row_ptr, row_ptr, 4 * (size_t)(n + 1), cudaMemcpyHostToDevice, s));

@@ -66,6 +66,7 @@ class Simulation {
   void reset_kernel_times() { ktimes_.clear(); }
   void synchronize();
   void timer_record(int slot);
+  void cg_trace(unsigned long long* out);
   double timer_elapsed(int a, int b);
 
  private:
@@ -77,9 +78,12 @@ class Simulation {
   void run_damage(bool relabel, bool keep_values, bool chi);
   void bsr_to_csr(const std::vector<double>& bval, double* vals) const;
   double run_cg(int max_iters);
+  void launch_cg();
 
   HostMesh mesh_;
   NodePattern pat_;
+  std::vector<int32_t> sell_ptr_;
+  int64_t sell_slots_ = 0;
   gf_material mat_;
   gf_solver_config cfg_;
   MatDev md_{};
@@ -95,6 +99,9 @@ class Simulation {
   cudaStream_t stream_ = nullptr;
   DevData d_{};
   CgLaunch cg_{};
+  int cg_kernel_ = 0;  // 0: dynamic-schedule SELL kernel (cg_sell.cu), 1: static kernel (cg.cu)
+  unsigned long long* d_ctr_ = nullptr;
+  double* d_slice_part_ = nullptr;
   std::vector<void*> allocs_;
   int32_t* d_fixed_nodes_ = nullptr;
   BcStep* d_bcstep_ = nullptr;
