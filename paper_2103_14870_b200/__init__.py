@@ -26,7 +26,7 @@ __all__ = [
 
 STABLE_NEO_HOOKEAN, STVK = 0, 1
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB = os.path.join(_HERE, "_lib", "libgrafem_b200.so")
+_LIB = os.environ.get("GF_LIB_PATH") or os.path.join(_HERE, "_lib", "libgrafem_b200.so")  # override: A/B tools
 
 F64P = C.POINTER(C.c_double)
 I32P = C.POINTER(C.c_int32)

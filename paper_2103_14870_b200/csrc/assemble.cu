@@ -188,10 +188,15 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_assemble(DevData d, MatDev m
       double K[9];
 #pragma unroll
       for (int r = 0; r < 9; ++r) K[r] = s_row[w][9 * c + r];
-      double* out = d.bval + sell_addr(d.sell_ptr, i, c, 0);  // entry r at out[32 * r]
+      // destination: SELL-32 (entry r at out[32 r]) or the upper block (entry r at out[r]); lower blocks of the
+      // symmetric format are not stored (row j writes (j,i) = (i,j)^T)
+      const int cu = d.mat_format ? __ldg(d.uslot + row0 + c) : c;
+      double* out = cu >= 0 ? d.bval + sell_addr(d.mat_format ? d.usp : d.sell_ptr, i, cu, 0) : nullptr;
+      constexpr int ostride = 32;
       if (kMode == kAssembleRawK) {
+        if (out)
 #pragma unroll
-        for (int r = 0; r < 9; ++r) out[32 * r] = K[r];
+          for (int r = 0; r < 9; ++r) out[ostride * r] = K[r];
       } else {
         const int j = __ldg(d.bcol + row0 + c);
         double vj[3];
@@ -220,8 +225,9 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_assemble(DevData d, MatDev m
 #pragma unroll
           for (int r = 0; r < 9; ++r) A[r] = 0.0;
         }
+        if (out)
 #pragma unroll
-        for (int r = 0; r < 9; ++r) out[32 * r] = A[r];
+          for (int r = 0; r < 9; ++r) out[ostride * r] = A[r];
         if (j == i) {
 #pragma unroll
           for (int a = 0; a < 3; ++a) {

@@ -20,12 +20,16 @@
 
 #include "dev_types.cuh"
 
+#ifndef GF_SELL_THREADS
+#define GF_SELL_THREADS 768
+#endif
+
 namespace cg = cooperative_groups;
 
 namespace gfb {
 namespace {
 
-constexpr int kThreads = 1024;
+constexpr int kThreads = GF_SELL_THREADS;
 constexpr int kWarpsPerCta = kThreads / 32;
 
 struct SellArgs {
@@ -83,39 +87,155 @@ __device__ __forceinline__ double ldm(const double* p) {
   else return __ldg(p);
 }
 
+#ifndef GF_SELL_GROUP
+#define GF_SELL_GROUP 2
+#endif
+constexpr int kGroup = GF_SELL_GROUP;
+#ifndef GF_GATHER_L1
+#define GF_GATHER_L1 1
+#endif
+// Vectors written in the previous phase are read through L1 (ld.global.nc): safe because every phase boundary
+// is a cooperative-groups grid barrier, whose gpu-scope fence invalidates L1 (CCTL.IVALL), and within a phase
+// the gathered vectors are read-only (the fused p update writes the other buffer).
+__device__ __forceinline__ double ldv(const double* p) {
+#if GF_GATHER_L1
+  return __ldg(p);
+#else
+  return __ldcg(p);
+#endif
+}
+
+// Software-pipelined: the column ids of the next group of kGroup slots are fetched while the current group's
+// p_j gathers and block values are in flight, so each group costs one memory round trip instead of two
+// (col -> gather dependency).
 template <bool kStream>
 __device__ __forceinline__ void slice_spmv(const CgLaunch& a, int sl, const double* src, const double* z, double beta,
                                            bool fused, double acc[3]) {
   const int lane = threadIdx.x & 31;
   const int k0 = __ldg(a.row_ptr + sl), k1 = __ldg(a.row_ptr + sl + 1);
   acc[0] = acc[1] = acc[2] = 0.0;
-#pragma unroll 2
-  for (int k = k0; k < k1; ++k) {
-    const size_t j = kStream ? (size_t)__ldcs(a.cols + (size_t)k * 32 + lane) : (size_t)__ldg(a.cols + (size_t)k * 32 + lane);
-    const double* v = a.vals + (size_t)k * 288 + lane;
-    double p0, p1, p2;
-    if (fused) {
-      p0 = __fma_rn(beta, __ldcg(src + 3 * j), __ldcg(z + 3 * j));
-      p1 = __fma_rn(beta, __ldcg(src + 3 * j + 1), __ldcg(z + 3 * j + 1));
-      p2 = __fma_rn(beta, __ldcg(src + 3 * j + 2), __ldcg(z + 3 * j + 2));
-    } else {
-      p0 = __ldcg(src + 3 * j);
-      p1 = __ldcg(src + 3 * j + 1);
-      p2 = __ldcg(src + 3 * j + 2);
+  auto col = [&](int k) -> int {
+    return kStream ? __ldcs(a.cols + (size_t)k * 32 + lane) : __ldg(a.cols + (size_t)k * 32 + lane);
+  };
+  int jc[kGroup];
+#pragma unroll
+  for (int g = 0; g < kGroup; ++g) jc[g] = (k0 + g < k1) ? col(k0 + g) : 0;
+  for (int kb = k0; kb < k1; kb += kGroup) {
+    int jn[kGroup];
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g) jn[g] = (kb + kGroup + g < k1) ? col(kb + kGroup + g) : 0;
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g) {
+      if (kb + g < k1) {
+        const size_t j = (size_t)jc[g];
+        const double* v = a.vals + (size_t)(kb + g) * 288 + lane;
+        double p0, p1, p2;
+        if (fused) {
+          p0 = __fma_rn(beta, ldv(src + 3 * j), ldv(z + 3 * j));
+          p1 = __fma_rn(beta, ldv(src + 3 * j + 1), ldv(z + 3 * j + 1));
+          p2 = __fma_rn(beta, ldv(src + 3 * j + 2), ldv(z + 3 * j + 2));
+        } else {
+          p0 = ldv(src + 3 * j);
+          p1 = ldv(src + 3 * j + 1);
+          p2 = ldv(src + 3 * j + 2);
+        }
+        acc[0] = __fma_rn(ldm<kStream>(v + 0), p0, acc[0]);
+        acc[0] = __fma_rn(ldm<kStream>(v + 32), p1, acc[0]);
+        acc[0] = __fma_rn(ldm<kStream>(v + 64), p2, acc[0]);
+        acc[1] = __fma_rn(ldm<kStream>(v + 96), p0, acc[1]);
+        acc[1] = __fma_rn(ldm<kStream>(v + 128), p1, acc[1]);
+        acc[1] = __fma_rn(ldm<kStream>(v + 160), p2, acc[1]);
+        acc[2] = __fma_rn(ldm<kStream>(v + 192), p0, acc[2]);
+        acc[2] = __fma_rn(ldm<kStream>(v + 224), p1, acc[2]);
+        acc[2] = __fma_rn(ldm<kStream>(v + 256), p2, acc[2]);
+      }
     }
-    acc[0] = __fma_rn(ldm<kStream>(v + 0), p0, acc[0]);
-    acc[0] = __fma_rn(ldm<kStream>(v + 32), p1, acc[0]);
-    acc[0] = __fma_rn(ldm<kStream>(v + 64), p2, acc[0]);
-    acc[1] = __fma_rn(ldm<kStream>(v + 96), p0, acc[1]);
-    acc[1] = __fma_rn(ldm<kStream>(v + 128), p1, acc[1]);
-    acc[1] = __fma_rn(ldm<kStream>(v + 160), p2, acc[1]);
-    acc[2] = __fma_rn(ldm<kStream>(v + 192), p0, acc[2]);
-    acc[2] = __fma_rn(ldm<kStream>(v + 224), p1, acc[2]);
-    acc[2] = __fma_rn(ldm<kStream>(v + 256), p2, acc[2]);
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g) jc[g] = jn[g];
   }
 }
 
-template <bool kStream>
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// diagnostics (GF_CG_TRACE): CTA 0 stamps 5 points per iteration; at iteration 10 every CTA stamps the end of
+// its phase-A and phase-B work (after a CTA barrier)
+#define SELL_STAMP(k, point)                                                          \
+  do {                                                                                \
+    if (a.trace && threadIdx.x == 0 && blockIdx.x == 0 && (k) < 200)                 \
+      a.trace[(k) * 5 + (point)] = gtimer();                                         \
+  } while (0)
+#define SELL_BLOCK_STAMP(k, slot)                                                     \
+  do {                                                                                \
+    if (a.trace && (k) == 10) {                                                       \
+      __syncthreads();                                                                \
+      if (threadIdx.x == 0) a.trace[(slot) + blockIdx.x] = gtimer();                 \
+    }                                                                                 \
+  } while (0)
+
+// Symmetric format: slot (base | T<<31, j) of row i contributes A p_j (T = 0, upper block (i,j)) or A^T p_j
+// (T = 1, block (j,i) stored by row j); entry q at vals[base + 32 q]. Half the matrix bytes of the full format;
+// the upper blocks (~62 MB at c3) and the CG vectors can stay resident in the 126 MB L2 across iterations.
+__device__ __forceinline__ void slice_spmv_sym(const CgLaunch& a, int sl, const double* src, const double* z,
+                                               double beta, bool fused, double acc[3]) {
+  const int lane = threadIdx.x & 31;
+  const int k0 = __ldg(a.row_ptr + sl), k1 = __ldg(a.row_ptr + sl + 1);
+  const int2* slots = reinterpret_cast<const int2*>(a.cols);
+  acc[0] = acc[1] = acc[2] = 0.0;
+  int2 sc[kGroup];
+#pragma unroll
+  for (int g = 0; g < kGroup; ++g) sc[g] = (k0 + g < k1) ? __ldg(slots + (size_t)(k0 + g) * 32 + lane) : make_int2(0, 0);
+  for (int kb = k0; kb < k1; kb += kGroup) {
+    int2 sn[kGroup];
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g)
+      sn[g] = (kb + kGroup + g < k1) ? __ldg(slots + (size_t)(kb + kGroup + g) * 32 + lane) : make_int2(0, 0);
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g) {
+      if (kb + g < k1) {
+        const size_t j = (size_t)sc[g].y;
+        const bool tr = sc[g].x < 0;
+        const size_t base = (size_t)(sc[g].x & 0x7fffffff);
+        double p0, p1, p2;
+        if (fused) {
+          p0 = __fma_rn(beta, ldv(src + 3 * j), ldv(z + 3 * j));
+          p1 = __fma_rn(beta, ldv(src + 3 * j + 1), ldv(z + 3 * j + 1));
+          p2 = __fma_rn(beta, ldv(src + 3 * j + 2), ldv(z + 3 * j + 2));
+        } else {
+          p0 = ldv(src + 3 * j);
+          p1 = ldv(src + 3 * j + 1);
+          p2 = ldv(src + 3 * j + 2);
+        }
+        const double* v = a.vals + base;
+        double m[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) m[q] = __ldcg(v + 32 * q);
+        if (!tr) {
+          acc[0] = __fma_rn(m[0], p0, acc[0]); acc[0] = __fma_rn(m[1], p1, acc[0]); acc[0] = __fma_rn(m[2], p2, acc[0]);
+          acc[1] = __fma_rn(m[3], p0, acc[1]); acc[1] = __fma_rn(m[4], p1, acc[1]); acc[1] = __fma_rn(m[5], p2, acc[1]);
+          acc[2] = __fma_rn(m[6], p0, acc[2]); acc[2] = __fma_rn(m[7], p1, acc[2]); acc[2] = __fma_rn(m[8], p2, acc[2]);
+        } else {
+          acc[0] = __fma_rn(m[0], p0, acc[0]); acc[0] = __fma_rn(m[3], p1, acc[0]); acc[0] = __fma_rn(m[6], p2, acc[0]);
+          acc[1] = __fma_rn(m[1], p0, acc[1]); acc[1] = __fma_rn(m[4], p1, acc[1]); acc[1] = __fma_rn(m[7], p2, acc[1]);
+          acc[2] = __fma_rn(m[2], p0, acc[2]); acc[2] = __fma_rn(m[5], p1, acc[2]); acc[2] = __fma_rn(m[8], p2, acc[2]);
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g) sc[g] = sn[g];
+  }
+}
+
+template <bool kStream, int kFmt>
+__device__ __forceinline__ void spmv_fmt(const CgLaunch& a, int sl, const double* src, const double* z, double beta,
+                                         bool fused, double acc[3]) {
+  if constexpr (kFmt == 1) slice_spmv_sym(a, sl, src, z, beta, fused, acc);
+  else slice_spmv<kStream>(a, sl, src, z, beta, fused, acc);
+}
+
+template <bool kStream, int kFmt>
 __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
   cg::grid_group grid = cg::this_grid();
   const CgLaunch& a = sa.a;
@@ -127,7 +247,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
   // setup (sparse.cpp:145-157): r = b - A x, z = D^-1 r, p = z; partials b.b, r.z, r.r per slice
   for (int sl = sch.next(ns); sl >= 0; sl = sch.next(ns)) {
     double acc[3];
-    slice_spmv<kStream>(a, sl, a.x, nullptr, 0.0, false, acc);
+    spmv_fmt<kStream, kFmt>(a, sl, a.x, nullptr, 0.0, false, acc);
     const int row = sl * 32 + lane;
     double bb = 0.0, rz = 0.0, rr = 0.0;
     if (row < nrows) {
@@ -174,17 +294,18 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
     bool done = false;
     for (int it = 0; it < a.max_iters; ++it) {
       const bool fused = it > 0;
+      SELL_STAMP(it, 0);
       // ---- phase A: q = A p
       for (int sl = sch.next(ns); sl >= 0; sl = sch.next(ns)) {
         double acc[3];
-        slice_spmv<kStream>(a, sl, pcur, a.z, beta, fused, acc);
+        spmv_fmt<kStream, kFmt>(a, sl, pcur, a.z, beta, fused, acc);
         const int row = sl * 32 + lane;
         double pq = 0.0;
         if (row < nrows) {
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const size_t dof = 3 * (size_t)row + c;
-            const double pr = fused ? __fma_rn(beta, __ldcg(pcur + dof), __ldcg(a.z + dof)) : __ldcg(pcur + dof);
+            const double pr = fused ? __fma_rn(beta, ldv(pcur + dof), ldv(a.z + dof)) : ldv(pcur + dof);
             a.Ap[dof] = acc[c];
             if (fused) pnext[dof] = pr;
             pq = __fma_rn(pr, acc[c], pq);
@@ -194,6 +315,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
         if (lane == 0) part(0)[sl] = pq;
       }
       sch.advance();
+      SELL_STAMP(it, 1);
+      SELL_BLOCK_STAMP(it, 3000);
       if (fused) {
         double* t = pcur;
         pcur = pnext;
@@ -203,6 +326,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       double pap[1];
       sum_slices<1>(part(0), ns, pap);
       parity ^= 1;
+      SELL_STAMP(it, 2);
       if (pap[0] <= 0.0) {  // sparse.cpp:160-168
         negcurv = pap[0] < 0.0;
         iterations = it;
@@ -238,10 +362,13 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
         }
       }
       sch.advance();
+      SELL_STAMP(it, 3);
+      SELL_BLOCK_STAMP(it, 2000);
       grid.sync();
       double red2[2];
       sum_slices<2>(part(0), ns, red2);
       parity ^= 1;
+      SELL_STAMP(it, 4);
       rr = red2[0];
       iterations = it + 1;
       const double rnorm = sqrt(rr);
@@ -276,13 +403,13 @@ int pcg_sell_grid() {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_sell<true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_sell<true, 1>, kThreads, 0);
     g_grid = sms * (per > 0 ? per : 1);
   }
   return g_grid;
 }
 
-void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_part, cudaStream_t s) {
+void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_part, cudaStream_t s, int mat_format) {
   static const int stream_matrix = [] {
     const char* e = std::getenv("GF_CG_STREAM");
     return e ? std::atoi(e) : 1;
@@ -290,7 +417,8 @@ void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_p
   SellArgs sa{a, stream_matrix, ctr, slice_part};
   cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s);
   void* args[] = {&sa};
-  const void* fn = stream_matrix ? (const void*)k_pcg_sell<true> : (const void*)k_pcg_sell<false>;
+  const void* fn = mat_format == 1 ? (const void*)k_pcg_sell<true, 1>
+                   : stream_matrix ? (const void*)k_pcg_sell<true, 0> : (const void*)k_pcg_sell<false, 0>;
   const cudaError_t err = cudaLaunchCooperativeKernel(fn, pcg_sell_grid(), kThreads, args, 0, s);
   if (err != cudaSuccess) {
     cudaGetLastError();
@@ -298,4 +426,24 @@ void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_p
   }
 }
 
+}  // namespace gfb
+
+namespace gfb {
+namespace {
+template <int kFmt>
+__global__ void __launch_bounds__(kThreads) k_spmv_fmt(CgLaunch a, const double* xin, double* y) {
+  const int lane = threadIdx.x & 31;
+  for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < a.nslices; sl += (gridDim.x * blockDim.x) >> 5) {
+    double acc[3];
+    spmv_fmt<true, kFmt>(a, sl, xin, nullptr, 0.0, false, acc);
+    const int row = sl * 32 + lane;
+    if (row < a.nrows)
+      for (int c = 0; c < 3; ++c) y[3 * (size_t)row + c] = acc[c];
+  }
+}
+}  // namespace
+void launch_spmv_fmt(const CgLaunch& a, const double* xin, double* y, int mat_format, cudaStream_t s) {
+  if (mat_format == 1) k_spmv_fmt<1><<<pcg_sell_grid(), kThreads, 0, s>>>(a, xin, y);
+  else k_spmv_fmt<0><<<pcg_sell_grid(), kThreads, 0, s>>>(a, xin, y);
+}
 }  // namespace gfb

@@ -13,6 +13,7 @@ namespace gfb {
 __host__ __device__ __forceinline__ size_t sell_addr(const int32_t* sell_ptr, int i, int c, int q) {
   return ((size_t)(sell_ptr[i >> 5] + c) * 9 + q) * 32 + (i & 31);
 }
+// value address of block (row i, CSR position c) for either format (symmetric: upper blocks only, c_u >= 0)
 
 struct MatDev {
   double mu, lambda, alpha_nh;  // alpha_nh = 1 + mu/lambda - mu/(4 lambda) (material.cpp:65-67)
@@ -77,6 +78,16 @@ struct DevData {
   const int32_t* sell_ptr;  // nslices+1
   const int32_t* sell_col;  // 32 * total slots (padding slots point at the row itself, zero values)
   int32_t nslices;
+  // symmetric format (mat_format == 1, default): only the upper blocks (j >= i) are stored, in their own SELL-32
+  // layout (slice s owns upper slots usp[s]..usp[s+1]; entry q of upper block (i, c_u) at
+  // ((usp[i/32] + c_u) * 9 + q) * 32 + i%32). uslot[b] maps a CSR block (row i, column c) to c_u, or -1 when
+  // j < i (that block is (j,i)^T, stored by row j). The SpMV slot list (SELL-32 over the full row, column order)
+  // holds int2 {value base | transpose<<31, j}; entry q of the slot's block is at base + 32 q. For interior
+  // rows the neighbour offsets are uniform across a slice, so both direct and transposed reads coalesce.
+  int32_t mat_format;       // 0 full SELL-32 values, 1 symmetric upper blocks
+  const int32_t* usp;       // nslices+1
+  const int32_t* uslot;     // nb
+  const int2* sell_slot;    // 32 * total slots
   // non-local table (r_d > 0), sliced-ELL over 32 consecutive tets: entry j of tet e (slice s = e/32) is at
   // (nl_sptr[s] + j) * 32 + e%32, j < nl_len[e]; table order (ascending neighbour id) is preserved per tet
   const int64_t* nl_sptr;
@@ -158,7 +169,8 @@ void launch_pcg1(const CgLaunch& a, cudaStream_t s);
 void launch_spmv3(const CgLaunch& a, const double* xin, double* y, cudaStream_t s);
 // ---- cg_sell.cu (production solver on the SELL-32 matrix) ----
 int pcg_sell_grid();
-void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_part, cudaStream_t s);
+void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_part, cudaStream_t s, int mat_format);
+void launch_spmv_fmt(const CgLaunch& a, const double* xin, double* y, int mat_format, cudaStream_t s);
 // ---- misc.cu ----
 void launch_bc_targets(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, double dt, cudaStream_t s);
 int collide_blocks(const DevData& d);

@@ -13,6 +13,10 @@ namespace {
 constexpr int kTpb = 256;
 inline int nblk(int64_t n) { return (int)((n + kTpb - 1) / kTpb); }
 
+__device__ __forceinline__ const double* diag_block(const DevData& d, int i) {  // entry q at [32 q]
+  return d.mat_format ? d.bval + sell_addr(d.usp, i, 0, 0) : d.bval + sell_addr(d.sell_ptr, i, d.bdiag[i], 0);
+}
+
 __device__ __forceinline__ void bc_disp(const BcStep& b, const double* X, const double* R, const double* d,
                                         double out[3]) {
   if (b.kind == 0) {
@@ -179,26 +183,29 @@ __global__ void k_absdiag(DevData d) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d.nn) return;
   const bool fixed = d.node_bc[i] >= 0;
-  const double* A = d.bval + sell_addr(d.sell_ptr, i, d.bdiag[i], 0);
+  const double* A = diag_block(d, i);
+  constexpr int st = 32;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) d.absdiag[3 * (size_t)i + a] = fixed ? 0.0 : fabs(A[32 * 4 * a]);
+  for (int a = 0; a < 3; ++a) d.absdiag[3 * (size_t)i + a] = fixed ? 0.0 : fabs(A[st * 4 * a]);
 }
 
 __global__ void k_shift_diag(DevData d, double shift) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d.nn) return;
-  double* A = d.bval + sell_addr(d.sell_ptr, i, d.bdiag[i], 0);
+  double* A = const_cast<double*>(diag_block(d, i));
+  constexpr int st = 32;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) A[32 * 4 * a] += shift * d.absdiag[3 * (size_t)i + a];
+  for (int a = 0; a < 3; ++a) A[st * 4 * a] += shift * d.absdiag[3 * (size_t)i + a];
 }
 
 __global__ void k_bsr_dinv(DevData d) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d.nn) return;
-  const double* A = d.bval + sell_addr(d.sell_ptr, i, d.bdiag[i], 0);
+  const double* A = diag_block(d, i);
+  constexpr int st = 32;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const double dd = A[32 * 4 * a];
+    const double dd = A[st * 4 * a];
     d.dinv[3 * (size_t)i + a] = (fabs(dd) > 1e-300) ? 1.0 / dd : 1.0;
   }
 }

@@ -254,6 +254,50 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     d_.sell_col = (const int32_t*)up(scol.data(), 4 * scol.size());
     d_.nslices = ns;
     sell_slots_ = sell_ptr_[ns];
+    // symmetric format: upper blocks (j >= i) in upper-CSR order + SELL-32 slot list {block | T<<31, j}
+    mat_format_ = 1;
+    if (const char* e = std::getenv("GF_MATRIX")) mat_format_ = std::string(e) == "full" ? 0 : 1;
+    d_.mat_format = mat_format_;
+    uslot_.assign(pat_.cols.size(), -1);
+    std::vector<int32_t> ucount(nn, 0);
+    for (int32_t i = 0; i < nn; ++i)
+      for (int32_t q = pat_.row_ptr[i]; q < pat_.row_ptr[i + 1]; ++q)
+        if (pat_.cols[q] >= i) uslot_[q] = ucount[i]++;
+    usp_.assign(ns + 1, 0);
+    for (int32_t sl = 0; sl < ns; ++sl) {
+      int32_t mx = 0;
+      for (int32_t i = 32 * sl; i < std::min(nn, 32 * sl + 32); ++i) mx = std::max(mx, ucount[i]);
+      usp_[sl + 1] = usp_[sl] + mx;
+    }
+    if ((int64_t)usp_[ns] * 288 >= (int64_t)1 << 31) throw GeometryError("symmetric value array exceeds 31-bit slot bases");
+    auto base_of = [&](int32_t owner, int32_t cu) {
+      return (int32_t)(((int64_t)(usp_[owner >> 5] + cu) * 9) * 32 + (owner & 31));
+    };
+    std::vector<int2> slot(32 * (size_t)sell_slots_);
+    const int32_t zero_base = (int32_t)((int64_t)usp_[ns] * 288);  // one extra all-zero 288-double group
+    for (int32_t sl = 0; sl < ns; ++sl)
+      for (int32_t l = 0; l < 32; ++l) {
+        const int32_t i = 32 * sl + l;
+        const int32_t deg = i < nn ? pat_.row_ptr[i + 1] - pat_.row_ptr[i] : 0;
+        for (int32_t c = 0; c < sell_ptr_[sl + 1] - sell_ptr_[sl]; ++c) {
+          int2 e = make_int2(zero_base + l, i < nn ? i : 0);  // padding: zero block, own row
+          if (c < deg) {
+            const int32_t q = pat_.row_ptr[i] + c, j = pat_.cols[q];
+            if (j >= i) {
+              e = make_int2(base_of(i, uslot_[q]), j);
+            } else {
+              const auto jb = pat_.cols.begin() + pat_.row_ptr[j], je = pat_.cols.begin() + pat_.row_ptr[j + 1];
+              const int32_t qj = pat_.row_ptr[j] + (int32_t)(std::lower_bound(jb, je, i) - jb);
+              e = make_int2(base_of(j, uslot_[qj]) | (int32_t)0x80000000u, j);
+            }
+          }
+          slot[32 * (size_t)(sell_ptr_[sl] + c) + l] = e;
+        }
+      }
+    d_.usp = (const int32_t*)up(usp_.data(), 4 * usp_.size());
+    d_.uslot = (const int32_t*)up(uslot_.data(), 4 * uslot_.size());
+    d_.sell_slot = (const int2*)up(slot.data(), 8 * slot.size());
+    GF_CUDA(cudaStreamSynchronize(stream_));
   }
   if (mat.r_d > 0.0) {
     const NonlocalTable tb = make_nonlocal_table(mesh_, mat.r_d);
@@ -302,7 +346,8 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   d_.screening = (double*)zeros(8 * (size_t)ne);
   d_.newly = (int32_t*)zeros(4 * (size_t)ne);
   d_.newly_count = (int32_t*)zeros(8);
-  d_.bval = (double*)zeros(8 * 9 * 32 * (size_t)sell_slots_);  // padding slots stay zero
+  bval_doubles_ = mat_format_ ? 288 * ((size_t)usp_[d_.nslices] + 1) : 288 * (size_t)sell_slots_;
+  d_.bval = (double*)zeros(8 * bval_doubles_);  // padding slots / the extra zero block stay zero
   d_.rhs = (double*)zeros(8 * nd);
   d_.dinv = (double*)zeros(8 * nd);
   d_.x = (double*)zeros(8 * nd);
@@ -349,7 +394,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
 
   cg_.nrows = nn;
   cg_.row_ptr = d_.sell_ptr;
-  cg_.cols = d_.sell_col;
+  cg_.cols = mat_format_ ? reinterpret_cast<const int32_t*>(d_.sell_slot) : d_.sell_col;
   cg_.nslices = d_.nslices;
   cg_.vals = d_.bval;
   cg_.b = d_.rhs;
@@ -497,7 +542,7 @@ void Simulation::upload_bc_step(double t, double dt) {
 }
 
 void Simulation::launch_cg() {
-  if (cg_kernel_ == 0) launch_pcg_sell(cg_, d_ctr_, d_slice_part_, stream_);
+  if (cg_kernel_ == 0 || mat_format_ == 1) launch_pcg_sell(cg_, d_ctr_, d_slice_part_, stream_, mat_format_);
   else launch_pcg3(cg_, stream_);
 }
 
@@ -674,10 +719,21 @@ void Simulation::eval_forces(double* f3n) {
 void Simulation::bsr_to_csr(const std::vector<double>& bval, double* vals) const {
   for (int32_t i = 0; i < mesh_.nn; ++i) {
     const int32_t r0 = pat_.row_ptr[i], deg = pat_.row_ptr[i + 1] - r0;
-    for (int a = 0; a < 3; ++a) {
-      const size_t start = 9 * (size_t)r0 + 3 * (size_t)a * deg;
-      for (int32_t q = 0; q < deg; ++q)
-        for (int b = 0; b < 3; ++b) vals[start + 3 * q + b] = bval[sell_addr(sell_ptr_.data(), i, q, 3 * a + b)];
+    for (int32_t q = 0; q < deg; ++q) {
+      const int32_t j = pat_.cols[r0 + q];
+      double blk[9];
+      if (mat_format_ == 0) {
+        for (int r = 0; r < 9; ++r) blk[r] = bval[sell_addr(sell_ptr_.data(), i, q, r)];
+      } else if (j >= i) {
+        for (int r = 0; r < 9; ++r) blk[r] = bval[sell_addr(usp_.data(), i, uslot_[r0 + q], r)];
+      } else {  // (i,j) = (j,i)^T
+        const auto jb = pat_.cols.begin() + pat_.row_ptr[j], je = pat_.cols.begin() + pat_.row_ptr[j + 1];
+        const int32_t qj = pat_.row_ptr[j] + (int32_t)(std::lower_bound(jb, je, i) - jb);
+        for (int a = 0; a < 3; ++a)
+          for (int c = 0; c < 3; ++c) blk[3 * a + c] = bval[sell_addr(usp_.data(), j, uslot_[qj], 3 * c + a)];
+      }
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) vals[9 * (size_t)r0 + 3 * (size_t)a * deg + 3 * q + c] = blk[3 * a + c];
     }
   }
 }
@@ -685,14 +741,14 @@ void Simulation::bsr_to_csr(const std::vector<double>& bval, double* vals) const
 void Simulation::eval_stiffness(double* vals) {
   StepCoeffs c{};
   launch("stiffness", 0.0, [&] { launch_assemble(d_, md_, c, kAssembleRawK, stream_); });
-  std::vector<double> b(9 * 32 * (size_t)sell_slots_);
+  std::vector<double> b(bval_doubles_);
   GF_CUDA(cudaMemcpyAsync(b.data(), d_.bval, 8 * b.size(), cudaMemcpyDeviceToHost, stream_));
   synchronize();
   bsr_to_csr(b, vals);
 }
 
 void Simulation::last_system(double* vals, double* rhs) {
-  std::vector<double> b(9 * 32 * (size_t)sell_slots_);
+  std::vector<double> b(bval_doubles_);
   GF_CUDA(cudaMemcpyAsync(b.data(), d_.bval, 8 * b.size(), cudaMemcpyDeviceToHost, stream_));
   if (rhs) GF_CUDA(cudaMemcpyAsync(rhs, d_.rhs, 24 * (size_t)mesh_.nn, cudaMemcpyDeviceToHost, stream_));
   synchronize();
@@ -716,7 +772,7 @@ void Simulation::eval_screening(double* screening, double* sigma_f6, uint8_t* de
 void Simulation::spmv(const double* x, double* y) {
   const size_t nd = 3 * (size_t)mesh_.nn;
   GF_CUDA(cudaMemcpyAsync(d_.z, x, 8 * nd, cudaMemcpyHostToDevice, stream_));
-  launch("spmv", 0.0, [&] { launch_spmv3(cg_, d_.z, d_.Ap, stream_); });
+  launch("spmv", 0.0, [&] { launch_spmv_fmt(cg_, d_.z, d_.Ap, mat_format_, stream_); });
   GF_CUDA(cudaMemcpyAsync(y, d_.Ap, 8 * nd, cudaMemcpyDeviceToHost, stream_));
   synchronize();
 }

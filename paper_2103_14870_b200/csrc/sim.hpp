@@ -84,6 +84,9 @@ class Simulation {
   NodePattern pat_;
   std::vector<int32_t> sell_ptr_;
   int64_t sell_slots_ = 0;
+  int mat_format_ = 1;
+  std::vector<int32_t> usp_, uslot_;
+  size_t bval_doubles_ = 0;
   gf_material mat_;
   gf_solver_config cfg_;
   MatDev md_{};

@@ -1,4 +1,4 @@
-"""Per-phase timing of the cooperative PCG kernel on the c3 system (GF_CG_TRACE). GPU box only."""
+"""Per-phase timing of the production PCG kernel on the c3 system (GF_CG_TRACE). GPU box only."""
 import ctypes as C, os, sys
 os.environ["GF_CG_TRACE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -11,17 +11,14 @@ for _ in range(4):
     st = sim.dynamic_step()
 buf = np.zeros(5000, np.uint64)
 g._check(g.lib().gf_sim_cg_trace(sim._h, buf.ctypes.data_as(C.POINTER(C.c_uint64))))
-t = buf[:2000].reshape(2, 200, 5).astype(np.float64)
 n = st.cg_iterations
-for b, name in [(0, "block0"), (1, "last")]:
-    d = np.diff(t[b, 1:n - 1], axis=1) / 1e3  # us: spmv_end-start? columns: [0->1 spmv, 1->2 reduceA, 2->3 phaseB, 3->4 reduceB]
-    it = (t[b, 2:n - 1, 0] - t[b, 1:n - 2, 0]) / 1e3
-    print(name, "iters", n, "us/iter %.2f" % it.mean(), "phases (spmv, redA, phaseB, redB) us:", np.round(d.mean(0), 2))
-buf = np.zeros(5000, np.uint64)
-g._check(g.lib().gf_sim_cg_trace(sim._h, buf.ctypes.data_as(C.POINTER(C.c_uint64))))
+t = buf[:1000].reshape(200, 5)[1:n - 1].astype(np.float64)
+d = np.diff(t, axis=1) / 1e3
+it = (t[1:, 0] - t[:-1, 0]) / 1e3
+print("iters", n, "us/iter %.2f" % it.mean(), "CTA0 phases [A work, A barrier+reduce, B work, B barrier+reduce] us:", np.round(d.mean(0), 2))
 nb = int((buf[2000:3000] > 0).sum())
-b_end = buf[2000:2000 + nb].astype(np.float64); a_end = buf[3000:3000 + nb].astype(np.float64)
+b_end = buf[2000:2000 + nb].astype(np.float64)
+a_end = buf[3000:3000 + nb].astype(np.float64)
 t0 = a_end.min()
-print("blocks", nb, "phaseA end spread (us): min 0 max %.2f" % ((a_end.max() - t0) / 1e3),
-      " phaseB end (us from first A end): min %.2f median %.2f max %.2f" % ((b_end.min() - t0) / 1e3, (np.median(b_end) - t0) / 1e3, (b_end.max() - t0) / 1e3))
-print("slowest phaseA blocks:", np.argsort(-a_end)[:8], " slowest phaseB blocks:", np.argsort(-b_end)[:8])
+print("CTAs", nb, "| phase-A end spread %.2f us | phase-B end (from first A end) min %.2f med %.2f max %.2f us" % (
+    (a_end.max() - t0) / 1e3, (b_end.min() - t0) / 1e3, (np.median(b_end) - t0) / 1e3, (b_end.max() - t0) / 1e3))
