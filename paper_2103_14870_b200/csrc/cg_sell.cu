@@ -47,13 +47,13 @@ __device__ __forceinline__ double lane_sum(double v) {  // fixed butterfly: same
 
 // every CTA sums all per-slice partials in the same order (thread stride, then a fixed block tree)
 template <int NV>
-__device__ __forceinline__ void sum_slices(const double* part, int ns, double (&out)[NV]) {
-  __shared__ double s_w[kWarpsPerCta][3];
+__device__ __forceinline__ void sum_slices(const double* part, int ns, double (&out)[NV], size_t qstride) {
+  __shared__ double s_w[kWarpsPerCta][4];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
     double x = 0.0;
-    for (int k = threadIdx.x; k < ns; k += blockDim.x) x += __ldcg(part + (size_t)q * ns + k);
+    for (int k = threadIdx.x; k < ns; k += blockDim.x) x += __ldcg(part + (size_t)q * qstride + k);
     x = lane_sum(x);
     if (lane == 0) s_w[w][q] = x;
   }
@@ -66,18 +66,18 @@ __device__ __forceinline__ void sum_slices(const double* part, int ns, double (&
   __syncthreads();
 }
 
-struct Sched {  // dynamic slice hand-out; each warp overshoots exactly once per phase
+struct Sched {  // dynamic work hand-out; each warp overshoots exactly once per phase
   unsigned long long* ctr;
   unsigned long long base;
-  unsigned long long stride;  // nslices + total warps
-  __device__ __forceinline__ int next(int ns) const {
+  unsigned long long nwarps;
+  __device__ __forceinline__ int next(int n) const {
     unsigned long long t = 0;
     if ((threadIdx.x & 31) == 0) t = atomicAdd(ctr, 1ull);
     t = __shfl_sync(0xffffffffu, t, 0);
     const unsigned long long idx = t - base;
-    return idx < (unsigned long long)ns ? (int)idx : -1;
+    return idx < (unsigned long long)n ? (int)idx : -1;
   }
-  __device__ __forceinline__ void advance() { base += stride; }
+  __device__ __forceinline__ void advance(int n) { base += (unsigned long long)n + nwarps; }
 };
 
 // y = A p for one slice (lane = row); p_j gathered as fused ? fma(beta, pold_j, z_j) : src_j
@@ -178,8 +178,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // Symmetric format: slot (base | T<<31, j) of row i contributes A p_j (T = 0, upper block (i,j)) or A^T p_j
 // (T = 1, block (j,i) stored by row j); entry q at vals[base + 32 q]. Half the matrix bytes of the full format;
 // the upper blocks (~62 MB at c3) and the CG vectors can stay resident in the 126 MB L2 across iterations.
-__device__ __forceinline__ void slice_spmv_sym(const CgLaunch& a, int sl, const double* src, const double* z,
-                                               double beta, bool fused, double acc[3]) {
+template <class G>
+__device__ __forceinline__ void slice_spmv_sym_g(const CgLaunch& a, int sl, const G& gat, double acc[3]) {
   const int lane = threadIdx.x & 31;
   const int k0 = __ldg(a.row_ptr + sl), k1 = __ldg(a.row_ptr + sl + 1);
   const int2* slots = reinterpret_cast<const int2*>(a.cols);
@@ -198,34 +198,107 @@ __device__ __forceinline__ void slice_spmv_sym(const CgLaunch& a, int sl, const 
         const size_t j = (size_t)sc[g].y;
         const bool tr = sc[g].x < 0;
         const size_t base = (size_t)(sc[g].x & 0x7fffffff);
-        double p0, p1, p2;
-        if (fused) {
-          p0 = __fma_rn(beta, ldv(src + 3 * j), ldv(z + 3 * j));
-          p1 = __fma_rn(beta, ldv(src + 3 * j + 1), ldv(z + 3 * j + 1));
-          p2 = __fma_rn(beta, ldv(src + 3 * j + 2), ldv(z + 3 * j + 2));
-        } else {
-          p0 = ldv(src + 3 * j);
-          p1 = ldv(src + 3 * j + 1);
-          p2 = ldv(src + 3 * j + 2);
-        }
+        const double3 p = gat(j);
         const double* v = a.vals + base;
         double m[9];
 #pragma unroll
         for (int q = 0; q < 9; ++q) m[q] = __ldcg(v + 32 * q);
         if (!tr) {
-          acc[0] = __fma_rn(m[0], p0, acc[0]); acc[0] = __fma_rn(m[1], p1, acc[0]); acc[0] = __fma_rn(m[2], p2, acc[0]);
-          acc[1] = __fma_rn(m[3], p0, acc[1]); acc[1] = __fma_rn(m[4], p1, acc[1]); acc[1] = __fma_rn(m[5], p2, acc[1]);
-          acc[2] = __fma_rn(m[6], p0, acc[2]); acc[2] = __fma_rn(m[7], p1, acc[2]); acc[2] = __fma_rn(m[8], p2, acc[2]);
+          acc[0] = __fma_rn(m[0], p.x, acc[0]); acc[0] = __fma_rn(m[1], p.y, acc[0]); acc[0] = __fma_rn(m[2], p.z, acc[0]);
+          acc[1] = __fma_rn(m[3], p.x, acc[1]); acc[1] = __fma_rn(m[4], p.y, acc[1]); acc[1] = __fma_rn(m[5], p.z, acc[1]);
+          acc[2] = __fma_rn(m[6], p.x, acc[2]); acc[2] = __fma_rn(m[7], p.y, acc[2]); acc[2] = __fma_rn(m[8], p.z, acc[2]);
         } else {
-          acc[0] = __fma_rn(m[0], p0, acc[0]); acc[0] = __fma_rn(m[3], p1, acc[0]); acc[0] = __fma_rn(m[6], p2, acc[0]);
-          acc[1] = __fma_rn(m[1], p0, acc[1]); acc[1] = __fma_rn(m[4], p1, acc[1]); acc[1] = __fma_rn(m[7], p2, acc[1]);
-          acc[2] = __fma_rn(m[2], p0, acc[2]); acc[2] = __fma_rn(m[5], p1, acc[2]); acc[2] = __fma_rn(m[8], p2, acc[2]);
+          acc[0] = __fma_rn(m[0], p.x, acc[0]); acc[0] = __fma_rn(m[3], p.y, acc[0]); acc[0] = __fma_rn(m[6], p.z, acc[0]);
+          acc[1] = __fma_rn(m[1], p.x, acc[1]); acc[1] = __fma_rn(m[4], p.y, acc[1]); acc[1] = __fma_rn(m[7], p.z, acc[1]);
+          acc[2] = __fma_rn(m[2], p.x, acc[2]); acc[2] = __fma_rn(m[5], p.y, acc[2]); acc[2] = __fma_rn(m[8], p.z, acc[2]);
         }
       }
     }
 #pragma unroll
     for (int g = 0; g < kGroup; ++g) sc[g] = sn[g];
   }
+}
+
+#ifndef GF_CG_R
+#define GF_CG_R 1
+#endif
+constexpr int kR = GF_CG_R;  // lanes per row in the symmetric phase-A SpMV (work unit = 32/kR rows of a slice)
+
+// kR lanes cooperate on one row (lane = r + (32/kR) t handles slots t, t+kR, ...; partial sums combined with a
+// fixed xor-shuffle tree): per-lane dependency chains are kR x shorter, so the phase tail (one unit) shrinks.
+template <class G>
+__device__ __forceinline__ int unit_spmv_sym(const CgLaunch& a, int unit, const G& gat, double acc[3]) {
+  constexpr int kRpu = 32 / kR;
+  const int lane = threadIdx.x & 31;
+  const int r = lane % kRpu, t = lane / kRpu;
+  const int sl = unit / kR, lr = (unit % kR) * kRpu + r;
+  const int k0 = __ldg(a.row_ptr + sl), k1 = __ldg(a.row_ptr + sl + 1);
+  const int2* slots = reinterpret_cast<const int2*>(a.cols);
+  acc[0] = acc[1] = acc[2] = 0.0;
+  int2 sc[kGroup];
+#pragma unroll
+  for (int g = 0; g < kGroup; ++g) {
+    const int k = k0 + t + kR * g;
+    sc[g] = (k < k1) ? __ldg(slots + (size_t)k * 32 + lr) : make_int2(0, 0);
+  }
+  for (int kb = k0 + t; kb < k1; kb += kR * kGroup) {
+    int2 sn[kGroup];
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g) {
+      const int k = kb + kR * (kGroup + g);
+      sn[g] = (k < k1) ? __ldg(slots + (size_t)k * 32 + lr) : make_int2(0, 0);
+    }
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g) {
+      if (kb + kR * g < k1) {
+        const size_t j = (size_t)sc[g].y;
+        const bool tr = sc[g].x < 0;
+        const double3 p = gat(j);
+        const double* v = a.vals + (size_t)(sc[g].x & 0x7fffffff);
+        double m[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) m[q] = __ldcg(v + 32 * q);
+        if (!tr) {
+          acc[0] = __fma_rn(m[0], p.x, acc[0]); acc[0] = __fma_rn(m[1], p.y, acc[0]); acc[0] = __fma_rn(m[2], p.z, acc[0]);
+          acc[1] = __fma_rn(m[3], p.x, acc[1]); acc[1] = __fma_rn(m[4], p.y, acc[1]); acc[1] = __fma_rn(m[5], p.z, acc[1]);
+          acc[2] = __fma_rn(m[6], p.x, acc[2]); acc[2] = __fma_rn(m[7], p.y, acc[2]); acc[2] = __fma_rn(m[8], p.z, acc[2]);
+        } else {
+          acc[0] = __fma_rn(m[0], p.x, acc[0]); acc[0] = __fma_rn(m[3], p.y, acc[0]); acc[0] = __fma_rn(m[6], p.z, acc[0]);
+          acc[1] = __fma_rn(m[1], p.x, acc[1]); acc[1] = __fma_rn(m[4], p.y, acc[1]); acc[1] = __fma_rn(m[7], p.z, acc[1]);
+          acc[2] = __fma_rn(m[2], p.x, acc[2]); acc[2] = __fma_rn(m[5], p.y, acc[2]); acc[2] = __fma_rn(m[8], p.z, acc[2]);
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g) sc[g] = sn[g];
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int o = kRpu; o < 32; o <<= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+  return (t == 0) ? sl * 32 + lr : -1;  // owner lane of the row (or -1)
+}
+
+struct GatherP {  // p_j = fused ? fma(beta, pold_j, z_j) : src_j
+  const double* src;
+  const double* z;
+  double beta;
+  bool fused;
+  __device__ __forceinline__ double3 operator()(size_t j) const {
+    if (fused)
+      return make_double3(__fma_rn(beta, ldv(src + 3 * j), ldv(z + 3 * j)),
+                          __fma_rn(beta, ldv(src + 3 * j + 1), ldv(z + 3 * j + 1)),
+                          __fma_rn(beta, ldv(src + 3 * j + 2), ldv(z + 3 * j + 2)));
+    return make_double3(ldv(src + 3 * j), ldv(src + 3 * j + 1), ldv(src + 3 * j + 2));
+  }
+};
+
+// Symmetric format: slot (base | T<<31, j) of row i contributes A p_j (T = 0, upper block (i,j)) or A^T p_j
+// (T = 1, block (j,i) stored by row j); entry q at vals[base + 32 q]. Half the matrix bytes of the full format;
+// the upper blocks (~62 MB at c3) and the CG vectors can stay resident in the 126 MB L2 across iterations.
+__device__ __forceinline__ void slice_spmv_sym(const CgLaunch& a, int sl, const double* src, const double* z,
+                                               double beta, bool fused, double acc[3]) {
+  slice_spmv_sym_g(a, sl, GatherP{src, z, beta, fused}, acc);
 }
 
 template <bool kStream, int kFmt>
@@ -240,9 +313,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
   cg::grid_group grid = cg::this_grid();
   const CgLaunch& a = sa.a;
   const int ns = a.nslices, nrows = a.nrows, lane = threadIdx.x & 31;
-  Sched sch{sa.ctr, 0ull, (unsigned long long)ns + (unsigned long long)((gridDim.x * blockDim.x) >> 5)};
+  Sched sch{sa.ctr, 0ull, (unsigned long long)((gridDim.x * blockDim.x) >> 5)};
   int parity = 0;
-  auto part = [&](int q) { return sa.slice_part + ((size_t)parity * 3 + q) * ns; };
+  auto part = [&](int q) { return sa.slice_part + ((size_t)parity * 4 + q) * (4 * (size_t)ns); };
 
   // setup (sparse.cpp:145-157): r = b - A x, z = D^-1 r, p = z; partials b.b, r.z, r.r per slice
   for (int sl = sch.next(ns); sl >= 0; sl = sch.next(ns)) {
@@ -274,10 +347,10 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       part(2)[sl] = rr;
     }
   }
-  sch.advance();
+  sch.advance(ns);
   grid.sync();
   double tot3[3];
-  sum_slices<3>(part(0), ns, tot3);
+  sum_slices<3>(part(0), ns, tot3, 4 * (size_t)ns);
   parity ^= 1;
   const double bnorm = sqrt(tot3[0]);
   double rz = tot3[1], rr = tot3[2];
@@ -296,12 +369,18 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       const bool fused = it > 0;
       SELL_STAMP(it, 0);
       // ---- phase A: q = A p
-      for (int sl = sch.next(ns); sl >= 0; sl = sch.next(ns)) {
+      const int nunits = kFmt == 1 ? ns * kR : ns;
+      for (int sl = sch.next(nunits); sl >= 0; sl = sch.next(nunits)) {
         double acc[3];
-        spmv_fmt<kStream, kFmt>(a, sl, pcur, a.z, beta, fused, acc);
-        const int row = sl * 32 + lane;
+        int row;
+        if constexpr (kFmt == 1) {
+          row = unit_spmv_sym(a, sl, GatherP{pcur, a.z, beta, fused}, acc);
+        } else {
+          spmv_fmt<kStream, kFmt>(a, sl, pcur, a.z, beta, fused, acc);
+          row = sl * 32 + lane;
+        }
         double pq = 0.0;
-        if (row < nrows) {
+        if (row >= 0 && row < nrows) {
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const size_t dof = 3 * (size_t)row + c;
@@ -314,7 +393,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
         pq = lane_sum(pq);
         if (lane == 0) part(0)[sl] = pq;
       }
-      sch.advance();
+      sch.advance(nunits);
       SELL_STAMP(it, 1);
       SELL_BLOCK_STAMP(it, 3000);
       if (fused) {
@@ -324,7 +403,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       }
       grid.sync();
       double pap[1];
-      sum_slices<1>(part(0), ns, pap);
+      sum_slices<1>(part(0), nunits, pap, 4 * (size_t)ns);
       parity ^= 1;
       SELL_STAMP(it, 2);
       if (pap[0] <= 0.0) {  // sparse.cpp:160-168
@@ -361,12 +440,12 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
           part(1)[sl] = rzp;
         }
       }
-      sch.advance();
+      sch.advance(ns);
       SELL_STAMP(it, 3);
       SELL_BLOCK_STAMP(it, 2000);
       grid.sync();
       double red2[2];
-      sum_slices<2>(part(0), ns, red2);
+      sum_slices<2>(part(0), ns, red2, 4 * (size_t)ns);
       parity ^= 1;
       SELL_STAMP(it, 4);
       rr = red2[0];
@@ -394,6 +473,218 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
   }
 }
 
+
+// ---------------------------------------------------------------- single-barrier PCG (default)
+// Chronopoulos-Gear form of the same Jacobi-PCG: one fused pass and ONE grid barrier per iteration.
+//   given alpha_k, beta_k (identical in every CTA) and r_k, w_k = A z_k, s_{k-1}, p_{k-1}:
+//     s_k = w_k + beta_k s_{k-1} (= A p_k),  p_k = z_k + beta_k p_{k-1},  x += alpha_k p_k,
+//     r_{k+1} = r_k - alpha_k s_k,  z_{k+1} = D^-1 r_{k+1},  w_{k+1} = A z_{k+1}
+//   where every gathered z_{k+1,j} is recomputed from (r_k, w_k, s_{k-1}, D^-1)_j with the same FMA sequence the
+//   row owner uses (bit-identical), all four vectors double-buffered; per slice: partials r.z, z.w, r.r.
+//   After the barrier: rr -> the reference's ||r||/||b|| <= tol test (sparse.cpp:172-178);
+//   beta = rz'/rz, eta = zw' - beta rz'/alpha = (p_{k+1}, A p_{k+1}) -> the pAp <= 0 exit (sparse.cpp:160-168);
+//   alpha = rz'/eta. Mathematically identical iterates to cg_solve; rounding differs at the 1e-16 level.
+struct Cg1Vec {
+  const double* r;   // r_k
+  const double* w;   // w_k
+  const double* s;   // s_{k-1}
+  const double* dinv;
+  double alpha, beta;
+  __device__ __forceinline__ double znew(size_t d) const {
+    const double sk = __fma_rn(beta, ldv(s + d), ldv(w + d));
+    const double r1 = __fma_rn(-alpha, sk, ldv(r + d));
+    return __ldg(dinv + d) * r1;
+  }
+  __device__ __forceinline__ double3 operator()(size_t j) const {
+    return make_double3(znew(3 * j), znew(3 * j + 1), znew(3 * j + 2));
+  }
+};
+struct GatherZ0 {  // z_0 = D^-1 r_0
+  const double* r;
+  const double* dinv;
+  __device__ __forceinline__ double3 operator()(size_t j) const {
+    return make_double3(__ldg(dinv + 3 * j) * ldv(r + 3 * j), __ldg(dinv + 3 * j + 1) * ldv(r + 3 * j + 1),
+                        __ldg(dinv + 3 * j + 2) * ldv(r + 3 * j + 2));
+  }
+};
+struct GatherX {
+  const double* x;
+  __device__ __forceinline__ double3 operator()(size_t j) const {
+    return make_double3(ldv(x + 3 * j), ldv(x + 3 * j + 1), ldv(x + 3 * j + 2));
+  }
+};
+
+struct Cg1Args {
+  CgLaunch a;
+  unsigned long long* ctr;
+  double* slice_part;   // 2 parities x 4 values x nslices
+  double* r2;           // second buffers (3N each): r, w, s, p are double-buffered
+  double* w0;
+  double* w1;
+  double* s0;
+  double* s1;
+};
+
+__global__ void __launch_bounds__(kThreads) k_pcg_cg1(Cg1Args ca) {
+  cg::grid_group grid = cg::this_grid();
+  const CgLaunch& a = ca.a;
+  const int ns = a.nslices, nrows = a.nrows, lane = threadIdx.x & 31;
+  Sched sch{ca.ctr, 0ull, (unsigned long long)((gridDim.x * blockDim.x) >> 5)};
+  int parity = 0;
+  auto part = [&](int q) { return ca.slice_part + ((size_t)parity * 4 + q) * (4 * (size_t)ns); };
+  double* rb[2] = {a.r, ca.r2};
+  double* wb[2] = {ca.w0, ca.w1};
+  double* sb[2] = {ca.s0, ca.s1};
+  double* pb[2] = {a.p0, a.p1};
+
+  // setup 1: r0 = b - A x0; zero s_{-1}, p_{-1}; partial b.b
+  for (int sl = sch.next(ns); sl >= 0; sl = sch.next(ns)) {
+    double acc[3];
+    slice_spmv_sym_g(a, sl, GatherX{a.x}, acc);
+    const int row = sl * 32 + lane;
+    double bb = 0.0;
+    if (row < nrows) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const size_t d = 3 * (size_t)row + c;
+        const double bi = a.b[d];
+        rb[0][d] = bi - acc[c];
+        sb[0][d] = 0.0;
+        pb[0][d] = 0.0;
+        bb = __fma_rn(bi, bi, bb);
+      }
+    }
+    bb = lane_sum(bb);
+    if (lane == 0) part(3)[sl] = bb;
+  }
+  sch.advance(ns);
+  grid.sync();
+  // setup 2: w0 = A z0; partials r0.z0, z0.w0, r0.r0
+  for (int sl = sch.next(ns); sl >= 0; sl = sch.next(ns)) {
+    double acc[3];
+    slice_spmv_sym_g(a, sl, GatherZ0{rb[0], a.dinv}, acc);
+    const int row = sl * 32 + lane;
+    double rz = 0.0, zw = 0.0, rr = 0.0;
+    if (row < nrows) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const size_t d = 3 * (size_t)row + c;
+        const double ri = ldv(rb[0] + d);
+        const double zi = __ldg(a.dinv + d) * ri;
+        wb[0][d] = acc[c];
+        rz = __fma_rn(ri, zi, rz);
+        zw = __fma_rn(zi, acc[c], zw);
+        rr = __fma_rn(ri, ri, rr);
+      }
+    }
+    rz = lane_sum(rz);
+    zw = lane_sum(zw);
+    rr = lane_sum(rr);
+    if (lane == 0) {
+      part(0)[sl] = rz;
+      part(1)[sl] = zw;
+      part(2)[sl] = rr;
+    }
+  }
+  sch.advance(ns);
+  grid.sync();
+  double t4[4];
+  sum_slices<4>(part(0), ns, t4, 4 * (size_t)ns);
+  parity ^= 1;
+  const double bnorm = sqrt(t4[3]);
+  double rz = t4[0], eta = t4[1], rr = t4[2];
+  int iterations = 0, converged = 0, negcurv = 0;
+  double relres = 0.0;
+  int cur = 0;
+  if (bnorm == 0.0) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * (size_t)nrows; i += (size_t)gridDim.x * blockDim.x)
+      a.x[i] = 0.0;
+    converged = 1;
+  } else {
+    double beta = 0.0;
+    bool done = false;
+    for (int it = 0; it < a.max_iters; ++it) {
+      if (eta <= 0.0) {  // (p_it, A p_it) <= 0  (sparse.cpp:160-168)
+        negcurv = eta < 0.0;
+        iterations = it;
+        relres = sqrt(rr) / bnorm;
+        converged = relres <= a.tol;
+        done = true;
+        break;
+      }
+      const double alpha = rz / eta;
+      SELL_STAMP(it, 0);
+      const int nx = cur ^ 1;
+      const Cg1Vec gv{rb[cur], wb[cur], sb[cur], a.dinv, alpha, beta};
+      for (int sl = sch.next(ns); sl >= 0; sl = sch.next(ns)) {
+        double acc[3];
+        slice_spmv_sym_g(a, sl, gv, acc);
+        const int row = sl * 32 + lane;
+        double prz = 0.0, pzw = 0.0, prr = 0.0;
+        if (row < nrows) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const size_t d = 3 * (size_t)row + c;
+            const double rk = ldv(rb[cur] + d), wk = ldv(wb[cur] + d), sprev = ldv(sb[cur] + d);
+            const double di = __ldg(a.dinv + d);
+            const double sk = __fma_rn(beta, sprev, wk);                 // s_k = w_k + beta s_{k-1}
+            const double pk = __fma_rn(beta, ldv(pb[cur] + d), di * rk);  // p_k = z_k + beta p_{k-1}
+            a.x[d] = __fma_rn(alpha, pk, ldv(a.x + d));
+            const double r1 = __fma_rn(-alpha, sk, rk);                  // identical to Cg1Vec::znew
+            const double z1 = di * r1;
+            sb[nx][d] = sk;
+            pb[nx][d] = pk;
+            rb[nx][d] = r1;
+            wb[nx][d] = acc[c];
+            prz = __fma_rn(r1, z1, prz);
+            pzw = __fma_rn(z1, acc[c], pzw);
+            prr = __fma_rn(r1, r1, prr);
+          }
+        }
+        prz = lane_sum(prz);
+        pzw = lane_sum(pzw);
+        prr = lane_sum(prr);
+        if (lane == 0) {
+          part(0)[sl] = prz;
+          part(1)[sl] = pzw;
+          part(2)[sl] = prr;
+        }
+      }
+      sch.advance(ns);
+      SELL_STAMP(it, 1);
+      SELL_BLOCK_STAMP(it, 3000);
+      grid.sync();
+      double t3[3];
+      sum_slices<3>(part(0), ns, t3, 4 * (size_t)ns);
+      parity ^= 1;
+      SELL_STAMP(it, 2);
+      cur = nx;
+      rr = t3[2];
+      iterations = it + 1;
+      const double rnorm = sqrt(rr);
+      if (rnorm / bnorm <= a.tol) {
+        relres = rnorm / bnorm;
+        converged = 1;
+        done = true;
+        break;
+      }
+      beta = t3[0] / rz;
+      eta = t3[1] - beta * t3[0] / alpha;
+      rz = t3[0];
+    }
+    if (!done) {
+      relres = sqrt(rr) / bnorm;
+      converged = relres <= a.tol;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.out[0] = iterations;
+    a.out[1] = converged;
+    a.out[2] = negcurv;
+    a.out[3] = relres;
+  }
+}
+
 int g_grid = 0;
 
 }  // namespace
@@ -407,6 +698,18 @@ int pcg_sell_grid() {
     g_grid = sms * (per > 0 ? per : 1);
   }
   return g_grid;
+}
+
+void launch_pcg_cg1(const CgLaunch& a, unsigned long long* ctr, double* slice_part, double* extra, cudaStream_t s) {
+  const size_t n = 3 * (size_t)a.nrows;
+  Cg1Args ca{a, ctr, slice_part, extra, extra + n, extra + 2 * n, extra + 3 * n, extra + 4 * n};
+  cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s);
+  void* args[] = {&ca};
+  const cudaError_t err = cudaLaunchCooperativeKernel((const void*)k_pcg_cg1, pcg_sell_grid(), kThreads, args, 0, s);
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    throw std::runtime_error(std::string("cooperative CG launch failed: ") + cudaGetErrorString(err));
+  }
 }
 
 void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_part, cudaStream_t s, int mat_format) {

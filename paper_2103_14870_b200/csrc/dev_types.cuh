@@ -170,6 +170,8 @@ void launch_spmv3(const CgLaunch& a, const double* xin, double* y, cudaStream_t 
 // ---- cg_sell.cu (production solver on the SELL-32 matrix) ----
 int pcg_sell_grid();
 void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_part, cudaStream_t s, int mat_format);
+// single-barrier (Chronopoulos-Gear) PCG on the symmetric format; extra = 5 x 3N doubles (r2, w0, w1, s0, s1)
+void launch_pcg_cg1(const CgLaunch& a, unsigned long long* ctr, double* slice_part, double* extra, cudaStream_t s);
 void launch_spmv_fmt(const CgLaunch& a, const double* xin, double* y, int mat_format, cudaStream_t s);
 // ---- misc.cu ----
 void launch_bc_targets(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, double dt, cudaStream_t s);

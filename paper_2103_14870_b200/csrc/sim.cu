@@ -407,7 +407,10 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   if (const char* e = std::getenv("GF_CG_MAP")) cg_.mapping = std::atoi(e);
   if (const char* e = std::getenv("GF_CG_KERNEL")) cg_kernel_ = std::atoi(e);
   d_ctr_ = (unsigned long long*)zeros(64);
-  d_slice_part_ = (double*)zeros(8 * 2 * 3 * (size_t)d_.nslices);
+  d_slice_part_ = (double*)zeros(8 * 2 * 4 * 4 * (size_t)d_.nslices);
+  d_cg_extra_ = (double*)zeros(8 * 5 * 3 * (size_t)nn);
+  cg_algo_ = 0;  // the single-barrier variant (1) measured slower at c3: 2.98 vs 2.73 ms/step
+  if (const char* e = std::getenv("GF_CG_ALGO")) cg_algo_ = std::atoi(e);
   if (std::getenv("GF_CG_TRACE")) cg_.trace = (unsigned long long*)zeros(8 * 5000);
   cg_.tol = cfg.cg_tol;
   GF_CUDA(cudaStreamSynchronize(stream_));
@@ -542,7 +545,8 @@ void Simulation::upload_bc_step(double t, double dt) {
 }
 
 void Simulation::launch_cg() {
-  if (cg_kernel_ == 0 || mat_format_ == 1) launch_pcg_sell(cg_, d_ctr_, d_slice_part_, stream_, mat_format_);
+  if (mat_format_ == 1 && cg_algo_ == 1) launch_pcg_cg1(cg_, d_ctr_, d_slice_part_, d_cg_extra_, stream_);
+  else if (cg_kernel_ == 0 || mat_format_ == 1) launch_pcg_sell(cg_, d_ctr_, d_slice_part_, stream_, mat_format_);
   else launch_pcg3(cg_, stream_);
 }
 

@@ -105,6 +105,8 @@ class Simulation {
   int cg_kernel_ = 0;  // 0: dynamic-schedule SELL kernel (cg_sell.cu), 1: static kernel (cg.cu)
   unsigned long long* d_ctr_ = nullptr;
   double* d_slice_part_ = nullptr;
+  double* d_cg_extra_ = nullptr;
+  int cg_algo_ = 0;  // 0: two-barrier PCG (default), 1: single-barrier Chronopoulos-Gear PCG (symmetric format)
   std::vector<void*> allocs_;
   int32_t* d_fixed_nodes_ = nullptr;
   BcStep* d_bcstep_ = nullptr;
