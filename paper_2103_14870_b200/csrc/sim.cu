@@ -508,16 +508,14 @@ std::vector<gf_kernel_time> Simulation::kernel_times() {
 
 // ---------------------------------------------------------------- damage pass (solver.cpp:90-103)
 void Simulation::run_damage(bool relabel, bool keep_values, bool chi) {
-  const double N = mesh_.nn, T = mesh_.nt, E = mesh_.ne;
+  // algorithmic bytes: SURVEY.md §8(d) B_D = 16n + 128T + 10E + 12S + 4 n_new (n = 3N dofs), split by kernel
+  const double n = 3.0 * mesh_.nn, T = mesh_.nt, E = mesh_.ne;
   const bool local = mat_.r_d <= 0.0;
-  launch("tet_stress", 48 * N + (16 + 72 + 24 + 48 + 48 + 1) * T + 8 * E + (local ? 16 * E : 0),
-         [&] { launch_tet_stress(d_, md_, local, stream_); });
-  if (!local)
-    launch("nonlocal", 48 * N + (16 + 24 + 1 + 8 + 48) * T + 12.0 * nl_entries_ + 24 * E,
-           [&] { launch_nonlocal(d_, stream_); });
+  launch("tet_stress", 16 * n + 112 * T + 8 * E, [&] { launch_tet_stress(d_, md_, local, stream_); });
+  if (!local) launch("nonlocal", 12.0 * nl_entries_, [&] { launch_nonlocal(d_, stream_); });
   GF_CUDA(cudaMemsetAsync(d_.newly_count, 0, 4, stream_));
-  launch("relabel", 18 * E, [&] { launch_relabel(d_, mat_.sigma_thres, relabel, keep_values, stream_); });
-  if (chi) launch("chi", (24 + 1 + 48 + 16) * T + E, [&] { launch_chi(d_, md_, stream_); });
+  launch("relabel", 2 * E, [&] { launch_relabel(d_, mat_.sigma_thres, relabel, keep_values, stream_); });
+  if (chi) launch("chi", 16 * T, [&] { launch_chi(d_, md_, stream_); });
 }
 
 std::vector<int32_t> Simulation::damage_pass() {
@@ -606,11 +604,10 @@ gf_step_stats Simulation::dynamic_step() {
   c.rhs_kv_scale = dt * mat_.damp_stiff_coeff + dt * dt;
   c.kscale = dt * mat_.damp_stiff_coeff + dt * dt;
   c.mscale = 1.0 + dt * mat_.damp_mass_coeff;
-  const double N = mesh_.nn, T = mesh_.nt, NB = pat_.cols.size();
+  // algorithmic bytes: SURVEY.md §8(d) B_F = 16n + 104T + 8Z (n = 3N dofs, Z scalar nonzeros)
+  const double n = 3.0 * mesh_.nn, T = mesh_.nt, Z = 9.0 * pat_.cols.size();
   d_.fint_out = nullptr;
-  launch("assemble", (24 + 4 + 4 + 24 + 8 + 4 + 24 + 24 + 24) * N + (16 + 72 + 8 + 8 + 16 + 16) * T +
-                         (72 + 4) * NB + (24 + 24 + 24) * N,
-         [&] { launch_assemble(d_, md_, c, kAssembleSystem, stream_); });
+  launch("assemble", 16 * n + 104 * T + 8 * Z, [&] { launch_assemble(d_, md_, c, kAssembleSystem, stream_); });
 
   // solve_linear (solver.cpp:105-136): first attempt, 4x retry, then cumulative diagonal shifts
   cg_.max_iters = cfg_.cg_max_iters;
@@ -619,9 +616,10 @@ gf_step_stats Simulation::dynamic_step() {
   GF_CUDA(cudaMemcpyAsync(h_stats_ + 4, d_load_, 8, cudaMemcpyDeviceToHost, stream_));
   GF_CUDA(cudaMemcpyAsync(h_stats_ + 5, d_.newly_count, 4, cudaMemcpyDeviceToHost, stream_));
   synchronize();
-  const double cg_bytes_per_iter = (72 + 4) * NB + 4 * (N + 1) + 240 * N;  // algorithmic (no SELL padding)
+  // SURVEY.md §8(d) B_CG = 12Z + 4(n+1) + 56n per PCG iteration (the reference's scalar-CSR SpMV + vectors)
+  const double cg_bytes_per_iter = 12 * Z + 4 * (n + 1) + 56 * n;
   auto account = [&](double iters) {
-    if (profiling_) ktimes_["pcg"].bytes += iters * cg_bytes_per_iter + 200 * N;
+    if (profiling_) ktimes_["pcg"].bytes += iters * cg_bytes_per_iter;
   };
   int32_t newly = 0;
   std::memcpy(&newly, h_stats_ + 5, 4);
@@ -655,7 +653,7 @@ gf_step_stats Simulation::dynamic_step() {
       throw SolveError(msg.str());
     }
   }
-  launch("integrate", 24.0 * 5 * N, [&] { launch_integrate(d_, dt, stream_); });
+  launch("integrate", 40 * n, [&] { launch_integrate(d_, dt, stream_); });  // B_int = 40n
   time_ = t + dt;
   st.residual = 0.0;
   return st;
