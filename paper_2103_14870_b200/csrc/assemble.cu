@@ -142,9 +142,12 @@ __device__ __forceinline__ double warp_sum(double v) {
 template <int kMode>
 __global__ void __launch_bounds__(32 * kWarps, 4) k_assemble(DevData d, MatDev m, StepCoeffs sc) {
   constexpr bool kBlocks = kMode != kAssembleForcesOnly;
-  __shared__ double s_blk[kBlocks ? kWarps : 1][32 * 36];
+  extern __shared__ double s_dyn[];  // kBlocks: s_blk[kWarps][32 * 36] (dynamic: > 48 KB static limit)
+  double(*s_blk)[32 * 36] = reinterpret_cast<double(*)[32 * 36]>(s_dyn);
   __shared__ double s_row[kBlocks ? kWarps : 1][kMaxDeg * 9];
   __shared__ double s_frc[kWarps][32][3];
+  __shared__ int s_cptr[kBlocks ? kWarps : 1][kMaxDeg + 1];
+  __shared__ uint8_t s_item[kBlocks ? kWarps : 1][4 * kMaxValence];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kWarps + w;
   if (i >= d.nn) return;
@@ -175,11 +178,18 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_assemble(DevData d, MatDev m
   const bool fixed_i = __ldg(d.node_bc + i) >= 0;
   double kv[3] = {0.0, 0.0, 0.0}, corr[3] = {0.0, 0.0, 0.0};
   if (kBlocks) {
+    // the row's contribution lists (<= 4 * 32 items, <= 33 offsets) staged in shared memory by one coalesced
+    // warp load each, so the reduction below touches only shared memory
+    const int ibase = __ldg(d.contrib_ptr + row0);
+    if (lane <= deg) s_cptr[w][lane] = __ldg(d.contrib_ptr + row0 + lane) - ibase;
+    const int nitems = 4 * np;
+    for (int k = lane; k < nitems; k += 32) s_item[w][k] = __ldg(d.contrib_item + ibase + k);
+    __syncwarp();
     for (int o = lane; o < 9 * deg; o += 32) {
       const int c = o / 9, q = o - 9 * c;
-      const int it0 = __ldg(d.contrib_ptr + row0 + c), it1 = __ldg(d.contrib_ptr + row0 + c + 1);
+      const int it0 = s_cptr[w][c], it1 = s_cptr[w][c + 1];
       double sum = 0.0;
-      for (int it = it0; it < it1; ++it) sum += s_blk[w][9 * (int)__ldg(d.contrib_item + it) + q];
+      for (int it = it0; it < it1; ++it) sum += s_blk[w][9 * (int)s_item[w][it] + q];
       s_row[w][o] = sum;
     }
     __syncwarp();
@@ -312,8 +322,15 @@ __global__ void __launch_bounds__(256) k_energy(DevData d, MatDev m, double* par
 
 void launch_assemble(const DevData& d, const MatDev& m, const StepCoeffs& c, int mode, cudaStream_t s) {
   const int grid = (d.nn + kWarps - 1) / kWarps;
-  if (mode == kAssembleSystem) k_assemble<kAssembleSystem><<<grid, 32 * kWarps, 0, s>>>(d, m, c);
-  else if (mode == kAssembleRawK) k_assemble<kAssembleRawK><<<grid, 32 * kWarps, 0, s>>>(d, m, c);
+  constexpr int kDyn = kWarps * 32 * 36 * sizeof(double);
+  static bool attr = [] {
+    cudaFuncSetAttribute(k_assemble<kAssembleSystem>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+    cudaFuncSetAttribute(k_assemble<kAssembleRawK>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+    return true;
+  }();
+  (void)attr;
+  if (mode == kAssembleSystem) k_assemble<kAssembleSystem><<<grid, 32 * kWarps, kDyn, s>>>(d, m, c);
+  else if (mode == kAssembleRawK) k_assemble<kAssembleRawK><<<grid, 32 * kWarps, kDyn, s>>>(d, m, c);
   else k_assemble<kAssembleForcesOnly><<<grid, 32 * kWarps, 0, s>>>(d, m, c);
 }
 

@@ -50,10 +50,20 @@ template <int NV>
 __device__ __forceinline__ void sum_slices(const double* part, int ns, double (&out)[NV], size_t qstride) {
   __shared__ double s_w[kWarpsPerCta][4];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int kB = 8;  // loads issued back to back per batch (one L2 round trip per batch, not per element)
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
     double x = 0.0;
-    for (int k = threadIdx.x; k < ns; k += blockDim.x) x += __ldcg(part + (size_t)q * qstride + k);
+    for (int k0 = 0; k0 < ns; k0 += kB * (int)blockDim.x) {
+      double v[kB];
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const int k = k0 + b * (int)blockDim.x + (int)threadIdx.x;
+        v[b] = (k < ns) ? __ldcg(part + (size_t)q * qstride + k) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < kB; ++b) x += v[b];
+    }
     x = lane_sum(x);
     if (lane == 0) s_w[w][q] = x;
   }
@@ -165,7 +175,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define SELL_STAMP(k, point)                                                          \
   do {                                                                                \
     if (a.trace && threadIdx.x == 0 && blockIdx.x == 0 && (k) < 200)                 \
-      a.trace[(k) * 5 + (point)] = gtimer();                                         \
+      a.trace[(k) * 8 + (point)] = gtimer();                                         \
   } while (0)
 #define SELL_BLOCK_STAMP(k, slot)                                                     \
   do {                                                                                \
@@ -401,8 +411,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
         pcur = pnext;
         pnext = t;
       }
-      grid.sync();
       double pap[1];
+      grid.sync();
+      SELL_STAMP(it, 5);
       sum_slices<1>(part(0), nunits, pap, 4 * (size_t)ns);
       parity ^= 1;
       SELL_STAMP(it, 2);
@@ -443,8 +454,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       sch.advance(ns);
       SELL_STAMP(it, 3);
       SELL_BLOCK_STAMP(it, 2000);
-      grid.sync();
       double red2[2];
+      grid.sync();
+      SELL_STAMP(it, 6);
       sum_slices<2>(part(0), ns, red2, 4 * (size_t)ns);
       parity ^= 1;
       SELL_STAMP(it, 4);

@@ -12,10 +12,11 @@ for _ in range(4):
 buf = np.zeros(5000, np.uint64)
 g._check(g.lib().gf_sim_cg_trace(sim._h, buf.ctypes.data_as(C.POINTER(C.c_uint64))))
 n = st.cg_iterations
-t = buf[:1000].reshape(200, 5)[1:n - 1].astype(np.float64)
-d = np.diff(t, axis=1) / 1e3
+t = buf[:1600].reshape(200, 8)[1:n - 1].astype(np.float64)
 it = (t[1:, 0] - t[:-1, 0]) / 1e3
-print("iters", n, "us/iter %.2f" % it.mean(), "CTA0 phases [A work, A barrier+reduce, B work, B barrier+reduce] us:", np.round(d.mean(0), 2))
+us = lambda a, b: np.round(((t[:, b] - t[:, a]) / 1e3).mean(), 2)
+print("iters", n, "us/iter %.2f" % it.mean(), "| CTA0: A work", us(0, 1), "A wait+barrier", us(1, 5), "A reduce", us(5, 2),
+      "B work", us(2, 3), "B wait+barrier", us(3, 6), "B reduce", us(6, 4))
 nb = int((buf[2000:3000] > 0).sum())
 b_end = buf[2000:2000 + nb].astype(np.float64)
 a_end = buf[3000:3000 + nb].astype(np.float64)
