@@ -352,3 +352,132 @@ def test_damage_pass_bit_exact_c3_full_size():
     assert np.array_equal(got_new, ref_new)
     assert np.array_equal(gs.state().edge_damage, os_.get_state()["zeta"])
     assert same_bits_or_zero(gs.state().element_chi, os_.get_state()["chi"])
+
+
+# ---------------------------------------------------------------- feature coverage vs the oracle
+def _pair_custom(mesh_args, mat_args, cfg, bcs=(), colliders=(), u0=None, v0=None):
+    gm = g.make_box_mesh(*mesh_args)
+    om = o.Mesh.make_box(*mesh_args)
+    gmat = g.MaterialParams.from_youngs(*mat_args)
+    omat = o.material_from_youngs(*mat_args)
+    gcfg = g.SolverConfig(**cfg)
+    ocfg = o.solver_config(**cfg)
+    gb = []
+    for b in bcs:
+        if b.get("kind") == "rotate":
+            gb.append(g.BoundaryCondition(nodes=b["nodes"], kind="rotate", angle=g.Schedule3(b["times"], b["values"]),
+                                          axis_point=b["axis_point"], axis_dir=b["axis_dir"]))
+        else:
+            gb.append(g.BoundaryCondition(nodes=b["nodes"], translation=g.Schedule3(b["times"], b["values"])))
+    gc = [g.Collider(kind=c["kind"], center=g.Schedule3(c.get("times", ()), c.get("values", ())),
+                     radius=c.get("radius", 0.0), point=c.get("point", (0, 0, 0)), normal=c.get("normal", (0, 0, 1)),
+                     stiffness=c["stiffness"], restitution=c.get("restitution", 0.0), friction=c.get("friction", 0.0))
+          for c in colliders]
+    gs = g.Simulation(gm, gmat, gcfg, gb, gc)
+    os_ = o.Sim(om, omat, ocfg, list(bcs), list(colliders))
+    if u0 is not None or v0 is not None:
+        os_.set_state(u=u0, v=v0)
+        gs.set_state(displacements=u0, velocities=v0)
+    return gs, os_, om
+
+
+def _compare_steps(gs, os_, om, steps, tol=TRAJ_TOL):
+    scale = np.abs(om.arrays()["rest"]).max()
+    loads = []
+    for _ in range(steps):
+        a = os_.dynamic_step()
+        b = gs.dynamic_step()
+        assert a.newly_broken == b.newly_broken
+        assert b.load == pytest.approx(a.load, rel=1e-9, abs=1e-12)
+        loads.append(a.load)
+    ost, gst = os_.get_state(), gs.state()
+    assert np.array_equal(gst.edge_damage, ost["zeta"])
+    assert np.abs(gst.displacements - ost["u"]).max() / scale < tol
+    assert np.abs(gst.velocities - ost["v"]).max() <= tol * max(1.0, np.abs(ost["v"]).max())
+    return loads
+
+
+def test_sphere_collider_moving_with_friction():  # collision.cpp:49-111 sphere branch + Schedule3::rate
+    col = dict(kind="sphere", times=[0.0, 1.0], values=[[0.05, 0.05, 0.13], [0.05, 0.05, 0.03]], radius=0.04,
+               stiffness=1e5, restitution=0.5, friction=0.3)
+    gs, os_, om = _pair_custom(((0.1, 0.1, 0.1), (4, 4, 4)), (1e6, 0.3, 1000, 1e9, 0, g.STVK),
+                               dict(dt=1e-3, collision_substeps=3), colliders=[col],
+                               v0=np.tile([0.01, -0.02, 0.0], (125, 1)))
+    loads = _compare_steps(gs, os_, om, 15)
+    assert max(loads) > 0
+
+
+def test_rotate_bc_and_rayleigh_damping():  # solver.cpp:22-29 rotate branch; solver.cpp:279-289 alpha/beta
+    om_tmp = o.Mesh.make_box((0.2, 0.1, 0.1), (4, 2, 2))
+    X = om_tmp.arrays()["rest"]
+    left = np.nonzero(X[:, 0] <= 1e-9)[0]
+    right = np.nonzero(X[:, 0] >= 0.2 - 1e-9)[0]
+    bcs = [dict(nodes=left, times=[0, 1], values=[[0, 0, 0], [0, 0, 0]]),
+           dict(kind="rotate", nodes=right, times=[0, 1], values=[[0, 0, 0], [np.pi, 0, 0]],
+                axis_point=(0.2, 0.05, 0.05), axis_dir=(1, 0, 0))]
+    mat = (1e6, 0.3, 1000, 1e9, 0, g.STABLE_NEO_HOOKEAN)
+    gmat = g.MaterialParams.from_youngs(*mat)
+    gmat.damp_mass_coeff, gmat.damp_stiff_coeff = 2.0, 1e-4
+    omat = o.material_from_youngs(*mat)
+    omat.damp_mass_coeff, omat.damp_stiff_coeff = 2.0, 1e-4
+    gm, om = g.make_box_mesh((0.2, 0.1, 0.1), (4, 2, 2)), o.Mesh.make_box((0.2, 0.1, 0.1), (4, 2, 2))
+    gb = [g.BoundaryCondition(nodes=left, translation=g.Schedule3([0, 1], [[0, 0, 0], [0, 0, 0]])),
+          g.BoundaryCondition(nodes=right, kind="rotate", angle=g.Schedule3([0, 1], [[0, 0, 0], [np.pi, 0, 0]]),
+                              axis_point=(0.2, 0.05, 0.05), axis_dir=(1, 0, 0))]
+    gs = g.Simulation(gm, gmat, g.SolverConfig(dt=1e-3), gb)
+    os_ = o.Sim(om, omat, o.solver_config(dt=1e-3), bcs)
+    _compare_steps(gs, os_, om, 12)
+    # pinned rotated nodes follow the schedule (same host formula, same device op order as the oracle)
+    assert np.array_equal(gs.state().displacements[right], os_.get_state()["u"][right])
+
+
+def test_cg_retry_and_shift_ladder_matches_oracle():  # solver.cpp:105-136
+    s = cf.scaled("c2", (4, 4, 4))
+    probe, _ = build_oracle(s)
+    k = probe.dynamic_step().cg_iterations
+    s.cg_max_iters = max(2, k // 3)  # first attempt fails, the 4x retry (continuing from x) succeeds
+    gs, os_, gm, om = pair(s)
+    for _ in range(3):
+        a = os_.dynamic_step()
+        b = gs.dynamic_step()
+        assert abs(a.cg_iterations - b.cg_iterations) <= 2
+    scale = np.abs(om.arrays()["rest"]).max()
+    assert np.abs(gs.state().displacements - os_.get_state()["u"]).max() / scale < 1e-6
+
+
+def test_solve_error_raised_like_the_reference():
+    s = cf.scaled("c2", (4, 4, 4))
+    s.cg_max_iters, s.cg_tol = 1, 1e-15
+    gs, os_, gm, om = pair(s)
+    with pytest.raises(o.SolveError):
+        os_.dynamic_step()
+    with pytest.raises(g.SolveError):
+        gs.dynamic_step()
+
+
+def test_gravity_external_load_and_substeps_trajectory():
+    s = cf.scaled("c1", (4, 4, 16), steps=20)
+    s.point_load = (s.point_load[0], (0.0, -500.0 / 8, 0.0))
+    s.gravity = (0.0, -9.81, 0.0)
+    worst, resyncs, _ = run_pair(s, s.steps)
+    assert worst < TRAJ_TOL
+
+
+def test_huge_radius_single_and_tetgen_meshes():
+    # r_d larger than the body: every tet averages over all tets (fracture.cpp:40-52), plus a TetGen-loaded mesh
+    s = cf.scaled("c3", (3, 3, 3))
+    s.r_d = 10.0
+    rng = np.random.default_rng(31)
+    gs, os_, gm, om = pair(s, rng, disp=0.2)
+    assert np.array_equal(gs.damage_pass(), os_.damage_pass())
+    node = "5 3 0 0\n1 0 0 0\n2 1 0 0\n3 0 1 0\n4 0 0 1\n5 1 1 1\n"
+    ele = "2 4 0\n1 1 2 3 4\n2 2 3 4 5\n"
+    gt, ot = g.load_tetgen(node, ele), o.Mesh.load_tetgen(node, ele)
+    mat = (1e6, 0.3, 1000, 10.0, 0.7, g.STVK)
+    sg = g.Simulation(gt, g.MaterialParams.from_youngs(*mat), g.SolverConfig(dt=1e-3))
+    so = o.Sim(ot, o.material_from_youngs(*mat), o.solver_config(dt=1e-3))
+    u = np.random.default_rng(2).uniform(-0.1, 0.1, (5, 3))
+    sg.set_state(displacements=u)
+    so.set_state(u=u)
+    assert np.array_equal(sg.damage_pass(), so.damage_pass())
+    assert same_bits_or_zero(sg.state().element_chi, so.get_state()["chi"])
