@@ -1641,10 +1641,13 @@ static Csr csr_from(int32_t n, const int32_t* row_ptr, const int32_t* cols, cons
   return A;
 }
 void or_spmv_csr(int32_t n, const int32_t* row_ptr, const int32_t* cols, const double* vals, const double* x,
-                 double* y) {
-  const Csr A = csr_from(n, row_ptr, cols, vals);
-  const auto r = A.multiply(std::vector<double>(x, x + n));
-  std::memcpy(y, r.data(), sizeof(double) * n);
+                 double* y) {  // FixedPatternSparse::multiply (sparse.cpp:49-60) on caller-owned arrays, no copies
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < n; ++i) {
+    double acc = 0.0;
+    for (int k = row_ptr[i]; k < row_ptr[i + 1]; ++k) acc += vals[k] * x[cols[k]];
+    y[i] = acc;
+  }
 }
 void or_cg_solve_csr(int32_t n, const int32_t* row_ptr, const int32_t* cols, const double* vals, const double* b,
                      double* x, double tol, int32_t max_iters, or_cg_result* res) {
