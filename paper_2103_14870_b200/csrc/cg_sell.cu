@@ -101,6 +101,9 @@ __device__ __forceinline__ double ldm(const double* p) {
 #define GF_SELL_GROUP 2
 #endif
 constexpr int kGroup = GF_SELL_GROUP;
+#ifndef GF_QREC
+#define GF_QREC 1
+#endif
 #ifndef GF_GATHER_L1
 #define GF_GATHER_L1 1
 #endif
@@ -383,7 +386,27 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       for (int sl = sch.next(nunits); sl >= 0; sl = sch.next(nunits)) {
         double acc[3];
         int row;
-        if constexpr (kFmt == 1) {
+        if constexpr (kFmt == 1 && GF_QREC) {
+          // A p_{k+1} = A z_{k+1} + beta A p_k: only z is gathered (half the gather traffic of the L2-bound
+          // phase); q = A p and p are then updated in place by their row owner.
+          row = unit_spmv_sym(a, sl, GatherP{a.z, nullptr, 0.0, false}, acc);
+          double pq = 0.0;
+          if (row >= 0 && row < nrows) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const size_t dof = 3 * (size_t)row + c;
+              const double zi = ldv(a.z + dof);
+              const double pr = fused ? __fma_rn(beta, ldv(pcur + dof), zi) : zi;
+              const double qr = fused ? __fma_rn(beta, ldv(a.Ap + dof), acc[c]) : acc[c];
+              pcur[dof] = pr;
+              a.Ap[dof] = qr;
+              pq = __fma_rn(pr, qr, pq);
+            }
+          }
+          pq = lane_sum(pq);
+          if (lane == 0) part(0)[sl] = pq;
+          continue;
+        } else if constexpr (kFmt == 1) {
           row = unit_spmv_sym(a, sl, GatherP{pcur, a.z, beta, fused}, acc);
         } else {
           spmv_fmt<kStream, kFmt>(a, sl, pcur, a.z, beta, fused, acc);
@@ -406,7 +429,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       sch.advance(nunits);
       SELL_STAMP(it, 1);
       SELL_BLOCK_STAMP(it, 3000);
-      if (fused) {
+      if (fused && !(kFmt == 1 && GF_QREC)) {
         double* t = pcur;
         pcur = pnext;
         pnext = t;
