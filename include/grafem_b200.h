@@ -142,6 +142,11 @@ int gf_sim_create(const gf_mesh* mesh, const gf_material* material, const gf_sol
 void gf_sim_destroy(gf_sim* s);
 /* Simulation::dynamic_step (solver.hpp:71, solver.cpp:219-333) */
 int gf_sim_dynamic_step(gf_sim* s, gf_step_stats* stats);
+/* Simulation::quasi_static_step (solver.hpp:76, solver.cpp:138-217): Newton + energy line search to the load
+ * time t_load, load-increment halving (<= 10) on failure, then a damage pass; GF_SOLVE_ERROR like SolveError */
+int gf_sim_quasi_static_step(gf_sim* s, double t_load, gf_step_stats* stats);
+/* Simulation::newton_tolerance (solver.hpp:92, solver.cpp:57-59) */
+double gf_sim_newton_tolerance(const gf_sim* s);
 /* Simulation::damage_pass (solver.hpp:67, solver.cpp:90-103): ascending newly-broken edge ids */
 int gf_sim_damage_pass(gf_sim* s, int32_t* ids, int64_t cap, int64_t* n);
 /* Simulation::state() const / mutable (solver.hpp:79-80): SimState fields (fem.hpp:15-28); NULL skips */

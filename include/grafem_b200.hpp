@@ -121,6 +121,12 @@ class Simulation {
     check(gf_sim_dynamic_step(s_.get(), &st));
     return st;
   }
+  gf_step_stats quasi_static_step(double t_load) {  // solver.hpp:76
+    gf_step_stats st;
+    check(gf_sim_quasi_static_step(s_.get(), t_load, &st));
+    return st;
+  }
+  double newton_tolerance() const { return gf_sim_newton_tolerance(s_.get()); }  // solver.hpp:96
   std::vector<int> damage_pass() {  // solver.hpp:67
     std::vector<int32_t> ids(mesh_.num_edges());
     int64_t n = 0;

@@ -1313,6 +1313,91 @@ struct Sim {
     throw SolveError(msg.str());
   }
 
+  void apply_boundary_displacements(double t) {  // solver.cpp:74-77
+    for (const auto& bc : bcs)
+      for (int n : bc.nodes) st.u[n] = bc.displacement_at(mesh, n, t);
+  }
+
+  // quasi_static_step (solver.cpp:138-217): Newton on the zero-inertia equilibrium with a backtracking line
+  // search on the degraded strain energy, load halving on failure, then a damage pass.
+  double quasi_time = 0.0;
+  or_step_stats quasi_static_step(double t_load) {
+    or_step_stats stats{};
+    const auto fixed = fixed_dofs();
+    const int ndof = 3 * mesh.nn();
+    const std::vector<double> zero_fixed(ndof, 0.0);
+    auto newton_solve = [&]() -> bool {
+      for (int it = 0; it <= cfg.newton_max_iters; ++it) {
+        const auto f_int = assemble_forces(mesh, st, mat);
+        std::vector<double> residual = f_int;
+        for (int d : fixed) residual[d] = 0.0;
+        double rn = 0.0;
+        for (double x : residual) rn += x * x;
+        stats.residual = std::sqrt(rn);
+        stats.newton_iterations = it;
+        if (stats.residual <= newton_tol) return true;
+        if (it == cfg.newton_max_iters) return false;
+        assemble_stiffness(mesh, st, mat, K);
+        std::vector<double> rhs = residual;
+        std::vector<double> dx(ndof, 0.0);
+        solve_linear(dx, rhs, fixed, zero_fixed, &stats.cg_iterations);
+        const double e0 = total_strain_energy(mesh, st, mat);
+        double slope = -dot(residual, dx);
+        if (slope >= 0.0) {
+          dx = residual;
+          slope = -dot(residual, residual);
+        }
+        const std::vector<V3> saved = st.u;
+        double step = 1.0;
+        bool accepted = false;
+        for (int h = 0; h <= cfg.ls_max_halvings; ++h) {
+          for (int n = 0; n < mesh.nn(); ++n)
+            for (int a = 0; a < 3; ++a) st.u[n][a] = saved[n][a] + step * dx[3 * (size_t)n + a];
+          const double e1 = total_strain_energy(mesh, st, mat);
+          if (e1 <= e0 + cfg.ls_sufficient_decrease * step * slope) {
+            accepted = true;
+            break;
+          }
+          step *= cfg.ls_backtrack;
+        }
+        if (!accepted) st.u = saved;
+      }
+      return false;
+    };
+    double current = quasi_time;
+    double increment = t_load - current;
+    if (increment <= 0.0) {
+      apply_boundary_displacements(t_load);
+      if (!newton_solve()) throw SolveError("equilibrium solve failed at fixed load");
+    } else {
+      int halvings = 0;
+      State backup = st;
+      while (current < t_load - 1e-15) {
+        const double target = std::min(t_load, current + increment);
+        apply_boundary_displacements(target);
+        if (newton_solve()) {
+          current = target;
+          backup = st;
+        } else {
+          st = backup;
+          ++halvings;
+          if (halvings > 10) {
+            std::ostringstream msg;
+            msg << "quasi-static step failed: Newton did not reach " << newton_tol << " (residual " << stats.residual
+                << ") after 10 load halvings at load time " << target;
+            throw SolveError(msg.str());
+          }
+          increment *= 0.5;
+        }
+      }
+    }
+    quasi_time = t_load;
+    st.time = t_load;
+    const auto newly = damage_pass();
+    stats.newly_broken = (int)newly.size();
+    return stats;
+  }
+
   or_step_stats dynamic_step() {  // solver.cpp:219-333 (semi-implicit path)
     using clk = std::chrono::steady_clock;
     if (cfg.full_newton) throw FormatError("dynamic_full_newton is outside the ported hot path");
@@ -1781,6 +1866,13 @@ void or_sim_last_system(const or_sim* s, double* vals, double* rhs) {
   if (vals) std::memcpy(vals, s->s.K.val.data(), sizeof(double) * s->s.K.val.size());
   if (rhs && !s->s.last_rhs.empty()) std::memcpy(rhs, s->s.last_rhs.data(), sizeof(double) * s->s.last_rhs.size());
 }
+int or_sim_quasi_static_step(or_sim* s, double t_load, or_step_stats* stats) {
+  return guard([&] {
+    const or_step_stats r = s->s.quasi_static_step(t_load);
+    if (stats) *stats = r;
+  });
+}
+double or_sim_newton_tolerance(const or_sim* s) { return s->s.newton_tol; }
 void or_sim_phase_times(const or_sim* s, double t[4]) {
   for (int i = 0; i < 4; ++i) t[i] = s->s.phase[i];
 }

@@ -155,6 +155,8 @@ void or_sim_mass(const or_sim* s, double* m3n);
 void or_sim_last_system(const or_sim* s, double* vals, double* rhs);
 /* per-phase wall times (seconds) accumulated over dynamic_step calls: damage, assembly, solve, other */
 void or_sim_phase_times(const or_sim* s, double t[4]);
+int or_sim_quasi_static_step(or_sim* s, double t_load, or_step_stats* stats); /* solver.cpp:138-217 */
+double or_sim_newton_tolerance(const or_sim* s);
 
 #ifdef __cplusplus
 }

@@ -100,6 +100,7 @@ def lib():
         L.or_sim_last_collider_load.restype = C.c_double
         L.or_update_damage.restype = C.c_int32
         L.or_fragment_components.restype = C.c_int32
+        L.or_sim_newton_tolerance.restype = C.c_double
         _lib = L
     return _lib
 
@@ -431,6 +432,14 @@ class Sim:
         st = StepStats()
         _check(lib().or_sim_dynamic_step(self._h, C.byref(st)))
         return st
+
+    def quasi_static_step(self, t_load):
+        st = StepStats()
+        _check(lib().or_sim_quasi_static_step(self._h, C.c_double(t_load), C.byref(st)))
+        return st
+
+    def newton_tolerance(self):
+        return lib().or_sim_newton_tolerance(self._h)
 
     def damage_pass(self):
         ids = np.zeros(self.mesh.num_edges, np.int32)

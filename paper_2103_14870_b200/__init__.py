@@ -124,6 +124,7 @@ def lib():
         L.gf_mesh_nonlocal_table.argtypes = [C.c_void_p, C.c_double, I32P, I32P, F64P]
         L.gf_sim_pattern_hash.restype = C.c_uint64
         L.gf_sim_last_collider_load.restype = C.c_double
+        L.gf_sim_newton_tolerance.restype = C.c_double
         L.gf_host_alloc.restype = C.c_void_p
         L.gf_host_alloc.argtypes = [C.c_size_t]
         L.gf_host_free.argtypes = [C.c_void_p]
@@ -407,6 +408,15 @@ class Simulation:
         st = StepStats()
         _check(lib().gf_sim_dynamic_step(self._h, C.byref(st)))
         return st
+
+    def quasi_static_step(self, t_load: float) -> StepStats:
+        """Simulation::quasi_static_step (solver.cpp:138-217) on the GPU."""
+        st = StepStats()
+        _check(lib().gf_sim_quasi_static_step(self._h, C.c_double(t_load), C.byref(st)))
+        return st
+
+    def newton_tolerance(self) -> float:
+        return lib().gf_sim_newton_tolerance(self._h)
 
     def damage_pass(self) -> np.ndarray:
         ids = np.zeros(self.E, np.int32)

@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_assemble(DevData d, MatDev m
         d.x[dof] = d.fv[dof];
       } else {
         const double mv = __ldg(d.mass + i) * d.v[dof];
-        double r = sc.rhs_fint_scale * ((d.fext[dof] + d.fcoll[dof]) + fsum);
+        const double fe = sc.use_ext ? d.fext[dof] + d.fcoll[dof] : 0.0;
+        double r = sc.rhs_fint_scale * (fe + fsum);
         r -= sc.rhs_mv_scale * mv;
         r -= sc.rhs_kv_scale * kv[a];
         r -= corr[a];

@@ -167,6 +167,13 @@ int gf_sim_dynamic_step(gf_sim* s, gf_step_stats* stats) {
     if (stats) *stats = r;
   });
 }
+int gf_sim_quasi_static_step(gf_sim* s, double t_load, gf_step_stats* stats) {
+  return guard([&] {
+    const gf_step_stats r = s->s->quasi_static_step(t_load);
+    if (stats) *stats = r;
+  });
+}
+double gf_sim_newton_tolerance(const gf_sim* s) { return s->s->newton_tolerance(); }
 int gf_sim_damage_pass(gf_sim* s, int32_t* ids, int64_t cap, int64_t* n) {
   return guard([&] {
     const auto v = s->s->damage_pass();

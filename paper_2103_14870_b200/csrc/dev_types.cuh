@@ -28,6 +28,8 @@ struct StepCoeffs {  // per-step scalars of solver.cpp:279-289
   double rhs_kv_scale;    // dt*beta + dt*dt
   double kscale;          // dt*beta + dt*dt
   double mscale;          // 1 + dt*alpha
+  int32_t use_ext;        // 1: rhs includes f_ext + f_coll (dynamic); 0: internal forces only (quasi-static)
+  int32_t _pad;
 };
 
 // one entry per boundary condition, evaluated by the host each step (solver.cpp:22-29)
@@ -183,5 +185,8 @@ void launch_shift_diag(const DevData& d, double shift, cudaStream_t s);
 void launch_absdiag(const DevData& d, cudaStream_t s);
 void launch_bsr_dinv(const DevData& d, cudaStream_t s);
 void launch_fill(double* p, double v, int64_t n, cudaStream_t s);
+void launch_qs_bc(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, cudaStream_t s);
+void launch_qs_update(double* u, const double* saved, const double* dx, double step, int64_t n, cudaStream_t s);
+void launch_dot(const double* a, const double* b, int64_t n, double* partials, int nblocks, cudaStream_t s);
 
 }  // namespace gfb

@@ -4,6 +4,7 @@
 //   k_collide     per-vertex penalty + impulse + Coulomb response (detect_and_respond, collision.cpp:49-111)
 //                 on the substep probe u + tau v (solver.cpp:233-249), block partials for the load
 //   k_integrate   v += dv, u += dt v, then pin BC nodes (solver.cpp:296-328)
+//   k_qs_bc / k_qs_update / k_dot  quasi-static Newton helpers (solver.cpp:138-217)
 //   k_shift_diag  shift_diagonal on the node-block matrix (solver.cpp:119-129 ladder)
 #include "device_math.cuh"
 
@@ -218,6 +219,42 @@ __global__ void k_reset_x(DevData d) {  // dx.setZero(); dx[fixed] = fixed_value
   for (int a = 0; a < 3; ++a) d.x[3 * (size_t)i + a] = fixed ? d.fv[3 * (size_t)i + a] : 0.0;
 }
 
+// quasi-static load step (solver.cpp:74-77 apply_boundary_displacements + the zero prescribed Newton increment)
+__global__ void k_qs_bc(DevData d, int n_fixed, const int32_t* fixed_nodes) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n_fixed) return;
+  const int i = fixed_nodes[q];
+  const BcStep& b = d.bcstep[d.node_bc[i]];
+  double u1[3];
+  bc_disp(b, d.X + 3 * (size_t)i, b.R1, b.d1, u1);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    d.u[3 * (size_t)i + a] = u1[a];
+    d.fv[3 * (size_t)i + a] = 0.0;
+  }
+}
+
+// line-search trial point u = saved + step * dx (solver.cpp:176-177)
+__global__ void k_qs_update(double* u, const double* saved, const double* dx, double step, int64_t n) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) u[k] = saved[k] + step * dx[k];
+}
+
+// per-block partial dot products a.b (fixed grid, deterministic order; summed on the host)
+__global__ void __launch_bounds__(kTpb) k_dot(const double* a, const double* b, int64_t n, double* partials) {
+  __shared__ double s[kTpb];
+  double acc = 0.0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    acc += a[k] * b[k];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = kTpb / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = s[0];
+}
+
 __global__ void k_fill(double* p, double v, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -246,6 +283,15 @@ void launch_shift_diag(const DevData& d, double shift, cudaStream_t s) {
 void launch_absdiag(const DevData& d, cudaStream_t s) { k_absdiag<<<nblk(d.nn), kTpb, 0, s>>>(d); }
 void launch_bsr_dinv(const DevData& d, cudaStream_t s) { k_bsr_dinv<<<nblk(d.nn), kTpb, 0, s>>>(d); }
 void launch_reset_x(const DevData& d, cudaStream_t s) { k_reset_x<<<nblk(d.nn), kTpb, 0, s>>>(d); }
+void launch_qs_bc(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, cudaStream_t s) {
+  if (n_fixed > 0) k_qs_bc<<<nblk(n_fixed), kTpb, 0, s>>>(d, n_fixed, fixed_nodes);
+}
+void launch_qs_update(double* u, const double* saved, const double* dx, double step, int64_t n, cudaStream_t s) {
+  if (n > 0) k_qs_update<<<nblk(n), kTpb, 0, s>>>(u, saved, dx, step, n);
+}
+void launch_dot(const double* a, const double* b, int64_t n, double* partials, int nblocks, cudaStream_t s) {
+  k_dot<<<nblocks, kTpb, 0, s>>>(a, b, n, partials);
+}
 void launch_fill(double* p, double v, int64_t n, cudaStream_t s) {
   if (n > 0) k_fill<<<(int)((n + kTpb - 1) / kTpb), kTpb, 0, s>>>(p, v, n);
 }

@@ -385,6 +385,8 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   n_fixed_ = (int32_t)fixed.size();
   d_fixed_nodes_ = (int32_t*)up(fixed.data(), 4 * fixed.size());
   GF_CUDA(cudaMallocHost(&h_stats_, 8 * 8));
+  GF_CUDA(cudaMallocHost(&h_partials_, 8 * 1024));
+  newton_tol_ = cfg_.newton_tol > 0.0 ? cfg_.newton_tol : 1e-6 * mat_.sigma_thres * mesh_.mean_face_area();  // solver.cpp:57-59
   // static external force: m g (solver.cpp:230-231)
   std::vector<double> fext(nd);
   for (int32_t i = 0; i < nn; ++i)
@@ -430,6 +432,7 @@ Simulation::~Simulation() {
   if (h_bcstep_) cudaFreeHost(h_bcstep_);
   if (h_cols_) cudaFreeHost(h_cols_);
   if (h_stats_) cudaFreeHost(h_stats_);
+  if (h_partials_) cudaFreeHost(h_partials_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -558,6 +561,36 @@ double Simulation::run_cg(int max_iters) {
   return h_stats_[0];
 }
 
+// solve_linear retries (solver.cpp:113-135) after a first attempt whose outcome is `ok`: 4x iterations, then
+// cumulative diagonal shifts of |diag| (fixed dofs excluded) from 1e-8 up by 10x, 8 attempts, else SolveError
+template <class Acc>
+void Simulation::solve_ladder(bool ok, int32_t* iters, Acc&& account) {
+  if (!ok) {
+    *iters += (int32_t)run_cg(4 * cfg_.cg_max_iters);
+    account(h_stats_[0]);
+    ok = h_stats_[1] != 0.0;
+  }
+  if (!ok) {
+    launch("absdiag", 0.0, [&] { launch_absdiag(d_, stream_); });
+    double shift = 1e-8;
+    for (int attempt = 0; attempt < 8 && !ok; ++attempt) {
+      launch("shift_diag", 0.0, [&] { launch_shift_diag(d_, shift, stream_); });
+      launch("bsr_dinv", 0.0, [&] { launch_bsr_dinv(d_, stream_); });
+      launch("reset_x", 0.0, [&] { launch_reset_x(d_, stream_); });
+      *iters += (int32_t)run_cg(cfg_.cg_max_iters);
+      account(h_stats_[0]);
+      ok = h_stats_[1] != 0.0;
+      shift *= 10.0;
+    }
+    if (!ok) {
+      std::ostringstream msg;
+      msg << "linear solve failed: relative residual " << h_stats_[3] << " after " << (int)h_stats_[0]
+          << " iterations" << (h_stats_[2] != 0.0 ? " (negative curvature)" : "");
+      throw SolveError(msg.str());
+    }
+  }
+}
+
 gf_step_stats Simulation::dynamic_step() {
   gf_step_stats st{};
   const double t = time_, dt = cfg_.dt;
@@ -597,7 +630,8 @@ gf_step_stats Simulation::dynamic_step() {
     upload_bc_step(t, dt);
     launch("bc_targets", 96.0 * n_fixed_, [&] { launch_bc_targets(d_, n_fixed_, d_fixed_nodes_, dt, stream_); });
   }
-  StepCoeffs c;
+  StepCoeffs c{};
+  c.use_ext = 1;
   c.dt = dt;
   c.rhs_fint_scale = dt;
   c.rhs_mv_scale = dt * mat_.damp_mass_coeff;
@@ -628,34 +662,122 @@ gf_step_stats Simulation::dynamic_step() {
   st.load = last_load_;
   st.cg_iterations = (int32_t)h_stats_[0];
   account(h_stats_[0]);
-  bool ok = h_stats_[1] != 0.0;
-  if (!ok) {
-    st.cg_iterations += (int32_t)run_cg(4 * cfg_.cg_max_iters);
-    account(h_stats_[0]);
-    ok = h_stats_[1] != 0.0;
-  }
-  if (!ok) {
-    launch("absdiag", 0.0, [&] { launch_absdiag(d_, stream_); });
-    double shift = 1e-8;
-    for (int attempt = 0; attempt < 8 && !ok; ++attempt) {
-      launch("shift_diag", 0.0, [&] { launch_shift_diag(d_, shift, stream_); });
-      launch("bsr_dinv", 0.0, [&] { launch_bsr_dinv(d_, stream_); });
-      launch("reset_x", 0.0, [&] { launch_reset_x(d_, stream_); });
-      st.cg_iterations += (int32_t)run_cg(cfg_.cg_max_iters);
-      account(h_stats_[0]);
-      ok = h_stats_[1] != 0.0;
-      shift *= 10.0;
-    }
-    if (!ok) {
-      std::ostringstream msg;
-      msg << "linear solve failed: relative residual " << h_stats_[3] << " after " << (int)h_stats_[0]
-          << " iterations" << (h_stats_[2] != 0.0 ? " (negative curvature)" : "");
-      throw SolveError(msg.str());
-    }
-  }
+  solve_ladder(h_stats_[1] != 0.0, &st.cg_iterations, account);
   launch("integrate", 40 * n, [&] { launch_integrate(d_, dt, stream_); });  // B_int = 40n
   time_ = t + dt;
   st.residual = 0.0;
+  return st;
+}
+
+// ---------------------------------------------------------------- quasi-static step (solver.cpp:138-217)
+double Simulation::device_dot(const double* a, const double* b, int64_t n) {
+  constexpr int nblocks = 1024;
+  launch("dot", 16.0 * n, [&] { launch_dot(a, b, n, d_energy_partials_, nblocks, stream_); });
+  GF_CUDA(cudaMemcpyAsync(h_partials_, d_energy_partials_, 8 * nblocks, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  double s = 0.0;
+  for (int k = 0; k < nblocks; ++k) s += h_partials_[k];
+  return s;
+}
+
+double Simulation::device_strain_energy() {
+  constexpr int nblocks = 1024;
+  launch("energy", 0.0, [&] { launch_energy(d_, md_, d_energy_partials_, nblocks, stream_); });
+  GF_CUDA(cudaMemcpyAsync(h_partials_, d_energy_partials_, 8 * nblocks, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  double s = 0.0;
+  for (int k = 0; k < nblocks; ++k) s += h_partials_[k];
+  return s;
+}
+
+void Simulation::apply_boundary_displacements(double t) {  // solver.cpp:74-77, plus zero Newton increments
+  if (bcs_.empty()) return;
+  upload_bc_step(t, 0.0);
+  launch("qs_bc", 0.0, [&] { launch_qs_bc(d_, n_fixed_, d_fixed_nodes_, stream_); });
+}
+
+// newton_solve (solver.cpp:143-188): one fused assembly pass gives the residual (f_int, fixed dofs zeroed) and
+// the projected tangent K; the norm check precedes the solve, so the final (converged) pass's matrix is unused
+bool Simulation::newton_solve(gf_step_stats& st) {
+  const size_t nd = 3 * (size_t)mesh_.nn;
+  const double n = (double)nd, T = mesh_.nt, Z = 9.0 * pat_.cols.size();
+  StepCoeffs c{};
+  c.use_ext = 0;
+  c.rhs_fint_scale = 1.0;
+  c.kscale = 1.0;
+  d_.fint_out = nullptr;
+  auto account = [](double) {};
+  for (int it = 0; it <= cfg_.newton_max_iters; ++it) {
+    launch("assemble", 16 * n + 104 * T + 8 * Z, [&] { launch_assemble(d_, md_, c, kAssembleSystem, stream_); });
+    const double rr = device_dot(d_.rhs, d_.rhs, (int64_t)nd);
+    st.residual = std::sqrt(rr);
+    st.newton_iterations = it;
+    if (st.residual <= newton_tol_) return true;
+    if (it == cfg_.newton_max_iters) return false;
+    st.cg_iterations += (int32_t)run_cg(cfg_.cg_max_iters);
+    solve_ladder(h_stats_[1] != 0.0, &st.cg_iterations, account);
+    // line search on the degraded strain energy (solver.cpp:166-186)
+    const double e0 = device_strain_energy();
+    double slope = -device_dot(d_.rhs, d_.x, (int64_t)nd);
+    if (slope >= 0.0) {  // steepest-descent fallback
+      GF_CUDA(cudaMemcpyAsync(d_.x, d_.rhs, 8 * nd, cudaMemcpyDeviceToDevice, stream_));
+      slope = -rr;
+    }
+    GF_CUDA(cudaMemcpyAsync(d_usave_, d_.u, 8 * nd, cudaMemcpyDeviceToDevice, stream_));
+    double step = 1.0;
+    bool accepted = false;
+    for (int h = 0; h <= cfg_.ls_max_halvings; ++h) {
+      launch("qs_update", 24.0 * n, [&] { launch_qs_update(d_.u, d_usave_, d_.x, step, (int64_t)nd, stream_); });
+      const double e1 = device_strain_energy();
+      if (e1 <= e0 + cfg_.ls_sufficient_decrease * step * slope) {
+        accepted = true;
+        break;
+      }
+      step *= cfg_.ls_backtrack;
+    }
+    if (!accepted) GF_CUDA(cudaMemcpyAsync(d_.u, d_usave_, 8 * nd, cudaMemcpyDeviceToDevice, stream_));
+  }
+  return false;
+}
+
+gf_step_stats Simulation::quasi_static_step(double t_load) {
+  gf_step_stats st{};
+  const size_t nd = 3 * (size_t)mesh_.nn;
+  if (!d_usave_) {
+    d_usave_ = (double*)dalloc(8 * nd);
+    d_ubackup_ = (double*)dalloc(8 * nd);
+  }
+  double current = quasi_time_;
+  double increment = t_load - current;
+  if (increment <= 0.0) {
+    apply_boundary_displacements(t_load);
+    if (!newton_solve(st)) throw SolveError("equilibrium solve failed at fixed load");
+  } else {
+    int halvings = 0;
+    // only the displacements change inside a load increment, so they are the whole backup (solver.cpp:195)
+    GF_CUDA(cudaMemcpyAsync(d_ubackup_, d_.u, 8 * nd, cudaMemcpyDeviceToDevice, stream_));
+    while (current < t_load - 1e-15) {
+      const double target = std::min(t_load, current + increment);
+      apply_boundary_displacements(target);
+      if (newton_solve(st)) {
+        current = target;
+        GF_CUDA(cudaMemcpyAsync(d_ubackup_, d_.u, 8 * nd, cudaMemcpyDeviceToDevice, stream_));
+      } else {
+        GF_CUDA(cudaMemcpyAsync(d_.u, d_ubackup_, 8 * nd, cudaMemcpyDeviceToDevice, stream_));
+        ++halvings;
+        if (halvings > 10) {
+          std::ostringstream msg;
+          msg << "quasi-static step failed: Newton did not reach " << newton_tol_ << " (residual " << st.residual
+              << ") after 10 load halvings at load time " << target;
+          throw SolveError(msg.str());
+        }
+        increment *= 0.5;
+      }
+    }
+  }
+  quasi_time_ = t_load;
+  time_ = t_load;
+  st.newly_broken = (int32_t)damage_pass().size();
   return st;
 }
 

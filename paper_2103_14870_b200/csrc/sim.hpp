@@ -42,6 +42,8 @@ class Simulation {
   Simulation& operator=(const Simulation&) = delete;
 
   gf_step_stats dynamic_step();
+  gf_step_stats quasi_static_step(double t_load);
+  double newton_tolerance() const { return newton_tol_; }
   std::vector<int32_t> damage_pass();
   void get_state(double* u, double* v, uint8_t* zeta, double* chi, double* time);
   void set_state(const double* u, const double* v, const uint8_t* zeta, const double* chi, const double* time);
@@ -78,6 +80,12 @@ class Simulation {
   void run_damage(bool relabel, bool keep_values, bool chi);
   void bsr_to_csr(const std::vector<double>& bval, double* vals) const;
   double run_cg(int max_iters);
+  template <class Acc>
+  void solve_ladder(bool ok, int32_t* iters, Acc&& account);
+  double device_dot(const double* a, const double* b, int64_t n);
+  double device_strain_energy();
+  void apply_boundary_displacements(double t);
+  bool newton_solve(gf_step_stats& st);
   void launch_cg();
 
   HostMesh mesh_;
@@ -97,6 +105,10 @@ class Simulation {
   uint64_t hash_ = 0;
   int64_t nl_entries_ = 0;
   double time_ = 0.0, last_load_ = 0.0;
+  double newton_tol_ = 0.0, quasi_time_ = 0.0;
+  double* d_usave_ = nullptr;    // line-search base displacements (quasi-static only, allocated on first use)
+  double* d_ubackup_ = nullptr;  // last converged load increment
+  double* h_partials_ = nullptr; // pinned, 1024 block partials
   int32_t n_fixed_ = 0;
 
   cudaStream_t stream_ = nullptr;

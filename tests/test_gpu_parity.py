@@ -481,3 +481,86 @@ def test_huge_radius_single_and_tetgen_meshes():
     so.set_state(u=u)
     assert np.array_equal(sg.damage_pass(), so.damage_pass())
     assert same_bits_or_zero(sg.state().element_chi, so.get_state()["chi"])
+
+
+# ---------------------------------------------------------------- quasi-static Newton (solver.cpp:138-217)
+def _pull_pair(cells=(6, 3, 3), sigma=3e3, model=g.STVK, disp=0.002, cfg=None):
+    om_tmp = o.Mesh.make_box((0.2, 0.1, 0.1), cells)
+    X = om_tmp.arrays()["rest"]
+    bcs = [dict(nodes=np.nonzero(X[:, 0] <= 1e-9)[0], times=[0, 1], values=[[0, 0, 0], [-disp, 0, 0]]),
+           dict(nodes=np.nonzero(X[:, 0] >= 0.2 - 1e-9)[0], times=[0, 1], values=[[0, 0, 0], [disp, 0, 0]])]
+    return _pair_custom(((0.2, 0.1, 0.1), cells), (1e6, 0.3, 1000, sigma, 0, model), cfg or {}, bcs=bcs)
+
+
+def test_gpu_quasi_static_zero_load():  # test_solver.cpp:30-38
+    m = g.make_box_mesh((0.2, 0.1, 0.1), (4, 2, 2))
+    X = m.rest_positions
+    s = g.Simulation(m, g.MaterialParams.from_youngs(1e6, 0.3, 1000, 1e9, 0, g.STVK), g.SolverConfig(),
+                     [g.BoundaryCondition(nodes=np.nonzero(X[:, 0] <= 1e-9)[0])])
+    st = s.quasi_static_step(1.0)
+    assert st.newton_iterations == 0 and np.all(s.state().displacements == 0)
+
+
+def test_gpu_quasi_static_small_stretch():  # test_solver.cpp:40-68
+    strain, L = 1e-3, 0.2
+    m = g.make_box_mesh((L, 0.1, 0.1), (8, 4, 4))
+    X = m.rest_positions
+    bcs = [g.BoundaryCondition(nodes=np.nonzero(X[:, 0] <= 1e-9)[0],
+                               translation=g.Schedule3([0, 1], [[0, 0, 0], [-0.5 * strain * L, 0, 0]])),
+           g.BoundaryCondition(nodes=np.nonzero(X[:, 0] >= L - 1e-9)[0],
+                               translation=g.Schedule3([0, 1], [[0, 0, 0], [0.5 * strain * L, 0, 0]]))]
+    s = g.Simulation(m, g.MaterialParams.from_youngs(1e6, 0.3, 1000, 1e9, 0, g.STVK), g.SolverConfig(cg_tol=1e-10),
+                     bcs)
+    st = s.quasi_static_step(1.0)
+    assert st.residual <= s.newton_tolerance()
+    om = o.Mesh.make_box((L, 0.1, 0.1), (8, 4, 4))
+    c = om.arrays()["centroid"][:, 0]
+    u = s.state().displacements
+    sel = np.nonzero((c >= L / 3) & (c <= 2 * L / 3))[0]
+    fxx = np.mean([om.deformation_gradient(u, e)[0, 0] for e in sel])
+    assert abs(fxx - (1 + strain)) < 0.05 * strain
+
+
+@pytest.mark.parametrize("model", [g.STVK, g.STABLE_NEO_HOOKEAN])
+def test_gpu_quasi_static_pull_matches_oracle(model):  # test_solver.cpp:70-87, 204-246 against the oracle
+    gs, os_, om = _pull_pair(model=model)
+    assert gs.newton_tolerance() == pytest.approx(os_.newton_tolerance(), rel=1e-15)
+    scale = np.abs(om.arrays()["rest"]).max()
+    h0 = gs.pattern_hash()
+    prev_chi = gs.state().element_chi
+    for k in range(1, 11):
+        a = os_.quasi_static_step(k / 10)
+        b = gs.quasi_static_step(k / 10)
+        ost, gst = os_.get_state(), gs.state()
+        assert a.newly_broken == b.newly_broken
+        assert a.newton_iterations == b.newton_iterations
+        assert np.array_equal(gst.edge_damage, ost["zeta"])
+        assert np.abs(gst.displacements - ost["u"]).max() / scale < TRAJ_TOL
+        assert b.residual <= gs.newton_tolerance()
+        assert gs.pattern_hash() == h0
+        assert np.all(gst.element_chi <= prev_chi + 1e-15) and np.all(gst.element_chi >= 0)
+        prev_chi = gst.element_chi
+        assert gst.time == k / 10
+    assert gs.state().edge_damage.sum() > 0
+
+
+def test_gpu_quasi_static_fixed_load_and_halving_match_oracle():  # solver.cpp:190-210 branches
+    # newton_max_iters=1 forces several load-increment halvings before the full load is reached
+    gs, os_, om = _pull_pair(cells=(4, 2, 2), sigma=1e9, model=g.STABLE_NEO_HOOKEAN, disp=0.03,
+                             cfg=dict(newton_max_iters=1))
+    outcome, cg = [], []
+    for sim, err in ((os_, o.SolveError), (gs, g.SolveError)):
+        try:
+            st = sim.quasi_static_step(1.0)
+            outcome.append(("ok", st.newton_iterations))
+            cg.append(st.cg_iterations)
+        except err:
+            outcome.append(("error", None))
+    assert outcome[0] == outcome[1] == ("ok", 1)
+    assert abs(cg[0] - cg[1]) <= 0.05 * cg[0]
+    if outcome[0][0] == "ok":
+        scale = np.abs(om.arrays()["rest"]).max()
+        assert np.abs(gs.state().displacements - os_.get_state()["u"]).max() / scale < TRAJ_TOL
+        # increment <= 0: re-solve at the same load (fixed-load branch)
+        a, b = os_.quasi_static_step(1.0), gs.quasi_static_step(1.0)
+        assert a.newton_iterations == b.newton_iterations == 0

@@ -636,3 +636,42 @@ def test_tetgen_parse():  # mesh.cpp:157-221 (one-based detection)
         o.Mesh.load_tetgen("4 2\n", ele)
     with pytest.raises(o.GeometryError):
         o.Mesh.create([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], [[0, 2, 1, 3]])
+
+
+# ------------------------------------------------------------------ quasi-static (test_solver.cpp:30-87)
+def test_quasi_static_zero_load_converges_immediately():  # test_solver.cpp:30-38
+    m = o.Mesh.make_box((0.2, 0.1, 0.1), (4, 2, 2))
+    X = m.arrays()["rest"]
+    s = o.Sim(m, o.material_from_youngs(1e6, 0.3, 1000, 1e9, 0, STVK), o.solver_config(),
+              [dict(nodes=_slab(X, -1.0, 1e-9))])
+    before = s.get_state()["u"].copy()
+    st = s.quasi_static_step(1.0)
+    assert st.newton_iterations == 0 and np.array_equal(s.get_state()["u"], before)
+
+
+def test_quasi_static_small_stretch_linear_profile():  # test_solver.cpp:40-68
+    strain, L = 1e-3, 0.2
+    m = o.Mesh.make_box((L, 0.1, 0.1), (8, 4, 4))
+    X = m.arrays()["rest"]
+    bcs = [dict(nodes=_slab(X, -1.0, 1e-9), times=[0, 1], values=[[0, 0, 0], [-0.5 * strain * L, 0, 0]]),
+           dict(nodes=_slab(X, L - 1e-9, 1.0), times=[0, 1], values=[[0, 0, 0], [0.5 * strain * L, 0, 0]])]
+    s = o.Sim(m, o.material_from_youngs(1e6, 0.3, 1000, 1e9, 0, STVK), o.solver_config(cg_tol=1e-10), bcs)
+    st = s.quasi_static_step(1.0)
+    assert st.residual <= s.newton_tolerance()
+    state = s.get_state()
+    assert state["zeta"].sum() == 0
+    c = m.arrays()["centroid"][:, 0]
+    sel = np.nonzero((c >= L / 3) & (c <= 2 * L / 3))[0]
+    fxx = np.mean([m.deformation_gradient(state["u"], e)[0, 0] for e in sel])
+    assert abs(fxx - (1 + strain)) < 0.05 * strain
+
+
+def test_quasi_static_pull_breaks_edges():  # test_solver.cpp:70-87
+    m = o.Mesh.make_box((0.2, 0.1, 0.1), (6, 3, 3))
+    X = m.arrays()["rest"]
+    bcs = [dict(nodes=_slab(X, -1.0, 1e-9), times=[0, 1], values=[[0, 0, 0], [-0.002, 0, 0]]),
+           dict(nodes=_slab(X, 0.2 - 1e-9, 1.0), times=[0, 1], values=[[0, 0, 0], [0.002, 0, 0]])]
+    s = o.Sim(m, o.material_from_youngs(1e6, 0.3, 1000, 3e3, 0, STVK), o.solver_config(), bcs)
+    for k in range(1, 11):
+        last = s.quasi_static_step(k / 10)
+    assert s.get_state()["zeta"].sum() > 0 and last.residual <= s.newton_tolerance()

@@ -1,0 +1,8 @@
+#!/bin/bash
+# A/B every kernel of library variants in ONE gpurun call
+cd "$(dirname "$0")/.."
+for rep in 1 2; do
+for v in "$@"; do
+  GF_LIB_PATH=paper_2103_14870_b200/_lib/variants/$v/libgrafem_b200.so python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err
+  python -c "import json,sys; d=json.load(open('gpurun_out/ab_$v.json')); k=d['roofline']['kernels']; print('$v', {n: round(x['avg_ms'],3) for n,x in k.items() if x['avg_ms']>0.03}, 'value %.4g' % d['value'])" || tail -3 gpurun_out/ab_$v.err
+done; done
