@@ -239,6 +239,23 @@ constexpr int kR = GF_CG_R;  // lanes per row in the symmetric phase-A SpMV (wor
 
 // kR lanes cooperate on one row (lane = r + (32/kR) t handles slots t, t+kR, ...; partial sums combined with a
 // fixed xor-shuffle tree): per-lane dependency chains are kR x shorter, so the phase tail (one unit) shrinks.
+#ifndef GF_PF
+#define GF_PF 0
+#endif
+#ifndef GF_MAT_L1
+#define GF_MAT_L1 1
+#endif
+constexpr int kPf = GF_PF;  // L1 prefetch distance in slot groups (0: off)
+
+__device__ __forceinline__ void pf_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+__device__ __forceinline__ double ldmat(const double* p) {
+#if GF_MAT_L1
+  return __ldg(p);
+#else
+  return __ldcg(p);
+#endif
+}
+
 template <class G>
 __device__ __forceinline__ int unit_spmv_sym(const CgLaunch& a, int unit, const G& gat, double acc[3]) {
   constexpr int kRpu = 32 / kR;
@@ -248,18 +265,50 @@ __device__ __forceinline__ int unit_spmv_sym(const CgLaunch& a, int unit, const 
   const int k0 = __ldg(a.row_ptr + sl), k1 = __ldg(a.row_ptr + sl + 1);
   const int2* slots = reinterpret_cast<const int2*>(a.cols);
   acc[0] = acc[1] = acc[2] = 0.0;
+  auto slot_at = [&](int k) { return (k < k1) ? __ldg(slots + (size_t)k * 32 + lr) : make_int2(0, 0); };
+  auto prefetch = [&](int k, int2 sv) {
+    if (k < k1) {
+      const double* v = a.vals + (size_t)(sv.x & 0x7fffffff);
+#pragma unroll
+      for (int q = 0; q < 9; ++q) pf_l1(v + 32 * q);
+      gat.prefetch((size_t)sv.y);
+    }
+  };
   int2 sc[kGroup];
 #pragma unroll
-  for (int g = 0; g < kGroup; ++g) {
-    const int k = k0 + t + kR * g;
-    sc[g] = (k < k1) ? __ldg(slots + (size_t)k * 32 + lr) : make_int2(0, 0);
+  for (int g = 0; g < kGroup; ++g) sc[g] = slot_at(k0 + t + kR * g);
+  // prefetch ring: slots of groups 1..kPf ahead are already loaded and their lines requested
+  int2 ring[kPf > 0 ? kPf : 1][kGroup];
+  if constexpr (kPf > 0) {
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g) prefetch(k0 + t + kR * g, sc[g]);
+#pragma unroll
+    for (int d = 0; d < kPf; ++d)
+#pragma unroll
+      for (int g = 0; g < kGroup; ++g) {
+        const int k = k0 + t + kR * ((d + 1) * kGroup + g);
+        ring[d][g] = slot_at(k);
+        prefetch(k, ring[d][g]);
+      }
   }
   for (int kb = k0 + t; kb < k1; kb += kR * kGroup) {
     int2 sn[kGroup];
+    if constexpr (kPf > 0) {
 #pragma unroll
-    for (int g = 0; g < kGroup; ++g) {
-      const int k = kb + kR * (kGroup + g);
-      sn[g] = (k < k1) ? __ldg(slots + (size_t)k * 32 + lr) : make_int2(0, 0);
+      for (int g = 0; g < kGroup; ++g) sn[g] = ring[0][g];
+#pragma unroll
+      for (int d = 0; d + 1 < kPf; ++d)
+#pragma unroll
+        for (int g = 0; g < kGroup; ++g) ring[d][g] = ring[d + 1][g];
+#pragma unroll
+      for (int g = 0; g < kGroup; ++g) {
+        const int k = kb + kR * ((kPf + 1) * kGroup + g);
+        ring[kPf - 1][g] = slot_at(k);
+        prefetch(k, ring[kPf - 1][g]);
+      }
+    } else {
+#pragma unroll
+      for (int g = 0; g < kGroup; ++g) sn[g] = slot_at(kb + kR * (kGroup + g));
     }
 #pragma unroll
     for (int g = 0; g < kGroup; ++g) {
@@ -270,7 +319,7 @@ __device__ __forceinline__ int unit_spmv_sym(const CgLaunch& a, int unit, const 
         const double* v = a.vals + (size_t)(sc[g].x & 0x7fffffff);
         double m[9];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) m[q] = __ldcg(v + 32 * q);
+        for (int q = 0; q < 9; ++q) m[q] = (kPf > 0) ? __ldg(v + 32 * q) : ldmat(v + 32 * q);
         if (!tr) {
           acc[0] = __fma_rn(m[0], p.x, acc[0]); acc[0] = __fma_rn(m[1], p.y, acc[0]); acc[0] = __fma_rn(m[2], p.z, acc[0]);
           acc[1] = __fma_rn(m[3], p.x, acc[1]); acc[1] = __fma_rn(m[4], p.y, acc[1]); acc[1] = __fma_rn(m[5], p.z, acc[1]);
@@ -297,6 +346,10 @@ struct GatherP {  // p_j = fused ? fma(beta, pold_j, z_j) : src_j
   const double* z;
   double beta;
   bool fused;
+  __device__ __forceinline__ void prefetch(size_t j) const {
+    pf_l1(src + 3 * j);
+    if (fused) pf_l1(z + 3 * j);
+  }
   __device__ __forceinline__ double3 operator()(size_t j) const {
     if (fused)
       return make_double3(__fma_rn(beta, ldv(src + 3 * j), ldv(z + 3 * j)),
@@ -321,50 +374,140 @@ __device__ __forceinline__ void spmv_fmt(const CgLaunch& a, int sl, const double
   else slice_spmv<kStream>(a, sl, src, z, beta, fused, acc);
 }
 
+// Work distribution of one phase over n units, without per-unit atomics on the critical path: unit gw (the
+// global warp id) is taken statically; the remaining n - nwarps units are handed out from the ticket counter,
+// each warp requesting its next ticket BEFORE working on the current unit so the atomic's round trip hides
+// behind the work (every warp takes exactly one overshooting ticket per phase). Statically taken units are
+// reduced per CTA in warp order (one partial per CTA); dynamic units keep one partial each. After the grid
+// barrier every CTA sums [CTA partials, dynamic-unit partials] in one fixed order, so alpha / beta / the stop
+// tests are bit-identical in every CTA and run to run.
+struct Phase {
+  unsigned long long* ctr;
+  unsigned long long base;
+  int nwarps, gw;
+  template <int NV, class Body>
+  __device__ __forceinline__ void run(int n, double* const (&part)[NV], double* const (&cta)[NV], Body&& body) {
+    __shared__ double s_acc[kWarpsPerCta][4];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned long long nd = n > nwarps ? (unsigned long long)(n - nwarps) : 0ull;
+    unsigned long long tk = 0;
+    if (nd && lane == 0) tk = atomicAdd(ctr, 1ull);
+    double sv[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) sv[q] = 0.0;
+    if (gw < n) body(gw, sv);
+    if (nd) {
+      for (;;) {
+        const unsigned long long idx = __shfl_sync(0xffffffffu, tk, 0) - base;
+        if (idx >= nd) break;
+        if (lane == 0) tk = atomicAdd(ctr, 1ull);
+        const int u = nwarps + (int)idx;
+        double v[NV];
+        body(u, v);
+        if (lane == 0)
+#pragma unroll
+          for (int q = 0; q < NV; ++q) part[q][u] = v[q];
+      }
+      base += nd + (unsigned long long)nwarps;
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < NV; ++q) s_acc[w][q] = sv[q];
+    __syncthreads();
+    if (threadIdx.x < NV) {
+      double x = 0.0;
+      for (int k = 0; k < kWarpsPerCta; ++k) x += s_acc[k][threadIdx.x];
+      cta[threadIdx.x][blockIdx.x] = x;
+    }
+  }
+};
+
+// sum over [cta[0..G), part[nwarps..n)] in one fixed order (thread stride, then a fixed block tree)
+template <int NV>
+__device__ __forceinline__ void sum_phase(double* const (&part)[NV], double* const (&cta)[NV], int G, int nwarps,
+                                          int n, double (&out)[NV]) {
+  __shared__ double s_w[kWarpsPerCta][4];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nd = n > nwarps ? n - nwarps : 0, total = G + nd;
+  constexpr int kB = 4;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    double x = 0.0;
+    for (int k0 = 0; k0 < total; k0 += kB * (int)blockDim.x) {
+      double v[kB];
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const int k = k0 + b * (int)blockDim.x + (int)threadIdx.x;
+        v[b] = (k < G) ? __ldcg(cta[q] + k) : (k < total) ? __ldcg(part[q] + nwarps + (k - G)) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < kB; ++b) x += v[b];
+    }
+    x = lane_sum(x);
+    if (lane == 0) s_w[w][q] = x;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    double x = (lane < kWarpsPerCta) ? s_w[lane][q] : 0.0;
+    out[q] = lane_sum(x);  // every warp computes the same total
+  }
+  __syncthreads();
+}
+
+__host__ __device__ inline size_t part_stride(int ns) { return 4 * (size_t)ns + 1024; }
+
 template <bool kStream, int kFmt>
 __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
   cg::grid_group grid = cg::this_grid();
   const CgLaunch& a = sa.a;
   const int ns = a.nslices, nrows = a.nrows, lane = threadIdx.x & 31;
-  Sched sch{sa.ctr, 0ull, (unsigned long long)((gridDim.x * blockDim.x) >> 5)};
+  const int nwarps = (int)((gridDim.x * blockDim.x) >> 5), G = (int)gridDim.x;
+  Phase ph{sa.ctr, 0ull, nwarps, (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5))};
   int parity = 0;
-  auto part = [&](int q) { return sa.slice_part + ((size_t)parity * 4 + q) * (4 * (size_t)ns); };
+  const size_t qs = part_stride(ns);
+  auto pq_ptr = [&](int q) { return sa.slice_part + ((size_t)parity * 4 + q) * qs; };
+  auto ptrs1 = [&](double* (&u)[1], double* (&c)[1]) { u[0] = pq_ptr(0); c[0] = u[0] + 4 * (size_t)ns; };
+  auto ptrs2 = [&](double* (&u)[2], double* (&c)[2]) {
+    for (int q = 0; q < 2; ++q) { u[q] = pq_ptr(q); c[q] = u[q] + 4 * (size_t)ns; }
+  };
+  auto ptrs3 = [&](double* (&u)[3], double* (&c)[3]) {
+    for (int q = 0; q < 3; ++q) { u[q] = pq_ptr(q); c[q] = u[q] + 4 * (size_t)ns; }
+  };
 
-  // setup (sparse.cpp:145-157): r = b - A x, z = D^-1 r, p = z; partials b.b, r.z, r.r per slice
-  for (int sl = sch.next(ns); sl >= 0; sl = sch.next(ns)) {
-    double acc[3];
-    spmv_fmt<kStream, kFmt>(a, sl, a.x, nullptr, 0.0, false, acc);
-    const int row = sl * 32 + lane;
-    double bb = 0.0, rz = 0.0, rr = 0.0;
-    if (row < nrows) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const size_t dof = 3 * (size_t)row + c;
-        const double bi = a.b[dof];
-        const double ri = bi - acc[c];
-        const double zi = __ldg(a.dinv + dof) * ri;
-        a.r[dof] = ri;
-        a.z[dof] = zi;
-        a.p0[dof] = zi;
-        bb = __fma_rn(bi, bi, bb);
-        rz = __fma_rn(ri, zi, rz);
-        rr = __fma_rn(ri, ri, rr);
-      }
-    }
-    bb = lane_sum(bb);
-    rz = lane_sum(rz);
-    rr = lane_sum(rr);
-    if (lane == 0) {
-      part(0)[sl] = bb;
-      part(1)[sl] = rz;
-      part(2)[sl] = rr;
-    }
-  }
-  sch.advance(ns);
-  grid.sync();
+  // setup (sparse.cpp:145-157): r = b - A x, z = D^-1 r, p = z; partials b.b, r.z, r.r per unit
   double tot3[3];
-  sum_slices<3>(part(0), ns, tot3, 4 * (size_t)ns);
-  parity ^= 1;
+  {
+    double *u3[3], *c3[3];
+    ptrs3(u3, c3);
+    ph.run<3>(ns, u3, c3, [&](int sl, double (&v)[3]) {
+      double acc[3];
+      spmv_fmt<kStream, kFmt>(a, sl, a.x, nullptr, 0.0, false, acc);
+      const int row = sl * 32 + lane;
+      double bb = 0.0, rz = 0.0, rr = 0.0;
+      if (row < nrows) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const size_t dof = 3 * (size_t)row + c;
+          const double bi = a.b[dof];
+          const double ri = bi - acc[c];
+          const double zi = __ldg(a.dinv + dof) * ri;
+          a.r[dof] = ri;
+          a.z[dof] = zi;
+          a.p0[dof] = zi;
+          bb = __fma_rn(bi, bi, bb);
+          rz = __fma_rn(ri, zi, rz);
+          rr = __fma_rn(ri, ri, rr);
+        }
+      }
+      v[0] = lane_sum(bb);
+      v[1] = lane_sum(rz);
+      v[2] = lane_sum(rr);
+    });
+    grid.sync();
+    sum_phase<3>(u3, c3, G, nwarps, ns, tot3);
+    parity ^= 1;
+  }
   const double bnorm = sqrt(tot3[0]);
   double rz = tot3[1], rr = tot3[2];
   int iterations = 0, converged = 0, negcurv = 0;
@@ -383,7 +526,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       SELL_STAMP(it, 0);
       // ---- phase A: q = A p
       const int nunits = kFmt == 1 ? ns * kR : ns;
-      for (int sl = sch.next(nunits); sl >= 0; sl = sch.next(nunits)) {
+      double *uA[1], *cA[1];
+      ptrs1(uA, cA);
+      ph.run<1>(nunits, uA, cA, [&](int sl, double (&v)[1]) {
         double acc[3];
         int row;
         if constexpr (kFmt == 1 && GF_QREC) {
@@ -403,9 +548,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
               pq = __fma_rn(pr, qr, pq);
             }
           }
-          pq = lane_sum(pq);
-          if (lane == 0) part(0)[sl] = pq;
-          continue;
+          v[0] = lane_sum(pq);
+          return;
         } else if constexpr (kFmt == 1) {
           row = unit_spmv_sym(a, sl, GatherP{pcur, a.z, beta, fused}, acc);
         } else {
@@ -423,10 +567,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
             pq = __fma_rn(pr, acc[c], pq);
           }
         }
-        pq = lane_sum(pq);
-        if (lane == 0) part(0)[sl] = pq;
-      }
-      sch.advance(nunits);
+        v[0] = lane_sum(pq);
+      });
       SELL_STAMP(it, 1);
       SELL_BLOCK_STAMP(it, 3000);
       if (fused && !(kFmt == 1 && GF_QREC)) {
@@ -437,7 +579,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       double pap[1];
       grid.sync();
       SELL_STAMP(it, 5);
-      sum_slices<1>(part(0), nunits, pap, 4 * (size_t)ns);
+      sum_phase<1>(uA, cA, G, nwarps, nunits, pap);
       parity ^= 1;
       SELL_STAMP(it, 2);
       if (pap[0] <= 0.0) {  // sparse.cpp:160-168
@@ -450,7 +592,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       }
       const double alpha = rz / pap[0];
       // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
-      for (int sl = sch.next(ns); sl >= 0; sl = sch.next(ns)) {
+      double *uB[2], *cB[2];
+      ptrs2(uB, cB);
+      ph.run<2>(ns, uB, cB, [&](int sl, double (&v)[2]) {
         double r2 = 0.0, rzp = 0.0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -467,20 +611,15 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
             rzp = __fma_rn(ri, zi, rzp);
           }
         }
-        r2 = lane_sum(r2);
-        rzp = lane_sum(rzp);
-        if (lane == 0) {
-          part(0)[sl] = r2;
-          part(1)[sl] = rzp;
-        }
-      }
-      sch.advance(ns);
+        v[0] = lane_sum(r2);
+        v[1] = lane_sum(rzp);
+      });
       SELL_STAMP(it, 3);
       SELL_BLOCK_STAMP(it, 2000);
       double red2[2];
       grid.sync();
       SELL_STAMP(it, 6);
-      sum_slices<2>(part(0), ns, red2, 4 * (size_t)ns);
+      sum_phase<2>(uB, cB, G, nwarps, ns, red2);
       parity ^= 1;
       SELL_STAMP(it, 4);
       rr = red2[0];
@@ -533,6 +672,11 @@ struct Cg1Vec {
   __device__ __forceinline__ double3 operator()(size_t j) const {
     return make_double3(znew(3 * j), znew(3 * j + 1), znew(3 * j + 2));
   }
+  __device__ __forceinline__ void prefetch(size_t j) const {
+    pf_l1(r + 3 * j);
+    pf_l1(w + 3 * j);
+    pf_l1(s + 3 * j);
+  }
 };
 struct GatherZ0 {  // z_0 = D^-1 r_0
   const double* r;
@@ -541,12 +685,14 @@ struct GatherZ0 {  // z_0 = D^-1 r_0
     return make_double3(__ldg(dinv + 3 * j) * ldv(r + 3 * j), __ldg(dinv + 3 * j + 1) * ldv(r + 3 * j + 1),
                         __ldg(dinv + 3 * j + 2) * ldv(r + 3 * j + 2));
   }
+  __device__ __forceinline__ void prefetch(size_t j) const { pf_l1(r + 3 * j); }
 };
 struct GatherX {
   const double* x;
   __device__ __forceinline__ double3 operator()(size_t j) const {
     return make_double3(ldv(x + 3 * j), ldv(x + 3 * j + 1), ldv(x + 3 * j + 2));
   }
+  __device__ __forceinline__ void prefetch(size_t j) const { pf_l1(x + 3 * j); }
 };
 
 struct Cg1Args {
@@ -566,7 +712,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_cg1(Cg1Args ca) {
   const int ns = a.nslices, nrows = a.nrows, lane = threadIdx.x & 31;
   Sched sch{ca.ctr, 0ull, (unsigned long long)((gridDim.x * blockDim.x) >> 5)};
   int parity = 0;
-  auto part = [&](int q) { return ca.slice_part + ((size_t)parity * 4 + q) * (4 * (size_t)ns); };
+  auto part = [&](int q) { return ca.slice_part + ((size_t)parity * 4 + q) * part_stride(ns); };
   double* rb[2] = {a.r, ca.r2};
   double* wb[2] = {ca.w0, ca.w1};
   double* sb[2] = {ca.s0, ca.s1};
@@ -757,6 +903,13 @@ void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_p
   void* args[] = {&sa};
   const void* fn = mat_format == 1 ? (const void*)k_pcg_sell<true, 1>
                    : stream_matrix ? (const void*)k_pcg_sell<true, 0> : (const void*)k_pcg_sell<false, 0>;
+#ifdef GF_CARVEOUT
+  static bool carve = [fn] {
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, GF_CARVEOUT);
+    return true;
+  }();
+  (void)carve;
+#endif
   const cudaError_t err = cudaLaunchCooperativeKernel(fn, pcg_sell_grid(), kThreads, args, 0, s);
   if (err != cudaSuccess) {
     cudaGetLastError();

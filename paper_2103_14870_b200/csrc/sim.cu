@@ -409,7 +409,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   if (const char* e = std::getenv("GF_CG_MAP")) cg_.mapping = std::atoi(e);
   if (const char* e = std::getenv("GF_CG_KERNEL")) cg_kernel_ = std::atoi(e);
   d_ctr_ = (unsigned long long*)zeros(512);  // [0]: work counter; +64 B: fused-reduce count/gen/totals
-  d_slice_part_ = (double*)zeros(8 * 2 * 4 * 4 * (size_t)d_.nslices);
+  d_slice_part_ = (double*)zeros(8 * 2 * 4 * (4 * (size_t)d_.nslices + 1024));  // part_stride (cg_sell.cu)
   d_cg_extra_ = (double*)zeros(8 * 5 * 3 * (size_t)nn);
   cg_algo_ = 0;  // the single-barrier variant (1) measured slower at c3: 2.98 vs 2.73 ms/step
   if (const char* e = std::getenv("GF_CG_ALGO")) cg_algo_ = std::atoi(e);
