@@ -180,9 +180,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (a.trace && threadIdx.x == 0 && blockIdx.x == 0 && (k) < 200)                 \
       a.trace[(k) * 8 + (point)] = gtimer();                                         \
   } while (0)
-#define SELL_BLOCK_STAMP(k, slot)                                                     \
+#define SELL_BLOCK_STAMP(k, slot) SELL_BLOCK_STAMP_AT(k, 10, slot)
+#define SELL_BLOCK_STAMP_AT(k, at, slot)                                              \
   do {                                                                                \
-    if (a.trace && (k) == 10) {                                                       \
+    if (a.trace && (k) == (at)) {                                                     \
       __syncthreads();                                                                \
       if (threadIdx.x == 0) a.trace[(slot) + blockIdx.x] = gtimer();                 \
     }                                                                                 \
@@ -340,6 +341,14 @@ __device__ __forceinline__ int unit_spmv_sym(const CgLaunch& a, int unit, const 
     for (int o = kRpu; o < 32; o <<= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
   return (t == 0) ? sl * 32 + lr : -1;  // owner lane of the row (or -1)
 }
+
+struct GatherX {
+  const double* x;
+  __device__ __forceinline__ double3 operator()(size_t j) const {
+    return make_double3(ldv(x + 3 * j), ldv(x + 3 * j + 1), ldv(x + 3 * j + 2));
+  }
+  __device__ __forceinline__ void prefetch(size_t j) const { pf_l1(x + 3 * j); }
+};
 
 struct GatherP {  // p_j = fused ? fma(beta, pold_j, z_j) : src_j
   const double* src;
@@ -571,6 +580,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       });
       SELL_STAMP(it, 1);
       SELL_BLOCK_STAMP(it, 3000);
+      SELL_BLOCK_STAMP_AT(it, 20, 4000);
       if (fused && !(kFmt == 1 && GF_QREC)) {
         double* t = pcur;
         pcur = pnext;
@@ -687,13 +697,6 @@ struct GatherZ0 {  // z_0 = D^-1 r_0
   }
   __device__ __forceinline__ void prefetch(size_t j) const { pf_l1(r + 3 * j); }
 };
-struct GatherX {
-  const double* x;
-  __device__ __forceinline__ double3 operator()(size_t j) const {
-    return make_double3(ldv(x + 3 * j), ldv(x + 3 * j + 1), ldv(x + 3 * j + 2));
-  }
-  __device__ __forceinline__ void prefetch(size_t j) const { pf_l1(x + 3 * j); }
-};
 
 struct Cg1Args {
   CgLaunch a;
@@ -710,70 +713,82 @@ __global__ void __launch_bounds__(kThreads) k_pcg_cg1(Cg1Args ca) {
   cg::grid_group grid = cg::this_grid();
   const CgLaunch& a = ca.a;
   const int ns = a.nslices, nrows = a.nrows, lane = threadIdx.x & 31;
-  Sched sch{ca.ctr, 0ull, (unsigned long long)((gridDim.x * blockDim.x) >> 5)};
+  const int nwarps = (int)((gridDim.x * blockDim.x) >> 5), G = (int)gridDim.x;
+  Phase ph{ca.ctr, 0ull, nwarps, (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5))};
   int parity = 0;
-  auto part = [&](int q) { return ca.slice_part + ((size_t)parity * 4 + q) * part_stride(ns); };
+  const size_t qs = part_stride(ns);
+  auto ptrs = [&](double* (&u)[3], double* (&c)[3]) {
+    for (int q = 0; q < 3; ++q) {
+      u[q] = ca.slice_part + ((size_t)parity * 4 + q) * qs;
+      c[q] = u[q] + 4 * (size_t)ns;
+    }
+  };
   double* rb[2] = {a.r, ca.r2};
   double* wb[2] = {ca.w0, ca.w1};
   double* sb[2] = {ca.s0, ca.s1};
   double* pb[2] = {a.p0, a.p1};
 
   // setup 1: r0 = b - A x0; zero s_{-1}, p_{-1}; partial b.b
-  for (int sl = sch.next(ns); sl >= 0; sl = sch.next(ns)) {
-    double acc[3];
-    slice_spmv_sym_g(a, sl, GatherX{a.x}, acc);
-    const int row = sl * 32 + lane;
-    double bb = 0.0;
-    if (row < nrows) {
+  double t1[3];
+  {
+    double *u[3], *c[3];
+    ptrs(u, c);
+    ph.run<3>(ns, u, c, [&](int sl, double (&v)[3]) {
+      double acc[3];
+      unit_spmv_sym(a, sl, GatherX{a.x}, acc);
+      const int row = sl * 32 + lane;
+      double bb = 0.0;
+      if (row < nrows) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const size_t d = 3 * (size_t)row + c;
-        const double bi = a.b[d];
-        rb[0][d] = bi - acc[c];
-        sb[0][d] = 0.0;
-        pb[0][d] = 0.0;
-        bb = __fma_rn(bi, bi, bb);
+        for (int c = 0; c < 3; ++c) {
+          const size_t d = 3 * (size_t)row + c;
+          const double bi = a.b[d];
+          rb[0][d] = bi - acc[c];
+          sb[0][d] = 0.0;
+          pb[0][d] = 0.0;
+          bb = __fma_rn(bi, bi, bb);
+        }
       }
-    }
-    bb = lane_sum(bb);
-    if (lane == 0) part(3)[sl] = bb;
+      v[0] = lane_sum(bb);
+      v[1] = 0.0;
+      v[2] = 0.0;
+    });
+    grid.sync();
+    sum_phase<3>(u, c, G, nwarps, ns, t1);
+    parity ^= 1;
   }
-  sch.advance(ns);
-  grid.sync();
   // setup 2: w0 = A z0; partials r0.z0, z0.w0, r0.r0
-  for (int sl = sch.next(ns); sl >= 0; sl = sch.next(ns)) {
-    double acc[3];
-    slice_spmv_sym_g(a, sl, GatherZ0{rb[0], a.dinv}, acc);
-    const int row = sl * 32 + lane;
-    double rz = 0.0, zw = 0.0, rr = 0.0;
-    if (row < nrows) {
+  double t3[3];
+  {
+    double *u[3], *c[3];
+    ptrs(u, c);
+    ph.run<3>(ns, u, c, [&](int sl, double (&v)[3]) {
+      double acc[3];
+      unit_spmv_sym(a, sl, GatherZ0{rb[0], a.dinv}, acc);
+      const int row = sl * 32 + lane;
+      double rz = 0.0, zw = 0.0, rr = 0.0;
+      if (row < nrows) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const size_t d = 3 * (size_t)row + c;
-        const double ri = ldv(rb[0] + d);
-        const double zi = __ldg(a.dinv + d) * ri;
-        wb[0][d] = acc[c];
-        rz = __fma_rn(ri, zi, rz);
-        zw = __fma_rn(zi, acc[c], zw);
-        rr = __fma_rn(ri, ri, rr);
+        for (int c = 0; c < 3; ++c) {
+          const size_t d = 3 * (size_t)row + c;
+          const double ri = ldv(rb[0] + d);
+          const double zi = __ldg(a.dinv + d) * ri;
+          wb[0][d] = acc[c];
+          rz = __fma_rn(ri, zi, rz);
+          zw = __fma_rn(zi, acc[c], zw);
+          rr = __fma_rn(ri, ri, rr);
+        }
       }
-    }
-    rz = lane_sum(rz);
-    zw = lane_sum(zw);
-    rr = lane_sum(rr);
-    if (lane == 0) {
-      part(0)[sl] = rz;
-      part(1)[sl] = zw;
-      part(2)[sl] = rr;
-    }
+      v[0] = lane_sum(rz);
+      v[1] = lane_sum(zw);
+      v[2] = lane_sum(rr);
+    });
+    grid.sync();
+    sum_phase<3>(u, c, G, nwarps, ns, t3);
+    parity ^= 1;
   }
-  sch.advance(ns);
-  grid.sync();
-  double t4[4];
-  sum_slices<4>(part(0), ns, t4, 4 * (size_t)ns);
-  parity ^= 1;
-  const double bnorm = sqrt(t4[3]);
-  double rz = t4[0], eta = t4[1], rr = t4[2];
+  const double bnorm = sqrt(t1[0]);
+  double rz = t3[0], eta = t3[1], rr = t3[2];
   int iterations = 0, converged = 0, negcurv = 0;
   double relres = 0.0;
   int cur = 0;
@@ -797,9 +812,11 @@ __global__ void __launch_bounds__(kThreads) k_pcg_cg1(Cg1Args ca) {
       SELL_STAMP(it, 0);
       const int nx = cur ^ 1;
       const Cg1Vec gv{rb[cur], wb[cur], sb[cur], a.dinv, alpha, beta};
-      for (int sl = sch.next(ns); sl >= 0; sl = sch.next(ns)) {
+      double *u[3], *c[3];
+      ptrs(u, c);
+      ph.run<3>(ns, u, c, [&](int sl, double (&v)[3]) {
         double acc[3];
-        slice_spmv_sym_g(a, sl, gv, acc);
+        unit_spmv_sym(a, sl, gv, acc);
         const int row = sl * 32 + lane;
         double prz = 0.0, pzw = 0.0, prr = 0.0;
         if (row < nrows) {
@@ -822,25 +839,20 @@ __global__ void __launch_bounds__(kThreads) k_pcg_cg1(Cg1Args ca) {
             prr = __fma_rn(r1, r1, prr);
           }
         }
-        prz = lane_sum(prz);
-        pzw = lane_sum(pzw);
-        prr = lane_sum(prr);
-        if (lane == 0) {
-          part(0)[sl] = prz;
-          part(1)[sl] = pzw;
-          part(2)[sl] = prr;
-        }
-      }
-      sch.advance(ns);
+        v[0] = lane_sum(prz);
+        v[1] = lane_sum(pzw);
+        v[2] = lane_sum(prr);
+      });
       SELL_STAMP(it, 1);
       SELL_BLOCK_STAMP(it, 3000);
+      SELL_BLOCK_STAMP_AT(it, 20, 4000);
       grid.sync();
-      double t3[3];
-      sum_slices<3>(part(0), ns, t3, 4 * (size_t)ns);
+      double t[3];
+      sum_phase<3>(u, c, G, nwarps, ns, t);
       parity ^= 1;
       SELL_STAMP(it, 2);
       cur = nx;
-      rr = t3[2];
+      rr = t[2];
       iterations = it + 1;
       const double rnorm = sqrt(rr);
       if (rnorm / bnorm <= a.tol) {
@@ -849,9 +861,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_cg1(Cg1Args ca) {
         done = true;
         break;
       }
-      beta = t3[0] / rz;
-      eta = t3[1] - beta * t3[0] / alpha;
-      rz = t3[0];
+      beta = t[0] / rz;
+      eta = t[1] - beta * t[0] / alpha;
+      rz = t[0];
     }
     if (!done) {
       relres = sqrt(rr) / bnorm;
