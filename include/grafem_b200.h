@@ -147,6 +147,10 @@ int gf_sim_dynamic_step(gf_sim* s, gf_step_stats* stats);
 int gf_sim_quasi_static_step(gf_sim* s, double t_load, gf_step_stats* stats);
 /* Simulation::newton_tolerance (solver.hpp:92, solver.cpp:57-59) */
 double gf_sim_newton_tolerance(const gf_sim* s);
+/* device layout of the non-local table: 0 local screening (r_d = 0), 1 general sliced-ELL
+ * table, 2 structured template layout (shift-invariant numbering, e.g. make_box_mesh); GF_NL_LAYOUT=general
+ * in the environment forces 1. Runtime utility, no reference counterpart. */
+int32_t gf_sim_nonlocal_layout(const gf_sim* s);
 /* Simulation::damage_pass (solver.hpp:67, solver.cpp:90-103): ascending newly-broken edge ids */
 int gf_sim_damage_pass(gf_sim* s, int32_t* ids, int64_t cap, int64_t* n);
 /* Simulation::state() const / mutable (solver.hpp:79-80): SimState fields (fem.hpp:15-28); NULL skips */

@@ -418,6 +418,10 @@ class Simulation:
     def newton_tolerance(self) -> float:
         return lib().gf_sim_newton_tolerance(self._h)
 
+    def nonlocal_layout(self) -> int:
+        """0: local screening (r_d = 0), 1: general sliced-ELL table, 2: structured template layout."""
+        return lib().gf_sim_nonlocal_layout(self._h)
+
     def damage_pass(self) -> np.ndarray:
         ids = np.zeros(self.E, np.int32)
         n = C.c_int64()

@@ -174,6 +174,7 @@ int gf_sim_quasi_static_step(gf_sim* s, double t_load, gf_step_stats* stats) {
   });
 }
 double gf_sim_newton_tolerance(const gf_sim* s) { return s->s->newton_tolerance(); }
+int32_t gf_sim_nonlocal_layout(const gf_sim* s) { return s->s->nonlocal_layout(); }
 int gf_sim_damage_pass(gf_sim* s, int32_t* ids, int64_t cap, int64_t* n) {
   return guard([&] {
     const auto v = s->s->damage_pass();

@@ -189,66 +189,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
     }                                                                                 \
   } while (0)
 
-// Symmetric format: slot (base | T<<31, j) of row i contributes A p_j (T = 0, upper block (i,j)) or A^T p_j
-// (T = 1, block (j,i) stored by row j); entry q at vals[base + 32 q]. Half the matrix bytes of the full format;
-// the upper blocks (~62 MB at c3) and the CG vectors can stay resident in the 126 MB L2 across iterations.
-template <class G>
-__device__ __forceinline__ void slice_spmv_sym_g(const CgLaunch& a, int sl, const G& gat, double acc[3]) {
-  const int lane = threadIdx.x & 31;
-  const int k0 = __ldg(a.row_ptr + sl), k1 = __ldg(a.row_ptr + sl + 1);
-  const int2* slots = reinterpret_cast<const int2*>(a.cols);
-  acc[0] = acc[1] = acc[2] = 0.0;
-  int2 sc[kGroup];
-#pragma unroll
-  for (int g = 0; g < kGroup; ++g) sc[g] = (k0 + g < k1) ? __ldg(slots + (size_t)(k0 + g) * 32 + lane) : make_int2(0, 0);
-  for (int kb = k0; kb < k1; kb += kGroup) {
-    int2 sn[kGroup];
-#pragma unroll
-    for (int g = 0; g < kGroup; ++g)
-      sn[g] = (kb + kGroup + g < k1) ? __ldg(slots + (size_t)(kb + kGroup + g) * 32 + lane) : make_int2(0, 0);
-#pragma unroll
-    for (int g = 0; g < kGroup; ++g) {
-      if (kb + g < k1) {
-        const size_t j = (size_t)sc[g].y;
-        const bool tr = sc[g].x < 0;
-        const size_t base = (size_t)(sc[g].x & 0x7fffffff);
-        const double3 p = gat(j);
-        const double* v = a.vals + base;
-        double m[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) m[q] = __ldcg(v + 32 * q);
-        if (!tr) {
-          acc[0] = __fma_rn(m[0], p.x, acc[0]); acc[0] = __fma_rn(m[1], p.y, acc[0]); acc[0] = __fma_rn(m[2], p.z, acc[0]);
-          acc[1] = __fma_rn(m[3], p.x, acc[1]); acc[1] = __fma_rn(m[4], p.y, acc[1]); acc[1] = __fma_rn(m[5], p.z, acc[1]);
-          acc[2] = __fma_rn(m[6], p.x, acc[2]); acc[2] = __fma_rn(m[7], p.y, acc[2]); acc[2] = __fma_rn(m[8], p.z, acc[2]);
-        } else {
-          acc[0] = __fma_rn(m[0], p.x, acc[0]); acc[0] = __fma_rn(m[3], p.y, acc[0]); acc[0] = __fma_rn(m[6], p.z, acc[0]);
-          acc[1] = __fma_rn(m[1], p.x, acc[1]); acc[1] = __fma_rn(m[4], p.y, acc[1]); acc[1] = __fma_rn(m[7], p.z, acc[1]);
-          acc[2] = __fma_rn(m[2], p.x, acc[2]); acc[2] = __fma_rn(m[5], p.y, acc[2]); acc[2] = __fma_rn(m[8], p.z, acc[2]);
-        }
-      }
-    }
-#pragma unroll
-    for (int g = 0; g < kGroup; ++g) sc[g] = sn[g];
-  }
-}
-
-#ifndef GF_CG_R
-#define GF_CG_R 1
-#endif
-constexpr int kR = GF_CG_R;  // lanes per row in the symmetric phase-A SpMV (work unit = 32/kR rows of a slice)
-
-// kR lanes cooperate on one row (lane = r + (32/kR) t handles slots t, t+kR, ...; partial sums combined with a
-// fixed xor-shuffle tree): per-lane dependency chains are kR x shorter, so the phase tail (one unit) shrinks.
-#ifndef GF_PF
-#define GF_PF 0
-#endif
+// Symmetric format: the packed slot (j << 6 | c) of row i contributes A_ij p_j when j >= i (c = ordinal of the
+// upper block (i, j) in row i) or A_ji^T p_j when j < i (block (j, i), ordinal c in row j's upper list); c = 63
+// marks a padding slot (the all-zero block at zero_base). Entry q of a block at vals[base + 32 q] with
+// base = (usp[owner / 32] + c) * 288 + owner % 32. 4 bytes per slot; half the matrix bytes of the full format:
+// the upper blocks (~62 MB at c3), the slot list (~7 MB) and the CG vectors stay resident in the 126 MB L2.
 #ifndef GF_MAT_L1
-#define GF_MAT_L1 1
+#define GF_MAT_L1 1  // block values through L1 (the transposed reads of neighbouring slices often hit)
 #endif
-constexpr int kPf = GF_PF;  // L1 prefetch distance in slot groups (0: off)
-
-__device__ __forceinline__ void pf_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 __device__ __forceinline__ double ldmat(const double* p) {
 #if GF_MAT_L1
   return __ldg(p);
@@ -258,69 +206,33 @@ __device__ __forceinline__ double ldmat(const double* p) {
 }
 
 template <class G>
-__device__ __forceinline__ int unit_spmv_sym(const CgLaunch& a, int unit, const G& gat, double acc[3]) {
-  constexpr int kRpu = 32 / kR;
+__device__ __forceinline__ void slice_spmv_sym_g(const CgLaunch& a, int sl, const G& gat, double acc[3]) {
   const int lane = threadIdx.x & 31;
-  const int r = lane % kRpu, t = lane / kRpu;
-  const int sl = unit / kR, lr = (unit % kR) * kRpu + r;
+  const int row = sl * 32 + lane;
   const int k0 = __ldg(a.row_ptr + sl), k1 = __ldg(a.row_ptr + sl + 1);
-  const int2* slots = reinterpret_cast<const int2*>(a.cols);
+  const uint32_t* slots = reinterpret_cast<const uint32_t*>(a.cols);
+  const int own_base = __ldg(a.usp + sl) * 288 + lane;
+  const int zero_base = a.zero_base + lane;
   acc[0] = acc[1] = acc[2] = 0.0;
-  auto slot_at = [&](int k) { return (k < k1) ? __ldg(slots + (size_t)k * 32 + lr) : make_int2(0, 0); };
-  auto prefetch = [&](int k, int2 sv) {
-    if (k < k1) {
-      const double* v = a.vals + (size_t)(sv.x & 0x7fffffff);
+  uint32_t sc[kGroup];
 #pragma unroll
-      for (int q = 0; q < 9; ++q) pf_l1(v + 32 * q);
-      gat.prefetch((size_t)sv.y);
-    }
-  };
-  int2 sc[kGroup];
+  for (int g = 0; g < kGroup; ++g) sc[g] = (k0 + g < k1) ? __ldg(slots + (size_t)(k0 + g) * 32 + lane) : 63u;
+  for (int kb = k0; kb < k1; kb += kGroup) {
+    uint32_t sn[kGroup];
 #pragma unroll
-  for (int g = 0; g < kGroup; ++g) sc[g] = slot_at(k0 + t + kR * g);
-  // prefetch ring: slots of groups 1..kPf ahead are already loaded and their lines requested
-  int2 ring[kPf > 0 ? kPf : 1][kGroup];
-  if constexpr (kPf > 0) {
-#pragma unroll
-    for (int g = 0; g < kGroup; ++g) prefetch(k0 + t + kR * g, sc[g]);
-#pragma unroll
-    for (int d = 0; d < kPf; ++d)
-#pragma unroll
-      for (int g = 0; g < kGroup; ++g) {
-        const int k = k0 + t + kR * ((d + 1) * kGroup + g);
-        ring[d][g] = slot_at(k);
-        prefetch(k, ring[d][g]);
-      }
-  }
-  for (int kb = k0 + t; kb < k1; kb += kR * kGroup) {
-    int2 sn[kGroup];
-    if constexpr (kPf > 0) {
-#pragma unroll
-      for (int g = 0; g < kGroup; ++g) sn[g] = ring[0][g];
-#pragma unroll
-      for (int d = 0; d + 1 < kPf; ++d)
-#pragma unroll
-        for (int g = 0; g < kGroup; ++g) ring[d][g] = ring[d + 1][g];
-#pragma unroll
-      for (int g = 0; g < kGroup; ++g) {
-        const int k = kb + kR * ((kPf + 1) * kGroup + g);
-        ring[kPf - 1][g] = slot_at(k);
-        prefetch(k, ring[kPf - 1][g]);
-      }
-    } else {
-#pragma unroll
-      for (int g = 0; g < kGroup; ++g) sn[g] = slot_at(kb + kR * (kGroup + g));
-    }
+    for (int g = 0; g < kGroup; ++g)
+      sn[g] = (kb + kGroup + g < k1) ? __ldg(slots + (size_t)(kb + kGroup + g) * 32 + lane) : 63u;
 #pragma unroll
     for (int g = 0; g < kGroup; ++g) {
-      if (kb + kR * g < k1) {
-        const size_t j = (size_t)sc[g].y;
-        const bool tr = sc[g].x < 0;
-        const double3 p = gat(j);
-        const double* v = a.vals + (size_t)(sc[g].x & 0x7fffffff);
+      if (kb + g < k1) {
+        const int j = (int)(sc[g] >> 6), c = (int)(sc[g] & 63u);
+        const bool tr = j < row;
+        const int base = c == 63 ? zero_base : tr ? (__ldg(a.usp + (j >> 5)) + c) * 288 + (j & 31) : own_base + 288 * c;
+        const double3 p = gat((size_t)j);
+        const double* v = a.vals + base;
         double m[9];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) m[q] = (kPf > 0) ? __ldg(v + 32 * q) : ldmat(v + 32 * q);
+        for (int q = 0; q < 9; ++q) m[q] = ldmat(v + 32 * q);
         if (!tr) {
           acc[0] = __fma_rn(m[0], p.x, acc[0]); acc[0] = __fma_rn(m[1], p.y, acc[0]); acc[0] = __fma_rn(m[2], p.z, acc[0]);
           acc[1] = __fma_rn(m[3], p.x, acc[1]); acc[1] = __fma_rn(m[4], p.y, acc[1]); acc[1] = __fma_rn(m[5], p.z, acc[1]);
@@ -335,11 +247,6 @@ __device__ __forceinline__ int unit_spmv_sym(const CgLaunch& a, int unit, const 
 #pragma unroll
     for (int g = 0; g < kGroup; ++g) sc[g] = sn[g];
   }
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int o = kRpu; o < 32; o <<= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
-  return (t == 0) ? sl * 32 + lr : -1;  // owner lane of the row (or -1)
 }
 
 struct GatherX {
@@ -347,7 +254,6 @@ struct GatherX {
   __device__ __forceinline__ double3 operator()(size_t j) const {
     return make_double3(ldv(x + 3 * j), ldv(x + 3 * j + 1), ldv(x + 3 * j + 2));
   }
-  __device__ __forceinline__ void prefetch(size_t j) const { pf_l1(x + 3 * j); }
 };
 
 struct GatherP {  // p_j = fused ? fma(beta, pold_j, z_j) : src_j
@@ -355,10 +261,6 @@ struct GatherP {  // p_j = fused ? fma(beta, pold_j, z_j) : src_j
   const double* z;
   double beta;
   bool fused;
-  __device__ __forceinline__ void prefetch(size_t j) const {
-    pf_l1(src + 3 * j);
-    if (fused) pf_l1(z + 3 * j);
-  }
   __device__ __forceinline__ double3 operator()(size_t j) const {
     if (fused)
       return make_double3(__fma_rn(beta, ldv(src + 3 * j), ldv(z + 3 * j)),
@@ -534,7 +436,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       const bool fused = it > 0;
       SELL_STAMP(it, 0);
       // ---- phase A: q = A p
-      const int nunits = kFmt == 1 ? ns * kR : ns;
+      const int nunits = ns;
       double *uA[1], *cA[1];
       ptrs1(uA, cA);
       ph.run<1>(nunits, uA, cA, [&](int sl, double (&v)[1]) {
@@ -543,7 +445,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
         if constexpr (kFmt == 1 && GF_QREC) {
           // A p_{k+1} = A z_{k+1} + beta A p_k: only z is gathered (half the gather traffic of the L2-bound
           // phase); q = A p and p are then updated in place by their row owner.
-          row = unit_spmv_sym(a, sl, GatherP{a.z, nullptr, 0.0, false}, acc);
+          slice_spmv_sym_g(a, sl, GatherP{a.z, nullptr, 0.0, false}, acc);
+          row = sl * 32 + lane;
           double pq = 0.0;
           if (row >= 0 && row < nrows) {
 #pragma unroll
@@ -560,7 +463,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
           v[0] = lane_sum(pq);
           return;
         } else if constexpr (kFmt == 1) {
-          row = unit_spmv_sym(a, sl, GatherP{pcur, a.z, beta, fused}, acc);
+          slice_spmv_sym_g(a, sl, GatherP{pcur, a.z, beta, fused}, acc);
+          row = sl * 32 + lane;
         } else {
           spmv_fmt<kStream, kFmt>(a, sl, pcur, a.z, beta, fused, acc);
           row = sl * 32 + lane;
@@ -682,11 +586,6 @@ struct Cg1Vec {
   __device__ __forceinline__ double3 operator()(size_t j) const {
     return make_double3(znew(3 * j), znew(3 * j + 1), znew(3 * j + 2));
   }
-  __device__ __forceinline__ void prefetch(size_t j) const {
-    pf_l1(r + 3 * j);
-    pf_l1(w + 3 * j);
-    pf_l1(s + 3 * j);
-  }
 };
 struct GatherZ0 {  // z_0 = D^-1 r_0
   const double* r;
@@ -695,7 +594,6 @@ struct GatherZ0 {  // z_0 = D^-1 r_0
     return make_double3(__ldg(dinv + 3 * j) * ldv(r + 3 * j), __ldg(dinv + 3 * j + 1) * ldv(r + 3 * j + 1),
                         __ldg(dinv + 3 * j + 2) * ldv(r + 3 * j + 2));
   }
-  __device__ __forceinline__ void prefetch(size_t j) const { pf_l1(r + 3 * j); }
 };
 
 struct Cg1Args {
@@ -735,7 +633,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_cg1(Cg1Args ca) {
     ptrs(u, c);
     ph.run<3>(ns, u, c, [&](int sl, double (&v)[3]) {
       double acc[3];
-      unit_spmv_sym(a, sl, GatherX{a.x}, acc);
+      slice_spmv_sym_g(a, sl, GatherX{a.x}, acc);
       const int row = sl * 32 + lane;
       double bb = 0.0;
       if (row < nrows) {
@@ -764,7 +662,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_cg1(Cg1Args ca) {
     ptrs(u, c);
     ph.run<3>(ns, u, c, [&](int sl, double (&v)[3]) {
       double acc[3];
-      unit_spmv_sym(a, sl, GatherZ0{rb[0], a.dinv}, acc);
+      slice_spmv_sym_g(a, sl, GatherZ0{rb[0], a.dinv}, acc);
       const int row = sl * 32 + lane;
       double rz = 0.0, zw = 0.0, rr = 0.0;
       if (row < nrows) {
@@ -816,7 +714,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_cg1(Cg1Args ca) {
       ptrs(u, c);
       ph.run<3>(ns, u, c, [&](int sl, double (&v)[3]) {
         double acc[3];
-        unit_spmv_sym(a, sl, gv, acc);
+        slice_spmv_sym_g(a, sl, gv, acc);
         const int row = sl * 32 + lane;
         double prz = 0.0, pzw = 0.0, prr = 0.0;
         if (row < nrows) {

@@ -20,6 +20,9 @@ namespace gfb {
 namespace {
 
 constexpr int kTpb = 256;
+#ifndef GF_NL_MINB
+#define GF_NL_MINB 3  // 3 x 256 threads per SM (<= 80 registers): the non-local gathers are latency bound
+#endif
 
 __device__ __forceinline__ void load_tet_positions(const DevData& d, int4 t, double x[4][3], double du[9]) {
   const int id[4] = {t.x, t.y, t.z, t.w};
@@ -61,8 +64,15 @@ __global__ void __launch_bounds__(kTpb) k_tet_stress(DevData d, MatDev m, int lo
   def_grad(du, B, F);
   const double J = pk1(F, m, P);
   cauchy6(F, P, J, c6);
+  if (d.nl_tpl) {  // cell-major double2 planes (see DevData::nl_tpl)
+    double2* s2 = reinterpret_cast<double2*>(d.sigc);
+    const size_t pos = (size_t)(e % 6) * d.nl_ncell + e / 6;
 #pragma unroll
-  for (int k = 0; k < 6; ++k) d.sigc[6 * (size_t)e + k] = c6[k];
+    for (int p = 0; p < 3; ++p) s2[(size_t)p * d.nt + pos] = make_double2(c6[2 * p], c6[2 * p + 1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 6; ++k) d.sigc[6 * (size_t)e + k] = c6[k];
+  }
 
   int te[6];
   double rl[6], T[6][6], sf[6];
@@ -86,7 +96,7 @@ __global__ void __launch_bounds__(kTpb) k_tet_stress(DevData d, MatDev m, int lo
   }
 }
 
-__global__ void __launch_bounds__(kTpb) k_nonlocal(DevData d) {
+__global__ void __launch_bounds__(kTpb, GF_NL_MINB) k_nonlocal(DevData d) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.nt) return;
   if (d.deg[e]) return;
@@ -113,6 +123,45 @@ __global__ void __launch_bounds__(kTpb) k_nonlocal(DevData d) {
   double rl[6], T[6][6];
   tet_rest_lengths(d, e, te, rl);
   build_T(x, rl, T);  // non-degenerate (checked by k_tet_stress with identical arithmetic)
+  double scr[6];
+  matvec6(T, avg, scr);
+  scatter_max(d, te, scr);
+}
+
+// structured layout: warp = template warp (DevData::nl_tpl); same sums in the same order as k_nonlocal
+__global__ void __launch_bounds__(kTpb, GF_NL_MINB) k_nonlocal_tpl(DevData d) {
+  const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (wid >= d.nl_nwarps) return;
+  const int4 info = __ldg(d.nl_warp + wid);
+  if (lane >= info.z) return;
+  const int e = 6 * (info.y + lane) + info.x;
+  if (d.deg[e]) return;
+  const int j0 = info.w, j1 = __ldg(&d.nl_warp[wid + 1].w);
+  const double2* s2 = reinterpret_cast<const double2*>(d.sigc);
+  const size_t plane = (size_t)d.nt;
+  double avg[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  // loads are unconditional (absent slots read lane 0's record of plane position 0) so consecutive slots
+  // pipeline; an absent slot leaves avg untouched (a select, not a multiply-add: exact whatever it read)
+#pragma unroll 4
+  for (int j = j0; j < j1; ++j) {
+    const double w = __ldcs(d.nl_tw + (size_t)j * 32 + lane);
+    const bool present = w != 0.0;
+    const size_t pos = present ? (size_t)__ldg(d.nl_spos + j) + lane : 0;
+    const double2 s01 = __ldg(s2 + pos), s23 = __ldg(s2 + plane + pos), s45 = __ldg(s2 + 2 * plane + pos);
+    avg[0] = present ? avg[0] + w * s01.x : avg[0];
+    avg[1] = present ? avg[1] + w * s01.y : avg[1];
+    avg[2] = present ? avg[2] + w * s23.x : avg[2];
+    avg[3] = present ? avg[3] + w * s23.y : avg[3];
+    avg[4] = present ? avg[4] + w * s45.x : avg[4];
+    avg[5] = present ? avg[5] + w * s45.y : avg[5];
+  }
+  const int4 t = __ldg(d.tets + e);
+  double x[4][3], du[9];
+  load_tet_positions(d, t, x, du);
+  int te[6];
+  double rl[6], T[6][6];
+  tet_rest_lengths(d, e, te, rl);
+  build_T(x, rl, T);
   double scr[6];
   matvec6(T, avg, scr);
   scatter_max(d, te, scr);
@@ -207,7 +256,10 @@ inline int nblk(int64_t n) { return (int)((n + kTpb - 1) / kTpb); }
 void launch_tet_stress(const DevData& d, const MatDev& m, bool local_screen, cudaStream_t s) {
   k_tet_stress<<<nblk(d.nt), kTpb, 0, s>>>(d, m, local_screen ? 1 : 0);
 }
-void launch_nonlocal(const DevData& d, cudaStream_t s) { k_nonlocal<<<nblk(d.nt), kTpb, 0, s>>>(d); }
+void launch_nonlocal(const DevData& d, cudaStream_t s) {
+  if (d.nl_tpl) k_nonlocal_tpl<<<nblk(32 * (int64_t)d.nl_nwarps), kTpb, 0, s>>>(d);
+  else k_nonlocal<<<nblk(d.nt), kTpb, 0, s>>>(d);
+}
 void launch_relabel(const DevData& d, double thres, bool relabel, bool keep_values, cudaStream_t s) {
   k_relabel<<<nblk(d.ne), kTpb, 0, s>>>(d, thres, relabel ? 1 : 0, keep_values ? 1 : 0);
 }

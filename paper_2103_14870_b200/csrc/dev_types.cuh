@@ -89,13 +89,26 @@ struct DevData {
   int32_t mat_format;       // 0 full SELL-32 values, 1 symmetric upper blocks
   const int32_t* usp;       // nslices+1
   const int32_t* uslot;     // nb
-  const int2* sell_slot;    // 32 * total slots
+  const uint32_t* sell_slot;  // 32 * total slots, packed (j << 6 | c) (cg_sell.cu)
   // non-local table (r_d > 0), sliced-ELL over 32 consecutive tets: entry j of tet e (slice s = e/32) is at
   // (nl_sptr[s] + j) * 32 + e%32, j < nl_len[e]; table order (ascending neighbour id) is preserved per tet
   const int64_t* nl_sptr;
   const int32_t* nl_len;
   const int32_t* nl_ids;
   const double* nl_w;
+  // structured non-local layout (nl_tpl = 1; chosen at setup when the table is shift-invariant, e.g. box meshes):
+  // a "template warp" holds 32 tets of one residue t = e mod 6 in consecutive cells q (e = 6 q + t); its slots
+  // are the union of the lanes' neighbour shifts d = o - e in ascending order (so every lane still visits its
+  // neighbours in table order). Slot j stores the sigma-plane position of lane 0's neighbour (lane k: + k) and
+  // per lane the table weight (0 = not a neighbour of that lane). sigma_c is then stored in cell-major planes
+  // (pos(e) = (e mod 6) * ncell + e / 6, three double2 planes) so the 32 lanes of a slot read 512 contiguous
+  // bytes per plane instead of 32 scattered records.
+  int32_t nl_tpl;
+  int32_t nl_nwarps;
+  int32_t nl_ncell;
+  const int4* nl_warp;      // {t, q0, nlanes, first slot}; slot range ends at the next warp's first slot
+  const int32_t* nl_spos;   // per slot
+  const double* nl_tw;      // per (slot, lane)
   // state
   double* u;                // 3nn
   double* v;                // 3nn
@@ -161,6 +174,8 @@ struct CgLaunch {
   double tol;
   int32_t max_iters;
   int32_t nslices;        // B=3: number of 32-row SELL slices
+  const int32_t* usp;     // symmetric format: upper-block slice pointer (cg_sell.cu slot decoding)
+  int32_t zero_base;      // symmetric format: value offset of the all-zero padding block
   unsigned* barrier;      // 2 zero-initialised words: grid-barrier counter + generation
   int32_t mapping;        // SpMV slice->warp mapping (tuning knob, GF_CG_MAP)
   unsigned long long* trace;  // optional per-phase %globaltimer stamps (GF_CG_TRACE), 2*200*5 entries

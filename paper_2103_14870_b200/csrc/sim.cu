@@ -97,6 +97,65 @@ void* Simulation::dalloc(size_t bytes) {
   return p;
 }
 
+// Structured non-local layout (DevData::nl_tpl): accepted when the table is shift-invariant over tets of one
+// residue mod 6 in consecutive cells (the box generator's numbering, primitives.cpp:26-38), i.e. when the padded
+// template slots cost at most 30% more warp steps than the sliced-ELL table. Any other mesh keeps the general
+// table. Summation order per tet is unchanged (slots ascend in neighbour id).
+template <class Up>
+bool Simulation::build_template_layout(const NonlocalTable& tb, Up&& up) {
+  const int32_t nt = mesh_.nt;
+  if (nt % 6 != 0) return false;
+  const int32_t nc = nt / 6;
+  int64_t ell_steps = 0;
+  for (int32_t sl = 0; sl < (nt + 31) / 32; ++sl) {
+    int64_t mx = 0;
+    for (int32_t e = 32 * sl; e < std::min(nt, 32 * sl + 32); ++e) mx = std::max(mx, tb.ptr[e + 1] - tb.ptr[e]);
+    ell_steps += mx;
+  }
+  const int64_t budget = ell_steps + ell_steps * 3 / 10;
+  std::vector<int4> warps;
+  std::vector<int32_t> spos, sh;
+  std::vector<double> tw;
+  auto fdiv = [](int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+  for (int t = 0; t < 6; ++t)
+    for (int32_t q0 = 0; q0 < nc; q0 += 32) {
+      const int n = (int)std::min<int32_t>(32, nc - q0);
+      sh.clear();
+      for (int k = 0; k < n; ++k) {
+        const int64_t e = 6 * (int64_t)(q0 + k) + t;
+        for (int64_t q = tb.ptr[e]; q < tb.ptr[e + 1]; ++q) sh.push_back((int32_t)(tb.ids[q] - e));
+      }
+      std::sort(sh.begin(), sh.end());
+      sh.erase(std::unique(sh.begin(), sh.end()), sh.end());
+      const int32_t s0 = (int32_t)spos.size();
+      if ((int64_t)s0 + (int64_t)sh.size() > budget) return false;
+      warps.push_back(make_int4(t, q0, n, s0));
+      for (int32_t d : sh) {  // sigma-plane position of lane 0's neighbour o0 = e_0 + d (lane k: + k)
+        const int64_t o0 = 6 * (int64_t)q0 + t + d;
+        spos.push_back((int32_t)((o0 - 6 * fdiv(o0, 6)) * nc + fdiv(o0, 6)));
+      }
+      tw.resize(32 * spos.size(), 0.0);
+      for (int k = 0; k < n; ++k) {
+        const int64_t e = 6 * (int64_t)(q0 + k) + t;
+        for (int64_t q = tb.ptr[e]; q < tb.ptr[e + 1]; ++q) {
+          const int64_t j = std::lower_bound(sh.begin(), sh.end(), (int32_t)(tb.ids[q] - e)) - sh.begin();
+          tw[32 * (size_t)(s0 + j) + k] = tb.w[q];
+        }
+      }
+    }
+  const int32_t nwarps = (int32_t)warps.size();
+  warps.push_back(make_int4(0, 0, 0, (int32_t)spos.size()));
+  d_.nl_tpl = 1;
+  d_.nl_nwarps = nwarps;
+  d_.nl_ncell = nc;
+  d_.nl_warp = (const int4*)up(warps.data(), sizeof(int4) * warps.size());
+  d_.nl_spos = (const int32_t*)up(spos.data(), 4 * spos.size());
+  d_.nl_tw = (const double*)up(tw.data(), 8 * tw.size());
+  nl_tpl_slots_ = (int64_t)spos.size();
+  GF_CUDA(cudaStreamSynchronize(stream_));  // host staging goes out of scope
+  return true;
+}
+
 Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_solver_config& cfg,
                        const gf_boundary_condition* bcs, int32_t n_bcs, const gf_collider* cols, int32_t n_cols)
     : mesh_(mesh), mat_(mat), cfg_(cfg) {
@@ -270,25 +329,25 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
       usp_[sl + 1] = usp_[sl] + mx;
     }
     if ((int64_t)usp_[ns] * 288 >= (int64_t)1 << 31) throw GeometryError("symmetric value array exceeds 31-bit slot bases");
-    auto base_of = [&](int32_t owner, int32_t cu) {
-      return (int32_t)(((int64_t)(usp_[owner >> 5] + cu) * 9) * 32 + (owner & 31));
-    };
-    std::vector<int2> slot(32 * (size_t)sell_slots_);
-    const int32_t zero_base = (int32_t)((int64_t)usp_[ns] * 288);  // one extra all-zero 288-double group
+    // packed slot (j << 6 | c): column block j and the ordinal c of the stored upper block ((i, j) in row i
+    // when j >= i, else (j, i) in row j); c = 63 marks padding (cg_sell.cu decodes the value base)
+    if (nn >= (1 << 26)) throw GeometryError("symmetric slot packing supports < 2^26 nodes");
+    std::vector<uint32_t> slot(32 * (size_t)sell_slots_);
+    zero_base_ = (int32_t)((int64_t)usp_[ns] * 288);  // one extra all-zero 288-double group
     for (int32_t sl = 0; sl < ns; ++sl)
       for (int32_t l = 0; l < 32; ++l) {
         const int32_t i = 32 * sl + l;
         const int32_t deg = i < nn ? pat_.row_ptr[i + 1] - pat_.row_ptr[i] : 0;
         for (int32_t c = 0; c < sell_ptr_[sl + 1] - sell_ptr_[sl]; ++c) {
-          int2 e = make_int2(zero_base + l, i < nn ? i : 0);  // padding: zero block, own row
+          uint32_t e = ((uint32_t)(i < nn ? i : 0) << 6) | 63u;  // padding: zero block, own row
           if (c < deg) {
             const int32_t q = pat_.row_ptr[i] + c, j = pat_.cols[q];
             if (j >= i) {
-              e = make_int2(base_of(i, uslot_[q]), j);
+              e = ((uint32_t)j << 6) | (uint32_t)uslot_[q];
             } else {
               const auto jb = pat_.cols.begin() + pat_.row_ptr[j], je = pat_.cols.begin() + pat_.row_ptr[j + 1];
               const int32_t qj = pat_.row_ptr[j] + (int32_t)(std::lower_bound(jb, je, i) - jb);
-              e = make_int2(base_of(j, uslot_[qj]) | (int32_t)0x80000000u, j);
+              e = ((uint32_t)j << 6) | (uint32_t)uslot_[qj];
             }
           }
           slot[32 * (size_t)(sell_ptr_[sl] + c) + l] = e;
@@ -296,12 +355,16 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
       }
     d_.usp = (const int32_t*)up(usp_.data(), 4 * usp_.size());
     d_.uslot = (const int32_t*)up(uslot_.data(), 4 * uslot_.size());
-    d_.sell_slot = (const int2*)up(slot.data(), 8 * slot.size());
+    d_.sell_slot = (const uint32_t*)up(slot.data(), 4 * slot.size());
     GF_CUDA(cudaStreamSynchronize(stream_));
   }
   if (mat.r_d > 0.0) {
     const NonlocalTable tb = make_nonlocal_table(mesh_, mat.r_d);
     nl_entries_ = (int64_t)tb.ids.size();
+    const char* nl_env = std::getenv("GF_NL_LAYOUT");  // "general" forces the sliced-ELL table
+    if (!(nl_env && std::string(nl_env) == "general") && build_template_layout(tb, up)) {
+      GF_CUDA(cudaStreamSynchronize(stream_));
+    } else {
     const int32_t ns = (nt + 31) / 32;
     std::vector<int64_t> sptr(ns + 1, 0);
     std::vector<int32_t> len(nt);
@@ -325,6 +388,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     d_.nl_ids = (const int32_t*)up(ids.data(), 4 * ids.size());
     d_.nl_w = (const double*)up(w.data(), 8 * w.size());
     GF_CUDA(cudaStreamSynchronize(stream_));  // host staging goes out of scope
+    }
   } else {
     nl_entries_ = nt;
   }
@@ -397,6 +461,8 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   cg_.nrows = nn;
   cg_.row_ptr = d_.sell_ptr;
   cg_.cols = mat_format_ ? reinterpret_cast<const int32_t*>(d_.sell_slot) : d_.sell_col;
+  cg_.usp = d_.usp;
+  cg_.zero_base = zero_base_;
   cg_.nslices = d_.nslices;
   cg_.vals = d_.bval;
   cg_.b = d_.rhs;
@@ -881,8 +947,20 @@ void Simulation::last_system(double* vals, double* rhs) {
 
 void Simulation::eval_cauchy(double* sigma6) {
   launch("tet_stress", 0.0, [&] { launch_tet_stress(d_, md_, false, stream_); });
-  GF_CUDA(cudaMemcpyAsync(sigma6, d_.sigc, 48 * (size_t)mesh_.nt, cudaMemcpyDeviceToHost, stream_));
+  if (!d_.nl_tpl) {
+    GF_CUDA(cudaMemcpyAsync(sigma6, d_.sigc, 48 * (size_t)mesh_.nt, cudaMemcpyDeviceToHost, stream_));
+    synchronize();
+    return;
+  }
+  const size_t nt = (size_t)mesh_.nt;
+  std::vector<double> planes(6 * nt);
+  GF_CUDA(cudaMemcpyAsync(planes.data(), d_.sigc, 48 * nt, cudaMemcpyDeviceToHost, stream_));
   synchronize();
+  for (size_t e = 0; e < nt; ++e) {
+    const size_t pos = (e % 6) * (size_t)d_.nl_ncell + e / 6;
+    for (int p = 0; p < 3; ++p)
+      for (int c = 0; c < 2; ++c) sigma6[6 * e + 2 * p + c] = planes[2 * (p * nt + pos) + c];
+  }
 }
 
 void Simulation::eval_screening(double* screening, double* sigma_f6, uint8_t* degenerate) {

@@ -44,6 +44,7 @@ class Simulation {
   gf_step_stats dynamic_step();
   gf_step_stats quasi_static_step(double t_load);
   double newton_tolerance() const { return newton_tol_; }
+  int32_t nonlocal_layout() const { return mat_.r_d <= 0.0 ? 0 : d_.nl_tpl ? 2 : 1; }
   std::vector<int32_t> damage_pass();
   void get_state(double* u, double* v, uint8_t* zeta, double* chi, double* time);
   void set_state(const double* u, const double* v, const uint8_t* zeta, const double* chi, const double* time);
@@ -87,11 +88,14 @@ class Simulation {
   void apply_boundary_displacements(double t);
   bool newton_solve(gf_step_stats& st);
   void launch_cg();
+  template <class Up>
+  bool build_template_layout(const NonlocalTable& tb, Up&& up);
 
   HostMesh mesh_;
   NodePattern pat_;
   std::vector<int32_t> sell_ptr_;
   int64_t sell_slots_ = 0;
+  int32_t zero_base_ = 0;
   int mat_format_ = 1;
   std::vector<int32_t> usp_, uslot_;
   size_t bval_doubles_ = 0;
@@ -104,6 +108,7 @@ class Simulation {
   std::vector<double> fuser_;
   uint64_t hash_ = 0;
   int64_t nl_entries_ = 0;
+  int64_t nl_tpl_slots_ = 0;
   double time_ = 0.0, last_load_ = 0.0;
   double newton_tol_ = 0.0, quasi_time_ = 0.0;
   double* d_usave_ = nullptr;    // line-search base displacements (quasi-static only, allocated on first use)

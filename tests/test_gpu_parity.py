@@ -564,3 +564,37 @@ def test_gpu_quasi_static_fixed_load_and_halving_match_oracle():  # solver.cpp:1
         # increment <= 0: re-solve at the same load (fixed-load branch)
         a, b = os_.quasi_static_step(1.0), gs.quasi_static_step(1.0)
         assert a.newton_iterations == b.newton_iterations == 0
+
+
+# ---------------------------------------------------------------- non-local table layouts
+@pytest.mark.parametrize("layout", ["template", "general"])
+@pytest.mark.parametrize("cells,rd_h", [((8, 8, 7), 2.0), ((7, 5, 9), 1.5), ((6, 9, 5), 3.1)])
+def test_nonlocal_layouts_bit_exact(layout, cells, rd_h, monkeypatch):
+    """Both device layouts of the non-local table give the oracle's screening values, labels and chi bit for
+    bit, including ragged template warps (cells not a multiple of 32) and other radii."""
+    if layout == "general":
+        monkeypatch.setenv("GF_NL_LAYOUT", "general")
+    s = cf.scaled("c3", cells)
+    s.r_d = rd_h * cf.H
+    rng = np.random.default_rng(41)
+    gs, os_, gm, om = pair(s, rng, disp=0.3, damage=0.2, chi_random=True)
+    assert gs.nonlocal_layout() == (2 if layout == "template" else 1)
+    st = os_.get_state()
+    sig = om.per_tet_cauchy(os_.mat, st["u"])
+    assert same_bits_or_zero(gs.eval_cauchy(), sig)
+    ref_scr, ref_sf, ref_deg = om.nonlocal_screen(st["u"], sig, s.r_d)
+    scr, sf, deg = gs.eval_screening()
+    assert np.array_equal(deg, ref_deg) and same_bits_or_zero(scr, ref_scr) and same_bits_or_zero(sf, ref_sf)
+    assert np.array_equal(gs.damage_pass(), os_.damage_pass())
+    assert same_bits_or_zero(gs.state().element_chi, os_.get_state()["chi"])
+
+
+def test_nonlocal_layout_falls_back_for_unstructured_meshes():
+    node = "5 3 0 0\n1 0 0 0\n2 1 0 0\n3 0 1 0\n4 0 0 1\n5 1 1 1\n"
+    ele = "2 4 0\n1 1 2 3 4\n2 2 3 4 5\n"
+    sg = g.Simulation(g.load_tetgen(node, ele), g.MaterialParams.from_youngs(1e6, 0.3, 1000, 10.0, 0.7, g.STVK),
+                      g.SolverConfig(dt=1e-3))
+    assert sg.nonlocal_layout() == 1
+    s0 = g.Simulation(g.make_box_mesh((0.1, 0.1, 0.1), (2, 2, 2)),
+                      g.MaterialParams.from_youngs(1e6, 0.3, 1000, 10.0, 0.0, g.STVK), g.SolverConfig(dt=1e-3))
+    assert s0.nonlocal_layout() == 0
