@@ -23,11 +23,12 @@ constexpr int kWarps = 4;
 constexpr int kMaxValence = 32;  // tets per node handled by one warp (validated at setup)
 constexpr int kMaxDeg = 32;      // column blocks per node row (validated at setup)
 
-// contribution of tet e to node-row i (local index li): force on i (returned) and the four blocks K(li, lj),
-// written straight to shared memory (blk[9*lj + r]) so they never occupy registers together
+// contribution of tet e to node-row i (local index li): force on i (returned), the diagonal block K(li, li)
+// (returned in dg) and the three off-diagonal blocks K(li, lj), written straight to shared memory at slot
+// s = lj < li ? lj : lj - 1 (blk[9 s + r]) so they never occupy registers together
 template <bool kBlocks>
 __device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, int e, int li, double scale,
-                                            double f[3], double* blk) {
+                                            double f[3], double* blk, double dg[9]) {
   const int4 t = __ldg(d.tets + e);
   const int id[4] = {t.x, t.y, t.z, t.w};
   double B[9], du[9], F[9];
@@ -86,7 +87,8 @@ __device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, i
         for (int c = 0; c < 3; ++c) {
           const double v = (r == c ? gSg : 0.0) + m.mu * aj[r] * ai[c] + m.mu * gij * FFt[3 * r + c] +
                            m.lambda * ai[r] * aj[c];
-          blk[9 * lj + 3 * r + c] = scale * v;
+          if (lj == li) dg[3 * r + c] = scale * v;
+          else blk[9 * (lj < li ? lj : lj - 1) + 3 * r + c] = scale * v;
         }
     }
   } else {
@@ -122,7 +124,8 @@ __device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, i
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double v = (r == c ? c1 * gij : 0.0) + c2 * ai[r] * aj[c] + m.lambda * bi[r] * bj[c] + c4 * hj[3 * r + c];
-          blk[9 * lj + 3 * r + c] = scale * v;
+          if (lj == li) dg[3 * r + c] = scale * v;
+          else blk[9 * (lj < li ? lj : lj - 1) + 3 * r + c] = scale * v;
         }
     }
   }
@@ -135,19 +138,22 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // One warp per node row i:
-//  1. lane l < valence(i) evaluates the l-th incident tet (ascending id): force on i -> s_frc, blocks -> s_blk
+//  1. lane l < valence(i) evaluates the l-th incident tet (ascending id): force and diagonal block are warp
+//     sums, the three off-diagonal blocks go to s_blk
 //  2. the row's 9*deg outputs (column c, entry q) are spread over the 32 lanes; each sums its precomputed
 //     contribution list (ascending tet order, deterministic) from s_blk into s_row
 //  3. lane c finishes column block c: K v, A = kscale K + mscale M, Dirichlet projection, SELL-32 store
+#ifndef GF_ASM_MINB
+#define GF_ASM_MINB 4
+#endif
 template <int kMode>
-__global__ void __launch_bounds__(32 * kWarps, 4) k_assemble(DevData d, MatDev m, StepCoeffs sc) {
+__global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d, MatDev m, StepCoeffs sc) {
   constexpr bool kBlocks = kMode != kAssembleForcesOnly;
-  extern __shared__ double s_dyn[];  // kBlocks: s_blk[kWarps][32 * 36] (dynamic: > 48 KB static limit)
-  double(*s_blk)[32 * 36] = reinterpret_cast<double(*)[32 * 36]>(s_dyn);
+  extern __shared__ double s_dyn[];  // kBlocks: s_blk[kWarps][32 * 27] (dynamic: > 48 KB static limit)
+  double(*s_blk)[32 * 27] = reinterpret_cast<double(*)[32 * 27]>(s_dyn);
   __shared__ double s_row[kBlocks ? kWarps : 1][kMaxDeg * 9];
-  __shared__ double s_frc[kWarps][32][3];
   __shared__ int s_cptr[kBlocks ? kWarps : 1][kMaxDeg + 1];
-  __shared__ uint8_t s_item[kBlocks ? kWarps : 1][4 * kMaxValence];
+  __shared__ uint8_t s_item[kBlocks ? kWarps : 1][3 * kMaxValence];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kWarps + w;
   if (i >= d.nn) return;
@@ -155,43 +161,59 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_assemble(DevData d, MatDev m
   const int row0 = __ldg(d.brow + i), deg = __ldg(d.brow + i + 1) - row0;
 
   double f[3] = {0.0, 0.0, 0.0};
+  double dg[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   if (lane < np) {
     const int e = __ldg(d.nt_tet + p0 + lane);
     const int4 t = __ldg(d.tets + e);
     const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
     const double scale = d.chi[e] * __ldg(d.vol + e);
-    double* blk = kBlocks ? &s_blk[w][36 * lane] : nullptr;
+    double* blk = kBlocks ? &s_blk[w][27 * lane] : nullptr;
     if (scale != 0.0) {  // fem.cpp:51 / fem.cpp:114 early-out
-      element_row<kBlocks>(d, m, e, li, scale, f, blk);
+      element_row<kBlocks>(d, m, e, li, scale, f, blk, dg);
     } else if (kBlocks) {
 #pragma unroll
-      for (int r = 0; r < 36; ++r) blk[r] = 0.0;
+      for (int r = 0; r < 27; ++r) blk[r] = 0.0;
     }
   }
+  // the row's force (fem.cpp:104-106) and its diagonal block (every incident tet contributes) are fixed
+  // butterfly sums over the lanes; only the off-diagonal blocks (the ~5 tets around each edge) go through
+  // the contribution lists below
+  double fsum = 0.0;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) s_frc[w][lane][a] = f[a];
-  __syncwarp();
-  double fsum = 0.0;  // lanes 0..2: force component, ascending tet order (fem.cpp:104-106)
-  if (lane < 3)
-    for (int l = 0; l < np; ++l) fsum += s_frc[w][l][lane];
+  for (int a = 0; a < 3; ++a) {
+    const double t = warp_sum(f[a]);
+    if (lane == a) fsum = t;
+  }
 
   const bool fixed_i = __ldg(d.node_bc + i) >= 0;
   double kv[3] = {0.0, 0.0, 0.0}, corr[3] = {0.0, 0.0, 0.0};
   if (kBlocks) {
+    const int jc = lane < deg ? __ldg(d.bcol + row0 + lane) : -1;
+    const int cdiag = __ffs(__ballot_sync(0xffffffffu, jc == i)) - 1;
+    double dsum = 0.0;  // lane q < 9: entry q of the diagonal block
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const double t = warp_sum(dg[q]);
+      if (lane == q) dsum = t;
+    }
     // the row's contribution lists (<= 4 * 32 items, <= 33 offsets) staged in shared memory by one coalesced
     // warp load each, so the reduction below touches only shared memory
     const int ibase = __ldg(d.contrib_ptr + row0);
     if (lane <= deg) s_cptr[w][lane] = __ldg(d.contrib_ptr + row0 + lane) - ibase;
-    const int nitems = 4 * np;
+    const int nitems = 3 * np;
     for (int k = lane; k < nitems; k += 32) s_item[w][k] = __ldg(d.contrib_item + ibase + k);
     __syncwarp();
-    for (int o = lane; o < 9 * deg; o += 32) {
-      const int c = o / 9, q = o - 9 * c;
+    // off-diagonal outputs (column c != cdiag, entry q), 9 (deg - 1) of them spread over the lanes
+    for (int o = lane; o < 9 * (deg - 1); o += 32) {
+      int c = o / 9;
+      const int q = o - 9 * c;
+      c += (c >= cdiag) ? 1 : 0;
       const int it0 = s_cptr[w][c], it1 = s_cptr[w][c + 1];
       double sum = 0.0;
       for (int it = it0; it < it1; ++it) sum += s_blk[w][9 * (int)s_item[w][it] + q];
-      s_row[w][o] = sum;
+      s_row[w][9 * c + q] = sum;
     }
+    if (lane < 9) s_row[w][9 * cdiag + lane] = dsum;
     __syncwarp();
     const int c = lane;
     if (c < deg) {
@@ -208,7 +230,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_assemble(DevData d, MatDev m
 #pragma unroll
           for (int r = 0; r < 9; ++r) out[ostride * r] = K[r];
       } else {
-        const int j = __ldg(d.bcol + row0 + c);
+        const int j = jc;
         double vj[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) vj[a] = d.v[3 * (size_t)j + a];
@@ -323,7 +345,7 @@ __global__ void __launch_bounds__(256) k_energy(DevData d, MatDev m, double* par
 
 void launch_assemble(const DevData& d, const MatDev& m, const StepCoeffs& c, int mode, cudaStream_t s) {
   const int grid = (d.nn + kWarps - 1) / kWarps;
-  constexpr int kDyn = kWarps * 32 * 36 * sizeof(double);
+  constexpr int kDyn = kWarps * 32 * 27 * sizeof(double);
   static bool attr = [] {
     cudaFuncSetAttribute(k_assemble<kAssembleSystem>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
     cudaFuncSetAttribute(k_assemble<kAssembleRawK>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);

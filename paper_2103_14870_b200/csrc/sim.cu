@@ -270,18 +270,31 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   d_.nt_ptr = (const int32_t*)up(ntets.ptr.data(), 4 * ntets.ptr.size());
   d_.nt_tet = (const int32_t*)up(ntets.tet.data(), 4 * ntets.tet.size());
   d_.nt_slot = (const uint32_t*)up(ntets.slot.data(), 4 * ntets.slot.size());
-  {  // contribution lists of the assembly reduction (assemble.cu): per block, items l*4+k, ascending l
+  {  // contribution lists of the assembly reduction (assemble.cu): per off-diagonal block, items 3 l + s
+     // (lane l = incident tet, s = its off-diagonal block slot), ascending l; diagonal blocks are warp sums
+    auto col_of = [&](int32_t q, int k) { return (int32_t)((ntets.slot[q] >> (8 * k)) & 0xff); };
+    auto local_of = [&](int32_t i, int32_t q) {
+      for (int k = 0; k < 4; ++k)
+        if (pat_.cols[pat_.row_ptr[i] + col_of(q, k)] == i) return k;
+      throw std::logic_error("incidence slot without the diagonal");
+    };
     std::vector<int32_t> cnt(pat_.cols.size() + 1, 0);
     for (int32_t i = 0; i < nn; ++i)
-      for (int32_t q = ntets.ptr[i]; q < ntets.ptr[i + 1]; ++q)
-        for (int k = 0; k < 4; ++k) cnt[pat_.row_ptr[i] + ((ntets.slot[q] >> (8 * k)) & 0xff) + 1]++;
+      for (int32_t q = ntets.ptr[i]; q < ntets.ptr[i + 1]; ++q) {
+        const int li = local_of(i, q);
+        for (int k = 0; k < 4; ++k)
+          if (k != li) cnt[pat_.row_ptr[i] + col_of(q, k) + 1]++;
+      }
     for (size_t b = 0; b < pat_.cols.size(); ++b) cnt[b + 1] += cnt[b];
     std::vector<uint8_t> items(cnt.back());
     std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
     for (int32_t i = 0; i < nn; ++i)
-      for (int32_t q = ntets.ptr[i]; q < ntets.ptr[i + 1]; ++q)
+      for (int32_t q = ntets.ptr[i]; q < ntets.ptr[i + 1]; ++q) {
+        const int li = local_of(i, q);
         for (int k = 0; k < 4; ++k)
-          items[cur[pat_.row_ptr[i] + ((ntets.slot[q] >> (8 * k)) & 0xff)]++] = (uint8_t)(4 * (q - ntets.ptr[i]) + k);
+          if (k != li)
+            items[cur[pat_.row_ptr[i] + col_of(q, k)]++] = (uint8_t)(3 * (q - ntets.ptr[i]) + (k < li ? k : k - 1));
+      }
     d_.contrib_ptr = (const int32_t*)up(cnt.data(), 4 * cnt.size());
     d_.contrib_item = (const uint8_t*)up(items.data(), items.size());
     GF_CUDA(cudaStreamSynchronize(stream_));
