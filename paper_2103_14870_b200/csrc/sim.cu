@@ -424,6 +424,9 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   d_.newly = (int32_t*)zeros(4 * (size_t)ne);
   d_.newly_count = (int32_t*)zeros(8);
   bval_doubles_ = mat_format_ ? 288 * ((size_t)usp_[d_.nslices] + 1) : 288 * (size_t)sell_slots_;
+  // GF_PAD_MB: allocation-placement experiment (tools/ab_pad.sh); the PCG time depends on where the system
+  // matrix lands in physical memory by up to ~8%
+  if (const char* e = std::getenv("GF_PAD_MB")) dalloc((size_t)std::atol(e) << 20);
   d_.bval = (double*)zeros(8 * bval_doubles_);  // padding slots / the extra zero block stay zero
   d_.rhs = (double*)zeros(8 * nd);
   d_.dinv = (double*)zeros(8 * nd);
