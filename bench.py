@@ -151,7 +151,7 @@ def run_cpu(s, steps, budget_s):
 def config_dict(s, scaling_note):
     return {"workload": s.name, "tets": s.num_tets, "cells": list(s.cells), "r_d_m": s.r_d, "dt": s.dt,
             "cg_tol": s.cg_tol, "material": "stable_neo_hookean" if s.model == 0 else "stvk",
-            "l2": "inputs larger than L2: BSR system matrix (~122 MB) + non-local table (~1.5 GB) streamed per step",
+            "l2": "inputs larger than L2: non-local table (~1.2 GB) + per-tet data streamed every step; the symmetric system matrix (~64 MB) is rebuilt each step and stays L2-resident only within the PCG",
             "parallelism": scaling_note}
 
 
