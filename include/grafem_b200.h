@@ -196,11 +196,10 @@ int gf_sim_synchronize(gf_sim* s);
  * the elapsed milliseconds between two recorded slots (synchronizes) */
 int gf_sim_timer_record(gf_sim* s, int32_t slot);
 int gf_sim_timer_elapsed(gf_sim* s, int32_t slot_a, int32_t slot_b, double* ms);
-/* diagnostics: %globaltimer stamps of the last CG solve, [block 0 | last block][iteration < 200][5 phase points]
- * (only when GF_CG_TRACE is set in the environment at gf_sim_create) */
+/* diagnostics: %globaltimer stamps of the last PCG solve (5000 words): CTA 0's 8 phase points per iteration
+ * (< 200) at [8 it + point], per-CTA phase ends of iterations 10 and 20 at [2000 + cta], [3000 + cta], [4000 + cta]
+ * (only when GF_CG_TRACE is set in the environment at gf_sim_create; tools/cg_trace.py, tools/cg_spread.py) */
 int gf_sim_cg_trace(gf_sim* s, uint64_t* out);
-/* diagnostics: microseconds per grid barrier (variant 0 cooperative-groups, 1 custom) */
-double gf_debug_barrier_bench(int32_t variant, int32_t iters, int32_t blocks, int32_t threads);
 /* select the CUDA device for subsequently created simulations (one process per GPU) */
 int gf_set_device(int32_t device);
 int gf_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor, char* name, int32_t name_cap);

@@ -220,10 +220,10 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
       double K[9];
 #pragma unroll
       for (int r = 0; r < 9; ++r) K[r] = s_row[w][9 * c + r];
-      // destination: SELL-32 (entry r at out[32 r]) or the upper block (entry r at out[r]); lower blocks of the
+      // destination: the upper block in SELL-32 (entry r at out[32 r]); lower blocks of the
       // symmetric format are not stored (row j writes (j,i) = (i,j)^T)
-      const int cu = d.mat_format ? __ldg(d.uslot + row0 + c) : c;
-      double* out = cu >= 0 ? d.bval + sell_addr(d.mat_format ? d.usp : d.sell_ptr, i, cu, 0) : nullptr;
+      const int cu = __ldg(d.uslot + row0 + c);
+      double* out = cu >= 0 ? d.bval + sell_addr(d.usp, i, cu, 0) : nullptr;
       constexpr int ostride = 32;
       if (kMode == kAssembleRawK) {
         if (out)

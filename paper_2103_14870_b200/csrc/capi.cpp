@@ -10,9 +10,6 @@
 #include "host_mesh.hpp"
 #include "sim.hpp"
 
-namespace gfb {
-double barrier_bench(int variant, int iters, int blocks, int threads);
-}
 using namespace gfb;
 
 struct gf_mesh {
@@ -265,9 +262,6 @@ int gf_sim_timer_elapsed(gf_sim* s, int32_t a, int32_t b, double* ms) {
 }
 int gf_sim_cg_trace(gf_sim* s, uint64_t* out) {
   return guard([&] { s->s->cg_trace(reinterpret_cast<unsigned long long*>(out)); });
-}
-double gf_debug_barrier_bench(int32_t variant, int32_t iters, int32_t blocks, int32_t threads) {
-  return gfb::barrier_bench(variant, iters, blocks, threads);
 }
 int gf_set_device(int32_t device) {
   return guard([&] {

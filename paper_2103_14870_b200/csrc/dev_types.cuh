@@ -73,20 +73,15 @@ struct DevData {
   // node-block pattern (CSR view: column ids per row, ascending)
   const int32_t* brow;      // nn+1
   const int32_t* bcol;      // nb
-  const int32_t* bdiag;     // nn: position of the diagonal block within the row
-  // SELL-32 storage of the system matrix values: slices of 32 consecutive node rows; slice s owns slots
-  // sell_ptr[s]..sell_ptr[s+1] (max row degree of the slice); entry q of block (row i, slot c) lives at
-  // ((sell_ptr[i/32] + c) * 9 + q) * 32 + i%32, so a warp owning a slice reads every slot coalesced.
+  // System matrix, symmetric SELL-32: slices of 32 consecutive node rows; only the upper blocks (j >= i) are
+  // stored: slice s owns upper slots usp[s]..usp[s+1] (max upper degree of its rows), entry q of upper block
+  // (i, c_u) at ((usp[i/32] + c_u) * 9 + q) * 32 + i%32, so a warp owning a slice reads every slot coalesced.
+  // uslot[b] maps a CSR block (row i, column c) to c_u, or -1 when j < i (that block is (j,i)^T, stored by row
+  // j). The SpMV slot list (SELL-32 over the full row in column order; slice s owns slots sell_ptr[s]..
+  // sell_ptr[s+1]) holds packed (j << 6 | c) words (cg_sell.cu). For interior rows the neighbour offsets are
+  // uniform across a slice, so both direct and transposed block reads coalesce.
   const int32_t* sell_ptr;  // nslices+1
-  const int32_t* sell_col;  // 32 * total slots (padding slots point at the row itself, zero values)
   int32_t nslices;
-  // symmetric format (mat_format == 1, default): only the upper blocks (j >= i) are stored, in their own SELL-32
-  // layout (slice s owns upper slots usp[s]..usp[s+1]; entry q of upper block (i, c_u) at
-  // ((usp[i/32] + c_u) * 9 + q) * 32 + i%32). uslot[b] maps a CSR block (row i, column c) to c_u, or -1 when
-  // j < i (that block is (j,i)^T, stored by row j). The SpMV slot list (SELL-32 over the full row, column order)
-  // holds int2 {value base | transpose<<31, j}; entry q of the slot's block is at base + 32 q. For interior
-  // rows the neighbour offsets are uniform across a slice, so both direct and transposed reads coalesce.
-  int32_t mat_format;       // 0 full SELL-32 values, 1 symmetric upper blocks
   const int32_t* usp;       // nslices+1
   const int32_t* uslot;     // nb
   const uint32_t* sell_slot;  // 32 * total slots, packed (j << 6 | c) (cg_sell.cu)
@@ -161,35 +156,30 @@ void launch_assemble(const DevData& d, const MatDev& m, const StepCoeffs& c, int
 void launch_energy(const DevData& d, const MatDev& m, double* out_partials, int nblocks, cudaStream_t s);
 // ---- cg.cu ----
 struct CgLaunch {
-  int32_t nrows;          // block rows (B=3: nodes) or scalar rows (B=1)
-  const int32_t* row_ptr; // B=1: scalar CSR; B=3: SELL-32 slice pointer
-  const int32_t* cols;    // B=1: CSR columns; B=3: SELL-32 slot columns
+  int32_t nrows;          // node rows (cg_sell.cu) or scalar rows (cg.cu)
+  const int32_t* row_ptr; // cg_sell.cu: SELL-32 slice pointer (full-row slots); cg.cu: scalar CSR row pointer
+  const int32_t* cols;    // cg_sell.cu: packed symmetric slots (uint32); cg.cu: CSR columns
   const double* vals;
   const double* b;
   double* x;
-  const double* dinv;     // may be null: computed from the diagonal
-  double* r; double* z; double* p0; double* p1; double* Ap;
-  double* partials;
+  const double* dinv;     // cg_sell.cu: from the assembly; cg.cu: computed from the diagonal
+  double* r; double* z; double* p0; double* p1; double* Ap;  // p1: cg.cu only (double-buffered p)
+  double* partials;       // cg.cu block partials
   double* out;            // [iterations, converged, negative_curvature, relative_residual]
   double tol;
   int32_t max_iters;
-  int32_t nslices;        // B=3: number of 32-row SELL slices
-  const int32_t* usp;     // symmetric format: upper-block slice pointer (cg_sell.cu slot decoding)
-  int32_t zero_base;      // symmetric format: value offset of the all-zero padding block
-  unsigned* barrier;      // 2 zero-initialised words: grid-barrier counter + generation
-  int32_t mapping;        // SpMV slice->warp mapping (tuning knob, GF_CG_MAP)
-  unsigned long long* trace;  // optional per-phase %globaltimer stamps (GF_CG_TRACE), 2*200*5 entries
+  int32_t nslices;        // cg_sell.cu: number of 32-row SELL slices
+  const int32_t* usp;     // cg_sell.cu: upper-block slice pointer (slot decoding)
+  int32_t zero_base;      // cg_sell.cu: value offset of the all-zero padding block
+  unsigned long long* trace;  // optional per-phase %globaltimer stamps (GF_CG_TRACE)
 };
-int cg_grid_size(int block_size);
-void launch_pcg3(const CgLaunch& a, cudaStream_t s);
-void launch_pcg1(const CgLaunch& a, cudaStream_t s);
-void launch_spmv3(const CgLaunch& a, const double* xin, double* y, cudaStream_t s);
-// ---- cg_sell.cu (production solver on the SELL-32 matrix) ----
+int cg_csr_grid();
+void launch_pcg_csr(const CgLaunch& a, cudaStream_t s);  // scalar CSR (gf_cg_solve_csr)
+// ---- cg_sell.cu (production solver on the symmetric SELL-32 matrix) ----
 int pcg_sell_grid();
-void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_part, cudaStream_t s, int mat_format);
-// single-barrier (Chronopoulos-Gear) PCG on the symmetric format; extra = 5 x 3N doubles (r2, w0, w1, s0, s1)
-void launch_pcg_cg1(const CgLaunch& a, unsigned long long* ctr, double* slice_part, double* extra, cudaStream_t s);
-void launch_spmv_fmt(const CgLaunch& a, const double* xin, double* y, int mat_format, cudaStream_t s);
+size_t pcg_sell_part_doubles(int nslices);  // size of the slice_part work array
+void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_part, cudaStream_t s);
+void launch_spmv_sym(const CgLaunch& a, const double* xin, double* y, cudaStream_t s);
 // ---- misc.cu ----
 void launch_bc_targets(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, double dt, cudaStream_t s);
 int collide_blocks(const DevData& d);

@@ -15,7 +15,7 @@ constexpr int kTpb = 256;
 inline int nblk(int64_t n) { return (int)((n + kTpb - 1) / kTpb); }
 
 __device__ __forceinline__ const double* diag_block(const DevData& d, int i) {  // entry q at [32 q]
-  return d.mat_format ? d.bval + sell_addr(d.usp, i, 0, 0) : d.bval + sell_addr(d.sell_ptr, i, d.bdiag[i], 0);
+  return d.bval + sell_addr(d.usp, i, 0, 0);  // the diagonal is the first upper block of its row
 }
 
 __device__ __forceinline__ void bc_disp(const BcStep& b, const double* X, const double* R, const double* d,

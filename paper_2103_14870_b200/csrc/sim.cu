@@ -302,10 +302,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   d_.brow = (const int32_t*)up(pat_.row_ptr.data(), 4 * pat_.row_ptr.size());
   d_.bcol = (const int32_t*)up(pat_.cols.data(), 4 * pat_.cols.size());
   {
-    std::vector<int32_t> dpos(nn);
-    for (int32_t i = 0; i < nn; ++i) dpos[i] = pat_.diag[i] - pat_.row_ptr[i];
-    d_.bdiag = (const int32_t*)up(dpos.data(), 4 * dpos.size());
-    // SELL-32 slices (dev_types.cuh): slots per slice = max degree of its 32 rows
+    // SELL-32 slices (dev_types.cuh): full-row slots per slice = max degree of its 32 rows
     const int32_t ns = (nn + 31) / 32;
     sell_ptr_.assign(ns + 1, 0);
     for (int32_t sl = 0; sl < ns; ++sl) {
@@ -313,23 +310,10 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
       for (int32_t i = 32 * sl; i < std::min(nn, 32 * sl + 32); ++i) mx = std::max(mx, pat_.row_ptr[i + 1] - pat_.row_ptr[i]);
       sell_ptr_[sl + 1] = sell_ptr_[sl] + mx;
     }
-    std::vector<int32_t> scol(32 * (size_t)sell_ptr_[ns]);
-    for (int32_t sl = 0; sl < ns; ++sl)
-      for (int32_t k = sell_ptr_[sl]; k < sell_ptr_[sl + 1]; ++k)
-        for (int32_t l = 0; l < 32; ++l) {
-          const int32_t i = 32 * sl + l, c = k - sell_ptr_[sl];
-          int32_t col = 0;
-          if (i < nn) col = (c < pat_.row_ptr[i + 1] - pat_.row_ptr[i]) ? pat_.cols[pat_.row_ptr[i] + c] : i;
-          scol[32 * (size_t)k + l] = col;
-        }
     d_.sell_ptr = (const int32_t*)up(sell_ptr_.data(), 4 * sell_ptr_.size());
-    d_.sell_col = (const int32_t*)up(scol.data(), 4 * scol.size());
     d_.nslices = ns;
     sell_slots_ = sell_ptr_[ns];
-    // symmetric format: upper blocks (j >= i) in upper-CSR order + SELL-32 slot list {block | T<<31, j}
-    mat_format_ = 1;
-    if (const char* e = std::getenv("GF_MATRIX")) mat_format_ = std::string(e) == "full" ? 0 : 1;
-    d_.mat_format = mat_format_;
+    // symmetric format: upper blocks (j >= i) in upper-CSR order per row, SELL-32 over slices
     uslot_.assign(pat_.cols.size(), -1);
     std::vector<int32_t> ucount(nn, 0);
     for (int32_t i = 0; i < nn; ++i)
@@ -423,7 +407,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   d_.screening = (double*)zeros(8 * (size_t)ne);
   d_.newly = (int32_t*)zeros(4 * (size_t)ne);
   d_.newly_count = (int32_t*)zeros(8);
-  bval_doubles_ = mat_format_ ? 288 * ((size_t)usp_[d_.nslices] + 1) : 288 * (size_t)sell_slots_;
+  bval_doubles_ = 288 * ((size_t)usp_[d_.nslices] + 1);  // + one all-zero padding group
   // GF_PAD_MB: allocation-placement experiment (tools/ab_pad.sh); the PCG time depends on where the system
   // matrix lands in physical memory by up to ~8%
   if (const char* e = std::getenv("GF_PAD_MB")) dalloc((size_t)std::atol(e) << 20);
@@ -440,9 +424,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   d_.r = (double*)zeros(8 * nd);
   d_.z = (double*)zeros(8 * nd);
   d_.p0 = (double*)zeros(8 * nd);
-  d_.p1 = (double*)zeros(8 * nd);
   d_.Ap = (double*)zeros(8 * nd);
-  d_.partials = (double*)zeros(8 * 2 * 3 * (size_t)std::max(cg_grid_size(3), cg_grid_size(1)));
   d_.cg_out = (double*)zeros(8 * 8);
   d_.n_colliders = (int32_t)cols_.size();
   const int nsub = cfg.collision_substeps;
@@ -476,7 +458,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
 
   cg_.nrows = nn;
   cg_.row_ptr = d_.sell_ptr;
-  cg_.cols = mat_format_ ? reinterpret_cast<const int32_t*>(d_.sell_slot) : d_.sell_col;
+  cg_.cols = reinterpret_cast<const int32_t*>(d_.sell_slot);
   cg_.usp = d_.usp;
   cg_.zero_base = zero_base_;
   cg_.nslices = d_.nslices;
@@ -484,17 +466,10 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   cg_.b = d_.rhs;
   cg_.x = d_.x;
   cg_.dinv = d_.dinv;
-  cg_.r = d_.r; cg_.z = d_.z; cg_.p0 = d_.p0; cg_.p1 = d_.p1; cg_.Ap = d_.Ap;
-  cg_.partials = d_.partials;
+  cg_.r = d_.r; cg_.z = d_.z; cg_.p0 = d_.p0; cg_.Ap = d_.Ap;
   cg_.out = d_.cg_out;
-  cg_.barrier = (unsigned*)zeros(64);
-  if (const char* e = std::getenv("GF_CG_MAP")) cg_.mapping = std::atoi(e);
-  if (const char* e = std::getenv("GF_CG_KERNEL")) cg_kernel_ = std::atoi(e);
-  d_ctr_ = (unsigned long long*)zeros(512);  // [0]: work counter; +64 B: fused-reduce count/gen/totals
-  d_slice_part_ = (double*)zeros(8 * 2 * 4 * (4 * (size_t)d_.nslices + 1024));  // part_stride (cg_sell.cu)
-  d_cg_extra_ = (double*)zeros(8 * 5 * 3 * (size_t)nn);
-  cg_algo_ = 0;  // the single-barrier variant (1) measured slower at c3: 2.98 vs 2.73 ms/step
-  if (const char* e = std::getenv("GF_CG_ALGO")) cg_algo_ = std::atoi(e);
+  d_ctr_ = (unsigned long long*)zeros(64);  // ticket counter of the PCG work distribution
+  d_slice_part_ = (double*)zeros(8 * pcg_sell_part_doubles(d_.nslices));
   if (std::getenv("GF_CG_TRACE")) cg_.trace = (unsigned long long*)zeros(8 * 5000);
   cg_.tol = cfg.cg_tol;
   GF_CUDA(cudaStreamSynchronize(stream_));
@@ -628,9 +603,7 @@ void Simulation::upload_bc_step(double t, double dt) {
 }
 
 void Simulation::launch_cg() {
-  if (mat_format_ == 1 && cg_algo_ == 1) launch_pcg_cg1(cg_, d_ctr_, d_slice_part_, d_cg_extra_, stream_);
-  else if (cg_kernel_ == 0 || mat_format_ == 1) launch_pcg_sell(cg_, d_ctr_, d_slice_part_, stream_, mat_format_);
-  else launch_pcg3(cg_, stream_);
+  launch_pcg_sell(cg_, d_ctr_, d_slice_part_, stream_);
 }
 
 double Simulation::run_cg(int max_iters) {
@@ -928,9 +901,7 @@ void Simulation::bsr_to_csr(const std::vector<double>& bval, double* vals) const
     for (int32_t q = 0; q < deg; ++q) {
       const int32_t j = pat_.cols[r0 + q];
       double blk[9];
-      if (mat_format_ == 0) {
-        for (int r = 0; r < 9; ++r) blk[r] = bval[sell_addr(sell_ptr_.data(), i, q, r)];
-      } else if (j >= i) {
+      if (j >= i) {
         for (int r = 0; r < 9; ++r) blk[r] = bval[sell_addr(usp_.data(), i, uslot_[r0 + q], r)];
       } else {  // (i,j) = (j,i)^T
         const auto jb = pat_.cols.begin() + pat_.row_ptr[j], je = pat_.cols.begin() + pat_.row_ptr[j + 1];
@@ -990,7 +961,7 @@ void Simulation::eval_screening(double* screening, double* sigma_f6, uint8_t* de
 void Simulation::spmv(const double* x, double* y) {
   const size_t nd = 3 * (size_t)mesh_.nn;
   GF_CUDA(cudaMemcpyAsync(d_.z, x, 8 * nd, cudaMemcpyHostToDevice, stream_));
-  launch("spmv", 0.0, [&] { launch_spmv_fmt(cg_, d_.z, d_.Ap, mat_format_, stream_); });
+  launch("spmv", 0.0, [&] { launch_spmv_sym(cg_, d_.z, d_.Ap, stream_); });
   GF_CUDA(cudaMemcpyAsync(y, d_.Ap, 8 * nd, cudaMemcpyDeviceToHost, stream_));
   synchronize();
 }
@@ -1056,10 +1027,8 @@ void cg_solve_csr(int32_t n, const int32_t* row_ptr, const int32_t* cols, const 
     a.p0 = (double*)alloc(8 * (size_t)n);
     a.p1 = (double*)alloc(8 * (size_t)n);
     a.Ap = (double*)alloc(8 * (size_t)n);
-    a.partials = (double*)alloc(8 * 2 * 3 * (size_t)cg_grid_size(1));
+    a.partials = (double*)alloc(8 * 2 * 3 * (size_t)cg_csr_grid());
     a.out = (double*)alloc(8 * 4);
-    a.barrier = (unsigned*)alloc(64);
-    GF_CUDA(cudaMemsetAsync(a.barrier, 0, 64, s));
     a.tol = tol;
     a.max_iters = max_iters;
     GF_CUDA(cudaMemcpyAsync((void*)a.row_ptr, row_ptr, 4 * (size_t)(n + 1), cudaMemcpyHostToDevice, s));
@@ -1067,7 +1036,7 @@ void cg_solve_csr(int32_t n, const int32_t* row_ptr, const int32_t* cols, const 
     GF_CUDA(cudaMemcpyAsync((void*)a.vals, vals, 8 * (size_t)nnz, cudaMemcpyHostToDevice, s));
     GF_CUDA(cudaMemcpyAsync((void*)a.b, b, 8 * (size_t)n, cudaMemcpyHostToDevice, s));
     GF_CUDA(cudaMemcpyAsync(a.x, x, 8 * (size_t)n, cudaMemcpyHostToDevice, s));
-    launch_pcg1(a, s);
+    launch_pcg_csr(a, s);
     double out[4];
     GF_CUDA(cudaMemcpyAsync(out, a.out, 32, cudaMemcpyDeviceToHost, s));
     GF_CUDA(cudaMemcpyAsync(x, a.x, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));

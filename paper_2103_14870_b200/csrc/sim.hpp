@@ -96,7 +96,6 @@ class Simulation {
   std::vector<int32_t> sell_ptr_;
   int64_t sell_slots_ = 0;
   int32_t zero_base_ = 0;
-  int mat_format_ = 1;
   std::vector<int32_t> usp_, uslot_;
   size_t bval_doubles_ = 0;
   gf_material mat_;
@@ -119,11 +118,8 @@ class Simulation {
   cudaStream_t stream_ = nullptr;
   DevData d_{};
   CgLaunch cg_{};
-  int cg_kernel_ = 0;  // 0: dynamic-schedule SELL kernel (cg_sell.cu), 1: static kernel (cg.cu)
   unsigned long long* d_ctr_ = nullptr;
   double* d_slice_part_ = nullptr;
-  double* d_cg_extra_ = nullptr;
-  int cg_algo_ = 0;  // 0: two-barrier PCG (default), 1: single-barrier Chronopoulos-Gear PCG (symmetric format)
   std::vector<void*> allocs_;
   int32_t* d_fixed_nodes_ = nullptr;
   BcStep* d_bcstep_ = nullptr;
