@@ -3,7 +3,7 @@
 //   k_bc_targets  prescribed dv / u(t+dt) / v(t+dt) of BC nodes (solver.cpp:255-262, 322-328)
 //   k_collide     per-vertex penalty + impulse + Coulomb response (detect_and_respond, collision.cpp:49-111)
 //                 on the substep probe u + tau v (solver.cpp:233-249), block partials for the load
-//   k_integrate   v += dv, u += dt v, then pin BC nodes (solver.cpp:296-328)
+//   k_integrate   v += dv, u += dt v, then pin BC nodes (solver.cpp:296-328); no-op unless the PCG converged
 //   k_qs_bc / k_qs_update / k_dot  quasi-static Newton helpers (solver.cpp:138-217)
 //   k_shift_diag  shift_diagonal on the node-block matrix (solver.cpp:119-129 ladder)
 #include "device_math.cuh"
@@ -162,7 +162,10 @@ __global__ void k_collide_load(const double* partials, int nblocks, int nc, int 
   if (threadIdx.x == 0) out[0] = best;
 }
 
+// enqueued right behind the PCG: it commits the step only when the solve converged (cg_out[1]), so the host
+// needs no round trip before it; after a failed solve the host runs the ladder and enqueues it again
 __global__ void k_integrate(DevData d, double dt) {
+  if (d.cg_out[1] == 0.0) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d.nn) return;
   const bool fixed = d.node_bc[i] >= 0;

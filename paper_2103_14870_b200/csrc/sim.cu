@@ -701,6 +701,7 @@ gf_step_stats Simulation::dynamic_step() {
   // solve_linear (solver.cpp:105-136): first attempt, 4x retry, then cumulative diagonal shifts
   cg_.max_iters = cfg_.cg_max_iters;
   launch("pcg", 0.0, [&] { launch_cg(); });
+  launch("integrate", 40 * n, [&] { launch_integrate(d_, dt, stream_); });  // B_int = 40n; no-op if not converged
   GF_CUDA(cudaMemcpyAsync(h_stats_, d_.cg_out, 32, cudaMemcpyDeviceToHost, stream_));
   GF_CUDA(cudaMemcpyAsync(h_stats_ + 4, d_load_, 8, cudaMemcpyDeviceToHost, stream_));
   GF_CUDA(cudaMemcpyAsync(h_stats_ + 5, d_.newly_count, 4, cudaMemcpyDeviceToHost, stream_));
@@ -717,8 +718,10 @@ gf_step_stats Simulation::dynamic_step() {
   st.load = last_load_;
   st.cg_iterations = (int32_t)h_stats_[0];
   account(h_stats_[0]);
-  solve_ladder(h_stats_[1] != 0.0, &st.cg_iterations, account);
-  launch("integrate", 40 * n, [&] { launch_integrate(d_, dt, stream_); });  // B_int = 40n
+  if (h_stats_[1] == 0.0) {
+    solve_ladder(false, &st.cg_iterations, account);
+    launch("integrate", 40 * n, [&] { launch_integrate(d_, dt, stream_); });
+  }
   time_ = t + dt;
   st.residual = 0.0;
   return st;
