@@ -5,8 +5,9 @@
 //   phase A  q = A p_k through q_k = A z_k + beta q_{k-1} (only z is gathered; p and q are updated in place by
 //            their row owner), partial p.q                                   -> barrier, pAp
 //   phase B  x += alpha p, r -= alpha q, z = D^-1 r, partials r.r and r.z   -> barrier, rr, rz
-// Work distribution (class Phase): warp w takes 32-row slice w statically, any remainder comes from a ticket
-// counter requested one unit ahead. Determinism: statically taken units are reduced per CTA in warp order, the
+// Work distribution (class Phase): warp w of CTA b takes slice cta_first[b] + w statically (ranges balanced by
+// slot count on the host, <= one slice per warp), any remainder comes from a ticket counter requested one unit
+// ahead. Determinism: statically taken units are reduced per CTA in warp order, the
 // dynamic ones keep one partial each, and after the barrier every CTA sums [CTA partials, unit partials] in one
 // fixed order, so alpha, beta and the stop decisions are bit-identical in every CTA and from run to run.
 #include <cooperative_groups.h>
@@ -157,31 +158,35 @@ struct GatherZ {
 struct Phase {
   unsigned long long* ctr;
   unsigned long long base;
-  int nwarps, gw;
+  const int32_t* cta_first;  // static units of CTA b: [cta_first[b], cta_first[b + 1]), one per warp
+  __device__ __forceinline__ int nstatic() const { return __ldg(cta_first + gridDim.x); }
   template <int NV, class Body>
   __device__ __forceinline__ void run(int n, double* const (&part)[NV], double* const (&cta)[NV], Body&& body) {
     __shared__ double s_acc[kWarpsPerCta][4];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const unsigned long long nd = n > nwarps ? (unsigned long long)(n - nwarps) : 0ull;
+    const int ns0 = nstatic();
+    const unsigned long long nd = n > ns0 ? (unsigned long long)(n - ns0) : 0ull;
+    const unsigned long long nwarps = (gridDim.x * blockDim.x) >> 5;
     unsigned long long tk = 0;
     if (nd && lane == 0) tk = atomicAdd(ctr, 1ull);
     double sv[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) sv[q] = 0.0;
-    if (gw < n) body(gw, sv);
+    const int mine = __ldg(cta_first + blockIdx.x) + w;
+    if (mine < __ldg(cta_first + blockIdx.x + 1) && mine < n) body(mine, sv);
     if (nd) {
       for (;;) {
         const unsigned long long idx = __shfl_sync(0xffffffffu, tk, 0) - base;
         if (idx >= nd) break;
         if (lane == 0) tk = atomicAdd(ctr, 1ull);
-        const int u = nwarps + (int)idx;
+        const int u = ns0 + (int)idx;
         double v[NV];
         body(u, v);
         if (lane == 0)
 #pragma unroll
           for (int q = 0; q < NV; ++q) part[q][u] = v[q];
       }
-      base += nd + (unsigned long long)nwarps;
+      base += nd + nwarps;
     }
     if (lane == 0)
 #pragma unroll
@@ -195,13 +200,13 @@ struct Phase {
   }
 };
 
-// sum over [cta[0..G), part[nwarps..n)] in one fixed order (thread stride, then a fixed block tree)
+// sum over [cta[0..G), part[ns0..n)] in one fixed order (thread stride, then a fixed block tree)
 template <int NV>
-__device__ __forceinline__ void sum_phase(double* const (&part)[NV], double* const (&cta)[NV], int G, int nwarps,
+__device__ __forceinline__ void sum_phase(double* const (&part)[NV], double* const (&cta)[NV], int G, int ns0,
                                           int n, double (&out)[NV]) {
   __shared__ double s_w[kWarpsPerCta][4];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int nd = n > nwarps ? n - nwarps : 0, total = G + nd;
+  const int nd = n > ns0 ? n - ns0 : 0, total = G + nd;
   constexpr int kB = 4;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
@@ -211,7 +216,7 @@ __device__ __forceinline__ void sum_phase(double* const (&part)[NV], double* con
 #pragma unroll
       for (int b = 0; b < kB; ++b) {
         const int k = k0 + b * (int)blockDim.x + (int)threadIdx.x;
-        v[b] = (k < G) ? __ldcg(cta[q] + k) : (k < total) ? __ldcg(part[q] + nwarps + (k - G)) : 0.0;
+        v[b] = (k < G) ? __ldcg(cta[q] + k) : (k < total) ? __ldcg(part[q] + ns0 + (k - G)) : 0.0;
       }
 #pragma unroll
       for (int b = 0; b < kB; ++b) x += v[b];
@@ -234,8 +239,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
   cg::grid_group grid = cg::this_grid();
   const CgLaunch& a = sa.a;
   const int ns = a.nslices, nrows = a.nrows, lane = threadIdx.x & 31;
-  const int nwarps = (int)((gridDim.x * blockDim.x) >> 5), G = (int)gridDim.x;
-  Phase ph{sa.ctr, 0ull, nwarps, (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5))};
+  const int G = (int)gridDim.x;
+  Phase ph{sa.ctr, 0ull, a.cta_first};
+  const int ns0 = ph.nstatic();
   int parity = 0;
   const size_t qs = part_stride(ns);
   auto ptrs = [&](auto& u, auto& c) {  // unit and CTA partial arrays of the current parity
@@ -275,7 +281,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       v[2] = lane_sum(rr);
     });
     grid.sync();
-    sum_phase<3>(u3, c3, G, nwarps, ns, tot3);
+    sum_phase<3>(u3, c3, G, ns0, ns, tot3);
     parity ^= 1;
   }
   const double bnorm = sqrt(tot3[0]);
@@ -322,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       double pap[1];
       grid.sync();
       SELL_STAMP(it, 5);
-      sum_phase<1>(uA, cA, G, nwarps, ns, pap);
+      sum_phase<1>(uA, cA, G, ns0, ns, pap);
       parity ^= 1;
       SELL_STAMP(it, 2);
       if (pap[0] <= 0.0) {  // sparse.cpp:160-168
@@ -361,7 +367,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       double red2[2];
       grid.sync();
       SELL_STAMP(it, 6);
-      sum_phase<2>(uB, cB, G, nwarps, ns, red2);
+      sum_phase<2>(uB, cB, G, ns0, ns, red2);
       parity ^= 1;
       SELL_STAMP(it, 4);
       rr = red2[0];
@@ -419,6 +425,7 @@ int pcg_sell_grid() {
 }
 
 size_t pcg_sell_part_doubles(int nslices) { return 2 * 4 * part_stride(nslices); }
+int pcg_sell_warps_per_cta() { return kWarpsPerCta; }
 
 void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_part, cudaStream_t s) {
   SellArgs sa{a, ctr, slice_part};
