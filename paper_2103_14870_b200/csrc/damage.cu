@@ -129,7 +129,11 @@ __global__ void __launch_bounds__(kTpb, GF_NL_MINB) k_nonlocal(DevData d) {
 }
 
 // structured layout: warp = template warp (DevData::nl_tpl); same sums in the same order as k_nonlocal
-__global__ void __launch_bounds__(kTpb, GF_NL_MINB) k_nonlocal_tpl(DevData d) {
+#ifndef GF_NL_TPB
+#define GF_NL_TPB 384  // two 32-cell ranges x six residues per CTA
+#endif
+constexpr int kNlTpb = GF_NL_TPB;  // template warps per CTA x 32
+__global__ void __launch_bounds__(kNlTpb, (GF_NL_MINB * 256) / kNlTpb) k_nonlocal_tpl(DevData d) {
   const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (wid >= d.nl_nwarps) return;
   const int4 info = __ldg(d.nl_warp + wid);
@@ -257,7 +261,7 @@ void launch_tet_stress(const DevData& d, const MatDev& m, bool local_screen, cud
   k_tet_stress<<<nblk(d.nt), kTpb, 0, s>>>(d, m, local_screen ? 1 : 0);
 }
 void launch_nonlocal(const DevData& d, cudaStream_t s) {
-  if (d.nl_tpl) k_nonlocal_tpl<<<nblk(32 * (int64_t)d.nl_nwarps), kTpb, 0, s>>>(d);
+  if (d.nl_tpl) k_nonlocal_tpl<<<(int)((32 * (int64_t)d.nl_nwarps + kNlTpb - 1) / kNlTpb), kNlTpb, 0, s>>>(d);
   else k_nonlocal<<<nblk(d.nt), kTpb, 0, s>>>(d);
 }
 void launch_relabel(const DevData& d, double thres, bool relabel, bool keep_values, cudaStream_t s) {

@@ -117,8 +117,10 @@ bool Simulation::build_template_layout(const NonlocalTable& tb, Up&& up) {
   std::vector<int32_t> spos, sh;
   std::vector<double> tw;
   auto fdiv = [](int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
-  for (int t = 0; t < 6; ++t)
-    for (int32_t q0 = 0; q0 < nc; q0 += 32) {
+  // warp order: the six residues of one 32-cell range are consecutive (one CTA), so their neighbourhoods — the
+  // same cells — are gathered while still in L1
+  for (int32_t q0 = 0; q0 < nc; q0 += 32)
+    for (int t = 0; t < 6; ++t) {
       const int n = (int)std::min<int32_t>(32, nc - q0);
       sh.clear();
       for (int k = 0; k < n; ++k) {
