@@ -5,13 +5,13 @@
 //   phase A  q = A p_k through q_k = A z_k + beta q_{k-1} (only z is gathered; p and q are updated in place by
 //            their row owner), partial p.q                                   -> barrier, pAp
 //   phase B  x += alpha p, r -= alpha q, z = D^-1 r, partials r.r and r.z   -> barrier, rr, rz
-// Work distribution (class Phase): warp w of CTA b takes slice cta_first[b] + w statically (ranges balanced by
-// slot count on the host, <= one slice per warp), any remainder comes from a ticket counter requested one unit
-// ahead. Determinism: statically taken units are reduced per CTA in warp order, the
-// dynamic ones keep one partial each, and after the barrier every CTA sums [CTA partials, unit partials] in one
-// fixed order, so alpha, beta and the stop decisions are bit-identical in every CTA and from run to run.
+// Work distribution (class Phase): CTA b owns the slice range [cta_first[b], cta_first[b+1]) (balanced by slot
+// count on the host), its warps stride through it; no atomics. Determinism: unit values are summed per warp
+// in unit order and per CTA in warp order, and after the barrier every CTA sums the CTA partials in one fixed
+// order, so alpha, beta and the stop decisions are bit-identical in every CTA and from run to run.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -32,8 +32,7 @@ constexpr int kWarpsPerCta = kThreads / 32;
 
 struct SellArgs {
   CgLaunch a;
-  unsigned long long* ctr;  // dynamic slice counter (zeroed by the host before the launch)
-  double* slice_part;       // 2 parities x 4 values x part_stride(nslices)
+  double* cta_part;  // 2 parities x 4 values x kMaxGrid CTA partials
 };
 
 __device__ __forceinline__ double lane_sum(double v) {  // fixed butterfly: same bits in every lane
@@ -156,37 +155,22 @@ struct GatherZ {
 };
 
 struct Phase {
-  unsigned long long* ctr;
-  unsigned long long base;
-  const int32_t* cta_first;  // static units of CTA b: [cta_first[b], cta_first[b + 1]), one per warp
-  __device__ __forceinline__ int nstatic() const { return __ldg(cta_first + gridDim.x); }
+  const int32_t* cta_first;  // units (slices) of CTA b: [cta_first[b], cta_first[b + 1])
+  // warp w of the CTA takes units first + w, first + w + W, ... (consecutive warps on consecutive slices); the
+  // unit values are summed per warp in unit order and per CTA in warp order: one partial per CTA, fixed order
   template <int NV, class Body>
-  __device__ __forceinline__ void run(int n, double* const (&part)[NV], double* const (&cta)[NV], Body&& body) {
+  __device__ __forceinline__ void run(double* const (&cta)[NV], Body&& body) {
     __shared__ double s_acc[kWarpsPerCta][4];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int ns0 = nstatic();
-    const unsigned long long nd = n > ns0 ? (unsigned long long)(n - ns0) : 0ull;
-    const unsigned long long nwarps = (gridDim.x * blockDim.x) >> 5;
-    unsigned long long tk = 0;
-    if (nd && lane == 0) tk = atomicAdd(ctr, 1ull);
     double sv[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) sv[q] = 0.0;
-    const int mine = __ldg(cta_first + blockIdx.x) + w;
-    if (mine < __ldg(cta_first + blockIdx.x + 1) && mine < n) body(mine, sv);
-    if (nd) {
-      for (;;) {
-        const unsigned long long idx = __shfl_sync(0xffffffffu, tk, 0) - base;
-        if (idx >= nd) break;
-        if (lane == 0) tk = atomicAdd(ctr, 1ull);
-        const int u = ns0 + (int)idx;
-        double v[NV];
-        body(u, v);
-        if (lane == 0)
+    const int u1 = __ldg(cta_first + blockIdx.x + 1);
+    for (int u = __ldg(cta_first + blockIdx.x) + w; u < u1; u += kWarpsPerCta) {
+      double v[NV];
+      body(u, v);
 #pragma unroll
-          for (int q = 0; q < NV; ++q) part[q][u] = v[q];
-      }
-      base += nd + nwarps;
+      for (int q = 0; q < NV; ++q) sv[q] += v[q];
     }
     if (lane == 0)
 #pragma unroll
@@ -200,27 +184,15 @@ struct Phase {
   }
 };
 
-// sum over [cta[0..G), part[ns0..n)] in one fixed order (thread stride, then a fixed block tree)
+// sum of the G CTA partials in one fixed order (thread k loads partial k, fixed lane and warp trees)
 template <int NV>
-__device__ __forceinline__ void sum_phase(double* const (&part)[NV], double* const (&cta)[NV], int G, int ns0,
-                                          int n, double (&out)[NV]) {
+__device__ __forceinline__ void sum_phase(double* const (&cta)[NV], int G, double (&out)[NV]) {
   __shared__ double s_w[kWarpsPerCta][4];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int nd = n > ns0 ? n - ns0 : 0, total = G + nd;
-  constexpr int kB = 4;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
     double x = 0.0;
-    for (int k0 = 0; k0 < total; k0 += kB * (int)blockDim.x) {
-      double v[kB];
-#pragma unroll
-      for (int b = 0; b < kB; ++b) {
-        const int k = k0 + b * (int)blockDim.x + (int)threadIdx.x;
-        v[b] = (k < G) ? __ldcg(cta[q] + k) : (k < total) ? __ldcg(part[q] + ns0 + (k - G)) : 0.0;
-      }
-#pragma unroll
-      for (int b = 0; b < kB; ++b) x += v[b];
-    }
+    for (int k = threadIdx.x; k < G; k += blockDim.x) x += __ldcg(cta[q] + k);
     x = lane_sum(x);
     if (lane == 0) s_w[w][q] = x;
   }
@@ -233,30 +205,25 @@ __device__ __forceinline__ void sum_phase(double* const (&part)[NV], double* con
   __syncthreads();
 }
 
-__host__ __device__ inline size_t part_stride(int ns) { return 4 * (size_t)ns + 1024; }
+constexpr int kMaxGrid = 1024;  // CTA partial slots per value
 
 __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
   cg::grid_group grid = cg::this_grid();
   const CgLaunch& a = sa.a;
   const int ns = a.nslices, nrows = a.nrows, lane = threadIdx.x & 31;
   const int G = (int)gridDim.x;
-  Phase ph{sa.ctr, 0ull, a.cta_first};
-  const int ns0 = ph.nstatic();
+  Phase ph{a.cta_first};
   int parity = 0;
-  const size_t qs = part_stride(ns);
-  auto ptrs = [&](auto& u, auto& c) {  // unit and CTA partial arrays of the current parity
-    for (int q = 0; q < (int)(sizeof(u) / sizeof(u[0])); ++q) {
-      u[q] = sa.slice_part + ((size_t)parity * 4 + q) * qs;
-      c[q] = u[q] + 4 * (size_t)ns;
-    }
+  auto ptrs = [&](auto& c) {  // CTA partial arrays of the current parity
+    for (int q = 0; q < (int)(sizeof(c) / sizeof(c[0])); ++q) c[q] = sa.cta_part + ((size_t)parity * 4 + q) * kMaxGrid;
   };
 
   // setup (sparse.cpp:145-157): r = b - A x, z = D^-1 r, p = z, q = 0; partials b.b, r.z, r.r per unit
   double tot3[3];
   {
-    double *u3[3], *c3[3];
-    ptrs(u3, c3);
-    ph.run<3>(ns, u3, c3, [&](int sl, double (&v)[3]) {
+    double* c3[3];
+    ptrs(c3);
+    ph.run<3>(c3, [&](int sl, double (&v)[3]) {
       double acc[3];
       slice_spmv_sym_g(a, sl, GatherX{a.x}, acc);
       const int row = sl * 32 + lane;
@@ -281,7 +248,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       v[2] = lane_sum(rr);
     });
     grid.sync();
-    sum_phase<3>(u3, c3, G, ns0, ns, tot3);
+    sum_phase<3>(c3, G, tot3);
     parity ^= 1;
   }
   const double bnorm = sqrt(tot3[0]);
@@ -301,9 +268,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       SELL_STAMP(it, 0);
       // ---- phase A: q = A p via A p_{k+1} = A z_{k+1} + beta A p_k: only z is gathered (half the gather
       // traffic of the L2-bound phase); q and p are then updated in place by their row owner
-      double *uA[1], *cA[1];
-      ptrs(uA, cA);
-      ph.run<1>(ns, uA, cA, [&](int sl, double (&v)[1]) {
+      double* cA[1];
+      ptrs(cA);
+      ph.run<1>(cA, [&](int sl, double (&v)[1]) {
         double acc[3];
         slice_spmv_sym_g(a, sl, GatherZ{a.z}, acc);
         const int row = sl * 32 + lane;
@@ -328,7 +295,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       double pap[1];
       grid.sync();
       SELL_STAMP(it, 5);
-      sum_phase<1>(uA, cA, G, ns0, ns, pap);
+      sum_phase<1>(cA, G, pap);
       parity ^= 1;
       SELL_STAMP(it, 2);
       if (pap[0] <= 0.0) {  // sparse.cpp:160-168
@@ -341,9 +308,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       }
       const double alpha = rz / pap[0];
       // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
-      double *uB[2], *cB[2];
-      ptrs(uB, cB);
-      ph.run<2>(ns, uB, cB, [&](int sl, double (&v)[2]) {
+      double* cB[2];
+      ptrs(cB);
+      ph.run<2>(cB, [&](int sl, double (&v)[2]) {
         double r2 = 0.0, rzp = 0.0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -367,7 +334,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       double red2[2];
       grid.sync();
       SELL_STAMP(it, 6);
-      sum_phase<2>(uB, cB, G, ns0, ns, red2);
+      sum_phase<2>(cB, G, red2);
       parity ^= 1;
       SELL_STAMP(it, 4);
       rr = red2[0];
@@ -419,17 +386,16 @@ int pcg_sell_grid() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_sell, kThreads, 0);
-    g_grid = sms * (per > 0 ? per : 1);
+    g_grid = std::min(kMaxGrid, sms * (per > 0 ? per : 1));
   }
   return g_grid;
 }
 
-size_t pcg_sell_part_doubles(int nslices) { return 2 * 4 * part_stride(nslices); }
+size_t pcg_sell_part_doubles() { return 2 * 4 * (size_t)kMaxGrid; }
 int pcg_sell_warps_per_cta() { return kWarpsPerCta; }
 
-void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_part, cudaStream_t s) {
-  SellArgs sa{a, ctr, slice_part};
-  cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s);
+void launch_pcg_sell(const CgLaunch& a, double* cta_part, cudaStream_t s) {
+  SellArgs sa{a, cta_part};
   void* args[] = {&sa};
   const cudaError_t err = cudaLaunchCooperativeKernel((const void*)k_pcg_sell, pcg_sell_grid(), kThreads, args, 0, s);
   if (err != cudaSuccess) {

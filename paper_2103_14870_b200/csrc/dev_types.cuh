@@ -171,16 +171,16 @@ struct CgLaunch {
   int32_t nslices;        // cg_sell.cu: number of 32-row SELL slices
   const int32_t* usp;     // cg_sell.cu: upper-block slice pointer (slot decoding)
   int32_t zero_base;      // cg_sell.cu: value offset of the all-zero padding block
-  const int32_t* cta_first;  // cg_sell.cu: static slice range of each CTA (grid + 1 entries)
+  const int32_t* cta_first;  // cg_sell.cu: slice range of each CTA (grid + 1 entries)
   unsigned long long* trace;  // optional per-phase %globaltimer stamps (GF_CG_TRACE)
 };
 int cg_csr_grid();
 void launch_pcg_csr(const CgLaunch& a, cudaStream_t s);  // scalar CSR (gf_cg_solve_csr)
 // ---- cg_sell.cu (production solver on the symmetric SELL-32 matrix) ----
 int pcg_sell_grid();
-size_t pcg_sell_part_doubles(int nslices);  // size of the slice_part work array
+size_t pcg_sell_part_doubles();  // size of the CTA partial work array
 int pcg_sell_warps_per_cta();
-void launch_pcg_sell(const CgLaunch& a, unsigned long long* ctr, double* slice_part, cudaStream_t s);
+void launch_pcg_sell(const CgLaunch& a, double* cta_part, cudaStream_t s);
 void launch_spmv_sym(const CgLaunch& a, const double* xin, double* y, cudaStream_t s);
 // ---- misc.cu ----
 void launch_bc_targets(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, double dt, cudaStream_t s);

@@ -470,39 +470,34 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   cg_.dinv = d_.dinv;
   cg_.r = d_.r; cg_.z = d_.z; cg_.p0 = d_.p0; cg_.Ap = d_.Ap;
   cg_.out = d_.cg_out;
-  d_ctr_ = (unsigned long long*)zeros(64);  // ticket counter of the PCG work distribution
-  d_slice_part_ = (double*)zeros(8 * pcg_sell_part_doubles(d_.nslices));
-  {  // static PCG work split (cg_sell.cu Phase): contiguous slice ranges, <= one slice per warp, balanced by the
-     // slices' slot counts (interior slices carry ~1.5x the slots of boundary ones); a larger matrix takes one
-     // slice per warp statically and hands out the rest dynamically
+  d_slice_part_ = (double*)zeros(8 * pcg_sell_part_doubles());
+  {  // PCG work split (cg_sell.cu Phase): contiguous slice ranges of at most K slices per warp (K = 1 while the
+     // matrix fits one slice per warp), balanced by the slices' slot counts (interior slices carry ~1.5x the
+     // slots of boundary ones): the smallest per-CTA slot budget that places every slice
     const int G = pcg_sell_grid(), W = pcg_sell_warps_per_cta(), ns = d_.nslices;
+    const int64_t cap_n = (int64_t)W * std::max<int64_t>(1, (ns + (int64_t)G * W - 1) / ((int64_t)G * W));
     std::vector<int32_t> first(G + 1, 0);
-    if ((int64_t)ns <= (int64_t)G * W) {
-      auto fill = [&](int64_t cap, bool write) {
-        int32_t sl = 0;
-        for (int b = 0; b < G; ++b) {
-          if (write) first[b] = sl;
-          int64_t acc = 0;
-          int cnt = 0;
-          while (sl < ns && cnt < W && acc + (sell_ptr_[sl + 1] - sell_ptr_[sl]) <= cap) {
-            acc += sell_ptr_[sl + 1] - sell_ptr_[sl];
-            ++sl;
-            ++cnt;
-          }
+    auto fill = [&](int64_t cap, bool write) {
+      int32_t sl = 0;
+      for (int b = 0; b < G; ++b) {
+        if (write) first[b] = sl;
+        int64_t acc = 0, cnt = 0;
+        while (sl < ns && cnt < cap_n && acc + (sell_ptr_[sl + 1] - sell_ptr_[sl]) <= cap) {
+          acc += sell_ptr_[sl + 1] - sell_ptr_[sl];
+          ++sl;
+          ++cnt;
         }
-        if (write) first[G] = sl;
-        return sl == ns;
-      };
-      int64_t lo = 1, hi = (int64_t)W * 64;  // slots per slice <= 63 (packed ordinals)
-      while (lo < hi) {  // smallest per-CTA slot budget that places every slice
-        const int64_t mid = (lo + hi) / 2;
-        if (fill(mid, false)) hi = mid;
-        else lo = mid + 1;
       }
-      fill(lo, true);
-    } else {
-      for (int b = 0; b <= G; ++b) first[b] = b * W;
+      if (write) first[G] = sl;
+      return sl == ns;
+    };
+    int64_t lo = 1, hi = cap_n * 64;  // slots per slice <= 63 (packed ordinals)
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (fill(mid, false)) hi = mid;
+      else lo = mid + 1;
     }
+    fill(lo, true);
     cg_.cta_first = (const int32_t*)up(first.data(), 4 * first.size());
   }
   if (std::getenv("GF_CG_TRACE")) cg_.trace = (unsigned long long*)zeros(8 * 5000);
@@ -638,7 +633,7 @@ void Simulation::upload_bc_step(double t, double dt) {
 }
 
 void Simulation::launch_cg() {
-  launch_pcg_sell(cg_, d_ctr_, d_slice_part_, stream_);
+  launch_pcg_sell(cg_, d_slice_part_, stream_);
 }
 
 double Simulation::run_cg(int max_iters) {

@@ -118,7 +118,6 @@ class Simulation {
   cudaStream_t stream_ = nullptr;
   DevData d_{};
   CgLaunch cg_{};
-  unsigned long long* d_ctr_ = nullptr;
   double* d_slice_part_ = nullptr;
   std::vector<void*> allocs_;
   int32_t* d_fixed_nodes_ = nullptr;
