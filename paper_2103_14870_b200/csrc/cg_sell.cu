@@ -6,9 +6,11 @@
 //            their row owner), partial p.q                                   -> barrier, pAp
 //   phase B  x += alpha p, r -= alpha q, z = D^-1 r, partials r.r and r.z   -> barrier, rr, rz
 // Work distribution (class Phase): CTA b owns the slice range [cta_first[b], cta_first[b+1]) (balanced by slot
-// count on the host), its warps stride through it; no atomics. Determinism: unit values are summed per warp
-// in unit order and per CTA in warp order, and after the barrier every CTA sums the CTA partials in one fixed
-// order, so alpha, beta and the stop decisions are bit-identical in every CTA and from run to run.
+// count on the host), its warps stride through it; no atomics. A matrix larger than one slice per warp takes
+// one slice per warp statically and hands out the rest dynamically (a ticket counter, requested one unit
+// ahead), which absorbs SM speed differences. Determinism: static unit values are summed per warp in unit order and per CTA in warp order,
+// dynamic units keep one partial each, and after the barrier every CTA sums [CTA partials, unit partials] in
+// one fixed order, so alpha, beta and the stop decisions are bit-identical in every CTA and run to run.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -32,7 +34,9 @@ constexpr int kWarpsPerCta = kThreads / 32;
 
 struct SellArgs {
   CgLaunch a;
-  double* cta_part;  // 2 parities x 4 values x kMaxGrid CTA partials
+  double* cta_part;         // 2 parities x 4 values x kMaxGrid CTA partials
+  double* dyn_part;         // 2 parities x 4 values x max(1, #dynamic units) unit partials
+  unsigned long long* ctr;  // dynamic ticket counter
 };
 
 __device__ __forceinline__ double lane_sum(double v) {  // fixed butterfly: same bits in every lane
@@ -155,22 +159,43 @@ struct GatherZ {
 };
 
 struct Phase {
-  const int32_t* cta_first;  // units (slices) of CTA b: [cta_first[b], cta_first[b + 1])
-  // warp w of the CTA takes units first + w, first + w + W, ... (consecutive warps on consecutive slices); the
-  // unit values are summed per warp in unit order and per CTA in warp order: one partial per CTA, fixed order
-  template <int NV, class Body>
-  __device__ __forceinline__ void run(double* const (&cta)[NV], Body&& body) {
+  const int32_t* cta_first;  // static units (slices) of CTA b: [cta_first[b], cta_first[b + 1])
+  int n;                     // all units; [cta_first[G], n) are handed out dynamically (large matrices only)
+  unsigned long long* ctr;   // ticket counter of the dynamic units (zeroed before the launch)
+  unsigned long long base;
+  // warp w of the CTA takes static units first + w, first + w + W, ... (consecutive warps on consecutive
+  // slices), then dynamic units by ticket (requested one unit ahead). Static unit values are summed per warp in
+  // unit order and per CTA in warp order (one partial per CTA); dynamic units keep one partial each.
+  template <bool kDyn, int NV, class Body>
+  __device__ __forceinline__ void run(double* const (&cta)[NV], double* const (&dyn)[NV], Body&& body) {
     __shared__ double s_acc[kWarpsPerCta][4];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nst = kDyn ? __ldg(cta_first + gridDim.x) : n;
+    const unsigned long long nd = (unsigned long long)(n - nst);
     double sv[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) sv[q] = 0.0;
+    unsigned long long tk = 0;
+    if (kDyn && lane == 0) tk = atomicAdd(ctr, 1ull);
     const int u1 = __ldg(cta_first + blockIdx.x + 1);
     for (int u = __ldg(cta_first + blockIdx.x) + w; u < u1; u += kWarpsPerCta) {
       double v[NV];
       body(u, v);
 #pragma unroll
       for (int q = 0; q < NV; ++q) sv[q] += v[q];
+    }
+    if (kDyn) {
+      for (;;) {
+        const unsigned long long idx = __shfl_sync(0xffffffffu, tk, 0) - base;
+        if (idx >= nd) break;
+        if (lane == 0) tk = atomicAdd(ctr, 1ull);
+        double v[NV];
+        body(nst + (int)idx, v);
+        if (lane == 0)
+#pragma unroll
+          for (int q = 0; q < NV; ++q) dyn[q][idx] = v[q];
+      }
+      base += nd + ((gridDim.x * blockDim.x) >> 5);  // every warp took exactly one overshooting ticket
     }
     if (lane == 0)
 #pragma unroll
@@ -184,15 +209,27 @@ struct Phase {
   }
 };
 
-// sum of the G CTA partials in one fixed order (thread k loads partial k, fixed lane and warp trees)
-template <int NV>
-__device__ __forceinline__ void sum_phase(double* const (&cta)[NV], int G, double (&out)[NV]) {
+// sum of [CTA partials, dynamic-unit partials] in one fixed order (thread stride, fixed lane and warp trees)
+template <bool kDyn, int NV>
+__device__ __forceinline__ void sum_phase(double* const (&cta)[NV], double* const (&dyn)[NV], int G, int nd,
+                                          double (&out)[NV]) {
   __shared__ double s_w[kWarpsPerCta][4];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
     double x = 0.0;
     for (int k = threadIdx.x; k < G; k += blockDim.x) x += __ldcg(cta[q] + k);
+    constexpr int kB = 8;  // loads issued back to back per batch (one L2 round trip per batch)
+    for (int k0 = 0; kDyn && k0 < nd; k0 += kB * (int)blockDim.x) {
+      double v[kB];
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const int k = k0 + b * (int)blockDim.x + (int)threadIdx.x;
+        v[b] = k < nd ? __ldcg(dyn[q] + k) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < kB; ++b) x += v[b];
+    }
     x = lane_sum(x);
     if (lane == 0) s_w[w][q] = x;
   }
@@ -207,23 +244,29 @@ __device__ __forceinline__ void sum_phase(double* const (&cta)[NV], int G, doubl
 
 constexpr int kMaxGrid = 1024;  // CTA partial slots per value
 
+template <bool kDyn>
 __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
   cg::grid_group grid = cg::this_grid();
   const CgLaunch& a = sa.a;
   const int ns = a.nslices, nrows = a.nrows, lane = threadIdx.x & 31;
   const int G = (int)gridDim.x;
-  Phase ph{a.cta_first};
+  Phase ph{a.cta_first, ns, sa.ctr, 0ull};
+  const int nd = ns - __ldg(a.cta_first + G);
+  const size_t dstride = nd > 0 ? (size_t)nd : 1;
   int parity = 0;
-  auto ptrs = [&](auto& c) {  // CTA partial arrays of the current parity
-    for (int q = 0; q < (int)(sizeof(c) / sizeof(c[0])); ++q) c[q] = sa.cta_part + ((size_t)parity * 4 + q) * kMaxGrid;
+  auto ptrs = [&](auto& c, auto& dp) {  // CTA and dynamic-unit partial arrays of the current parity
+    for (int q = 0; q < (int)(sizeof(c) / sizeof(c[0])); ++q) {
+      c[q] = sa.cta_part + ((size_t)parity * 4 + q) * kMaxGrid;
+      dp[q] = sa.dyn_part + ((size_t)parity * 4 + q) * dstride;
+    }
   };
 
   // setup (sparse.cpp:145-157): r = b - A x, z = D^-1 r, p = z, q = 0; partials b.b, r.z, r.r per unit
   double tot3[3];
   {
-    double* c3[3];
-    ptrs(c3);
-    ph.run<3>(c3, [&](int sl, double (&v)[3]) {
+    double *c3[3], *d3[3];
+    ptrs(c3, d3);
+    ph.run<kDyn, 3>(c3, d3, [&](int sl, double (&v)[3]) {
       double acc[3];
       slice_spmv_sym_g(a, sl, GatherX{a.x}, acc);
       const int row = sl * 32 + lane;
@@ -248,7 +291,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       v[2] = lane_sum(rr);
     });
     grid.sync();
-    sum_phase<3>(c3, G, tot3);
+    sum_phase<kDyn, 3>(c3, d3, G, nd, tot3);
     parity ^= 1;
   }
   const double bnorm = sqrt(tot3[0]);
@@ -268,9 +311,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       SELL_STAMP(it, 0);
       // ---- phase A: q = A p via A p_{k+1} = A z_{k+1} + beta A p_k: only z is gathered (half the gather
       // traffic of the L2-bound phase); q and p are then updated in place by their row owner
-      double* cA[1];
-      ptrs(cA);
-      ph.run<1>(cA, [&](int sl, double (&v)[1]) {
+      double *cA[1], *dA[1];
+      ptrs(cA, dA);
+      ph.run<kDyn, 1>(cA, dA, [&](int sl, double (&v)[1]) {
         double acc[3];
         slice_spmv_sym_g(a, sl, GatherZ{a.z}, acc);
         const int row = sl * 32 + lane;
@@ -295,7 +338,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       double pap[1];
       grid.sync();
       SELL_STAMP(it, 5);
-      sum_phase<1>(cA, G, pap);
+      sum_phase<kDyn, 1>(cA, dA, G, nd, pap);
       parity ^= 1;
       SELL_STAMP(it, 2);
       if (pap[0] <= 0.0) {  // sparse.cpp:160-168
@@ -308,9 +351,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       }
       const double alpha = rz / pap[0];
       // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
-      double* cB[2];
-      ptrs(cB);
-      ph.run<2>(cB, [&](int sl, double (&v)[2]) {
+      double *cB[2], *dB[2];
+      ptrs(cB, dB);
+      ph.run<kDyn, 2>(cB, dB, [&](int sl, double (&v)[2]) {
         double r2 = 0.0, rzp = 0.0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -334,7 +377,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       double red2[2];
       grid.sync();
       SELL_STAMP(it, 6);
-      sum_phase<2>(cB, G, red2);
+      sum_phase<kDyn, 2>(cB, dB, G, nd, red2);
       parity ^= 1;
       SELL_STAMP(it, 4);
       rr = red2[0];
@@ -385,19 +428,21 @@ int pcg_sell_grid() {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_sell, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_sell<true>, kThreads, 0);
     g_grid = std::min(kMaxGrid, sms * (per > 0 ? per : 1));
   }
   return g_grid;
 }
 
-size_t pcg_sell_part_doubles() { return 2 * 4 * (size_t)kMaxGrid; }
+size_t pcg_sell_part_doubles(int ndyn) { return 2 * 4 * ((size_t)kMaxGrid + (size_t)std::max(1, ndyn)); }
 int pcg_sell_warps_per_cta() { return kWarpsPerCta; }
 
-void launch_pcg_sell(const CgLaunch& a, double* cta_part, cudaStream_t s) {
-  SellArgs sa{a, cta_part};
+void launch_pcg_sell(const CgLaunch& a, double* part, int ndyn, unsigned long long* ctr, cudaStream_t s) {
+  SellArgs sa{a, part, part + 2 * 4 * (size_t)kMaxGrid, ctr};
+  if (ndyn > 0) cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s);
   void* args[] = {&sa};
-  const cudaError_t err = cudaLaunchCooperativeKernel((const void*)k_pcg_sell, pcg_sell_grid(), kThreads, args, 0, s);
+  const void* fn = ndyn > 0 ? (const void*)k_pcg_sell<true> : (const void*)k_pcg_sell<false>;
+  const cudaError_t err = cudaLaunchCooperativeKernel(fn, pcg_sell_grid(), kThreads, args, 0, s);
   if (err != cudaSuccess) {
     cudaGetLastError();
     throw std::runtime_error(std::string("cooperative CG launch failed: ") + cudaGetErrorString(err));

@@ -178,9 +178,9 @@ int cg_csr_grid();
 void launch_pcg_csr(const CgLaunch& a, cudaStream_t s);  // scalar CSR (gf_cg_solve_csr)
 // ---- cg_sell.cu (production solver on the symmetric SELL-32 matrix) ----
 int pcg_sell_grid();
-size_t pcg_sell_part_doubles();  // size of the CTA partial work array
+size_t pcg_sell_part_doubles(int ndyn);  // size of the partial work array (ndyn dynamic units)
 int pcg_sell_warps_per_cta();
-void launch_pcg_sell(const CgLaunch& a, double* cta_part, cudaStream_t s);
+void launch_pcg_sell(const CgLaunch& a, double* part, int ndyn, unsigned long long* ctr, cudaStream_t s);
 void launch_spmv_sym(const CgLaunch& a, const double* xin, double* y, cudaStream_t s);
 // ---- misc.cu ----
 void launch_bc_targets(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, double dt, cudaStream_t s);

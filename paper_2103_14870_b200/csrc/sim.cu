@@ -470,26 +470,30 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   cg_.dinv = d_.dinv;
   cg_.r = d_.r; cg_.z = d_.z; cg_.p0 = d_.p0; cg_.Ap = d_.Ap;
   cg_.out = d_.cg_out;
-  d_slice_part_ = (double*)zeros(8 * pcg_sell_part_doubles());
-  {  // PCG work split (cg_sell.cu Phase): contiguous slice ranges of at most K slices per warp (K = 1 while the
-     // matrix fits one slice per warp), balanced by the slices' slot counts (interior slices carry ~1.5x the
-     // slots of boundary ones): the smallest per-CTA slot budget that places every slice
+  {  // PCG work split (cg_sell.cu Phase): contiguous slice ranges of at most K slices per warp, balanced by the
+     // slices' slot counts (interior slices carry ~1.5x the slots of boundary ones): the smallest per-CTA slot
+     // budget that places the static slices. One slice per warp covers the matrix while it fits (c3: no
+     // dynamic units); a larger matrix places one slice per warp statically and hands out the rest by ticket.
     const int G = pcg_sell_grid(), W = pcg_sell_warps_per_cta(), ns = d_.nslices;
-    const int64_t cap_n = (int64_t)W * std::max<int64_t>(1, (ns + (int64_t)G * W - 1) / ((int64_t)G * W));
+    const int64_t gw = (int64_t)G * W;
+    double frac = 0.0;  // measured at c4 (28k slices): all-dynamic tail 22.5 ms, 50 % static 23.0, 80 % 26.2
+    if (const char* e = std::getenv("GF_CG_STATIC")) frac = std::atof(e);  // static share of a large matrix
+    const int32_t nstat = ns <= gw ? ns : (int32_t)std::min<int64_t>(ns, std::max<int64_t>(gw, (int64_t)(frac * ns)));
+    const int64_t cap_n = (int64_t)W * std::max<int64_t>(1, (nstat + gw - 1) / gw);
     std::vector<int32_t> first(G + 1, 0);
     auto fill = [&](int64_t cap, bool write) {
       int32_t sl = 0;
       for (int b = 0; b < G; ++b) {
         if (write) first[b] = sl;
         int64_t acc = 0, cnt = 0;
-        while (sl < ns && cnt < cap_n && acc + (sell_ptr_[sl + 1] - sell_ptr_[sl]) <= cap) {
+        while (sl < nstat && cnt < cap_n && acc + (sell_ptr_[sl + 1] - sell_ptr_[sl]) <= cap) {
           acc += sell_ptr_[sl + 1] - sell_ptr_[sl];
           ++sl;
           ++cnt;
         }
       }
       if (write) first[G] = sl;
-      return sl == ns;
+      return sl == nstat;
     };
     int64_t lo = 1, hi = cap_n * 64;  // slots per slice <= 63 (packed ordinals)
     while (lo < hi) {
@@ -498,6 +502,9 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
       else lo = mid + 1;
     }
     fill(lo, true);
+    cg_ndyn_ = ns - nstat;
+    d_slice_part_ = (double*)zeros(8 * pcg_sell_part_doubles(cg_ndyn_));
+    d_ctr_ = (unsigned long long*)zeros(64);
     cg_.cta_first = (const int32_t*)up(first.data(), 4 * first.size());
   }
   if (std::getenv("GF_CG_TRACE")) cg_.trace = (unsigned long long*)zeros(8 * 5000);
@@ -633,7 +640,7 @@ void Simulation::upload_bc_step(double t, double dt) {
 }
 
 void Simulation::launch_cg() {
-  launch_pcg_sell(cg_, d_slice_part_, stream_);
+  launch_pcg_sell(cg_, d_slice_part_, cg_ndyn_, d_ctr_, stream_);
 }
 
 double Simulation::run_cg(int max_iters) {

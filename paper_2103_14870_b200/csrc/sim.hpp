@@ -119,6 +119,8 @@ class Simulation {
   DevData d_{};
   CgLaunch cg_{};
   double* d_slice_part_ = nullptr;
+  unsigned long long* d_ctr_ = nullptr;
+  int cg_ndyn_ = 0;  // dynamically handed-out PCG slices (cg_sell.cu Phase)
   std::vector<void*> allocs_;
   int32_t* d_fixed_nodes_ = nullptr;
   BcStep* d_bcstep_ = nullptr;
