@@ -45,6 +45,9 @@ __device__ __forceinline__ double lane_sum(double v) {  // fixed butterfly: same
   return v;
 }
 
+#ifndef GF_CG_REGS
+#define GF_CG_REGS 2  // 1: x, r, D^-1 of the owner rows in registers; 2: also p, q and z
+#endif
 #ifndef GF_SELL_GROUP
 #define GF_SELL_GROUP 2
 #endif
@@ -261,6 +264,13 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
     }
   };
 
+  // One slice per warp (kRegs): the owner keeps x, r and D^-1 of its rows in registers for the whole solve
+  // (they are never gathered), so phase B reads only p and q and writes only z; x is stored once at the end.
+  constexpr bool kRegs = !kDyn && GF_CG_REGS;
+  constexpr bool kRegs2 = kRegs && GF_CG_REGS >= 2;  // p, q and the owner's z in registers too
+  double xv[3] = {0.0, 0.0, 0.0}, rv[3] = {0.0, 0.0, 0.0}, dv[3] = {0.0, 0.0, 0.0};
+  double pv[3] = {0.0, 0.0, 0.0}, qv[3] = {0.0, 0.0, 0.0}, zv[3] = {0.0, 0.0, 0.0};
+  int own_row = -1;
   // setup (sparse.cpp:145-157): r = b - A x, z = D^-1 r, p = z, q = 0; partials b.b, r.z, r.r per unit
   double tot3[3];
   {
@@ -277,10 +287,23 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
           const size_t dof = 3 * (size_t)row + c;
           const double bi = a.b[dof];
           const double ri = bi - acc[c];
-          const double zi = __ldg(a.dinv + dof) * ri;
-          a.r[dof] = ri;
+          const double di = __ldg(a.dinv + dof);
+          const double zi = di * ri;
+          if (kRegs) {
+            xv[c] = a.x[dof];
+            rv[c] = ri;
+            dv[c] = di;
+            own_row = row;
+          } else {
+            a.r[dof] = ri;
+          }
           a.z[dof] = zi;
-          a.p0[dof] = zi;
+          if (kRegs2) {
+            zv[c] = zi;
+            pv[c] = zi;
+          } else {
+            a.p0[dof] = zi;
+          }
           bb = __fma_rn(bi, bi, bb);
           rz = __fma_rn(ri, zi, rz);
           rr = __fma_rn(ri, ri, rr);
@@ -322,12 +345,20 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const size_t dof = 3 * (size_t)row + c;
-            const double zi = ldv(a.z + dof);
-            const double pr = fused ? __fma_rn(beta, ldv(p + dof), zi) : zi;
-            const double qr = fused ? __fma_rn(beta, ldv(a.Ap + dof), acc[c]) : acc[c];
-            p[dof] = pr;
-            a.Ap[dof] = qr;
-            pq = __fma_rn(pr, qr, pq);
+            if (kRegs2) {
+              const double pr = fused ? __fma_rn(beta, pv[c], zv[c]) : zv[c];
+              const double qr = fused ? __fma_rn(beta, qv[c], acc[c]) : acc[c];
+              pv[c] = pr;
+              qv[c] = qr;
+              pq = __fma_rn(pr, qr, pq);
+            } else {
+              const double zi = ldv(a.z + dof);
+              const double pr = fused ? __fma_rn(beta, ldv(p + dof), zi) : zi;
+              const double qr = fused ? __fma_rn(beta, ldv(a.Ap + dof), acc[c]) : acc[c];
+              p[dof] = pr;
+              a.Ap[dof] = qr;
+              pq = __fma_rn(pr, qr, pq);
+            }
           }
         }
         v[0] = lane_sum(pq);
@@ -355,18 +386,35 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       ptrs(cB, dB);
       ph.run<kDyn, 2>(cB, dB, [&](int sl, double (&v)[2]) {
         double r2 = 0.0, rzp = 0.0;
+        if (kRegs) {
+          const int row = sl * 32 + lane;
+          if (row < nrows) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const size_t dof = (size_t)sl * 96 + c * 32 + lane;  // 96 dofs of the slice, coalesced
-          if (dof < 3 * (size_t)nrows) {
-            const double pi = __ldcg(p + dof);
-            a.x[dof] = __fma_rn(alpha, pi, __ldcg(a.x + dof));
-            const double ri = __fma_rn(-alpha, __ldcg(a.Ap + dof), __ldcg(a.r + dof));
-            a.r[dof] = ri;
-            const double zi = __ldg(a.dinv + dof) * ri;
-            a.z[dof] = zi;
-            r2 = __fma_rn(ri, ri, r2);
-            rzp = __fma_rn(ri, zi, rzp);
+            for (int c = 0; c < 3; ++c) {
+              const size_t dof = 3 * (size_t)row + c;
+              xv[c] = __fma_rn(alpha, kRegs2 ? pv[c] : __ldcg(p + dof), xv[c]);
+              rv[c] = __fma_rn(-alpha, kRegs2 ? qv[c] : __ldcg(a.Ap + dof), rv[c]);
+              const double zi = dv[c] * rv[c];
+              if (kRegs2) zv[c] = zi;
+              a.z[dof] = zi;
+              r2 = __fma_rn(rv[c], rv[c], r2);
+              rzp = __fma_rn(rv[c], zi, rzp);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const size_t dof = (size_t)sl * 96 + c * 32 + lane;  // 96 dofs of the slice, coalesced
+            if (dof < 3 * (size_t)nrows) {
+              const double pi = __ldcg(p + dof);
+              a.x[dof] = __fma_rn(alpha, pi, __ldcg(a.x + dof));
+              const double ri = __fma_rn(-alpha, __ldcg(a.Ap + dof), __ldcg(a.r + dof));
+              a.r[dof] = ri;
+              const double zi = __ldg(a.dinv + dof) * ri;
+              a.z[dof] = zi;
+              r2 = __fma_rn(ri, ri, r2);
+              rzp = __fma_rn(ri, zi, rzp);
+            }
           }
         }
         v[0] = lane_sum(r2);
@@ -396,6 +444,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       relres = sqrt(rr) / bnorm;
       converged = relres <= a.tol;
     }
+    if (kRegs && own_row >= 0)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) a.x[3 * (size_t)own_row + c] = xv[c];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.out[0] = iterations;
