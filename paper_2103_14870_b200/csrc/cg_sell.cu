@@ -218,29 +218,38 @@ __device__ __forceinline__ void sum_phase(double* const (&cta)[NV], double* cons
                                           double (&out)[NV]) {
   __shared__ double s_w[kWarpsPerCta][4];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double x[NV];
+  // all values' CTA partials are loaded back to back (one L2 round trip), then reduced
+#pragma unroll
+  for (int q = 0; q < NV; ++q) x[q] = 0.0;
+  for (int k = threadIdx.x; k < G; k += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) x[q] += __ldcg(cta[q] + k);
+  if (kDyn) {
+    constexpr int kB = 8;  // loads issued back to back per batch (one L2 round trip per batch)
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+      for (int k0 = 0; k0 < nd; k0 += kB * (int)blockDim.x) {
+        double v[kB];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int k = k0 + b * (int)blockDim.x + (int)threadIdx.x;
+          v[b] = k < nd ? __ldcg(dyn[q] + k) : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < kB; ++b) x[q] += v[b];
+      }
+  }
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
-    double x = 0.0;
-    for (int k = threadIdx.x; k < G; k += blockDim.x) x += __ldcg(cta[q] + k);
-    constexpr int kB = 8;  // loads issued back to back per batch (one L2 round trip per batch)
-    for (int k0 = 0; kDyn && k0 < nd; k0 += kB * (int)blockDim.x) {
-      double v[kB];
-#pragma unroll
-      for (int b = 0; b < kB; ++b) {
-        const int k = k0 + b * (int)blockDim.x + (int)threadIdx.x;
-        v[b] = k < nd ? __ldcg(dyn[q] + k) : 0.0;
-      }
-#pragma unroll
-      for (int b = 0; b < kB; ++b) x += v[b];
-    }
-    x = lane_sum(x);
-    if (lane == 0) s_w[w][q] = x;
+    const double t = lane_sum(x[q]);
+    if (lane == 0) s_w[w][q] = t;
   }
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
-    double x = (lane < kWarpsPerCta) ? s_w[lane][q] : 0.0;
-    out[q] = lane_sum(x);  // every warp computes the same total
+    const double t = (lane < kWarpsPerCta) ? s_w[lane][q] : 0.0;
+    out[q] = lane_sum(t);  // every warp computes the same total
   }
   __syncthreads();
 }
