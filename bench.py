@@ -233,6 +233,10 @@ def main():
     roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+                "note": ("pcg algorithmic bytes = SURVEY §8(d) B_CG per iteration (the reference's scalar CSR: "
+                         "12Z + 4(n+1) + 56n) x iterations; the symmetric SELL matrix and the solver state stay "
+                         "L2-/register-resident during the solve (traffic = ncu DRAM bytes per launch), so frac > 1 "
+                         "is the format + residency gain over that byte model, not an HBM rate") if dname == "pcg" else None,
                 "share_of_step": d["total_ms"] / ms,
                 "kernels": {k: {"launches": v["launches"], "avg_ms": v["total_ms"] / max(1, v["launches"]),
                                 "share": v["total_ms"] / ms,
