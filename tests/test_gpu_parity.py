@@ -354,6 +354,25 @@ def test_damage_pass_bit_exact_c3_full_size():
     assert same_bits_or_zero(gs.state().element_chi, os_.get_state()["chi"])
 
 
+@pytest.mark.slow
+def test_large_matrix_dynamic_pcg_tail_matches_oracle():
+    """c4 physics (impact on a halfspace collider) on 52^3 cells: 148,877 nodes = 4,653 slices, more than one
+    slice per PCG warp, so the solver runs its dynamic-tail instance (cg_sell.cu k_pcg_sell<true>)."""
+    s = cf.scaled("c4", (52, 52, 52))
+    gs, os_, gm, om = pair(s)
+    assert (gm.num_nodes() + 31) // 32 > 148 * 24
+    scale = np.abs(om.arrays()["rest"]).max()
+    for _ in range(2):
+        a = os_.dynamic_step()
+        b = gs.dynamic_step()
+        assert abs(a.cg_iterations - b.cg_iterations) <= 2
+        assert b.load == pytest.approx(a.load, rel=1e-9)
+    ost, gst = os_.get_state(), gs.state()
+    assert np.array_equal(gst.edge_damage, ost["zeta"])
+    assert np.abs(gst.displacements - ost["u"]).max() / scale < TRAJ_TOL
+    assert np.abs(gst.velocities - ost["v"]).max() <= TRAJ_TOL * max(1.0, np.abs(ost["v"]).max())
+
+
 # ---------------------------------------------------------------- feature coverage vs the oracle
 def _pair_custom(mesh_args, mat_args, cfg, bcs=(), colliders=(), u0=None, v0=None):
     gm = g.make_box_mesh(*mesh_args)
