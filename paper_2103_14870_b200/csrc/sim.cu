@@ -1,14 +1,15 @@
 // sim.cu — host orchestration of the B200 Simulation (solver.cpp:31-333 restated B200-first).
 //
 // Per dynamic_step (solver.cpp:219-333) the host issues, on one stream and with no intermediate sync:
-//   damage    k_tet_stress [+ k_nonlocal] -> k_relabel -> k_chi              (solver.cpp:225, 90-103)
+//   damage    k_tet_stress [+ k_nonlocal_tpl | k_nonlocal] -> k_relabel -> k_chi  (solver.cpp:225, 90-103)
 //   f_ext     [k_collide x substeps -> k_collide_load]                        (solver.cpp:229-250)
 //   BCs       k_bc_targets                                                    (solver.cpp:255-262)
 //   system    k_assemble (forces, K, K v, rhs, A, projection, D^-1, x0)       (solver.cpp:275-295)
-//   solve     k_pcg (one cooperative kernel for the whole CG)                 (solver.cpp:105-136)
-//   update    k_integrate (v += dv, u += dt v, pin)                           (solver.cpp:296-328)
+//   solve     k_pcg_sell (one cooperative kernel for the whole CG)            (solver.cpp:105-136)
+//   update    k_integrate (v += dv, u += dt v, pin; no-op unless converged)   (solver.cpp:296-328)
 // and reads back one 48-byte stats record (CG result, newly-broken count, collider load); the
-// reference's retry/shift ladder (solver.cpp:110-135) runs only when that record says the CG failed.
+// reference's retry/shift ladder (solver.cpp:110-135) runs only when that record says the CG failed, after
+// which the integration is enqueued again. quasi_static_step (solver.cpp:138-217) reuses the same kernels.
 #include "sim.hpp"
 
 #include <algorithm>
