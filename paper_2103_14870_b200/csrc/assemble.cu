@@ -22,6 +22,7 @@ namespace {
 constexpr int kWarps = 4;
 constexpr int kMaxValence = 32;  // tets per node handled by one warp (validated at setup)
 constexpr int kMaxDeg = 32;      // column blocks per node row (validated at setup)
+constexpr int kBlkStride = 32 * 27 + 9;  // per warp: 27 doubles per lane + the zero block of padding items
 
 // contribution of tet e to node-row i (local index li): force on i (returned), the diagonal block K(li, li)
 // (returned in dg) and the three off-diagonal blocks K(li, lj), written straight to shared memory at slot
@@ -149,11 +150,10 @@ __device__ __forceinline__ double warp_sum(double v) {
 template <int kMode>
 __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d, MatDev m, StepCoeffs sc) {
   constexpr bool kBlocks = kMode != kAssembleForcesOnly;
-  extern __shared__ double s_dyn[];  // kBlocks: s_blk[kWarps][32 * 27] (dynamic: > 48 KB static limit)
-  double(*s_blk)[32 * 27] = reinterpret_cast<double(*)[32 * 27]>(s_dyn);
+  extern __shared__ double s_dyn[];  // kBlocks: s_blk[kWarps][32 * 27 + 9] (dynamic: > 48 KB static limit)
+  double(*s_blk)[kBlkStride] = reinterpret_cast<double(*)[kBlkStride]>(s_dyn);
   __shared__ double s_row[kBlocks ? kWarps : 1][kMaxDeg * 9];
-  __shared__ int s_cptr[kBlocks ? kWarps : 1][kMaxDeg + 1];
-  __shared__ uint8_t s_item[kBlocks ? kWarps : 1][3 * kMaxValence];
+  __shared__ uint8_t s_item[kBlocks ? kWarps : 1][16 * kMaxDeg];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kWarps + w;
   if (i >= d.nn) return;
@@ -196,21 +196,21 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
       const double t = warp_sum(dg[q]);
       if (lane == q) dsum = t;
     }
-    // the row's contribution lists (<= 4 * 32 items, <= 33 offsets) staged in shared memory by one coalesced
-    // warp load each, so the reduction below touches only shared memory
-    const int ibase = __ldg(d.contrib_ptr + row0);
-    if (lane <= deg) s_cptr[w][lane] = __ldg(d.contrib_ptr + row0 + lane) - ibase;
-    const int nitems = 3 * np;
-    for (int k = lane; k < nitems; k += 32) s_item[w][k] = __ldg(d.contrib_item + ibase + k);
+    // the row's padded contribution lists (mx <= 16 items per column) staged in shared memory, so
+    // the reduction below touches only shared memory with a uniform trip count
+    const int ib0 = __ldg(d.contrib_ptr + i), nitems = __ldg(d.contrib_ptr + i + 1) - ib0;
+    const int mx = nitems / deg;
+    for (int k = lane; k < nitems; k += 32) s_item[w][k] = __ldg(d.contrib_item + ib0 + k);
+    if (lane < 9) s_blk[w][32 * 27 + lane] = 0.0;  // the zero block padding items point at
     __syncwarp();
     // off-diagonal outputs (column c != cdiag, entry q), 9 (deg - 1) of them spread over the lanes
     for (int o = lane; o < 9 * (deg - 1); o += 32) {
       int c = o / 9;
       const int q = o - 9 * c;
       c += (c >= cdiag) ? 1 : 0;
-      const int it0 = s_cptr[w][c], it1 = s_cptr[w][c + 1];
+      const uint8_t* it = &s_item[w][c * mx];
       double sum = 0.0;
-      for (int it = it0; it < it1; ++it) sum += s_blk[w][9 * (int)s_item[w][it] + q];
+      for (int t = 0; t < mx; ++t) sum += s_blk[w][9 * (int)it[t] + q];
       s_row[w][9 * c + q] = sum;
     }
     if (lane < 9) s_row[w][9 * cdiag + lane] = dsum;
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(256) k_energy(DevData d, MatDev m, double* par
 
 void launch_assemble(const DevData& d, const MatDev& m, const StepCoeffs& c, int mode, cudaStream_t s) {
   const int grid = (d.nn + kWarps - 1) / kWarps;
-  constexpr int kDyn = kWarps * 32 * 27 * sizeof(double);
+  constexpr int kDyn = kWarps * kBlkStride * sizeof(double);
   static bool attr = [] {
     cudaFuncSetAttribute(k_assemble<kAssembleSystem>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
     cudaFuncSetAttribute(k_assemble<kAssembleRawK>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);

@@ -68,7 +68,7 @@ struct DevData {
   const int32_t* nt_tet;
   const uint32_t* nt_slot;
   // per block (CSR order) the contributions (pair l, local node k) as items l*4+k, ascending tet order
-  const int32_t* contrib_ptr;  // nb+1
+  const int32_t* contrib_ptr;  // nn+1: padded contribution items of row i start here (mx per column)
   const uint8_t* contrib_item;
   // node-block pattern (CSR view: column ids per row, ascending)
   const int32_t* brow;      // nn+1

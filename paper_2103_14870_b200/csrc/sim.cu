@@ -298,8 +298,25 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
           if (k != li)
             items[cur[pat_.row_ptr[i] + col_of(q, k)]++] = (uint8_t)(3 * (q - ntets.ptr[i]) + (k < li ? k : k - 1));
       }
-    d_.contrib_ptr = (const int32_t*)up(cnt.data(), 4 * cnt.size());
-    d_.contrib_item = (const uint8_t*)up(items.data(), items.size());
+    // padded per row: every column of row i gets mx_i items (the row's longest list), pad item 96 addresses a
+    // zero block, so the kernel's reduction loop has a uniform trip count across the warp
+    std::vector<int32_t> rptr(nn + 1, 0);
+    for (int32_t i = 0; i < nn; ++i) {
+      int32_t mx = 0;
+      for (int32_t b = pat_.row_ptr[i]; b < pat_.row_ptr[i + 1]; ++b) mx = std::max(mx, cnt[b + 1] - cnt[b]);
+      if (mx > 16) throw GeometryError("more than 16 tets around an edge are not supported by the assembly kernel");
+      rptr[i + 1] = rptr[i] + mx * (pat_.row_ptr[i + 1] - pat_.row_ptr[i]);
+    }
+    std::vector<uint8_t> padded(rptr[nn], 96);
+    for (int32_t i = 0; i < nn; ++i) {
+      const int32_t deg = pat_.row_ptr[i + 1] - pat_.row_ptr[i], mx = (rptr[i + 1] - rptr[i]) / std::max(1, deg);
+      for (int32_t c = 0; c < deg; ++c) {
+        const int32_t b = pat_.row_ptr[i] + c;
+        for (int32_t t = cnt[b]; t < cnt[b + 1]; ++t) padded[rptr[i] + c * mx + (t - cnt[b])] = items[t];
+      }
+    }
+    d_.contrib_ptr = (const int32_t*)up(rptr.data(), 4 * rptr.size());
+    d_.contrib_item = (const uint8_t*)up(padded.data(), std::max<size_t>(1, padded.size()));
     GF_CUDA(cudaStreamSynchronize(stream_));
   }
   d_.brow = (const int32_t*)up(pat_.row_ptr.data(), 4 * pat_.row_ptr.size());
