@@ -48,8 +48,11 @@ __device__ __forceinline__ double lane_sum(double v) {  // fixed butterfly: same
 #ifndef GF_CG_REGS
 #define GF_CG_REGS 2  // 1: x, r, D^-1 of the owner rows in registers; 2: also p, q and z
 #endif
+#ifndef GF_CG_SMEM
+#define GF_CG_SMEM 1  // per-lane solver state in shared memory: frees registers for the SpMV loads in flight
+#endif
 #ifndef GF_SELL_GROUP
-#define GF_SELL_GROUP 2
+#define GF_SELL_GROUP 4
 #endif
 constexpr int kGroup = GF_SELL_GROUP;
 #ifndef GF_GATHER_L1
@@ -277,8 +280,18 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
   // (they are never gathered), so phase B reads only p and q and writes only z; x is stored once at the end.
   constexpr bool kRegs = !kDyn && GF_CG_REGS;
   constexpr bool kRegs2 = kRegs && GF_CG_REGS >= 2;  // p, q and the owner's z in registers too
-  double xv[3] = {0.0, 0.0, 0.0}, rv[3] = {0.0, 0.0, 0.0}, dv[3] = {0.0, 0.0, 0.0};
-  double pv[3] = {0.0, 0.0, 0.0}, qv[3] = {0.0, 0.0, 0.0}, zv[3] = {0.0, 0.0, 0.0};
+#if GF_CG_SMEM
+  // per-lane solver state in shared memory ([warp][field][component][lane]: conflict-free), leaving the
+  // registers to the SpMV's loads in flight
+  extern __shared__ double s_state[];
+  const int wq = threadIdx.x >> 5;
+#define GF_SV(f, c) s_state[((wq * 6 + (f)) * 3 + (c)) * 32 + lane]
+#else
+  double xv_[3] = {0.0, 0.0, 0.0}, rv_[3] = {0.0, 0.0, 0.0}, dv_[3] = {0.0, 0.0, 0.0};
+  double pv_[3] = {0.0, 0.0, 0.0}, qv_[3] = {0.0, 0.0, 0.0}, zv_[3] = {0.0, 0.0, 0.0};
+  double* const svp[6] = {xv_, rv_, dv_, pv_, qv_, zv_};
+#define GF_SV(f, c) svp[f][c]
+#endif
   int own_row = -1;
   // setup (sparse.cpp:145-157): r = b - A x, z = D^-1 r, p = z, q = 0; partials b.b, r.z, r.r per unit
   double tot3[3];
@@ -299,17 +312,17 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
           const double di = __ldg(a.dinv + dof);
           const double zi = di * ri;
           if (kRegs) {
-            xv[c] = a.x[dof];
-            rv[c] = ri;
-            dv[c] = di;
+            GF_SV(0, c) = a.x[dof];
+            GF_SV(1, c) = ri;
+            GF_SV(2, c) = di;
             own_row = row;
           } else {
             a.r[dof] = ri;
           }
           a.z[dof] = zi;
           if (kRegs2) {
-            zv[c] = zi;
-            pv[c] = zi;
+            GF_SV(5, c) = zi;
+            GF_SV(3, c) = zi;
           } else {
             a.p0[dof] = zi;
           }
@@ -355,10 +368,10 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
           for (int c = 0; c < 3; ++c) {
             const size_t dof = 3 * (size_t)row + c;
             if (kRegs2) {
-              const double pr = fused ? __fma_rn(beta, pv[c], zv[c]) : zv[c];
-              const double qr = fused ? __fma_rn(beta, qv[c], acc[c]) : acc[c];
-              pv[c] = pr;
-              qv[c] = qr;
+              const double pr = fused ? __fma_rn(beta, GF_SV(3, c), GF_SV(5, c)) : GF_SV(5, c);
+              const double qr = fused ? __fma_rn(beta, GF_SV(4, c), acc[c]) : acc[c];
+              GF_SV(3, c) = pr;
+              GF_SV(4, c) = qr;
               pq = __fma_rn(pr, qr, pq);
             } else {
               const double zi = ldv(a.z + dof);
@@ -401,13 +414,13 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               const size_t dof = 3 * (size_t)row + c;
-              xv[c] = __fma_rn(alpha, kRegs2 ? pv[c] : __ldcg(p + dof), xv[c]);
-              rv[c] = __fma_rn(-alpha, kRegs2 ? qv[c] : __ldcg(a.Ap + dof), rv[c]);
-              const double zi = dv[c] * rv[c];
-              if (kRegs2) zv[c] = zi;
+              GF_SV(0, c) = __fma_rn(alpha, kRegs2 ? GF_SV(3, c) : __ldcg(p + dof), GF_SV(0, c));
+              GF_SV(1, c) = __fma_rn(-alpha, kRegs2 ? GF_SV(4, c) : __ldcg(a.Ap + dof), GF_SV(1, c));
+              const double zi = GF_SV(2, c) * GF_SV(1, c);
+              if (kRegs2) GF_SV(5, c) = zi;
               a.z[dof] = zi;
-              r2 = __fma_rn(rv[c], rv[c], r2);
-              rzp = __fma_rn(rv[c], zi, rzp);
+              r2 = __fma_rn(GF_SV(1, c), GF_SV(1, c), r2);
+              rzp = __fma_rn(GF_SV(1, c), zi, rzp);
             }
           }
         } else {
@@ -455,7 +468,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
     }
     if (kRegs && own_row >= 0)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) a.x[3 * (size_t)own_row + c] = xv[c];
+      for (int c = 0; c < 3; ++c) a.x[3 * (size_t)own_row + c] = GF_SV(0, c);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.out[0] = iterations;
@@ -502,7 +515,16 @@ void launch_pcg_sell(const CgLaunch& a, double* part, int ndyn, unsigned long lo
   if (ndyn > 0) cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s);
   void* args[] = {&sa};
   const void* fn = ndyn > 0 ? (const void*)k_pcg_sell<true> : (const void*)k_pcg_sell<false>;
-  const cudaError_t err = cudaLaunchCooperativeKernel(fn, pcg_sell_grid(), kThreads, args, 0, s);
+  const size_t smem = GF_CG_SMEM ? (size_t)kWarpsPerCta * 6 * 3 * 32 * sizeof(double) : 0;
+  if (GF_CG_SMEM) {
+    static bool attr = [&] {
+      cudaFuncSetAttribute((const void*)k_pcg_sell<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute((const void*)k_pcg_sell<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      return true;
+    }();
+    (void)attr;
+  }
+  const cudaError_t err = cudaLaunchCooperativeKernel(fn, pcg_sell_grid(), kThreads, args, smem, s);
   if (err != cudaSuccess) {
     cudaGetLastError();
     throw std::runtime_error(std::string("cooperative CG launch failed: ") + cudaGetErrorString(err));
