@@ -138,6 +138,86 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// column block c of row i (neighbour j): K v contribution, A = kscale K + mscale M, Dirichlet projection (fixed
+// row -> identity/zero, fixed column -> its A_ij dv_j moved to corr), SELL-32 upper-block store, D^-1 from the
+// diagonal; kv and corr accumulate
+template <int kMode>
+__device__ __forceinline__ void finish_column(const DevData& d, const StepCoeffs& sc, int i, int row0, int c, int j,
+                                              const double K[9], bool fixed_i, double kv[3], double corr[3]) {
+  // destination: the upper block in SELL-32 (entry r at out[32 r]); lower blocks of the symmetric format are
+  // not stored (row j writes (j,i) = (i,j)^T)
+  const int cu = __ldg(d.uslot + row0 + c);
+  double* out = cu >= 0 ? d.bval + sell_addr(d.usp, i, cu, 0) : nullptr;
+  constexpr int ostride = 32;
+  if (kMode == kAssembleRawK) {
+    if (out)
+#pragma unroll
+      for (int r = 0; r < 9; ++r) out[ostride * r] = K[r];
+    return;
+  }
+  double vj[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) vj[a] = d.v[3 * (size_t)j + a];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) kv[a] += K[3 * a] * vj[0] + K[3 * a + 1] * vj[1] + K[3 * a + 2] * vj[2];
+  double A[9];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) A[r] = sc.kscale * K[r];
+  if (j == i) {
+    const double md = sc.mscale * __ldg(d.mass + i);
+    A[0] += md;
+    A[4] += md;
+    A[8] += md;
+  }
+  if (fixed_i) {  // project_dirichlet: fixed row zeroed, unit diagonal
+#pragma unroll
+    for (int r = 0; r < 9; ++r) A[r] = (j == i && r % 4 == 0) ? 1.0 : 0.0;
+  } else if (__ldg(d.node_bc + j) >= 0) {  // fixed column: move A_ij * dv_j to the rhs, zero it
+    double fj[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) fj[a] = d.fv[3 * (size_t)j + a];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) corr[a] += A[3 * a] * fj[0] + A[3 * a + 1] * fj[1] + A[3 * a + 2] * fj[2];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) A[r] = 0.0;
+  }
+  if (out)
+#pragma unroll
+    for (int r = 0; r < 9; ++r) out[ostride * r] = A[r];
+  if (j == i) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double dd = A[4 * a];
+      d.dinv[3 * (size_t)i + a] = (fabs(dd) > 1e-300) ? 1.0 / dd : 1.0;  // sparse.cpp:133-136
+    }
+  }
+}
+
+// row i's rhs / CG initial guess / force output (lanes 0..2), after the kv and corr warp sums
+template <int kMode>
+__device__ __forceinline__ void finish_row(const DevData& d, const StepCoeffs& sc, int i, int lane, double fsum,
+                                           bool fixed_i, const double kv[3], const double corr[3]) {
+  if (lane >= 3) return;
+  const int a = lane;
+  const size_t dof = 3 * (size_t)i + a;
+  if (d.fint_out) d.fint_out[dof] = fsum;
+  if (kMode == kAssembleSystem) {
+    if (fixed_i) {
+      d.rhs[dof] = d.fv[dof];
+      d.x[dof] = d.fv[dof];
+    } else {
+      const double mv = __ldg(d.mass + i) * d.v[dof];
+      const double fe = sc.use_ext ? d.fext[dof] + d.fcoll[dof] : 0.0;
+      double r = sc.rhs_fint_scale * (fe + fsum);
+      r -= sc.rhs_mv_scale * mv;
+      r -= sc.rhs_kv_scale * kv[a];
+      r -= corr[a];
+      d.rhs[dof] = r;
+      d.x[dof] = 0.0;
+    }
+  }
+}
+
 // One warp per node row i:
 //  1. lane l < valence(i) evaluates the l-th incident tet (ascending id): force and diagonal block are warp
 //     sums, the three off-diagonal blocks go to s_blk
@@ -159,6 +239,7 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
   if (i >= d.nn) return;
   const int p0 = __ldg(d.nt_ptr + i), np = __ldg(d.nt_ptr + i + 1) - p0;
   const int row0 = __ldg(d.brow + i), deg = __ldg(d.brow + i + 1) - row0;
+  if (np > kMaxValence || deg > kMaxDeg) return;  // warp-uniform: k_assemble_big handles this row
 
   double f[3] = {0.0, 0.0, 0.0};
   double dg[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -220,54 +301,7 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
       double K[9];
 #pragma unroll
       for (int r = 0; r < 9; ++r) K[r] = s_row[w][9 * c + r];
-      // destination: the upper block in SELL-32 (entry r at out[32 r]); lower blocks of the
-      // symmetric format are not stored (row j writes (j,i) = (i,j)^T)
-      const int cu = __ldg(d.uslot + row0 + c);
-      double* out = cu >= 0 ? d.bval + sell_addr(d.usp, i, cu, 0) : nullptr;
-      constexpr int ostride = 32;
-      if (kMode == kAssembleRawK) {
-        if (out)
-#pragma unroll
-          for (int r = 0; r < 9; ++r) out[ostride * r] = K[r];
-      } else {
-        const int j = jc;
-        double vj[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) vj[a] = d.v[3 * (size_t)j + a];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) kv[a] = K[3 * a] * vj[0] + K[3 * a + 1] * vj[1] + K[3 * a + 2] * vj[2];
-        double A[9];
-#pragma unroll
-        for (int r = 0; r < 9; ++r) A[r] = sc.kscale * K[r];
-        if (j == i) {
-          const double md = sc.mscale * __ldg(d.mass + i);
-          A[0] += md;
-          A[4] += md;
-          A[8] += md;
-        }
-        if (fixed_i) {  // project_dirichlet: fixed row zeroed, unit diagonal
-#pragma unroll
-          for (int r = 0; r < 9; ++r) A[r] = (j == i && r % 4 == 0) ? 1.0 : 0.0;
-        } else if (__ldg(d.node_bc + j) >= 0) {  // fixed column: move A_ij * dv_j to the rhs, zero it
-          double fj[3];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) fj[a] = d.fv[3 * (size_t)j + a];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) corr[a] = A[3 * a] * fj[0] + A[3 * a + 1] * fj[1] + A[3 * a + 2] * fj[2];
-#pragma unroll
-          for (int r = 0; r < 9; ++r) A[r] = 0.0;
-        }
-        if (out)
-#pragma unroll
-          for (int r = 0; r < 9; ++r) out[ostride * r] = A[r];
-        if (j == i) {
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            const double dd = A[4 * a];
-            d.dinv[3 * (size_t)i + a] = (fabs(dd) > 1e-300) ? 1.0 / dd : 1.0;  // sparse.cpp:133-136
-          }
-        }
-      }
+      finish_column<kMode>(d, sc, i, row0, c, jc, K, fixed_i, kv, corr);
     }
   }
   if (kMode == kAssembleSystem) {
@@ -277,26 +311,111 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
       corr[a] = warp_sum(corr[a]);
     }
   }
-  if (lane < 3) {
-    const int a = lane;
-    const size_t dof = 3 * (size_t)i + a;
-    if (d.fint_out) d.fint_out[dof] = fsum;
-    if (kMode == kAssembleSystem) {
-      if (fixed_i) {
-        d.rhs[dof] = d.fv[dof];
-        d.x[dof] = d.fv[dof];
-      } else {
-        const double mv = __ldg(d.mass + i) * d.v[dof];
-        const double fe = sc.use_ext ? d.fext[dof] + d.fcoll[dof] : 0.0;
-        double r = sc.rhs_fint_scale * (fe + fsum);
-        r -= sc.rhs_mv_scale * mv;
-        r -= sc.rhs_kv_scale * kv[a];
-        r -= corr[a];
-        d.rhs[dof] = r;
-        d.x[dof] = 0.0;
+  finish_row<kMode>(d, sc, i, lane, fsum, fixed_i, kv, corr);
+}
+
+
+// Rows with more than 32 incident tets or 32 neighbour blocks (unstructured meshes; none in the box meshes):
+// the same computation with the incident tets taken 32 at a time. Per chunk the lanes' off-diagonal blocks go to
+// shared memory and every output adds the items of its (padded, ascending) list that fall in the chunk; forces
+// and diagonal blocks accumulate per lane across chunks, then one butterfly. Items are 3 l + s (l < 85), 255 pads.
+constexpr int kBigDeg = 64;
+template <int kMode>
+__global__ void __launch_bounds__(32 * kWarps) k_assemble_big(DevData d, MatDev m, StepCoeffs sc) {
+  constexpr bool kBlocks = kMode != kAssembleForcesOnly;
+  extern __shared__ double s_dyn[];
+  double(*s_blk)[kBlkStride] = reinterpret_cast<double(*)[kBlkStride]>(s_dyn);
+  __shared__ double s_row[kWarps][kBigDeg * 9];
+  __shared__ uint8_t s_item[kWarps][16 * kBigDeg];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bi = blockIdx.x * kWarps + w;
+  if (bi >= d.n_big) return;
+  const int i = __ldg(d.big_rows + bi);
+  const int p0 = __ldg(d.nt_ptr + i), np = __ldg(d.nt_ptr + i + 1) - p0;
+  const int row0 = __ldg(d.brow + i), deg = __ldg(d.brow + i + 1) - row0;
+  int mx = 0;
+  if (kBlocks) {
+    const int ib0 = __ldg(d.contrib_ptr + i), nitems = __ldg(d.contrib_ptr + i + 1) - ib0;
+    mx = nitems / deg;
+    for (int k = lane; k < nitems; k += 32) s_item[w][k] = __ldg(d.contrib_item + ib0 + k);
+    for (int o = lane; o < 9 * deg; o += 32) s_row[w][o] = 0.0;
+    __syncwarp();
+  }
+  double facc[3] = {0.0, 0.0, 0.0}, dacc[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int ch = 0; ch < np; ch += 32) {
+    const int l = ch + lane;
+    double f[3] = {0.0, 0.0, 0.0}, dg[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    double* blk = kBlocks ? &s_blk[w][27 * lane] : nullptr;
+    bool wrote = false;
+    if (l < np) {
+      const int e = __ldg(d.nt_tet + p0 + l);
+      const int4 t = __ldg(d.tets + e);
+      const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
+      const double scale = d.chi[e] * __ldg(d.vol + e);
+      if (scale != 0.0) {
+        element_row<kBlocks>(d, m, e, li, scale, f, blk, dg);
+        wrote = true;
       }
     }
+    if (kBlocks && !wrote)
+#pragma unroll
+      for (int r = 0; r < 27; ++r) blk[r] = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) facc[a] += f[a];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) dacc[q] += dg[q];
+    if (kBlocks) {
+      __syncwarp();
+      for (int o = lane; o < 9 * deg; o += 32) {
+        const int c = o / 9, q = o - 9 * c;
+        const uint8_t* it = &s_item[w][c * mx];
+        double sum = 0.0;
+        for (int t = 0; t < mx; ++t) {
+          const int item = it[t];
+          const int li = item / 3;
+          if (item != 255 && li >= ch && li < ch + 32) sum += s_blk[w][27 * (li - ch) + 9 * (item - 3 * li) + q];
+        }
+        s_row[w][o] += sum;
+      }
+      __syncwarp();
+    }
   }
+  double fsum = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double t = warp_sum(facc[a]);
+    if (lane == a) fsum = t;
+  }
+  const bool fixed_i = __ldg(d.node_bc + i) >= 0;
+  double kv[3] = {0.0, 0.0, 0.0}, corr[3] = {0.0, 0.0, 0.0};
+  if (kBlocks) {
+    int cdiag = -1;
+    for (int c0 = 0; c0 < deg; c0 += 32) {
+      const int c = c0 + lane;
+      const unsigned bal = __ballot_sync(0xffffffffu, c < deg && __ldg(d.bcol + row0 + c) == i);
+      if (bal) cdiag = c0 + __ffs(bal) - 1;
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const double t = warp_sum(dacc[q]);
+      if (lane == q) s_row[w][9 * cdiag + q] = t;
+    }
+    __syncwarp();
+    for (int c = lane; c < deg; c += 32) {
+      double K[9];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) K[r] = s_row[w][9 * c + r];
+      finish_column<kMode>(d, sc, i, row0, c, __ldg(d.bcol + row0 + c), K, fixed_i, kv, corr);
+    }
+  }
+  if (kMode == kAssembleSystem) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      kv[a] = warp_sum(kv[a]);
+      corr[a] = warp_sum(corr[a]);
+    }
+  }
+  finish_row<kMode>(d, sc, i, lane, fsum, fixed_i, kv, corr);
 }
 
 // per-tet strain energy chi*V*Psi(F) (fem.cpp:190-199), block partial sums (deterministic order)
@@ -355,6 +474,19 @@ void launch_assemble(const DevData& d, const MatDev& m, const StepCoeffs& c, int
   if (mode == kAssembleSystem) k_assemble<kAssembleSystem><<<grid, 32 * kWarps, kDyn, s>>>(d, m, c);
   else if (mode == kAssembleRawK) k_assemble<kAssembleRawK><<<grid, 32 * kWarps, kDyn, s>>>(d, m, c);
   else k_assemble<kAssembleForcesOnly><<<grid, 32 * kWarps, 0, s>>>(d, m, c);
+  if (d.n_big > 0) {
+    static bool big_attr = [] {
+      cudaFuncSetAttribute(k_assemble_big<kAssembleSystem>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+      cudaFuncSetAttribute(k_assemble_big<kAssembleRawK>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+      cudaFuncSetAttribute(k_assemble_big<kAssembleForcesOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+      return true;
+    }();
+    (void)big_attr;
+    const int bg = (d.n_big + kWarps - 1) / kWarps;
+    if (mode == kAssembleSystem) k_assemble_big<kAssembleSystem><<<bg, 32 * kWarps, kDyn, s>>>(d, m, c);
+    else if (mode == kAssembleRawK) k_assemble_big<kAssembleRawK><<<bg, 32 * kWarps, kDyn, s>>>(d, m, c);
+    else k_assemble_big<kAssembleForcesOnly><<<bg, 32 * kWarps, kDyn, s>>>(d, m, c);
+  }
 }
 
 void launch_energy(const DevData& d, const MatDev& m, double* partials, int nblocks, cudaStream_t s) {

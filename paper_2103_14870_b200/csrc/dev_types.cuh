@@ -69,6 +69,8 @@ struct DevData {
   const uint32_t* nt_slot;
   // per block (CSR order) the contributions (pair l, local node k) as items l*4+k, ascending tet order
   const int32_t* contrib_ptr;  // nn+1: padded contribution items of row i start here (mx per column)
+  const int32_t* big_rows;     // rows with > 32 incident tets or > 32 neighbour blocks (k_assemble_big)
+  int32_t n_big;
   const uint8_t* contrib_item;
   // node-block pattern (CSR view: column ids per row, ascending)
   const int32_t* brow;      // nn+1

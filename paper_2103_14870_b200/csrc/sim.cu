@@ -236,9 +236,9 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
 
   // host setup: pattern, incidence, table, mass (fem.cpp:140-179, fracture.cpp:32-54)
   pat_ = make_node_pattern(mesh_);
-  if (pat_.max_degree > 32) throw GeometryError("node rows with more than 32 neighbour blocks are not supported by the assembly kernel");
+  if (pat_.max_degree > 64) throw GeometryError("node rows with more than 64 neighbour blocks are not supported by the assembly kernel");
   const NodeTets ntets = make_node_tets(mesh_, pat_);
-  if (ntets.max_valence > 32) throw GeometryError("nodes shared by more than 32 tets are not supported by the assembly kernel");
+  if (ntets.max_valence > 84) throw GeometryError("nodes shared by more than 84 tets are not supported by the assembly kernel");
   hash_ = pat_.structure_hash(mesh_.nn);
   mass_.assign(mesh_.nn, 0.0);
   for (int32_t e = 0; e < mesh_.nt; ++e) {  // lumped_mass (fem.cpp:171-179), ascending tet order
@@ -307,14 +307,24 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
       if (mx > 16) throw GeometryError("more than 16 tets around an edge are not supported by the assembly kernel");
       rptr[i + 1] = rptr[i] + mx * (pat_.row_ptr[i + 1] - pat_.row_ptr[i]);
     }
+    // rows beyond one warp's lanes (> 32 incident tets or > 32 neighbour blocks) go to k_assemble_big, whose
+    // padding item is 255; the one-warp rows pad with 96 (the zero block after the 32 lanes' blocks)
+    std::vector<int32_t> big;
     std::vector<uint8_t> padded(rptr[nn], 96);
     for (int32_t i = 0; i < nn; ++i) {
       const int32_t deg = pat_.row_ptr[i + 1] - pat_.row_ptr[i], mx = (rptr[i + 1] - rptr[i]) / std::max(1, deg);
+      const bool is_big = ntets.ptr[i + 1] - ntets.ptr[i] > 32 || deg > 32;
+      if (is_big) {
+        big.push_back(i);
+        std::fill(padded.begin() + rptr[i], padded.begin() + rptr[i + 1], (uint8_t)255);
+      }
       for (int32_t c = 0; c < deg; ++c) {
         const int32_t b = pat_.row_ptr[i] + c;
         for (int32_t t = cnt[b]; t < cnt[b + 1]; ++t) padded[rptr[i] + c * mx + (t - cnt[b])] = items[t];
       }
     }
+    d_.n_big = (int32_t)big.size();
+    d_.big_rows = big.empty() ? nullptr : (const int32_t*)up(big.data(), 4 * big.size());
     d_.contrib_ptr = (const int32_t*)up(rptr.data(), 4 * rptr.size());
     d_.contrib_item = (const uint8_t*)up(padded.data(), std::max<size_t>(1, padded.size()));
     GF_CUDA(cudaStreamSynchronize(stream_));
@@ -339,6 +349,8 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     for (int32_t i = 0; i < nn; ++i)
       for (int32_t q = pat_.row_ptr[i]; q < pat_.row_ptr[i + 1]; ++q)
         if (pat_.cols[q] >= i) uslot_[q] = ucount[i]++;
+    for (int32_t i = 0; i < nn; ++i)
+      if (ucount[i] > 63) throw GeometryError("node rows with more than 63 upper neighbour blocks are not supported");
     usp_.assign(ns + 1, 0);
     for (int32_t sl = 0; sl < ns; ++sl) {
       int32_t mx = 0;

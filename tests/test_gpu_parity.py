@@ -619,3 +619,75 @@ def test_nonlocal_layout_falls_back_for_unstructured_meshes():
     s0 = g.Simulation(g.make_box_mesh((0.1, 0.1, 0.1), (2, 2, 2)),
                       g.MaterialParams.from_youngs(1e6, 0.3, 1000, 10.0, 0.0, g.STVK), g.SolverConfig(dt=1e-3))
     assert s0.nonlocal_layout() == 0
+
+
+# ---------------------------------------------------------------- high-valence (unstructured) rows
+def _icosphere_fan(radius=0.1, levels=1, layers=2):
+    """Nested icospheres joined by prisms split into tets plus a fan around the centre node: the centre has
+    80 incident tets and 43 neighbour blocks (beyond one warp: k_assemble_big), the rest are ordinary rows."""
+    t = (1 + 5 ** 0.5) / 2
+    v = [(-1, t, 0), (1, t, 0), (-1, -t, 0), (1, -t, 0), (0, -1, t), (0, 1, t), (0, -1, -t), (0, 1, -t),
+         (t, 0, -1), (t, 0, 1), (-t, 0, -1), (-t, 0, 1)]
+    f = [(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11), (1, 5, 9), (5, 11, 4), (11, 10, 2), (10, 7, 6),
+         (7, 1, 8), (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9), (4, 9, 5), (2, 4, 11), (6, 2, 10),
+         (8, 6, 7), (9, 8, 1)]
+    v = [np.array(p, float) / np.linalg.norm(p) for p in v]
+    for _ in range(levels):
+        mid = {}
+        def m(a, b):
+            k = (min(a, b), max(a, b))
+            if k not in mid:
+                p = v[a] + v[b]
+                v.append(p / np.linalg.norm(p))
+                mid[k] = len(v) - 1
+            return mid[k]
+        f = [tri for a, b, c in f for tri in ((a, m(a, b), m(c, a)), (b, m(b, c), m(a, b)), (c, m(c, a), m(b, c)),
+                                               (m(a, b), m(b, c), m(c, a)))]
+    nv = len(v)
+    nodes = [np.zeros(3)]
+    for L in range(1, layers + 1):
+        nodes += [radius * L / layers * p for p in v]
+    nodes = np.array(nodes)
+    tets = []
+    shell = lambda L, k: 1 + (L - 1) * nv + k
+    for a, b, c in f:  # fan around the centre
+        tets.append([0, shell(1, a), shell(1, b), shell(1, c)])
+    for L in range(1, layers):  # prism between shells L and L+1, split into 3 tets (consistent by index order)
+        for a, b, c in f:
+            lo = sorted((a, b, c))
+            A, B, C = (shell(L, k) for k in lo)
+            D, E, F = (shell(L + 1, k) for k in lo)
+            tets += [[A, B, C, F], [A, B, F, E], [A, E, F, D]]
+    for tt in tets:  # positive orientation
+        p = nodes[tt]
+        if np.linalg.det(np.stack([p[1] - p[0], p[2] - p[0], p[3] - p[0]], 1)) < 0:
+            tt[2], tt[3] = tt[3], tt[2]
+    return nodes, np.array(tets, np.int32)
+
+
+@pytest.mark.parametrize("model", [0, 1])
+def test_high_valence_rows_match_oracle(model):
+    nodes, tets = _icosphere_fan()
+    gm, om = g.make_mesh(nodes, tets), o.Mesh.create(nodes, tets)
+    mat = (1e6, 0.3, 1000, 1e9, 0.0, model)
+    outer = np.nonzero(np.linalg.norm(nodes, axis=1) > 0.099)[0][:20]
+    cfg = dict(dt=1e-3, gravity=(0.0, -9.81, 0.0))
+    bc = dict(nodes=outer, times=[0, 1], values=[[0, 0, 0], [0.002, 0, 0]])
+    gs = g.Simulation(gm, g.MaterialParams.from_youngs(*mat), g.SolverConfig(**cfg),
+                      [g.BoundaryCondition(nodes=outer, translation=g.Schedule3([0, 1], [[0, 0, 0], [0.002, 0, 0]]))])
+    os_ = o.Sim(om, o.material_from_youngs(*mat), o.solver_config(**cfg), [bc])
+    rng = np.random.default_rng(51)
+    u = rng.uniform(-2e-3, 2e-3, nodes.shape)
+    chi = rng.uniform(0.3, 1.0, len(tets))
+    gs.set_state(displacements=u, element_chi=chi)
+    os_.set_state(u=u, chi=chi)
+    assert rel_err(gs.eval_forces(), om.assemble_forces(os_.mat, u, chi)) < FORCE_TOL
+    assert rel_err(gs.eval_stiffness(), om.assemble_stiffness(os_.mat, u, chi)) < FORCE_TOL
+    for _ in range(5):
+        a = os_.dynamic_step()
+        b = gs.dynamic_step()
+        assert abs(a.cg_iterations - b.cg_iterations) <= 2
+    a_ref, r_ref = os_.last_system()
+    a_got, r_got = gs.last_system()
+    assert rel_err(a_got, a_ref) < FORCE_TOL and rel_err(r_got, r_ref) < FORCE_TOL
+    assert np.abs(gs.state().displacements - os_.get_state()["u"]).max() / 0.1 < TRAJ_TOL
