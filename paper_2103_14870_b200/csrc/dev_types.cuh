@@ -66,7 +66,6 @@ struct DevData {
   // node -> tet incidence (ascending tet) with packed column slots
   const int32_t* nt_ptr;
   const int32_t* nt_tet;
-  const uint32_t* nt_slot;
   // per block (CSR order) the contributions (pair l, local node k) as items l*4+k, ascending tet order
   const int32_t* contrib_ptr;  // nn+1: padded contribution items of row i start here (mx per column)
   const int32_t* big_rows;     // rows with > 32 incident tets or > 32 neighbour blocks (k_assemble_big)
@@ -135,9 +134,7 @@ struct DevData {
   double* r;
   double* z;
   double* p0;
-  double* p1;
   double* Ap;
-  double* partials;         // per-block reduction slots
   double* cg_out;           // [iterations, converged, negcurv, relres]
   // misc
   const BcStep* bcstep;
