@@ -1124,6 +1124,8 @@ struct Collider {
 struct CollisionResult {
   std::vector<double> force;
   std::vector<double> per_collider;
+  int contact_count = 0, deep_penetrations = 0;  // collision.hpp:37-41
+  double max_depth = 0.0;
 };
 static CollisionResult detect_and_respond(const Mesh& m, const std::vector<V3>& u, const std::vector<V3>& v,
                                           const std::vector<double>& mass, const std::vector<Collider>& cols,
@@ -1147,12 +1149,15 @@ static CollisionResult detect_and_respond(const Mesh& m, const std::vector<V3>& 
         depth = col.radius - dist;
         if (depth <= 0.0) continue;
         normal = dist > 1e-12 ? V3{rel[0] / dist, rel[1] / dist, rel[2] / dist} : V3{0, 0, 1};
+        if (depth > 0.5 * col.radius) out.deep_penetrations++;
       } else {
         const V3 rel = sub3(x, col.point);
         depth = -((rel[0] * col.normal[0] + rel[1] * col.normal[1]) + rel[2] * col.normal[2]);
         if (depth <= 0.0) continue;
         normal = col.normal;
       }
+      out.contact_count++;
+      out.max_depth = std::max(out.max_depth, depth);
       const double kd = col.stiffness * depth;
       V3 f = {kd * normal[0], kd * normal[1], kd * normal[2]};
       const V3 vrel = sub3(v[i], cv);
@@ -1763,6 +1768,49 @@ void or_solver_config_default(or_solver_config* c) {
   c->dynamic_full_newton = 0; c->collision_substeps = d.collision_substeps;
 }
 
+static Collider collider_from(const or_collider& c) {
+  Collider cl;
+  cl.kind = c.kind;
+  cl.center = sched_from(c.n_keys, c.key_times, c.key_values);
+  cl.radius = c.radius;
+  cl.point = {c.point[0], c.point[1], c.point[2]};
+  cl.normal = {c.normal[0], c.normal[1], c.normal[2]};
+  cl.stiffness = c.stiffness; cl.restitution = c.restitution; cl.friction = c.friction;
+  return cl;
+}
+
+void or_schedule_eval(int32_t n_keys, const double* times, const double* values, double t, double val[3],
+                      double rate[3]) {
+  const Sched s = sched_from(n_keys, times, values);
+  const V3 a = s.eval(t), b = s.rate(t);
+  for (int k = 0; k < 3; ++k) { val[k] = a[k]; rate[k] = b[k]; }
+}
+
+int or_collider_validate(const or_collider* c) {
+  return guard([&] { collider_from(*c).validate(); });
+}
+
+int or_detect_and_respond(const or_mesh* mesh, const double* u, const double* v, const double* mass3n,
+                          const or_collider* cols, int32_t n_cols, double t, double dt, double* force3n,
+                          double* per_collider, int32_t counts[2], double* max_depth) {
+  return guard([&] {
+    const Mesh& m = mesh->m;
+    const int n = m.nn();
+    std::vector<V3> uu(n), vv(n);
+    for (int i = 0; i < n; ++i)
+      for (int a = 0; a < 3; ++a) { uu[i][a] = u[3 * i + a]; vv[i][a] = v[3 * i + a]; }
+    std::vector<double> mass(mass3n, mass3n + 3 * (size_t)n);
+    std::vector<Collider> cs;
+    for (int i = 0; i < n_cols; ++i) cs.push_back(collider_from(cols[i]));
+    const CollisionResult r = detect_and_respond(m, uu, vv, mass, cs, t, dt);
+    std::copy(r.force.begin(), r.force.end(), force3n);
+    std::copy(r.per_collider.begin(), r.per_collider.end(), per_collider);
+    counts[0] = r.contact_count;
+    counts[1] = r.deep_penetrations;
+    *max_depth = r.max_depth;
+  });
+}
+
 int or_sim_create(const or_mesh* mesh, const or_material* mat, const or_solver_config* cfg,
                   const or_boundary_condition* bcs, int32_t n_bcs, const or_collider* cols, int32_t n_cols,
                   or_sim** out) {
@@ -1790,16 +1838,7 @@ int or_sim_create(const or_mesh* mesh, const or_material* mat, const or_solver_c
       b.axis_dir = {bcs[i].axis_dir[0], bcs[i].axis_dir[1], bcs[i].axis_dir[2]};
       s.bcs.push_back(std::move(b));
     }
-    for (int i = 0; i < n_cols; ++i) {
-      Collider cl;
-      cl.kind = cols[i].kind;
-      cl.center = sched_from(cols[i].n_keys, cols[i].key_times, cols[i].key_values);
-      cl.radius = cols[i].radius;
-      cl.point = {cols[i].point[0], cols[i].point[1], cols[i].point[2]};
-      cl.normal = {cols[i].normal[0], cols[i].normal[1], cols[i].normal[2]};
-      cl.stiffness = cols[i].stiffness; cl.restitution = cols[i].restitution; cl.friction = cols[i].friction;
-      s.cols.push_back(cl);
-    }
+    for (int i = 0; i < n_cols; ++i) s.cols.push_back(collider_from(cols[i]));
     // member-initialiser order of Simulation::Simulation (solver.cpp:31-60)
     s.st = rest_state(s.mesh);
     s.K = make_system_pattern(s.mesh);

@@ -137,6 +137,15 @@ void or_project_dirichlet_csr(int32_t n, const int32_t* row_ptr, const int32_t* 
                               const int32_t* dofs, int32_t n_dofs, const double* values, double* rhs);
 
 /* ---- simulation (solver.cpp) ---- */
+/* collision.cpp:8-111 (Schedule3::eval/rate, Collider::validate, detect_and_respond); counts = {contact_count,
+   deep_penetrations} */
+void or_schedule_eval(int32_t n_keys, const double* times, const double* values, double t, double val[3],
+                      double rate[3]);
+int or_collider_validate(const or_collider* c);
+int or_detect_and_respond(const or_mesh* mesh, const double* u, const double* v, const double* mass3n,
+                          const or_collider* cols, int32_t n_cols, double t, double dt, double* force3n,
+                          double* per_collider, int32_t counts[2], double* max_depth);
+
 int or_sim_create(const or_mesh* mesh, const or_material* mat, const or_solver_config* cfg,
                   const or_boundary_condition* bcs, int32_t n_bcs, const or_collider* cols, int32_t n_cols,
                   or_sim** out);

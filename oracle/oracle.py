@@ -381,6 +381,60 @@ def _sched_arrays(times, values):
     return t, v
 
 
+def _colliders(colliders, keep):
+    Cs = (Collider * max(1, len(colliders)))()
+    for i, c in enumerate(colliders):
+        t, v = _sched_arrays(np.zeros(0) if c.get("times") is None else c["times"],
+                             np.zeros((0, 3)) if c.get("values") is None else c["values"])
+        keep += [t, v]
+        Cs[i].kind = 1 if c.get("kind", "sphere") == "halfspace" else 0
+        Cs[i].n_keys = len(t)
+        Cs[i].key_times = _p(t, F64P)
+        Cs[i].key_values = _p(v, F64P)
+        Cs[i].radius = c.get("radius", 0.0)
+        Cs[i].point[:] = list(c.get("point", (0, 0, 0)))
+        Cs[i].normal[:] = list(c.get("normal", (0, 0, 1)))
+        Cs[i].stiffness = c.get("stiffness", 1e6)
+        Cs[i].restitution = c.get("restitution", 0.0)
+        Cs[i].friction = c.get("friction", 0.0)
+    return Cs
+
+
+def schedule_eval(times, values, t):
+    """Schedule3::eval / rate (collision.cpp:8-30) -> (value[3], rate[3])."""
+    tt, vv = _sched_arrays(times, values)
+    val, rate = np.zeros(3), np.zeros(3)
+    lib().or_schedule_eval(C.c_int32(len(tt)), _p(tt, F64P), _p(vv, F64P), C.c_double(t), _p(val, F64P),
+                           _p(rate, F64P))
+    return val, rate
+
+
+def collider_validate(collider):
+    """Collider::validate (collision.cpp:32-40); raises FormatError."""
+    keep = []
+    _check(lib().or_collider_validate(_colliders([collider], keep)))
+
+
+def detect_and_respond(mesh, u, v, mass, colliders, t, dt):
+    """detect_and_respond (collision.cpp:49-111) -> dict(force (n,3), per_collider, contact_count,
+    deep_penetrations, max_depth)."""
+    n = mesh.num_nodes
+    keep = []
+    Cs = _colliders(colliders, keep)
+    u = np.ascontiguousarray(u, np.float64).reshape(n, 3)
+    v = np.ascontiguousarray(v, np.float64).reshape(n, 3)
+    mass = np.ascontiguousarray(mass, np.float64).reshape(-1)
+    force = np.zeros((n, 3))
+    per = np.zeros(max(1, len(colliders)))
+    counts = np.zeros(2, np.int32)
+    md = C.c_double(0.0)
+    _check(lib().or_detect_and_respond(mesh._h, _p(u, F64P), _p(v, F64P), _p(mass, F64P), Cs,
+                                       C.c_int32(len(colliders)), C.c_double(t), C.c_double(dt), _p(force, F64P),
+                                       _p(per, F64P), _p(counts, I32P), C.byref(md)))
+    return dict(force=force, per_collider=per[:len(colliders)], contact_count=int(counts[0]),
+                deep_penetrations=int(counts[1]), max_depth=md.value)
+
+
 class Sim:
     """Oracle Simulation (solver.cpp). bcs: list of dicts {kind, nodes, times, values, axis_point, axis_dir};
     colliders: list of dicts {kind, times, values, radius, point, normal, stiffness, restitution, friction}."""
@@ -400,21 +454,7 @@ class Sim:
             B[i].key_values = _p(v, F64P)
             B[i].axis_point[:] = list(bc.get("axis_point", (0, 0, 0)))
             B[i].axis_dir[:] = list(bc.get("axis_dir", (1, 0, 0)))
-        Cs = (Collider * max(1, len(colliders)))()
-        for i, c in enumerate(colliders):
-            t, v = _sched_arrays(np.zeros(0) if c.get("times") is None else c["times"],
-                                 np.zeros((0, 3)) if c.get("values") is None else c["values"])
-            keep += [t, v]
-            Cs[i].kind = 1 if c.get("kind", "sphere") == "halfspace" else 0
-            Cs[i].n_keys = len(t)
-            Cs[i].key_times = _p(t, F64P)
-            Cs[i].key_values = _p(v, F64P)
-            Cs[i].radius = c.get("radius", 0.0)
-            Cs[i].point[:] = list(c.get("point", (0, 0, 0)))
-            Cs[i].normal[:] = list(c.get("normal", (0, 0, 1)))
-            Cs[i].stiffness = c.get("stiffness", 1e6)
-            Cs[i].restitution = c.get("restitution", 0.0)
-            Cs[i].friction = c.get("friction", 0.0)
+        Cs = _colliders(colliders, keep)
         h = C.c_void_p()
         _check(lib().or_sim_create(mesh._h, C.byref(mat), C.byref(cfg), B, C.c_int32(len(bcs)), Cs,
                                    C.c_int32(len(colliders)), C.byref(h)))

@@ -400,14 +400,14 @@ def _pair_custom(mesh_args, mat_args, cfg, bcs=(), colliders=(), u0=None, v0=Non
     return gs, os_, om
 
 
-def _compare_steps(gs, os_, om, steps, tol=TRAJ_TOL):
+def _compare_steps(gs, os_, om, steps, tol=TRAJ_TOL, load_rel=1e-9):
     scale = np.abs(om.arrays()["rest"]).max()
     loads = []
     for _ in range(steps):
         a = os_.dynamic_step()
         b = gs.dynamic_step()
         assert a.newly_broken == b.newly_broken
-        assert b.load == pytest.approx(a.load, rel=1e-9, abs=1e-12)
+        assert b.load == pytest.approx(a.load, rel=load_rel, abs=1e-12)
         loads.append(a.load)
     ost, gst = os_.get_state(), gs.state()
     assert np.array_equal(gst.edge_damage, ost["zeta"])
@@ -424,6 +424,34 @@ def test_sphere_collider_moving_with_friction():  # collision.cpp:49-111 sphere 
                                v0=np.tile([0.01, -0.02, 0.0], (125, 1)))
     loads = _compare_steps(gs, os_, om, 15)
     assert max(loads) > 0
+
+
+def test_block_settles_on_floor_matches_oracle():  # test_collision.cpp:133-166 on both sides
+    col = dict(kind="halfspace", point=(0, 0, 0), normal=(0, 1, 0), stiffness=2e5, restitution=0.0)
+    om = o.Mesh.make_box((0.1, 0.1, 0.1), (2, 2, 2))
+    # damp_mass_coeff = 40 on both sides (the reference test's "settle quickly")
+    gmat = g.MaterialParams.from_youngs(5e6, 0.3, 1000.0, 1e9, 0.0, g.STVK)
+    omat = o.material_from_youngs(5e6, 0.3, 1000.0, 1e9, 0.0, g.STVK)
+    gmat.damp_mass_coeff = omat.damp_mass_coeff = 40.0
+    gs = g.Simulation(g.make_box_mesh((0.1, 0.1, 0.1), (2, 2, 2)), gmat,
+                      g.SolverConfig(dt=1e-3, gravity=(0, -9.81, 0), cg_tol=1e-10),
+                      [], [g.Collider(kind="halfspace", normal=(0, 1, 0), stiffness=2e5)])
+    os_ = o.Sim(om, omat, o.solver_config(dt=1e-3, gravity=(0, -9.81, 0), cg_tol=1e-10), [], [col])
+    # The load is k * depth over ~1e-5 m penetrations: a 1e-14 m position difference (PCG roundoff, within the
+    # trajectory tolerance) is already 1e-9 of it, so the load is held to 1e-6 here. Penalty + impulse contact
+    # with restitution 0 has a lateral mode that amplifies any roundoff difference by ~2x per 10 steps
+    # (tools/settle_diag.py: 4e-14 at step 20, 3e-10 at 100, 2e-7 at 190), so the trajectories are compared over
+    # the first 100 steps and the reference test's physical properties checked on the GPU run at step 200.
+    _compare_steps(gs, os_, om, 100, load_rel=1e-6)
+    for _ in range(100):
+        gs.dynamic_step()
+    st = gs.state()
+    weight = 1000.0 * om.arrays()["vol"].sum() * 9.81
+    depth = -(om.arrays()["rest"][:, 1] + st.displacements[:, 1])
+    total = 2e5 * depth[depth > 0].sum()
+    assert 0.0 < depth.max() <= weight / 2e5
+    assert 0.5 * weight < total < 1.5 * weight
+    assert np.all(np.linalg.norm(st.velocities, axis=1) < 5 * 9.81 * 1e-3)
 
 
 def test_rotate_bc_and_rayleigh_damping():  # solver.cpp:22-29 rotate branch; solver.cpp:279-289 alpha/beta

@@ -317,6 +317,18 @@ def test_transform_rows_and_hydrostatic():  # test_fracture.cpp:28-46
     assert np.abs(T[3] - [0.5, 0.5, 0, -0.5, 0, 0]).max() < 1e-15
 
 
+def test_uniaxial_stress_on_inclined_edge_and_zero_stress():  # test_fracture.cpp:48-57, 75-81
+    m = unit_tet()
+    stress = 2.5e5
+    for theta in (0.0, 0.3, 0.7, 1.2):
+        u = np.zeros((4, 3))
+        u[1] = [math.cos(theta) - 1.0, math.sin(theta), 0.0]  # local edge 0 = (0,1) along (cos t, sin t, 0)
+        ok, T = m.build_T(u, 0)
+        assert ok
+        assert T[0] @ [stress, 0, 0, 0, 0, 0] == pytest.approx(stress * math.cos(theta) ** 2, rel=1e-12, abs=1e-9)
+        assert np.all(T @ np.zeros(6) == 0.0)
+
+
 def test_build_T_rotation_and_degenerate():  # test_fracture.cpp:59-73
     m = unit_tet()
     X = m.arrays()["rest"]
@@ -625,6 +637,152 @@ def test_halfspace_penalty_and_impulse():  # test_collision.cpp:48-87 via one dy
     s.dynamic_step()
     # four bottom nodes penetrate 1 mm: penalty k*d each, no inward velocity at rest
     assert s.last_collider_load() == pytest.approx(4 * 1e5 * 0.001, rel=1e-12)
+
+
+def _col(**kw):
+    d = dict(kind="halfspace", point=(0, 0, 0), normal=(0, 1, 0), stiffness=1e6, restitution=0.0, friction=0.0)
+    d.update(kw)
+    return d
+
+
+def _rest_uv(m):
+    return np.zeros((m.num_nodes, 3)), np.zeros((m.num_nodes, 3))
+
+
+def test_schedule_interpolate_and_clamp():  # test_collision.cpp:20-31
+    t, v = [0.0, 1.0, 3.0], [[0, 0, 0], [2, 0, 0], [2, 4, 0]]
+    assert np.array_equal(o.schedule_eval(t, v, -1.0)[0], [0, 0, 0])
+    assert np.linalg.norm(o.schedule_eval(t, v, 0.5)[0] - [1, 0, 0]) < 1e-15
+    assert np.linalg.norm(o.schedule_eval(t, v, 2.0)[0] - [2, 2, 0]) < 1e-15
+    assert np.array_equal(o.schedule_eval(t, v, 9.0)[0], [2, 4, 0])
+    assert np.linalg.norm(o.schedule_eval(t, v, 0.5)[1] - [2, 0, 0]) < 1e-15
+    assert np.linalg.norm(o.schedule_eval(t, v, 2.0)[1] - [0, 2, 0]) < 1e-15
+
+
+def test_no_penetration_zero_force():  # test_collision.cpp:33-48
+    m = unit_tet()
+    u, v = _rest_uv(m)
+    hit = o.detect_and_respond(m, u, v, m.lumped_mass(stvk_soft()), [_col(point=(0, -1, 0))], 0.0, 1e-3)
+    assert np.linalg.norm(hit["force"]) == 0.0 and hit["contact_count"] == 0
+
+
+def test_resting_vertex_penalty():  # test_collision.cpp:50-66
+    m = unit_tet()
+    u, v = _rest_uv(m)
+    u[0] = (0, -0.01, 0)
+    hit = o.detect_and_respond(m, u, v, m.lumped_mass(stvk_soft()), [_col(stiffness=5e4)], 0.0, 1e-3)
+    assert hit["contact_count"] == 1
+    assert np.linalg.norm(hit["force"][0] - [0, 5e4 * 0.01, 0]) < 1e-9
+
+
+def test_impulse_reverses_normal_velocity_at_restitution_1():  # test_collision.cpp:68-87
+    m = unit_tet()
+    mass = m.lumped_mass(stvk_soft())
+    u, v = _rest_uv(m)
+    u[0] = (0, -1e-6, 0)
+    v[0] = (0, -2.0, 0)
+    dt = 1e-3
+    hit = o.detect_and_respond(m, u, v, mass, [_col(stiffness=1e-9, restitution=1.0)], 0.0, dt)
+    v_after = v[0] + dt * hit["force"][0] / mass[0]
+    assert v_after[1] == pytest.approx(2.0, rel=1e-6)
+
+
+def test_moving_sphere_opposes_relative_velocity():  # test_collision.cpp:89-108
+    m = unit_tet()
+    u, v = _rest_uv(m)
+    ball = dict(kind="sphere", radius=0.5, stiffness=1e3, restitution=0.0, times=[0.0, 1.0],
+                values=[[-0.4, 0, 0], [0.6, 0, 0]])
+    hit = o.detect_and_respond(m, u, v, m.lumped_mass(stvk_soft()), [ball], 0.0, 1e-3)
+    assert hit["contact_count"] >= 1
+    assert hit["force"][0, 0] > 0.0 and hit["per_collider"][0] > 0.0
+
+
+def test_friction_clamped_by_coulomb_cone():  # test_collision.cpp:110-131
+    m = unit_tet()
+    u, v = _rest_uv(m)
+    u[0] = (0, -1e-3, 0)
+    v[0] = (5.0, 0, 0)
+    hit = o.detect_and_respond(m, u, v, m.lumped_mass(stvk_soft()), [_col(stiffness=1e4, friction=0.5)], 0.0,
+                               1e-3)
+    f = hit["force"][0]
+    normal_mag = 1e4 * 1e-3
+    assert f[0] < 0.0 and abs(f[0]) <= 0.5 * normal_mag * (1 + 1e-12)
+    assert f[1] == pytest.approx(normal_mag)
+
+
+def test_block_settles_on_floor():  # test_collision.cpp:133-166
+    m = o.Mesh.make_box((0.1, 0.1, 0.1), (2, 2, 2))
+    p = o.material_from_youngs(5e6, 0.3, 1000.0, 1e9, 0.0, STVK)
+    p.damp_mass_coeff = 40.0
+    s = o.Sim(m, p, o.solver_config(dt=1e-3, gravity=(0, -9.81, 0), cg_tol=1e-10),
+              colliders=[_col(stiffness=2e5)])
+    for _ in range(200):
+        s.dynamic_step()
+    st = s.get_state()
+    weight = 1000.0 * m.arrays()["vol"].sum() * 9.81
+    depth = -(m.arrays()["rest"][:, 1] + st["u"][:, 1])
+    total = 2e5 * depth[depth > 0].sum()
+    assert 0.0 < depth.max() <= weight / 2e5
+    assert 0.5 * weight < total < 1.5 * weight
+    assert np.all(np.linalg.norm(st["v"], axis=1) < 5 * 9.81 * 1e-3)
+
+
+def test_collider_validation():  # test_collision.cpp:168-179
+    with pytest.raises(o.FormatError):
+        o.collider_validate(dict(kind="sphere", radius=0.0))
+    with pytest.raises(o.FormatError):
+        o.collider_validate(dict(kind="sphere", radius=1.0, restitution=1.5))
+    with pytest.raises(o.FormatError):
+        o.collider_validate(dict(kind="sphere", radius=1.0, restitution=0.5, friction=-1.0))
+    o.collider_validate(dict(kind="sphere", radius=1.0, restitution=0.5))
+
+
+def test_rotation_bc_moves_nodes_on_circles():  # test_solver.cpp:157-173 (through one step landing on t = 1)
+    m = o.Mesh.make_box((0.2, 0.1, 0.1), (2, 1, 1))
+    rest = m.arrays()["rest"][3]
+    axis = np.array([0, 0.05, 0.05])
+    bc = dict(kind="rotate", nodes=[3], axis_point=axis, axis_dir=(1, 0, 0), times=[0, 1],
+              values=[[0, 0, 0], [math.pi / 2, 0, 0]])
+    s = o.Sim(m, o.material_from_youngs(1e6, 0.3, 1000, 1e9, 0, STVK), o.solver_config(dt=1.0), [bc])
+    s.dynamic_step()
+    rel0, rel1 = rest - axis, rest + s.get_state()["u"][3] - axis
+    assert np.linalg.norm(rel1) == pytest.approx(np.linalg.norm(rel0), rel=1e-12)
+    assert abs(rel0 @ rel1 - rel0[0] * rel1[0]) < 1e-12
+
+
+def test_rayleigh_damping_in_the_step_system():  # test_fem.cpp:257-279 restated on the implicit-Euler system
+    m = unit_tet()
+    rng = np.random.default_rng(31)
+    u = rng.uniform(-0.05, 0.05, (4, 3))
+    v = np.sin(np.arange(1, 13, dtype=float)).reshape(4, 3)
+    dt = 1e-3
+
+    def system(a, b):
+        p = stvk_soft(1e12)
+        p.damp_mass_coeff, p.damp_stiff_coeff = a, b
+        s = o.Sim(m, p, o.solver_config(dt=dt))
+        s.set_state(u=u, v=v)
+        s.dynamic_step()
+        return s.last_system()
+
+    p = stvk_soft(1e12)
+    K = m.assemble_stiffness(p, u)
+    rp, cols, _ = m.pattern()
+    mass = m.lumped_mass(p)
+    Kd = np.zeros((12, 12))
+    for i in range(12):
+        Kd[i, cols[rp[i]:rp[i + 1]]] = K[rp[i]:rp[i + 1]]
+    diag = np.array([np.nonzero(cols[rp[i]:rp[i + 1]] == i)[0][0] + rp[i] for i in range(12)])
+    A0, r0 = system(0.0, 0.0)
+    A1, r1 = system(2.5, 0.0)
+    A2, r2 = system(2.5, 0.1)
+    # alpha only: mass-proportional diagonal and rhs terms, stiffness part untouched
+    dA = A1 - A0
+    assert np.allclose(dA[diag], dt * 2.5 * mass, rtol=1e-12) and np.all(np.delete(dA, diag) == 0)
+    assert np.allclose(r1 - r0, -dt * 2.5 * mass * v.reshape(-1), rtol=1e-9, atol=1e-15)
+    # beta: stiffness-proportional matrix and rhs terms scale with dt * beta
+    assert np.allclose(A2 - A1, dt * 0.1 * K, rtol=1e-9, atol=1e-12 * np.abs(A2).max())
+    assert np.allclose(r2 - r1, -dt * 0.1 * Kd @ v.reshape(-1), rtol=1e-9, atol=1e-12 * np.abs(r2).max())
 
 
 def test_tetgen_parse():  # mesh.cpp:157-221 (one-based detection)
