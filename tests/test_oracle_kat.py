@@ -60,6 +60,17 @@ def test_stvk_energy_kat():  # test_material.cpp:62-67
     assert o.energy_density(2 * np.eye(3), p) == pytest.approx(16.875, rel=1e-14)
 
 
+def test_stvk_energy_stationary_at_rest():  # test_material.cpp:155-170
+    p = o.material_lame(1.0, 1.0, STVK)
+    rng = np.random.default_rng(59)
+    h = 1e-7
+    for _ in range(10):
+        d = rng.uniform(-1, 1, (3, 3))
+        d /= np.linalg.norm(d)
+        slope = (o.energy_density(np.eye(3) + h * d, p) - o.energy_density(np.eye(3) - h * d, p)) / (2 * h)
+        assert abs(slope) < 100 * h
+
+
 def test_nh_rest_energy_kat():  # test_material.cpp:69-74
     p = o.material_lame(1.0, 1.0, NH)
     assert o.energy_density(np.eye(3), p) == pytest.approx(0.5 * 0.5625 - 0.5 * math.log(4.0), rel=1e-14)
