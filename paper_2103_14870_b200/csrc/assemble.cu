@@ -138,6 +138,28 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Warp reduce-scatter of N values (N a power of two <= 32): every butterfly level halves the values a lane
+// carries (the lanes with the level's bit set keep the upper half), so N values cost N - 1 + log2(32 / N)
+// shuffles instead of 5 N. Returns the warp sum of value (lane >> (5 - log2 N)): value k ends up in lanes
+// k 32/N .. (k + 1) 32/N - 1. Fixed order: deterministic and identical in the lanes that hold a value.
+template <int N>
+__device__ __forceinline__ double warp_reduce_scatter(double (&v)[N], int lane) {
+  int o = 16;
+#pragma unroll
+  for (int h = N / 2; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < h; ++k) {
+      const double send = up ? v[k] : v[h + k];
+      const double keep = up ? v[h + k] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+#pragma unroll
+  for (; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  return v[0];
+}
+
 // column block c of row i (neighbour j): K v contribution, A = kscale K + mscale M, Dirichlet projection (fixed
 // row -> identity/zero, fixed column -> its A_ij dv_j moved to corr), SELL-32 upper-block store, D^-1 from the
 // diagonal; kv and corr accumulate
@@ -196,7 +218,7 @@ __device__ __forceinline__ void finish_column(const DevData& d, const StepCoeffs
 // row i's rhs / CG initial guess / force output (lanes 0..2), after the kv and corr warp sums
 template <int kMode>
 __device__ __forceinline__ void finish_row(const DevData& d, const StepCoeffs& sc, int i, int lane, double fsum,
-                                           bool fixed_i, const double kv[3], const double corr[3]) {
+                                           bool fixed_i, double kva, double corra) {
   if (lane >= 3) return;
   const int a = lane;
   const size_t dof = 3 * (size_t)i + a;
@@ -210,8 +232,8 @@ __device__ __forceinline__ void finish_row(const DevData& d, const StepCoeffs& s
       const double fe = sc.use_ext ? d.fext[dof] + d.fcoll[dof] : 0.0;
       double r = sc.rhs_fint_scale * (fe + fsum);
       r -= sc.rhs_mv_scale * mv;
-      r -= sc.rhs_kv_scale * kv[a];
-      r -= corr[a];
+      r -= sc.rhs_kv_scale * kva;
+      r -= corra;
       d.rhs[dof] = r;
       d.x[dof] = 0.0;
     }
@@ -259,24 +281,17 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
   // the row's force (fem.cpp:104-106) and its diagonal block (every incident tet contributes) are fixed
   // butterfly sums over the lanes; only the off-diagonal blocks (the ~5 tets around each edge) go through
   // the contribution lists below
-  double fsum = 0.0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const double t = warp_sum(f[a]);
-    if (lane == a) fsum = t;
-  }
+  // force (3) and diagonal block (9) in one reduce-scatter: value k in lanes 2k, 2k + 1
+  double red[16] = {f[0], f[1], f[2], dg[0], dg[1], dg[2], dg[3], dg[4], dg[5], dg[6], dg[7], dg[8], 0.0, 0.0, 0.0, 0.0};
+  const double rsum = warp_reduce_scatter<16>(red, lane);
+  const double fsum = __shfl_sync(0xffffffffu, rsum, 2 * (lane < 3 ? lane : 0));  // lanes 0..2: force component
 
   const bool fixed_i = __ldg(d.node_bc + i) >= 0;
   double kv[3] = {0.0, 0.0, 0.0}, corr[3] = {0.0, 0.0, 0.0};
   if (kBlocks) {
     const int jc = lane < deg ? __ldg(d.bcol + row0 + lane) : -1;
     const int cdiag = __ffs(__ballot_sync(0xffffffffu, jc == i)) - 1;
-    double dsum = 0.0;  // lane q < 9: entry q of the diagonal block
-#pragma unroll
-    for (int q = 0; q < 9; ++q) {
-      const double t = warp_sum(dg[q]);
-      if (lane == q) dsum = t;
-    }
+    const double dsum = __shfl_sync(0xffffffffu, rsum, 2 * (lane < 9 ? 3 + lane : 3));  // lane q < 9: entry q
     // the row's padded contribution lists (mx <= 16 items per column) staged in shared memory, so
     // the reduction below touches only shared memory with a uniform trip count
     const int ib0 = __ldg(d.contrib_ptr + i), nitems = __ldg(d.contrib_ptr + i + 1) - ib0;
@@ -304,14 +319,14 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
       finish_column<kMode>(d, sc, i, row0, c, jc, K, fixed_i, kv, corr);
     }
   }
-  if (kMode == kAssembleSystem) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      kv[a] = warp_sum(kv[a]);
-      corr[a] = warp_sum(corr[a]);
-    }
+  double kva = 0.0, corra = 0.0;
+  if (kMode == kAssembleSystem) {  // value k in lanes 4k .. 4k + 3
+    double kc[8] = {kv[0], kv[1], kv[2], corr[0], corr[1], corr[2], 0.0, 0.0};
+    const double ksum = warp_reduce_scatter<8>(kc, lane);
+    kva = __shfl_sync(0xffffffffu, ksum, 4 * (lane < 3 ? lane : 0));
+    corra = __shfl_sync(0xffffffffu, ksum, 4 * (lane < 3 ? 3 + lane : 3));
   }
-  finish_row<kMode>(d, sc, i, lane, fsum, fixed_i, kv, corr);
+  finish_row<kMode>(d, sc, i, lane, fsum, fixed_i, kva, corra);
 }
 
 
@@ -415,7 +430,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_assemble_big(DevData d, MatDev 
       corr[a] = warp_sum(corr[a]);
     }
   }
-  finish_row<kMode>(d, sc, i, lane, fsum, fixed_i, kv, corr);
+  finish_row<kMode>(d, sc, i, lane, fsum, fixed_i, kv[lane < 3 ? lane : 0], corr[lane < 3 ? lane : 0]);
 }
 
 // per-tet strain energy chi*V*Psi(F) (fem.cpp:190-199), block partial sums (deterministic order)

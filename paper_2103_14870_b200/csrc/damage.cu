@@ -132,7 +132,10 @@ __global__ void __launch_bounds__(kTpb, GF_NL_MINB) k_nonlocal(DevData d) {
 #ifndef GF_NL_TPB
 #define GF_NL_TPB 384  // two 32-cell ranges x six residues per CTA
 #endif
-constexpr int kNlTpb = GF_NL_TPB;  // template warps per CTA x 32
+constexpr int kNlTpb = GF_NL_TPB;
+#ifndef GF_NL_PRED
+#define GF_NL_PRED 1
+#endif  // template warps per CTA x 32
 __global__ void __launch_bounds__(kNlTpb, (GF_NL_MINB * 256) / kNlTpb) k_nonlocal_tpl(DevData d) {
   const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (wid >= d.nl_nwarps) return;
@@ -152,12 +155,23 @@ __global__ void __launch_bounds__(kNlTpb, (GF_NL_MINB * 256) / kNlTpb) k_nonloca
     const bool present = w != 0.0;
     const size_t pos = present ? (size_t)__ldg(d.nl_spos + j) + lane : 0;
     const double2 s01 = __ldg(s2 + pos), s23 = __ldg(s2 + plane + pos), s45 = __ldg(s2 + 2 * plane + pos);
+#if GF_NL_PRED
+    if (present) {  // predicated adds: half the instructions of per-component selects
+      avg[0] = avg[0] + w * s01.x;
+      avg[1] = avg[1] + w * s01.y;
+      avg[2] = avg[2] + w * s23.x;
+      avg[3] = avg[3] + w * s23.y;
+      avg[4] = avg[4] + w * s45.x;
+      avg[5] = avg[5] + w * s45.y;
+    }
+#else
     avg[0] = present ? avg[0] + w * s01.x : avg[0];
     avg[1] = present ? avg[1] + w * s01.y : avg[1];
     avg[2] = present ? avg[2] + w * s23.x : avg[2];
     avg[3] = present ? avg[3] + w * s23.y : avg[3];
     avg[4] = present ? avg[4] + w * s45.x : avg[4];
     avg[5] = present ? avg[5] + w * s45.y : avg[5];
+#endif
   }
   const int4 t = __ldg(d.tets + e);
   double x[4][3], du[9];

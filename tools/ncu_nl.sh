@@ -1,0 +1,10 @@
+#!/bin/bash
+# ncu --set full of the non-local screening kernel for library variants: tools/ncu_nl.sh VARIANT...
+cd "$(dirname "$0")/.."
+for v in "$@"; do
+  lib=paper_2103_14870_b200/_lib/variants/$v/libgrafem_b200.so
+  GF_LIB_PATH=$lib timeout 300 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/nl_$v.json 2>&1 && \
+  GF_LIB_PATH=$lib timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_nonlocal -s 1 -c 1 \
+    -o gpurun_out/nl_$v -f python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/ncu_nl_$v.log 2>&1
+  echo "$v rc=$?"
+done
