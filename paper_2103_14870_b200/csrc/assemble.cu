@@ -28,13 +28,10 @@ constexpr int kBlkStride = 32 * 27 + 9;  // per warp: 27 doubles per lane + the 
 // (returned in dg) and the three off-diagonal blocks K(li, lj), written straight to shared memory at slot
 // s = lj < li ? lj : lj - 1 (blk[9 s + r]) so they never occupy registers together
 template <bool kBlocks>
-__device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, int e, int li, double scale,
-                                            double f[3], double* blk, double dg[9]) {
-  const int4 t = __ldg(d.tets + e);
+__device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, int4 t, const double B[9], int li,
+                                            double scale, double f[3], double* blk, double dg[9]) {
   const int id[4] = {t.x, t.y, t.z, t.w};
-  double B[9], du[9], F[9];
-#pragma unroll
-  for (int q = 0; q < 9; ++q) B[q] = __ldg(d.binv + 9 * (size_t)e + q);
+  double du[9], F[9];
   {
     double u0[3];
 #pragma unroll
@@ -269,10 +266,12 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
     const int e = __ldg(d.nt_tet + p0 + lane);
     const int4 t = __ldg(d.tets + e);
     const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
-    const double scale = d.chi[e] * __ldg(d.vol + e);
+    double B[9], vol;
+    load_rest(d, e, B, vol);
+    const double scale = d.chi[e] * vol;
     double* blk = kBlocks ? &s_blk[w][27 * lane] : nullptr;
     if (scale != 0.0) {  // fem.cpp:51 / fem.cpp:114 early-out
-      element_row<kBlocks>(d, m, e, li, scale, f, blk, dg);
+      element_row<kBlocks>(d, m, t, B, li, scale, f, blk, dg);
     } else if (kBlocks) {
 #pragma unroll
       for (int r = 0; r < 27; ++r) blk[r] = 0.0;
@@ -366,9 +365,11 @@ __global__ void __launch_bounds__(32 * kWarps) k_assemble_big(DevData d, MatDev 
       const int e = __ldg(d.nt_tet + p0 + l);
       const int4 t = __ldg(d.tets + e);
       const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
-      const double scale = d.chi[e] * __ldg(d.vol + e);
+      double B[9], vol;
+      load_rest(d, e, B, vol);
+      const double scale = d.chi[e] * vol;
       if (scale != 0.0) {
-        element_row<kBlocks>(d, m, e, li, scale, f, blk, dg);
+        element_row<kBlocks>(d, m, t, B, li, scale, f, blk, dg);
         wrote = true;
       }
     }
@@ -438,13 +439,13 @@ __global__ void __launch_bounds__(256) k_energy(DevData d, MatDev m, double* par
   __shared__ double s[256];
   double acc = 0.0;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d.nt; e += gridDim.x * blockDim.x) {
-    const double scale = d.chi[e] * d.vol[e];
+    double B[9], vol;
+    load_rest(d, e, B, vol);
+    const double scale = d.chi[e] * vol;
     if (scale == 0.0) continue;
     const int4 t = d.tets[e];
     const int id[4] = {t.x, t.y, t.z, t.w};
-    double du[9], B[9], F[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) B[q] = d.binv[9 * (size_t)e + q];
+    double du[9], F[9];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll

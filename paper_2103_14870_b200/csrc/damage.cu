@@ -59,8 +59,8 @@ __global__ void __launch_bounds__(kTpb) k_tet_stress(DevData d, MatDev m, int lo
   const int4 t = __ldg(d.tets + e);
   double x[4][3], du[9], B[9], F[9], P[9], c6[6];
   load_tet_positions(d, t, x, du);
-#pragma unroll
-  for (int q = 0; q < 9; ++q) B[q] = __ldg(d.binv + 9 * (size_t)e + q);
+  double vol;
+  load_rest(d, e, B, vol);
   def_grad(du, B, F);
   const double J = pk1(F, m, P);
   cauchy6(F, P, J, c6);

@@ -55,8 +55,7 @@ struct DevData {
   // mesh (read-only)
   const double* X;          // 3nn
   const int4* tets;         // nt
-  const double* binv;       // 9nt row-major AoS
-  const double* vol;        // nt
+  const double2* bv;        // 5nt: per tet B^-1 row-major (9 doubles) then V -- one 80-byte record, 5 x 16-byte loads
   const int32_t* tet_edges; // 6nt AoS
   const double* rest_len;   // ne
   const int32_t* et_ptr;    // ne+1 (edge -> tets, ascending)
@@ -194,5 +193,15 @@ void launch_fill(double* p, double v, int64_t n, cudaStream_t s);
 void launch_qs_bc(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, cudaStream_t s);
 void launch_qs_update(double* u, const double* saved, const double* dx, double step, int64_t n, cudaStream_t s);
 void launch_dot(const double* a, const double* b, int64_t n, double* partials, int nblocks, cudaStream_t s);
+
+#ifdef __CUDACC__
+// the tet's rest record: B^-1 (row-major) and volume V
+__device__ __forceinline__ void load_rest(const DevData& d, int e, double B[9], double& vol) {
+  const double2* r = d.bv + 5 * (size_t)e;
+  const double2 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2), f = __ldg(r + 3), g = __ldg(r + 4);
+  B[0] = a.x; B[1] = a.y; B[2] = b.x; B[3] = b.y; B[4] = c.x; B[5] = c.y; B[6] = f.x; B[7] = f.y; B[8] = g.x;
+  vol = g.y;
+}
+#endif
 
 }  // namespace gfb

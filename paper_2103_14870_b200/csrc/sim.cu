@@ -262,8 +262,15 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   d_.nn = nn; d_.nt = nt; d_.ne = ne; d_.nb = nb;
   d_.X = (const double*)up(mesh_.X.data(), 8 * mesh_.X.size());
   d_.tets = (const int4*)up(mesh_.tets.data(), 4 * mesh_.tets.size());
-  d_.binv = (const double*)up(mesh_.binv.data(), 8 * mesh_.binv.size());
-  d_.vol = (const double*)up(mesh_.vol.data(), 8 * mesh_.vol.size());
+  {
+    std::vector<double> rec(10 * (size_t)mesh_.nt);
+    for (size_t e = 0; e < (size_t)mesh_.nt; ++e) {
+      for (int q = 0; q < 9; ++q) rec[10 * e + q] = mesh_.binv[9 * e + q];
+      rec[10 * e + 9] = mesh_.vol[e];
+    }
+    d_.bv = (const double2*)up(rec.data(), 8 * rec.size());
+    GF_CUDA(cudaStreamSynchronize(stream_));  // host staging goes out of scope
+  }
   d_.tet_edges = (const int32_t*)up(mesh_.tet_edges.data(), 4 * mesh_.tet_edges.size());
   d_.rest_len = (const double*)up(mesh_.rest_len.data(), 8 * mesh_.rest_len.size());
   d_.et_ptr = (const int32_t*)up(mesh_.et_ptr.data(), 4 * mesh_.et_ptr.size());
