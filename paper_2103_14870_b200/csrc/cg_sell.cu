@@ -48,6 +48,9 @@ __device__ __forceinline__ double lane_sum(double v) {  // fixed butterfly: same
 #ifndef GF_CG_REGS
 #define GF_CG_REGS 2  // 1: x, r, D^-1 of the owner rows in registers; 2: also p, q and z
 #endif
+#ifndef GF_CG_DEFER
+#define GF_CG_DEFER 1
+#endif
 #ifndef GF_CG_SMEM
 #define GF_CG_SMEM 1  // per-lane solver state in shared memory: frees registers for the SpMV loads in flight
 #endif
@@ -215,12 +218,29 @@ struct Phase {
   }
 };
 
+// fixed lane and warp trees over the CTA's per-thread values; every thread gets the same totals
+template <int NV>
+__device__ __forceinline__ void cta_tree(const double (&x)[NV], double (&out)[NV]) {
+  __shared__ double s_w[kWarpsPerCta][4];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const double t = lane_sum(x[q]);
+    if (lane == 0) s_w[w][q] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const double t = (lane < kWarpsPerCta) ? s_w[lane][q] : 0.0;
+    out[q] = lane_sum(t);  // every warp computes the same total
+  }
+  __syncthreads();
+}
+
 // sum of [CTA partials, dynamic-unit partials] in one fixed order (thread stride, fixed lane and warp trees)
 template <bool kDyn, int NV>
 __device__ __forceinline__ void sum_phase(double* const (&cta)[NV], double* const (&dyn)[NV], int G, int nd,
                                           double (&out)[NV]) {
-  __shared__ double s_w[kWarpsPerCta][4];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double x[NV];
   // all values' CTA partials are loaded back to back (one L2 round trip), then reduced
 #pragma unroll
@@ -243,18 +263,7 @@ __device__ __forceinline__ void sum_phase(double* const (&cta)[NV], double* cons
         for (int b = 0; b < kB; ++b) x[q] += v[b];
       }
   }
-#pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    const double t = lane_sum(x[q]);
-    if (lane == 0) s_w[w][q] = t;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    const double t = (lane < kWarpsPerCta) ? s_w[lane][q] : 0.0;
-    out[q] = lane_sum(t);  // every warp computes the same total
-  }
-  __syncthreads();
+  cta_tree<NV>(x, out);
 }
 
 constexpr int kMaxGrid = 1024;  // CTA partial slots per value
@@ -280,6 +289,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
   // (they are never gathered), so phase B reads only p and q and writes only z; x is stored once at the end.
   constexpr bool kRegs = !kDyn && GF_CG_REGS;
   constexpr bool kRegs2 = kRegs && GF_CG_REGS >= 2;  // p, q and the owner's z in registers too
+  constexpr bool kDefer = kRegs2 && GF_CG_DEFER;      // phase B's reduction overlapped with the next SpMV
 #if GF_CG_SMEM
   // per-lane solver state in shared memory ([warp][field][component][lane]: conflict-free), leaving the
   // registers to the SpMV's loads in flight
@@ -351,6 +361,112 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
     double* const p = a.p0;
     double beta = 0.0;
     bool done = false;
+    if constexpr (kDefer) {
+      // Same recurrences and decisions as the loop below, with phase B's reduction (r.r -> stop test, r.z ->
+      // beta) deferred into the next phase A: its partials are loaded before that phase's SpMV (which gathers
+      // only z and needs no scalar) and reduced after it, so the reduction's L2 round trip overlaps the SpMV.
+      // One slice per warp (kRegs): the warp's SpMV result waits in registers for beta.
+      const int u0 = __ldg(a.cta_first + blockIdx.x) + (int)(threadIdx.x >> 5);
+      const bool has = u0 < __ldg(a.cta_first + blockIdx.x + 1);
+      double* cBp[2] = {nullptr, nullptr};
+      for (int it = 0;; ++it) {
+        SELL_STAMP(it, 0);
+        double pb[2] = {0.0, 0.0};
+        if (it > 0 && (int)threadIdx.x < G) {
+          pb[0] = __ldcg(cBp[0] + threadIdx.x);
+          pb[1] = __ldcg(cBp[1] + threadIdx.x);
+        }
+        double acc[3] = {0.0, 0.0, 0.0};
+        if (has && it < a.max_iters) slice_spmv_sym_g(a, u0, GatherZ{a.z}, acc);
+        if (it > 0) {  // previous iteration's phase-B totals
+          double red2[2];
+          cta_tree<2>(pb, red2);
+          rr = red2[0];
+          iterations = it;
+          const double rnorm = sqrt(rr);
+          if (rnorm / bnorm <= a.tol) {  // sparse.cpp:172-178
+            relres = rnorm / bnorm;
+            converged = 1;
+            done = true;
+            break;
+          }
+          if (it < a.max_iters) {
+            beta = red2[1] / rz;
+            rz = red2[1];
+          }
+        }
+        if (it >= a.max_iters) break;
+        const bool fused = it > 0;
+        double *cA[1], *dA[1];
+        ptrs(cA, dA);
+        ph.run<false, 1>(cA, dA, [&](int sl, double (&v)[1]) {
+          const int row = sl * 32 + lane;
+          double pq = 0.0;
+          if (row < nrows) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const double pr = fused ? __fma_rn(beta, GF_SV(3, c), GF_SV(5, c)) : GF_SV(5, c);
+              const double qr = fused ? __fma_rn(beta, GF_SV(4, c), acc[c]) : acc[c];
+              GF_SV(3, c) = pr;
+              GF_SV(4, c) = qr;
+              pq = __fma_rn(pr, qr, pq);
+            }
+          }
+          v[0] = lane_sum(pq);
+        });
+        SELL_STAMP(it, 1);
+        SELL_BLOCK_STAMP(it, 3000);
+        SELL_BLOCK_STAMP_AT(it, 20, 4000);
+        double pap[1];
+        grid.sync();
+        SELL_STAMP(it, 5);
+        sum_phase<false, 1>(cA, dA, G, 0, pap);
+        parity ^= 1;
+        SELL_STAMP(it, 2);
+        if (pap[0] <= 0.0) {  // sparse.cpp:160-168
+          negcurv = pap[0] < 0.0;
+          iterations = it;
+          relres = sqrt(rr) / bnorm;
+          converged = relres <= a.tol;
+          done = true;
+          break;
+        }
+        const double alpha = rz / pap[0];
+        double *cB[2], *dB[2];
+        ptrs(cB, dB);
+        ph.run<false, 2>(cB, dB, [&](int sl, double (&v)[2]) {
+          double r2 = 0.0, rzp = 0.0;
+          const int row = sl * 32 + lane;
+          if (row < nrows) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const size_t dof = 3 * (size_t)row + c;
+              GF_SV(0, c) = __fma_rn(alpha, GF_SV(3, c), GF_SV(0, c));
+              GF_SV(1, c) = __fma_rn(-alpha, GF_SV(4, c), GF_SV(1, c));
+              const double zi = GF_SV(2, c) * GF_SV(1, c);
+              GF_SV(5, c) = zi;
+              a.z[dof] = zi;
+              r2 = __fma_rn(GF_SV(1, c), GF_SV(1, c), r2);
+              rzp = __fma_rn(GF_SV(1, c), zi, rzp);
+            }
+          }
+          v[0] = lane_sum(r2);
+          v[1] = lane_sum(rzp);
+        });
+        SELL_STAMP(it, 3);
+        SELL_BLOCK_STAMP(it, 2000);
+        grid.sync();
+        SELL_STAMP(it, 6);
+        SELL_STAMP(it, 4);
+        cBp[0] = cB[0];
+        cBp[1] = cB[1];
+        parity ^= 1;
+      }
+      if (!done) {
+        relres = sqrt(rr) / bnorm;
+        converged = relres <= a.tol;
+      }
+    } else
     for (int it = 0; it < a.max_iters; ++it) {
       const bool fused = it > 0;
       SELL_STAMP(it, 0);

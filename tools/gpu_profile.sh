@@ -11,8 +11,9 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $o/bench_ref
 timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > $o/plain.json 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $o/launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > $o/ncu_launches.log 2>&1; echo "launches rc=$?"
-timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $o/plain2.json 2>&1 && \
-timeout 1500 ncu --set full --clock-control none --import-source on -k 'regex:k_pcg_sell|k_nonlocal_tpl|k_assemble<' -s 9 -c 3 \
-  -o $o/top3 -f python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $o/ncu_top3.log 2>&1; echo "top3 rc=$?"
+for k in k_pcg_sell k_nonlocal_tpl k_assemble; do
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
+    -o $o/ncu_$k -f python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $o/ncu_$k.log 2>&1; echo "ncu $k rc=$?"
+done
 for c in c1 c2 c3; do timeout 1500 python tools/trajectory.py $c >> $o/trajectories.jsonl 2>> $o/trajectories.err; echo "traj $c rc=$?"; done
 timeout 900 python tools/trajectory.py c4 --steps 10 >> $o/trajectories.jsonl 2>> $o/trajectories.err; echo "traj c4 rc=$?"
