@@ -103,6 +103,7 @@ typedef struct {
 
 typedef struct gf_mesh gf_mesh;
 typedef struct gf_sim gf_sim;
+typedef struct gf_viz gf_viz;
 
 const char* gf_last_error(void);
 const char* gf_version(void);
@@ -200,6 +201,39 @@ int gf_sim_timer_elapsed(gf_sim* s, int32_t slot_a, int32_t slot_b, double* ms);
  * (< 200) at [8 it + point], per-CTA phase ends of iterations 10 and 20 at [2000 + cta], [3000 + cta], [4000 + cta]
  * (only when GF_CG_TRACE is set in the environment at gf_sim_create; tools/cg_trace.py, tools/cg_spread.py) */
 int gf_sim_cg_trace(gf_sim* s, uint64_t* out);
+/* ---------------------------------------------------------------- render-side consumer (host)
+ * grafem::VizMesh (viz.hpp:17-82): render-only companion mesh that splits at broken edges. Host code, no GPU.
+ * State arguments are the caller's read-back SimState pieces: displacements (3N, interleaved) and edge_damage
+ * (E labels, canonical edge order) as returned by gf_sim_get_state. */
+/* VizMesh::VizMesh (viz.cpp:20-66); keeps its own copy of the mesh */
+int gf_viz_create(const gf_mesh* mesh, gf_viz** out);
+void gf_viz_destroy(gf_viz* v);
+/* Simulation::viz (solver.hpp:83-84): the simulation's own companion, created on first call (splitting at the
+ * edges already broken) and from then on fed by every damage pass with newly broken edges (solver.cpp:94).
+ * Borrowed: owned and released by the simulation (gf_viz_destroy ignores it). */
+int gf_sim_viz(gf_sim* s, gf_viz** out);
+/* VizMesh::apply_splits (viz.cpp:183-195): the step's newly broken edges (e.g. the ascending list of
+ * gf_sim_damage_pass); GF_GEOMETRY_ERROR on an unknown edge id */
+int gf_viz_apply_splits(gf_viz* v, const int32_t* newly_broken, int64_t n, const uint8_t* edge_damage);
+/* VizMesh::children (viz.hpp:62): count, and child c's kind (0 edge, 1 face, 2 tet), entity, rep, rest
+ * position and parents_at_creation (<= 4) */
+int64_t gf_viz_child_count(const gf_viz* v);
+int gf_viz_child(const gf_viz* v, int64_t c, int32_t* kind, int32_t* entity, int32_t* rep, double rest_pos[3],
+                 int32_t parents[4], int32_t* n_parents);
+/* VizMesh::child_position (viz.cpp:197-203) */
+int gf_viz_child_position(const gf_viz* v, int64_t c, const double* displacements, const uint8_t* edge_damage,
+                          double out[3]);
+/* VizMesh::build_surface (viz.cpp:222-317): builds and keeps the surface; returns its sizes. Then
+ * gf_viz_surface copies it out: vertices (3 per vertex) and 0-based triangles (3 per triangle). */
+int gf_viz_build_surface(gf_viz* v, const double* displacements, const uint8_t* edge_damage, int64_t* n_vertices,
+                         int64_t* n_triangles, int64_t* n_original);
+int gf_viz_surface(const gf_viz* v, double* vertices, int32_t* triangles);
+/* VizMesh::export_frame (viz.cpp:319-331): Wavefront OBJ; GF_FORMAT_ERROR when the file cannot be written */
+int gf_viz_export_frame(const gf_viz* v, const char* path, const double* displacements, const uint8_t* edge_damage);
+/* VizMesh::fragment_volumes (viz.cpp:333-412) */
+int gf_viz_fragment_volumes(const gf_viz* v, int32_t tet, const double* displacements, const uint8_t* edge_damage,
+                            double out[4]);
+
 /* select the CUDA device for subsequently created simulations (one process per GPU) */
 int gf_set_device(int32_t device);
 int gf_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor, char* name, int32_t name_cap);

@@ -105,6 +105,8 @@ struct SimState {
   }
 };
 
+class VizMesh;
+
 // Simulation (solver.hpp:60-118)
 class Simulation {
  public:
@@ -166,6 +168,7 @@ class Simulation {
     return m;
   }
   const TetMesh& mesh() const { return mesh_; }
+  VizMesh& viz();  // solver.hpp:83 (defined after VizMesh)
 
  private:
   struct Del {
@@ -173,6 +176,84 @@ class Simulation {
   };
   TetMesh mesh_;
   std::unique_ptr<gf_sim, Del> s_;
+  std::unique_ptr<VizMesh> viz_;
 };
+
+// VizMesh (viz.hpp:17-82): render-only companion mesh, host code; consumes damage_pass() / the state
+class VizMesh {
+ public:
+  enum class EntityKind : int { edge = 0, face = 1, tet = 2 };
+  struct Child {
+    EntityKind kind;
+    int entity, rep;
+    Vec3 rest_pos;
+    std::vector<int> parents_at_creation;
+  };
+  struct Surface {
+    std::vector<Vec3> vertices;
+    std::vector<std::array<int, 3>> triangles;
+    int original_vertex_count = 0;
+  };
+  explicit VizMesh(const TetMesh& mesh) {
+    gf_viz* v = nullptr;
+    check(gf_viz_create(mesh.raw(), &v));
+    v_.reset(v);
+  }
+  explicit VizMesh(gf_viz* borrowed) : v_(borrowed) {}  // a simulation's own companion (gf_sim_viz)
+  void apply_splits(const std::vector<int>& newly_broken_edges, const SimState& state) {  // viz.cpp:183
+    check(gf_viz_apply_splits(v_.get(), newly_broken_edges.data(), (int64_t)newly_broken_edges.size(),
+                              state.edge_damage.data()));
+  }
+  std::vector<Child> children() const {  // viz.hpp:62 (copy)
+    std::vector<Child> out((size_t)gf_viz_child_count(v_.get()));
+    for (size_t c = 0; c < out.size(); ++c) {
+      int32_t k = 0, e = 0, r = 0, p[4], n = 0;
+      check(gf_viz_child(v_.get(), (int64_t)c, &k, &e, &r, out[c].rest_pos.data(), p, &n));
+      out[c].kind = (EntityKind)k;
+      out[c].entity = e;
+      out[c].rep = r;
+      out[c].parents_at_creation.assign(p, p + n);
+    }
+    return out;
+  }
+  Vec3 child_position(int child, const SimState& state) const {  // viz.cpp:197
+    Vec3 p;
+    check(gf_viz_child_position(v_.get(), child, state.displacements[0].data(), state.edge_damage.data(), p.data()));
+    return p;
+  }
+  Surface build_surface(const SimState& state) const {  // viz.cpp:222
+    int64_t nv = 0, nt = 0, no = 0;
+    check(gf_viz_build_surface(v_.get(), state.displacements[0].data(), state.edge_damage.data(), &nv, &nt, &no));
+    Surface s;
+    s.vertices.resize(nv);
+    s.triangles.resize(nt);
+    check(gf_viz_surface(v_.get(), nv ? s.vertices[0].data() : nullptr, nt ? s.triangles[0].data() : nullptr));
+    s.original_vertex_count = (int)no;
+    return s;
+  }
+  void export_frame(const std::string& path, const SimState& state) const {  // viz.cpp:319
+    check(gf_viz_export_frame(v_.get(), path.c_str(), state.displacements[0].data(), state.edge_damage.data()));
+  }
+  std::array<double, 4> fragment_volumes(int tet, const SimState& state) const {  // viz.cpp:333
+    std::array<double, 4> v;
+    check(gf_viz_fragment_volumes(v_.get(), tet, state.displacements[0].data(), state.edge_damage.data(), v.data()));
+    return v;
+  }
+
+ private:
+  struct Del {
+    void operator()(gf_viz* v) const { gf_viz_destroy(v); }
+  };
+  std::unique_ptr<gf_viz, Del> v_;
+};
+
+inline VizMesh& Simulation::viz() {
+  if (!viz_) {
+    gf_viz* v = nullptr;
+    check(gf_sim_viz(s_.get(), &v));
+    viz_.reset(new VizMesh(v));
+  }
+  return *viz_;
+}
 
 }  // namespace grafem_b200

@@ -128,6 +128,12 @@ def lib():
         L.gf_host_alloc.restype = C.c_void_p
         L.gf_host_alloc.argtypes = [C.c_size_t]
         L.gf_host_free.argtypes = [C.c_void_p]
+        L.gf_viz_child_count.restype = C.c_int64
+        L.gf_viz_child_count.argtypes = [C.c_void_p]
+        for f in ("gf_viz_child", "gf_viz_child_position"):
+            getattr(L, f).argtypes = [C.c_void_p, C.c_int64] + [C.c_void_p] * (6 if f == "gf_viz_child" else 3)
+        L.gf_viz_apply_splits.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+        L.gf_viz_fragment_volumes.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -418,6 +424,13 @@ class Simulation:
     def newton_tolerance(self) -> float:
         return lib().gf_sim_newton_tolerance(self._h)
 
+    def viz(self) -> "VizMesh":
+        """Simulation::viz (solver.hpp:83-84): the render companion; created on first call, then fed by every
+        damage pass (solver.cpp:94)."""
+        h = C.c_void_p()
+        _check(lib().gf_sim_viz(self._h, C.byref(h)))
+        return VizMesh(None, _borrowed=h, _owner=self)
+
     def nonlocal_layout(self) -> int:
         """0: local screening (r_d = 0), 1: general sliced-ELL table, 2: structured template layout."""
         return lib().gf_sim_nonlocal_layout(self._h)
@@ -557,6 +570,81 @@ class Simulation:
         ms = C.c_double()
         _check(lib().gf_sim_timer_elapsed(self._h, C.c_int32(a), C.c_int32(b), C.byref(ms)))
         return ms.value
+
+
+class VizMesh:
+    """VizMesh (viz.hpp:17-82): render-only companion mesh that splits at broken edges (host code, SURVEY
+    §8(f)-4). It consumes the ascending newly-broken lists of Simulation.damage_pass / dynamic_step and the
+    state read back from the GPU; neither the mesh nor the simulation state is touched."""
+    EDGE, FACE, TET = 0, 1, 2
+
+    def __init__(self, mesh: TetMesh, _borrowed=None, _owner=None):
+        if _borrowed is not None:  # Simulation.viz(): the simulation's own companion
+            self._h, self._owner, self._own = _borrowed, _owner, False
+            return
+        h = C.c_void_p()
+        _check(lib().gf_viz_create(mesh._h, C.byref(h)))
+        self._h, self._mesh, self._own = h, mesh, True
+
+    def __del__(self):
+        if getattr(self, "_own", False) and getattr(self, "_h", None) and _lib is not None:
+            _lib.gf_viz_destroy(self._h)
+            self._h = None
+
+    @staticmethod
+    def _state(state):
+        u = np.ascontiguousarray(state.displacements, dtype=np.float64)
+        z = np.ascontiguousarray(state.edge_damage, dtype=np.uint8)
+        return u, z
+
+    def apply_splits(self, newly_broken_edges, state):
+        """VizMesh::apply_splits (viz.cpp:183-195)."""
+        ids = np.ascontiguousarray(newly_broken_edges, dtype=np.int32)
+        _, z = self._state(state)
+        _check(lib().gf_viz_apply_splits(self._h, ids.ctypes.data, C.c_int64(len(ids)), z.ctypes.data))
+
+    def children(self):
+        """VizMesh::children (viz.hpp:62): list of dicts kind / entity / rep / rest_pos / parents_at_creation."""
+        out = []
+        for c in range(lib().gf_viz_child_count(self._h)):
+            k, e, r, n = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+            rest = np.zeros(3)
+            par = np.zeros(4, np.int32)
+            _check(lib().gf_viz_child(self._h, C.c_int64(c), C.byref(k), C.byref(e), C.byref(r), rest.ctypes.data,
+                                      par.ctypes.data, C.byref(n)))
+            out.append(dict(kind=k.value, entity=e.value, rep=r.value, rest_pos=rest,
+                            parents_at_creation=par[:n.value].tolist()))
+        return out
+
+    def child_position(self, child: int, state) -> np.ndarray:
+        """VizMesh::child_position (viz.cpp:197-203)."""
+        u, z = self._state(state)
+        out = np.zeros(3)
+        _check(lib().gf_viz_child_position(self._h, C.c_int64(child), u.ctypes.data, z.ctypes.data, out.ctypes.data))
+        return out
+
+    def build_surface(self, state):
+        """VizMesh::build_surface (viz.cpp:222-317) -> (vertices (V, 3), triangles (F, 3) 0-based,
+        original_vertex_count)."""
+        u, z = self._state(state)
+        nv, nt, no = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().gf_viz_build_surface(self._h, _p(u, F64P), _p(z, U8P), C.byref(nv), C.byref(nt), C.byref(no)))
+        v = np.zeros((nv.value, 3))
+        t = np.zeros((nt.value, 3), np.int32)
+        _check(lib().gf_viz_surface(self._h, _p(v, F64P), _p(t, I32P)))
+        return v, t, no.value
+
+    def export_frame(self, path: str, state):
+        """VizMesh::export_frame (viz.cpp:319-331): Wavefront OBJ."""
+        u, z = self._state(state)
+        _check(lib().gf_viz_export_frame(self._h, os.fsencode(path), _p(u, F64P), _p(z, U8P)))
+
+    def fragment_volumes(self, tet: int, state) -> np.ndarray:
+        """VizMesh::fragment_volumes (viz.cpp:333-412)."""
+        u, z = self._state(state)
+        out = np.zeros(4)
+        _check(lib().gf_viz_fragment_volumes(self._h, C.c_int32(tet), u.ctypes.data, z.ctypes.data, out.ctypes.data))
+        return out
 
 
 def cg_solve_csr(row_ptr, cols, vals, b, x0, tol, max_iters):

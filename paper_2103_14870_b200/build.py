@@ -28,7 +28,7 @@ CU_SOURCES = {  # file -> extra flags
     "cg_sell.cu": [],
     "sim.cu": [],
 }
-CPP_SOURCES = ["host_mesh.cpp", "capi.cpp"]
+CPP_SOURCES = ["host_mesh.cpp", "host_viz.cpp", "capi.cpp"]
 
 
 def _nvcc():

@@ -8,6 +8,7 @@
 
 #include "../../include/grafem_b200.h"
 #include "host_mesh.hpp"
+#include "host_viz.hpp"
 #include "sim.hpp"
 
 using namespace gfb;
@@ -15,8 +16,14 @@ using namespace gfb;
 struct gf_mesh {
   HostMesh m;
 };
+struct gf_viz {
+  std::unique_ptr<RenderMesh> own;  // null for the simulation's own companion (borrowed: gf_sim_viz)
+  RenderMesh* r;
+  RenderMesh::Surface surf;
+};
 struct gf_sim {
   std::unique_ptr<Simulation> s;
+  std::unique_ptr<gf_viz> viz;
 };
 
 namespace {
@@ -287,6 +294,75 @@ int gf_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor, char
       std::strncpy(name, prop.name, name_cap - 1);
       name[name_cap - 1] = 0;
     }
+  });
+}
+
+// ---------------------------------------------------------------- render-side consumer (host_viz.hpp)
+int gf_viz_create(const gf_mesh* mesh, gf_viz** out) {
+  return guard([&] {
+    auto own = std::make_unique<RenderMesh>(mesh->m);
+    RenderMesh* r = own.get();
+    *out = new gf_viz{std::move(own), r, {}};
+  });
+}
+void gf_viz_destroy(gf_viz* v) {
+  if (v && v->own) delete v;  // the simulation's own companion is released with the simulation
+}
+int gf_sim_viz(gf_sim* s, gf_viz** out) {
+  return guard([&] {
+    if (!s->viz) s->viz.reset(new gf_viz{nullptr, &s->s->viz(), {}});
+    *out = s->viz.get();
+  });
+}
+int gf_viz_apply_splits(gf_viz* v, const int32_t* newly_broken, int64_t n, const uint8_t* edge_damage) {
+  return guard([&] { v->r->apply_splits(newly_broken, n, edge_damage); });
+}
+int64_t gf_viz_child_count(const gf_viz* v) { return (int64_t)v->r->children().size(); }
+int gf_viz_child(const gf_viz* v, int64_t c, int32_t* kind, int32_t* entity, int32_t* rep, double rest_pos[3],
+                 int32_t parents[4], int32_t* n_parents) {
+  return guard([&] {
+    if (c < 0 || c >= (int64_t)v->r->children().size()) throw FormatError("child index out of range");
+    const RenderMesh::Child& ch = v->r->children()[c];
+    if (kind) *kind = ch.kind;
+    if (entity) *entity = ch.entity;
+    if (rep) *rep = ch.rep;
+    if (rest_pos)
+      for (int a = 0; a < 3; ++a) rest_pos[a] = ch.rest[a];
+    if (parents)
+      for (size_t k = 0; k < ch.parents.size(); ++k) parents[k] = ch.parents[k];
+    if (n_parents) *n_parents = (int32_t)ch.parents.size();
+  });
+}
+int gf_viz_child_position(const gf_viz* v, int64_t c, const double* displacements, const uint8_t* edge_damage,
+                          double out[3]) {
+  return guard([&] {
+    const auto p = v->r->child_position(c, displacements, edge_damage);
+    for (int a = 0; a < 3; ++a) out[a] = p[a];
+  });
+}
+int gf_viz_build_surface(gf_viz* v, const double* displacements, const uint8_t* edge_damage, int64_t* n_vertices,
+                         int64_t* n_triangles, int64_t* n_original) {
+  return guard([&] {
+    v->surf = v->r->build_surface(displacements, edge_damage);
+    if (n_vertices) *n_vertices = (int64_t)v->surf.xyz.size() / 3;
+    if (n_triangles) *n_triangles = (int64_t)v->surf.tris.size();
+    if (n_original) *n_original = v->surf.n_original;
+  });
+}
+int gf_viz_surface(const gf_viz* v, double* vertices, int32_t* triangles) {
+  return guard([&] {
+    if (vertices) std::memcpy(vertices, v->surf.xyz.data(), 8 * v->surf.xyz.size());
+    if (triangles) std::memcpy(triangles, v->surf.tris.data(), 12 * v->surf.tris.size());
+  });
+}
+int gf_viz_export_frame(const gf_viz* v, const char* path, const double* displacements, const uint8_t* edge_damage) {
+  return guard([&] { v->r->export_frame(path, displacements, edge_damage); });
+}
+int gf_viz_fragment_volumes(const gf_viz* v, int32_t tet, const double* displacements, const uint8_t* edge_damage,
+                            double out[4]) {
+  return guard([&] {
+    const auto vol = v->r->fragment_volumes(tet, displacements, edge_damage);
+    for (int k = 0; k < 4; ++k) out[k] = vol[k];
   });
 }
 

@@ -659,7 +659,30 @@ std::vector<int32_t> Simulation::damage_pass() {
   std::vector<int32_t> ids(n);
   if (n) GF_CUDA(cudaMemcpy(ids.data(), d_.newly, 4 * (size_t)n, cudaMemcpyDeviceToHost));
   std::sort(ids.begin(), ids.end());  // update_damage returns ascending ids (fracture.hpp:48-50)
+  if (viz_ && !ids.empty()) feed_viz(ids);
   return ids;
+}
+
+void Simulation::feed_viz(std::vector<int32_t> ids) {
+  std::vector<uint8_t> zeta(mesh_.ne);
+  GF_CUDA(cudaMemcpyAsync(zeta.data(), d_.zeta, zeta.size(), cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  std::sort(ids.begin(), ids.end());
+  viz_->apply_splits(ids.data(), (int64_t)ids.size(), zeta.data());
+}
+
+RenderMesh& Simulation::viz() {
+  if (!viz_) {
+    viz_ = std::make_unique<RenderMesh>(mesh_);
+    std::vector<uint8_t> zeta(mesh_.ne);
+    GF_CUDA(cudaMemcpyAsync(zeta.data(), d_.zeta, zeta.size(), cudaMemcpyDeviceToHost, stream_));
+    synchronize();
+    std::vector<int32_t> broken;  // edges broken before the companion existed, ascending
+    for (int32_t e = 0; e < mesh_.ne; ++e)
+      if (zeta[e]) broken.push_back(e);
+    viz_->apply_splits(broken.data(), (int64_t)broken.size(), zeta.data());
+  }
+  return *viz_;
 }
 
 // ---------------------------------------------------------------- dynamic step (solver.cpp:219-333)
@@ -787,6 +810,11 @@ gf_step_stats Simulation::dynamic_step() {
   int32_t newly = 0;
   std::memcpy(&newly, h_stats_ + 5, 4);
   st.newly_broken = newly;
+  if (viz_ && newly > 0) {  // the render companion follows this step's damage pass (solver.cpp:94)
+    std::vector<int32_t> ids(newly);
+    GF_CUDA(cudaMemcpyAsync(ids.data(), d_.newly, 4 * (size_t)newly, cudaMemcpyDeviceToHost, stream_));
+    feed_viz(std::move(ids));
+  }
   last_load_ = cols_.empty() ? 0.0 : h_stats_[4];
   st.load = last_load_;
   st.cg_iterations = (int32_t)h_stats_[0];

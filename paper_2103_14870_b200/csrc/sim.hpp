@@ -3,12 +3,14 @@
 #pragma once
 
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "../../include/grafem_b200.h"
 #include "dev_types.cuh"
 #include "host_mesh.hpp"
+#include "host_viz.hpp"
 
 namespace gfb {
 
@@ -46,6 +48,9 @@ class Simulation {
   double newton_tolerance() const { return newton_tol_; }
   int32_t nonlocal_layout() const { return mat_.r_d <= 0.0 ? 0 : d_.nl_tpl ? 2 : 1; }
   std::vector<int32_t> damage_pass();
+  // Simulation::viz (solver.hpp:83-84): the render companion, created on first use (catching up on the edges
+  // already broken); from then on every damage pass with newly broken edges feeds it (solver.cpp:94)
+  RenderMesh& viz();
   void get_state(double* u, double* v, uint8_t* zeta, double* chi, double* time);
   void set_state(const double* u, const double* v, const uint8_t* zeta, const double* chi, const double* time);
   void set_external_forces(const double* f3n);
@@ -131,6 +136,8 @@ class Simulation {
   BcStep* h_bcstep_ = nullptr;
   ColliderDev* h_cols_ = nullptr;
   double* h_stats_ = nullptr;  // [cg_out(4), load, newly_count]
+  std::unique_ptr<RenderMesh> viz_;
+  void feed_viz(std::vector<int32_t> ids);  // newly broken ids (any order) of the damage pass just run
   // profiling
   bool profiling_ = false;
   struct Pending { std::string name; cudaEvent_t a, b; double bytes; };

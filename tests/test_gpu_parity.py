@@ -3,6 +3,8 @@
 Bars (north_star): damage labels / newly-broken sets / chi / Cauchy stresses / screening values bit-exact
 from an identical state; forces and matrix entries within 1e-9 relative (fp64); trajectories within 1e-6
 relative in node positions."""
+from types import SimpleNamespace
+
 import numpy as np
 import pytest
 
@@ -719,3 +721,49 @@ def test_high_valence_rows_match_oracle(model):
     a_got, r_got = gs.last_system()
     assert rel_err(a_got, a_ref) < FORCE_TOL and rel_err(r_got, r_ref) < FORCE_TOL
     assert np.abs(gs.state().displacements - os_.get_state()["u"]).max() / 0.1 < TRAJ_TOL
+
+
+# ---------------------------------------------------------------- render-side consumer
+def test_render_companion_follows_the_gpu_damage_passes(tmp_path):
+    """Simulation.viz() fed by the GPU damage passes (solver.cpp:94) matches a VizMesh fed the oracle's
+    newly-broken lists: same children (kind, entity, representative, parents, rest position), same surface
+    triangles, vertices within the position tolerance; the OBJ export parses back to that surface."""
+    s = cf.scaled("c3", (8, 8, 7))
+    s.sigma_thres = 500.0
+    gs, gm = cf.build_gpu(s)
+    os_, _ = build_oracle(s)
+    rng = np.random.default_rng(0)
+    u = rng.uniform(-0.05 * cf.H, 0.05 * cf.H, os_.get_state()["u"].shape)
+    os_.set_state(u=u)
+    gs.set_state(displacements=u)
+    viz_g, viz_o = gs.viz(), g.VizMesh(gm)
+    total = 0
+    for _ in range(3):
+        z0 = os_.get_state()["zeta"].copy()
+        os_.dynamic_step()
+        stats = gs.dynamic_step()
+        ost = os_.get_state()
+        newly = np.flatnonzero((ost["zeta"] != 0) & (z0 == 0)).astype(np.int32)  # update_damage's ascending list
+        assert stats.newly_broken == len(newly)
+        total += len(newly)
+        viz_o.apply_splits(newly, SimpleNamespace(displacements=ost["u"], edge_damage=ost["zeta"]))
+    assert total > 0
+    gst = gs.state()
+    assert np.array_equal(gst.edge_damage, ost["zeta"])
+    cg, co = viz_g.children(), viz_o.children()
+    assert len(cg) == len(co) > 0
+    for a, b in zip(cg, co):
+        assert (a["kind"], a["entity"], a["rep"], a["parents_at_creation"]) == \
+               (b["kind"], b["entity"], b["rep"], b["parents_at_creation"])
+        assert np.array_equal(a["rest_pos"], b["rest_pos"])
+    vg, tg, ng = viz_g.build_surface(gst)
+    vo, to, no = viz_o.build_surface(SimpleNamespace(displacements=ost["u"], edge_damage=ost["zeta"]))
+    assert ng == no and np.array_equal(tg, to)
+    scale = np.abs(vo).max()
+    assert np.abs(vg - vo).max() / scale < 1e-6
+    path = tmp_path / "frame.obj"
+    viz_g.export_frame(str(path), gst)
+    lines = path.read_text().splitlines()
+    v = np.array([[float(x) for x in l.split()[1:]] for l in lines if l.startswith("v ")])
+    f = np.array([[int(x) for x in l.split()[1:]] for l in lines if l.startswith("f ")]) - 1
+    assert np.array_equal(v, vg) and np.array_equal(f, tg)
