@@ -189,6 +189,8 @@ int gf_cg_solve_csr(int32_t n, const int32_t* row_ptr, const int32_t* cols, cons
 /* ---------------------------------------------------------------- runtime utilities */
 void* gf_host_alloc(size_t bytes); /* pinned host memory for zero-stall state transfers */
 void gf_host_free(void* p);
+/* per-kernel timing: 0 off, 1 CUDA events around every kernel, 2 events around the PCG solve only (launch counts
+ * and algorithmic bytes for every kernel) */
 int gf_sim_set_profiling(gf_sim* s, int32_t enable);
 int gf_sim_kernel_times(gf_sim* s, gf_kernel_time* out, int32_t cap, int32_t* n);
 int gf_sim_reset_kernel_times(gf_sim* s);

@@ -547,8 +547,9 @@ class Simulation:
         return y
 
     # runtime utilities
-    def set_profiling(self, on: bool):
-        _check(lib().gf_sim_set_profiling(self._h, C.c_int32(int(on))))
+    def set_profiling(self, level):
+        """0 / False off, 1 / True events around every kernel, 2 events around the PCG solve only."""
+        _check(lib().gf_sim_set_profiling(self._h, C.c_int32(int(level))))
 
     def kernel_times(self):
         arr = (KernelTime * 64)()

@@ -246,7 +246,7 @@ void gf_host_free(void* p) {
   if (p) cudaFreeHost(p);
 }
 int gf_sim_set_profiling(gf_sim* s, int32_t enable) {
-  return guard([&] { s->s->set_profiling(enable != 0); });
+  return guard([&] { s->s->set_profiling(enable < 0 || enable > 2 ? 1 : enable); });
 }
 int gf_sim_kernel_times(gf_sim* s, gf_kernel_time* out, int32_t cap, int32_t* n) {
   return guard([&] {
