@@ -55,6 +55,7 @@ __device__ __forceinline__ void scatter_max(const DevData& d, const int te[6], c
 
 __global__ void __launch_bounds__(kTpb) k_tet_stress(DevData d, MatDev m, int local_screen) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e == 0) *d.newly_count = 0;  // this pass's relabel compacts from zero (stream order: tet_stress first)
   if (e >= d.nt) return;
   const int4 t = __ldg(d.tets + e);
   double x[4][3], du[9], B[9], F[9], P[9], c6[6];

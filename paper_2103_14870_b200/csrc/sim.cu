@@ -444,7 +444,9 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   d_.scr_key = (unsigned long long*)dalloc(8 * (size_t)ne);
   d_.screening = (double*)zeros(8 * (size_t)ne);
   d_.newly = (int32_t*)zeros(4 * (size_t)ne);
-  d_.newly_count = (int32_t*)zeros(8);
+  // one 64-byte stats record read back once per step: [cg_out (4 doubles), collider load, newly-broken count]
+  d_stats_ = (double*)zeros(64);
+  d_.newly_count = reinterpret_cast<int32_t*>(d_stats_ + 5);
   bval_doubles_ = 288 * ((size_t)usp_[d_.nslices] + 1);  // + one all-zero padding group
   // GF_PAD_MB: allocation-placement experiment (tools/ab_pad.sh); the PCG time depends on where the system
   // matrix lands in physical memory by up to ~8%
@@ -463,7 +465,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   d_.z = (double*)zeros(8 * nd);
   d_.p0 = (double*)zeros(8 * nd);
   d_.Ap = (double*)zeros(8 * nd);
-  d_.cg_out = (double*)zeros(8 * 8);
+  d_.cg_out = d_stats_;
   d_.n_colliders = (int32_t)cols_.size();
   const int nsub = cfg.collision_substeps;
   if (!cols_.empty()) {
@@ -472,7 +474,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     d_.coll_partials = (double*)zeros(8 * (size_t)nsub * cols_.size() * 3 * collide_blocks(d_));
     GF_CUDA(cudaMallocHost(&h_cols_, sizeof(ColliderDev) * cols_.size() * nsub));
   }
-  d_load_ = (double*)zeros(8);
+  d_load_ = d_stats_ + 4;
   d_energy_partials_ = (double*)zeros(8 * 1024);
   if (!bcs_.empty()) {
     d_bcstep_ = (BcStep*)dalloc(sizeof(BcStep) * bcs_.size());
@@ -655,7 +657,6 @@ void Simulation::run_damage(bool relabel, bool keep_values, bool chi) {
   const bool local = mat_.r_d <= 0.0;
   launch("tet_stress", 16 * n + 112 * T + 8 * E, [&] { launch_tet_stress(d_, md_, local, stream_); });
   if (!local) launch("nonlocal", 12.0 * nl_entries_, [&] { launch_nonlocal(d_, stream_); });
-  GF_CUDA(cudaMemsetAsync(d_.newly_count, 0, 4, stream_));
   launch("relabel", 2 * E, [&] { launch_relabel(d_, mat_.sigma_thres, relabel, keep_values, stream_); });
   if (chi) launch("chi", 16 * T, [&] { launch_chi(d_, md_, stream_); });
 }
@@ -807,9 +808,7 @@ gf_step_stats Simulation::dynamic_step() {
   cg_.max_iters = cfg_.cg_max_iters;
   launch("pcg", 0.0, [&] { launch_cg(); });
   launch("integrate", 40 * n, [&] { launch_integrate(d_, dt, stream_); });  // B_int = 40n; no-op if not converged
-  GF_CUDA(cudaMemcpyAsync(h_stats_, d_.cg_out, 32, cudaMemcpyDeviceToHost, stream_));
-  GF_CUDA(cudaMemcpyAsync(h_stats_ + 4, d_load_, 8, cudaMemcpyDeviceToHost, stream_));
-  GF_CUDA(cudaMemcpyAsync(h_stats_ + 5, d_.newly_count, 4, cudaMemcpyDeviceToHost, stream_));
+  GF_CUDA(cudaMemcpyAsync(h_stats_, d_stats_, 48, cudaMemcpyDeviceToHost, stream_));  // cg_out, load, newly
   synchronize();
   // SURVEY.md §8(d) B_CG = 12Z + 4(n+1) + 56n per PCG iteration (the reference's scalar-CSR SpMV + vectors)
   const double cg_bytes_per_iter = 12 * Z + 4 * (n + 1) + 56 * n;

@@ -138,6 +138,7 @@ class Simulation {
   BcStep* h_bcstep_ = nullptr;
   ColliderDev* h_cols_ = nullptr;
   double* h_stats_ = nullptr;  // [cg_out(4), load, newly_count]
+  double* d_stats_ = nullptr;  // the same record on the device
   std::unique_ptr<RenderMesh> viz_;
   void feed_viz(std::vector<int32_t> ids);  // newly broken ids (any order) of the damage pass just run
   // profiling
