@@ -120,12 +120,12 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel):
-    """dram bytes per launch of `kernel` from the committed ncu --set full summary, if present."""
+def ncu_traffic(workload, kernel):
+    """dram bytes per launch of `kernel` on `workload` from the committed ncu --set full summary, if present."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        return json.load(open(p)).get(kernel)
-    except (OSError, ValueError):
+        return (json.load(open(p)).get(workload) or {}).get(kernel)
+    except (OSError, ValueError, AttributeError):
         return None
 
 
@@ -242,7 +242,7 @@ def main():
     bytes_per_launch = d["bytes"] / max(1, d["launches"])
     achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
     peak, peak_src = measured_peak_hbm()
-    traffic = ncu_traffic(dname)
+    traffic = ncu_traffic(s.name, dname)
     roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
