@@ -310,8 +310,13 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
     ptrs(c3, d3);
     ph.run<kDyn, 3>(c3, d3, [&](int sl, double (&v)[3]) {
       double acc[3];
-      slice_spmv_sym_g(a, sl, GatherX{a.x}, acc);
       const int row = sl * 32 + lane;
+      if (a.x0_identity) {  // A x0 = x0 (see CgLaunch::x0_identity): no SpMV
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] = row < nrows ? a.x[3 * (size_t)row + c] : 0.0;
+      } else {
+        slice_spmv_sym_g(a, sl, GatherX{a.x}, acc);
+      }
       double bb = 0.0, rz = 0.0, rr = 0.0;
       if (row < nrows) {
 #pragma unroll

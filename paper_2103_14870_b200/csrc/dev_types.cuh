@@ -171,6 +171,10 @@ struct CgLaunch {
   int32_t zero_base;      // cg_sell.cu: value offset of the all-zero padding block
   const int32_t* cta_first;  // cg_sell.cu: slice range of each CTA (grid + 1 entries)
   unsigned long long* trace;  // optional per-phase %globaltimer stamps (GF_CG_TRACE)
+  // cg_sell.cu: 1 when the initial guess is the assembly's projected one (prescribed values on Dirichlet rows,
+  // zero elsewhere): those rows are identity rows and their columns are zero, so A x0 = x0 exactly (up to the
+  // sign of zero) and the setup's SpMV is skipped. The solve_linear retries start from a solve's result: 0.
+  int32_t x0_identity;
 };
 int cg_csr_grid();
 void launch_pcg_csr(const CgLaunch& a, cudaStream_t s);  // scalar CSR (gf_cg_solve_csr)

@@ -806,7 +806,9 @@ gf_step_stats Simulation::dynamic_step() {
 
   // solve_linear (solver.cpp:105-136): first attempt, 4x retry, then cumulative diagonal shifts
   cg_.max_iters = cfg_.cg_max_iters;
+  cg_.x0_identity = 1;  // x0 from the assembly's epilogue (fixed rows: prescribed values, identity rows)
   launch("pcg", 0.0, [&] { launch_cg(); });
+  cg_.x0_identity = 0;
   launch("integrate", 40 * n, [&] { launch_integrate(d_, dt, stream_); });  // B_int = 40n; no-op if not converged
   GF_CUDA(cudaMemcpyAsync(h_stats_, d_stats_, 48, cudaMemcpyDeviceToHost, stream_));  // cg_out, load, newly
   synchronize();
