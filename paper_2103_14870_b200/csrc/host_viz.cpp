@@ -116,15 +116,21 @@ int RenderMesh::group(Kind k, int32_t entity, int32_t node, const uint8_t* zeta,
   // the entity's edges as (local a, local b, edge id), in the reference's order (viz.cpp:79-107)
   int32_t le[6][3];
   int ne = 0;
+  auto add = [&](int a, int b, int32_t id) {
+    le[ne][0] = a;
+    le[ne][1] = b;
+    le[ne][2] = id;
+    ++ne;
+  };
   if (k == kEdge) {
-    le[ne++][0] = 0, le[0][1] = 1, le[0][2] = entity;
+    add(0, 1, entity);
   } else if (k == kFace) {
     const auto& fe = face_edges_[entity];
-    const int pairs[3][2] = {{0, 1}, {0, 2}, {1, 2}};
-    for (int q = 0; q < 3; ++q) le[ne][0] = pairs[q][0], le[ne][1] = pairs[q][1], le[ne++][2] = fe[q];
+    add(0, 1, fe[0]);
+    add(0, 2, fe[1]);
+    add(1, 2, fe[2]);
   } else {
-    for (int q = 0; q < 6; ++q)
-      le[ne][0] = kLocalEdge[q][0], le[ne][1] = kLocalEdge[q][1], le[ne++][2] = m_.tet_edges[6 * (size_t)entity + q];
+    for (int q = 0; q < 6; ++q) add(kLocalEdge[q][0], kLocalEdge[q][1], m_.tet_edges[6 * (size_t)entity + q]);
   }
   int label[4] = {0, 1, 2, 3};
   auto root = [&label](int i) {
