@@ -130,7 +130,7 @@ def ncu_traffic(workload, kernel):
 
 
 # ---------------------------------------------------------------- CPU baseline (oracle)
-def run_cpu(s, steps, budget_s):
+def run_cpu(s, steps, budget_s, single_thread=False):
     """Times the CPU oracle (reference's algorithm + OpenMP layout) on a bounded sample of the workload."""
     from oracle import oracle as o
     from oracle.scenario import build_oracle
@@ -143,9 +143,19 @@ def run_cpu(s, steps, budget_s):
         if time.perf_counter() - t0 > budget_s:
             break
     el = time.perf_counter() - t0
-    return dict(value=s.num_tets * done / el, unit=UNIT, cores=o.num_threads(), kind="port",
-                sample=f"{done} dynamic_step(s) of {s.name} after 1 untimed step ({el:.1f} s, "
-                       f"OMP threads={o.num_threads()}); oracle/grafem_oracle.cpp -O3 -fopenmp")
+    out = dict(value=s.num_tets * done / el, unit=UNIT, cores=o.num_threads(), kind="port",
+               sample=f"{done} dynamic_step(s) of {s.name} after 1 untimed step ({el:.1f} s, "
+                      f"OMP threads={o.num_threads()}); oracle/grafem_oracle.cpp -O3 -fopenmp")
+    if single_thread:  # SURVEY §8(d) CPU timing plan: the 1-thread time next to the all-threads one
+        threads = o.num_threads()
+        o.set_num_threads(1)
+        t1 = time.perf_counter()
+        sim.dynamic_step()
+        el1 = time.perf_counter() - t1
+        o.set_num_threads(threads)
+        out["single_thread"] = {"value": s.num_tets / el1, "unit": UNIT, "cores": 1,
+                                "sample": f"1 dynamic_step of {s.name} on 1 OMP thread ({el1:.1f} s)"}
+    return out
 
 
 def config_dict(s, scaling_note):
@@ -166,6 +176,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=25.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-1t", action="store_true", help="skip the 1-thread CPU sample (~15 s at c3)")
     args = ap.parse_args()
     rank, world, local = dist_env()
 
@@ -289,7 +300,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = run_cpu(s, args.cpu_steps, args.cpu_budget)
+        cpu = run_cpu(s, args.cpu_steps, args.cpu_budget, single_thread=not args.no_cpu_1t)
     dist.close()
     if rank != 0:
         return

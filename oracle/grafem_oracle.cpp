@@ -1547,6 +1547,13 @@ int or_num_threads(void) {
   return 1;
 #endif
 }
+void or_set_num_threads(int n) {  // CPU-baseline timing at a chosen thread count (bench.py)
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
 
 int or_mesh_create(const double* nodes, int32_t n_nodes, const int32_t* tets, int32_t n_tets, or_mesh** out) {
   return guard([&] {

@@ -80,6 +80,7 @@ typedef struct or_sim or_sim;
 
 const char* or_last_error(void);
 int or_num_threads(void);
+void or_set_num_threads(int n);
 
 /* ---- mesh (mesh.cpp:34-109, primitives.cpp:13-79) ---- */
 int or_mesh_create(const double* nodes, int32_t n_nodes, const int32_t* tets, int32_t n_tets, or_mesh** out);

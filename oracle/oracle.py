@@ -77,8 +77,10 @@ _lib = None
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB_PATH):
-        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    srcs = [os.path.join(_HERE, f) for f in ("grafem_oracle.cpp", "oracle.h", "Makefile")]
+    stale = not os.path.exists(_LIB_PATH) or any(os.path.getmtime(f) > os.path.getmtime(_LIB_PATH) for f in srcs)
+    if force or stale:
+        subprocess.run(["make", "-s", "-C", _HERE] + (["-B"] if force else []), check=True)
     return _LIB_PATH
 
 
@@ -541,3 +543,7 @@ class Sim:
 
 def num_threads():
     return int(lib().or_num_threads())
+
+
+def set_num_threads(n: int):
+    lib().or_set_num_threads(C.c_int(int(n)))
