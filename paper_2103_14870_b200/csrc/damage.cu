@@ -97,6 +97,36 @@ __global__ void __launch_bounds__(kTpb) k_tet_stress(DevData d, MatDev m, int lo
   }
 }
 
+// screened values of one non-degenerate tet, T * avg (fracture.cpp:77), max-reduced into its edges
+// (fracture.cpp:80-87): build_T + matvec6 row by row -- the same operations in the same order, without
+// materialising T (fewer live registers in the gather kernels) and without the degeneracy test, which
+// k_tet_stress already made with identical arithmetic (deg[e])
+__device__ __forceinline__ void screen_tet(const DevData& d, int e, const double avg[6]) {
+  const int4 t = __ldg(d.tets + e);
+  const int id[4] = {t.x, t.y, t.z, t.w};
+  double x[4][3];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) x[k][a] = __ldg(d.X + 3 * (size_t)id[k] + a) + __ldg(d.u + 3 * (size_t)id[k] + a);
+  constexpr int le[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const double dx = x[le[k][1]][0] - x[le[k][0]][0];
+    const double dy = x[le[k][1]][1] - x[le[k][0]][1];
+    const double dz = x[le[k][1]][2] - x[le[k][0]][2];
+    const double len = sqrt((dx * dx + dy * dy) + dz * dz);
+    const double nx = dx / len, ny = dy / len, nz = dz / len;
+    double acc = (nx * nx) * avg[0];
+    acc = acc + (ny * ny) * avg[1];
+    acc = acc + (nz * nz) * avg[2];
+    acc = acc + (nx * ny) * avg[3];
+    acc = acc + (nx * nz) * avg[4];
+    acc = acc + (ny * nz) * avg[5];
+    atomicMax(d.scr_key + __ldg(d.tet_edges + 6 * (size_t)e + k), dkey(acc));
+  }
+}
+
 __global__ void __launch_bounds__(kTpb, GF_NL_MINB) k_nonlocal(DevData d) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= d.nt) return;
@@ -117,16 +147,7 @@ __global__ void __launch_bounds__(kTpb, GF_NL_MINB) k_nonlocal(DevData d) {
     avg[4] = avg[4] + w * s45.x;
     avg[5] = avg[5] + w * s45.y;
   }
-  const int4 t = __ldg(d.tets + e);
-  double x[4][3], du[9];
-  load_tet_positions(d, t, x, du);
-  int te[6];
-  double rl[6], T[6][6];
-  tet_rest_lengths(d, e, te, rl);
-  build_T(x, rl, T);  // non-degenerate (checked by k_tet_stress with identical arithmetic)
-  double scr[6];
-  matvec6(T, avg, scr);
-  scatter_max(d, te, scr);
+  screen_tet(d, e, avg);  // non-degenerate (checked by k_tet_stress with identical arithmetic)
 }
 
 // structured layout: warp = template warp (DevData::nl_tpl); same sums in the same order as k_nonlocal
@@ -174,16 +195,7 @@ __global__ void __launch_bounds__(kNlTpb, (GF_NL_MINB * 256) / kNlTpb) k_nonloca
     avg[5] = present ? avg[5] + w * s45.y : avg[5];
 #endif
   }
-  const int4 t = __ldg(d.tets + e);
-  double x[4][3], du[9];
-  load_tet_positions(d, t, x, du);
-  int te[6];
-  double rl[6], T[6][6];
-  tet_rest_lengths(d, e, te, rl);
-  build_T(x, rl, T);
-  double scr[6];
-  matvec6(T, avg, scr);
-  scatter_max(d, te, scr);
+  screen_tet(d, e, avg);
 }
 
 __global__ void __launch_bounds__(kTpb) k_relabel(DevData d, double thres, int relabel, int keep_values) {
