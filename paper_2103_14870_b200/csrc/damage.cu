@@ -40,20 +40,15 @@ __device__ __forceinline__ void load_tet_positions(const DevData& d, int4 t, dou
     for (int r = 0; r < 3; ++r) du[3 * r + c] = u[c + 1][r] - u[0][r];
 }
 
-__device__ __forceinline__ void tet_rest_lengths(const DevData& d, int e, int te[6], double rl[6]) {
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    te[k] = __ldg(d.tet_edges + 6 * (size_t)e + k);
-    rl[k] = __ldg(d.rest_len + te[k]);
-  }
-}
-
 __device__ __forceinline__ void scatter_max(const DevData& d, const int te[6], const double scr[6]) {
 #pragma unroll
   for (int k = 0; k < 6; ++k) atomicMax(d.scr_key + te[k], dkey(scr[k]));
 }
 
-__global__ void __launch_bounds__(kTpb) k_tet_stress(DevData d, MatDev m, int local_screen) {
+#ifndef GF_TS_MINB
+#define GF_TS_MINB 3  // 3 x 256 threads per SM (80 registers): measured faster than 2 at c3 and c4
+#endif
+__global__ void __launch_bounds__(kTpb, GF_TS_MINB) k_tet_stress(DevData d, MatDev m, int local_screen) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e == 0) *d.newly_count = 0;  // this pass's relabel compacts from zero (stream order: tet_stress first)
   if (e >= d.nt) return;
@@ -75,26 +70,42 @@ __global__ void __launch_bounds__(kTpb) k_tet_stress(DevData d, MatDev m, int lo
     for (int k = 0; k < 6; ++k) d.sigc[6 * (size_t)e + k] = c6[k];
   }
 
+  // build_T (fracture.cpp:16-28) and T sigma_c (fracture.cpp:74) row by row: each row's operations in build_T's
+  // and matvec6's order, without materialising T (fewer live registers); outputs only after every row passed
+  // the degeneracy test, as build_T's early return implies
   int te[6];
-  double rl[6], T[6][6], sf[6];
-  tet_rest_lengths(d, e, te, rl);
-  const bool ok = build_T(x, rl, T);
+  double sf[6], scr[6], avg[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) avg[k] = 0.0 + 1.0 * c6[k];  // r_d = 0: table {(e, 1.0)} -> avg = 0 + 1.0 sigma_c
+  bool ok = true;
+  constexpr int le[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    te[k] = __ldg(d.tet_edges + 6 * (size_t)e + k);
+    const double rl = __ldg(d.rest_len + te[k]);
+    const double dx = x[le[k][1]][0] - x[le[k][0]][0];
+    const double dy = x[le[k][1]][1] - x[le[k][0]][1];
+    const double dz = x[le[k][1]][2] - x[le[k][0]][2];
+    const double len = sqrt((dx * dx + dy * dy) + dz * dz);
+    const double mx = (1.0 < rl) ? rl : 1.0;  // std::max(1.0, rl)
+    ok = ok && !(len < 1e-14 * mx);
+    const double nx = dx / len, ny = dy / len, nz = dz / len;
+    const double row[6] = {nx * nx, ny * ny, nz * nz, nx * ny, nx * nz, ny * nz};
+    double a = row[0] * c6[0];
+#pragma unroll
+    for (int j = 1; j < 6; ++j) a = a + row[j] * c6[j];
+    sf[k] = a;
+    if (local_screen) {
+      double b = row[0] * avg[0];
+#pragma unroll
+      for (int j = 1; j < 6; ++j) b = b + row[j] * avg[j];
+      scr[k] = b;
+    }
+  }
   d.deg[e] = ok ? 0 : 1;
-  if (!ok) {
 #pragma unroll
-    for (int k = 0; k < 6; ++k) d.sigf[6 * (size_t)e + k] = 0.0;  // tet_edge_stress stays Zero
-    return;
-  }
-  matvec6(T, c6, sf);
-#pragma unroll
-  for (int k = 0; k < 6; ++k) d.sigf[6 * (size_t)e + k] = sf[k];
-  if (local_screen) {  // r_d = 0: table {(e, 1.0)} -> avg = 0 + 1.0 * sigma_c
-    double avg[6], scr[6];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) avg[k] = 0.0 + 1.0 * c6[k];
-    matvec6(T, avg, scr);
-    scatter_max(d, te, scr);
-  }
+  for (int k = 0; k < 6; ++k) d.sigf[6 * (size_t)e + k] = ok ? sf[k] : 0.0;  // degenerate: tet_edge_stress stays Zero
+  if (ok && local_screen) scatter_max(d, te, scr);
 }
 
 // screened values of one non-degenerate tet, T * avg (fracture.cpp:77), max-reduced into its edges
