@@ -767,3 +767,26 @@ def test_render_companion_follows_the_gpu_damage_passes(tmp_path):
     v = np.array([[float(x) for x in l.split()[1:]] for l in lines if l.startswith("v ")])
     f = np.array([[int(x) for x in l.split()[1:]] for l in lines if l.startswith("f ")]) - 1
     assert np.array_equal(v, vg) and np.array_equal(f, tg)
+
+
+# ---------------------------------------------------------------- timing plumbing of bench.py
+def test_profiling_levels_time_what_they_claim():
+    """Level 2 (bench value region): CUDA events around the PCG solve only, launch counts and algorithmic bytes
+    for every kernel; level 1 (breakdown region): events around every kernel."""
+    s = cf.scaled("c3", (8, 8, 7))
+    gs, _ = cf.build_gpu(s)
+    gs.dynamic_step()
+    gs.set_profiling(2)
+    gs.reset_kernel_times()
+    gs.dynamic_step()
+    kt = gs.kernel_times()
+    assert {"tet_stress", "nonlocal", "relabel", "chi", "bc_targets", "assemble", "pcg", "integrate"} <= set(kt)
+    assert all(v["launches"] == 1 for v in kt.values())
+    assert kt["pcg"]["total_ms"] > 0 and all(v["total_ms"] == 0 for k, v in kt.items() if k != "pcg")
+    assert kt["pcg"]["bytes"] > 0 and kt["assemble"]["bytes"] > 0 and kt["nonlocal"]["bytes"] > 0
+    gs.set_profiling(1)
+    gs.reset_kernel_times()
+    gs.dynamic_step()
+    kt = gs.kernel_times()
+    assert all(v["launches"] == 1 and v["total_ms"] > 0 for v in kt.values())
+    gs.set_profiling(0)
