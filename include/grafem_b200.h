@@ -159,6 +159,10 @@ int gf_sim_get_state(gf_sim* s, double* displacements, double* velocities, uint8
                      double* element_chi, double* time);
 int gf_sim_set_state(gf_sim* s, const double* displacements, const double* velocities,
                      const uint8_t* edge_damage, const double* element_chi, const double* time);
+/* stream-ordered variant of gf_sim_set_state for pinned host buffers (gf_host_alloc): returns once the copies
+ * are enqueued; the buffers must stay unchanged until the next synchronous call on the simulation (the next
+ * step reads the new state). Runtime utility for zero-stall pipelines, no reference counterpart. */
+int gf_sim_set_state_async(gf_sim* s, const double* displacements, const double* velocities);
 /* external nodal load f_ext (3N, constant until reset; NULL clears). SPEC.md:397 hook; not in the
  * reference's solver.cpp:229-249, which only has gravity and colliders */
 int gf_sim_set_external_forces(gf_sim* s, const double* f3n);

@@ -469,11 +469,14 @@ class Simulation:
         _check(lib().gf_sim_get_state(self._h, ptr(u, F64P), ptr(v, F64P), ptr(zeta, U8P), ptr(chi, F64P), None))
 
     def set_state_from(self, u=None, v=None):
+        """Stream-ordered upload of u, v from pinned buffers (gf_sim_set_state_async)."""
         def ptr(a):
             if a is None:
                 return None
             return C.cast(a, F64P) if isinstance(a, int) else a.ctypes.data_as(F64P)
-        _check(lib().gf_sim_set_state(self._h, ptr(u), ptr(v), None, None, None))
+        # pinned buffers: stream-ordered upload, no host round trip (the next step reads the new state; the
+        # caller must not modify the buffers before its next synchronous call on the simulation)
+        _check(lib().gf_sim_set_state_async(self._h, ptr(u), ptr(v)))
 
     def set_external_forces(self, f3n=None):
         if f3n is None:

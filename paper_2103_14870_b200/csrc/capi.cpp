@@ -194,6 +194,9 @@ int gf_sim_set_state(gf_sim* s, const double* u, const double* v, const uint8_t*
                      const double* time) {
   return guard([&] { s->s->set_state(u, v, zeta, chi, time); });
 }
+int gf_sim_set_state_async(gf_sim* s, const double* u, const double* v) {
+  return guard([&] { s->s->set_state(u, v, nullptr, nullptr, nullptr, true); });
+}
 int gf_sim_set_external_forces(gf_sim* s, const double* f3n) {
   return guard([&] { s->s->set_external_forces(f3n); });
 }

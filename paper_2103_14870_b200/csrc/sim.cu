@@ -962,14 +962,14 @@ void Simulation::get_state(double* u, double* v, uint8_t* zeta, double* chi, dou
 }
 
 void Simulation::set_state(const double* u, const double* v, const uint8_t* zeta, const double* chi,
-                           const double* time) {
+                           const double* time, bool async) {
   const size_t nd = 3 * (size_t)mesh_.nn;
   if (u) GF_CUDA(cudaMemcpyAsync(d_.u, u, 8 * nd, cudaMemcpyHostToDevice, stream_));
   if (v) GF_CUDA(cudaMemcpyAsync(d_.v, v, 8 * nd, cudaMemcpyHostToDevice, stream_));
   if (zeta) GF_CUDA(cudaMemcpyAsync(d_.zeta, zeta, mesh_.ne, cudaMemcpyHostToDevice, stream_));
   if (chi) GF_CUDA(cudaMemcpyAsync(d_.chi, chi, 8 * (size_t)mesh_.nt, cudaMemcpyHostToDevice, stream_));
   if (time) time_ = *time;
-  synchronize();
+  if (!async) synchronize();  // async (pinned sources): the copies are stream-ordered before the next step
 }
 
 void Simulation::set_external_forces(const double* f3n) {

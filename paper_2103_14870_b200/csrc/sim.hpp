@@ -52,7 +52,8 @@ class Simulation {
   // already broken); from then on every damage pass with newly broken edges feeds it (solver.cpp:94)
   RenderMesh& viz();
   void get_state(double* u, double* v, uint8_t* zeta, double* chi, double* time);
-  void set_state(const double* u, const double* v, const uint8_t* zeta, const double* chi, const double* time);
+  void set_state(const double* u, const double* v, const uint8_t* zeta, const double* chi, const double* time,
+                 bool async = false);
   void set_external_forces(const double* f3n);
   uint64_t pattern_hash() const { return hash_; }
   int32_t dof_count() const { return 3 * mesh_.nn; }
