@@ -57,7 +57,6 @@ __device__ __forceinline__ double lane_sum(double v) {  // fixed butterfly: same
 #ifndef GF_SELL_GROUP
 #define GF_SELL_GROUP 4
 #endif
-constexpr int kGroup = GF_SELL_GROUP;
 #ifndef GF_GATHER_L1
 #define GF_GATHER_L1 1
 #endif
@@ -109,7 +108,10 @@ __device__ __forceinline__ double ldmat(const double* p) {
 #endif
 }
 
-template <class G>
+#ifndef GF_SELL_GROUP_DYN
+#define GF_SELL_GROUP_DYN 8  // the large-matrix (HBM-streaming) instance: more block loads in flight (c4: -0.8 %)
+#endif
+template <class G, int kGroup = GF_SELL_GROUP>
 __device__ __forceinline__ void slice_spmv_sym_g(const CgLaunch& a, int sl, const G& gat, double acc[3]) {
   const int lane = threadIdx.x & 31;
   const int row = sl * 32 + lane;
@@ -481,7 +483,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       ptrs(cA, dA);
       ph.run<kDyn, 1>(cA, dA, [&](int sl, double (&v)[1]) {
         double acc[3];
-        slice_spmv_sym_g(a, sl, GatherZ{a.z}, acc);
+        slice_spmv_sym_g<GatherZ, kDyn ? GF_SELL_GROUP_DYN : GF_SELL_GROUP>(a, sl, GatherZ{a.z}, acc);
         const int row = sl * 32 + lane;
         double pq = 0.0;
         if (row < nrows) {
