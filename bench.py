@@ -80,6 +80,33 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        # NVML polled every 5 ms from a thread (the value region is ~70 ms at c3, shorter than nvidia-smi's
+        # start-up); nvidia-smi -lms 100 only when NVML is unavailable
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            bits = [getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+                    getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                    getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                    getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4)]
+            self.stop_flag = threading.Event()
+
+            def poll():
+                while not self.stop_flag.is_set():
+                    r = get_reasons(h)
+                    self.rows.append([str(self.index), str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), str(smax),
+                                      "0", "0"] + ["Active" if r & b else "Not Active" for b in bits])
+                    time.sleep(0.005)
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            self.nvml = True
+            return
+        except Exception:
+            self.nvml = False
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -94,22 +121,27 @@ class ClockSampler:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def stop(self):
-        if self.proc is None:
+        if getattr(self, "nvml", False):
+            self.stop_flag.set()
+            self.thread.join(timeout=2)
+        elif self.proc is None:
             return None
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        self.thread.join(timeout=2)
+        else:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
         sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
         if not sm:
             return None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in self.rows if len(r) >= 9 for n, v in zip(names, r[5:9]) if v == "Active"})
         smax = max(float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit())
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": reasons, "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": reasons, "samples": len(sm),
+                "source": "NVML, 5 ms polling" if getattr(self, "nvml", False) else "nvidia-smi -lms 100"}
 
 
 def measured_peak_hbm():
