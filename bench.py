@@ -95,11 +95,15 @@ class ClockSampler:
                     getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4)]
             self.stop_flag = threading.Event()
 
+            def sample():
+                r = get_reasons(h)
+                self.rows.append([str(self.index), str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), str(smax),
+                                  "0", "0"] + ["Active" if r & b else "Not Active" for b in bits])
+            self.sample = sample  # stop() also reads once synchronously: never zero samples
+
             def poll():
                 while not self.stop_flag.is_set():
-                    r = get_reasons(h)
-                    self.rows.append([str(self.index), str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), str(smax),
-                                      "0", "0"] + ["Active" if r & b else "Not Active" for b in bits])
+                    sample()
                     time.sleep(0.005)
             self.thread = threading.Thread(target=poll, daemon=True)
             self.thread.start()
@@ -122,6 +126,7 @@ class ClockSampler:
 
     def stop(self):
         if getattr(self, "nvml", False):
+            self.sample()  # the region has just ended: the SM clock still reads its under-load value
             self.stop_flag.set()
             self.thread.join(timeout=2)
         elif self.proc is None:
