@@ -167,12 +167,14 @@ def ncu_traffic(workload, kernel):
 
 
 # ---------------------------------------------------------------- CPU baseline (oracle)
-def run_cpu(s, steps, budget_s, single_thread=False):
-    """Times the CPU oracle (reference's algorithm + OpenMP layout) on a bounded sample of the workload."""
+def run_cpu(s, steps, budget_s, single_thread=False, warmup=1):
+    """Times the CPU oracle (reference's algorithm + OpenMP layout) on a bounded sample of the workload: `warmup`
+    untimed steps from rest (the GPU arm's window: its timed steps follow the same warm-up), then up to `steps`."""
     from oracle import oracle as o
     from oracle.scenario import build_oracle
     sim, mesh = build_oracle(s)
-    sim.dynamic_step()  # one untimed step (first-touch)
+    for _ in range(max(1, warmup)):
+        sim.dynamic_step()  # untimed (first-touch; same step window as the GPU arm)
     done, t0 = 0, time.perf_counter()
     while done < steps:
         sim.dynamic_step()
@@ -181,7 +183,7 @@ def run_cpu(s, steps, budget_s, single_thread=False):
             break
     el = time.perf_counter() - t0
     out = dict(value=s.num_tets * done / el, unit=UNIT, cores=o.num_threads(), kind="port",
-               sample=f"{done} dynamic_step(s) of {s.name} after 1 untimed step ({el:.1f} s, "
+               sample=f"{done} dynamic_step(s) of {s.name} after {max(1, warmup)} untimed step(s) ({el:.1f} s, "
                       f"OMP threads={o.num_threads()}); oracle/grafem_oracle.cpp -O3 -fopenmp")
     if single_thread:  # SURVEY §8(d) CPU timing plan: the 1-thread time next to the all-threads one
         threads = o.num_threads()
@@ -198,8 +200,121 @@ def run_cpu(s, steps, budget_s, single_thread=False):
 def config_dict(s, scaling_note):
     return {"workload": s.name, "tets": s.num_tets, "cells": list(s.cells), "r_d_m": s.r_d, "dt": s.dt,
             "cg_tol": s.cg_tol, "material": "stable_neo_hookean" if s.model == 0 else "stvk",
-            "l2": "inputs larger than L2: non-local table (~1.2 GB) + per-tet data streamed every step; the symmetric system matrix (~64 MB) is rebuilt each step and stays L2-resident only within the PCG",
+            "l2": "inputs larger than L2: non-local table (~1.2 GB) + per-tet data streamed every step; the symmetric "
+                  "system matrix (~62 MB) is rebuilt each step and stays L2-resident only within the PCG",
             "parallelism": scaling_note}
+
+
+def pcg_models(info):
+    """PCG bytes per iteration of the symmetric SELL-32 format.
+
+    l2:  bytes between L2 and the SMs -- every block of the full matrix is served once per iteration (an upper block
+         serves its own row and, transposed, its column's row: 72 B x node_blocks), the slot words, and the vectors
+         that leave the chip (z gathered once + written once when the solver state is on chip; p, q, x, r, D^-1 too
+         for large matrices);
+    hbm: the same with every STORED block once (72 B x upper_blocks): the format's minimum if nothing stays cached;
+    working set: what must stay L2-resident for the solve to run from L2."""
+    N = info["nodes"]
+    dyn = info["pcg_dynamic_units"] > 0
+    vec = (312 if dyn else 48) * N
+    l2 = 72 * info["node_blocks"] + 4 * info["spmv_slots"] + vec
+    hbm = 72 * info["upper_blocks"] + 4 * info["spmv_slots"] + vec
+    ws = 72 * info["upper_block_slots"] + 4 * info["spmv_slots"] + (144 if dyn else 24) * N
+    survey = 12 * 9 * info["node_blocks"] + 4 * (3 * N + 1) + 56 * 3 * N  # SURVEY §8(d) B_CG (scalar CSR)
+    return dict(l2_bytes_per_iter=l2, hbm_bytes_per_iter=hbm, working_set_bytes=ws, survey_bytes_per_iter=survey,
+                solver_state="global (large matrix)" if dyn else "on chip (one slice per warp)")
+
+
+L2_ROOF_BUFFER = 64 << 20  # the c3 PCG working set (~72 MB) is of this order
+
+
+def timed_steps(sim, steps, level=2):
+    """steps dynamic_steps between CUDA events on the simulation stream (profiling level 2: PCG events only)."""
+    sim.reset_kernel_times()
+    sim.set_profiling(level)
+    sim.synchronize()
+    sim.timer_record(0)
+    iters, newly = 0, 0
+    for _ in range(steps):
+        st = sim.dynamic_step()
+        iters += st.cg_iterations
+        newly += st.newly_broken
+    sim.timer_record(1)
+    ms = sim.timer_elapsed_ms(0, 1)
+    sim.synchronize()
+    sim.set_profiling(False)
+    return ms, iters, newly, sim.kernel_times()
+
+
+def e2e_steps(g, sim, steps, N, T, E, dist=None, n=1):
+    nd = 3 * N
+    pu, pv = g.host_alloc(8 * nd), g.host_alloc(8 * nd)
+    pz, pc = g.host_alloc(E), g.host_alloc(8 * T)
+    sim.get_state_into(pu, pv, pz, pc)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        sim.set_state_from(pu, pv)              # H2D: caller-owned state (u, v)
+        sim.dynamic_step()
+        sim.get_state_into(pu, pv, pz, pc)      # D2H: the step's result (u, v, labels, chi)
+    el = time.perf_counter() - t0
+    if dist:
+        el = dist.max(el)
+    for p in (pu, pv, pz, pc):
+        g.host_free(p)
+    return {"value": n * T * steps / el, "unit": UNIT, "h2d_bytes_per_step": 16 * nd,
+            "d2h_bytes_per_step": 16 * nd + E + 8 * T, "steps": steps, "timing": "host wall clock, max over ranks"}
+
+
+def pcg_roofline(models, iters, pcg_ms, l2_roof, hbm_peak):
+    """roofline of the PCG solve over a timed region: bound L2 when its working set fits L2, else HBM."""
+    l2_bound = models["working_set_bytes"] <= 100e6
+    b_l2 = models["l2_bytes_per_iter"] * iters
+    b_hbm = models["hbm_bytes_per_iter"] * iters
+    out = {"bound": "l2" if l2_bound else "hbm", "iterations": iters, "ms": pcg_ms,
+           "l2_GBps": b_l2 / pcg_ms / 1e6, "l2_frac": b_l2 / pcg_ms / 1e6 / l2_roof if l2_roof else None,
+           "hbm_GBps": b_hbm / pcg_ms / 1e6, "hbm_frac": b_hbm / pcg_ms / 1e6 / hbm_peak,
+           "us_per_iteration": 1e3 * pcg_ms / max(1, iters)}
+    out.update(models)
+    return out
+
+
+def sub_record(g, cf, name, steps, warmup, hbm_peak, l2_roof, e2e=False, env=None):
+    """another BASELINE config (or layout) measured in the same run: setup, whole-step rate, PCG roofline."""
+    old = {}
+    for k, v in (env or {}).items():
+        old[k] = os.environ.get(k)
+        os.environ[k] = v
+    try:
+        s = cf.get(name)
+        t0 = time.perf_counter()
+        sim, mesh = cf.build_gpu(s)
+        sim.synchronize()
+        setup_wall = time.perf_counter() - t0
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    N, T, E = mesh.num_nodes(), mesh.num_tets(), mesh.num_edges()
+    info = sim.info()
+    for _ in range(warmup):
+        sim.dynamic_step()
+    ms, iters, newly, kt = timed_steps(sim, steps)
+    pcg = kt.get("pcg", {"total_ms": 0.0})
+    rec = {"workload": s.name, "tets": T, "value": T * steps / (ms / 1e3), "unit": UNIT, "steps": steps,
+           "warmup": warmup, "ms_per_step": ms / steps, "cg_iterations_per_step": iters / steps,
+           "newly_broken_in_region": newly, "nonlocal_layout": {0: "local", 1: "general sliced-ELL", 2: "template"}[info["nl_layout"]],
+           "setup_s": dict(info["setup_s"], wall_incl_mesh=setup_wall),
+           "pcg": pcg_roofline(pcg_models(info), iters, pcg["total_ms"], l2_roof, hbm_peak),
+           "step_hbm_GBps": sum(v["bytes"] for v in kt.values()) / ms / 1e6}
+    rec["step_hbm_frac"] = rec["step_hbm_GBps"] / hbm_peak
+    if e2e:
+        rec["e2e"] = e2e_steps(g, sim, max(1, steps // 2), N, T, E)
+    sim.close()
+    return rec
 
 
 def main():
@@ -213,6 +328,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=25.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the c1/c2/c4 and general-layout sub-records")
+    ap.add_argument("--sub", default="c1,c2,c4,c3-general", help="sub-records to measure (comma separated)")
     ap.add_argument("--no-cpu-1t", action="store_true", help="skip the 1-thread CPU sample (~15 s at c3)")
     args = ap.parse_args()
     rank, world, local = dist_env()
@@ -220,16 +337,17 @@ def main():
     from paper_2103_14870_b200 import configs as cf
     s = cf.get(args.config)
     n = max(world, args.gpus)
+    note = f"replicas x{n}" if n > 1 else "single process"
 
     if args.impl == "reference":
         if rank != 0:
             return
         budget = 150.0
-        r = run_cpu(s, args.steps, budget)
+        r = run_cpu(s, args.steps, budget, warmup=args.warmup)
         line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": n, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * s.num_tets / r["value"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded jittered box mesh)",
-                "config": config_dict(s, "cpu"), "impl": "reference", "cpu_baseline": r,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded jittered box mesh, BASELINE configs[2] shapes)",
+                "config": config_dict(s, note), "impl": "reference", "cpu_baseline": r,
                 "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -240,8 +358,18 @@ def main():
         torch.cuda.set_device(local)
     g.set_device(local)
     dist = Dist(world, "nccl")
+    peak, peak_src = measured_peak_hbm()
+    # roofline denominators measured live on this GPU: the L2 read roof (the c3 PCG runs from L2) and the HBM copy
+    # rate next to the driver's MEASURED_PEAKS.json figure
+    l2_roof = g.measure_bandwidth("l2", L2_ROOF_BUFFER, 50)
+    hbm_copy_live = g.measure_bandwidth("hbm", 2 << 30, 5)
+    t_setup = time.perf_counter()
     sim, mesh = cf.build_gpu(s)
+    sim.synchronize()
+    setup_wall = time.perf_counter() - t_setup
     N, T, E = mesh.num_nodes(), mesh.num_tets(), mesh.num_edges()
+    info = sim.info()
+    models = pcg_models(info)
 
     for _ in range(args.warmup):
         sim.dynamic_step()
@@ -249,91 +377,90 @@ def main():
     # ---------------- timed region (device, CUDA events on the simulation stream). Per-kernel events cost ~3 % of
     # the step, so this region times the dominant kernel (the PCG solve) with its own events and only counts the
     # other launches; the per-kernel breakdown comes from a second, separately timed region of the same length.
-    sim.reset_kernel_times()
-    sim.set_profiling(2)
     clocks = ClockSampler(local)
     clocks.start()
     dist.barrier()
-    sim.synchronize()
-    sim.timer_record(0)
-    cg_iters, newly = 0, 0
-    for _ in range(args.steps):
-        st = sim.dynamic_step()
-        cg_iters += st.cg_iterations
-        newly += st.newly_broken
-    sim.timer_record(1)
-    ms = sim.timer_elapsed_ms(0, 1)
-    sim.synchronize()
+    ms, cg_iters, newly, kt = timed_steps(sim, args.steps)
     dist.barrier()
     clk = clocks.stop()
-    sim.set_profiling(False)
-    kt = sim.kernel_times()
     ms_max = dist.max(ms)
     value = n * T * args.steps / (ms_max / 1e3)
     launches = int(sum(v["launches"] for v in kt.values()))
     # breakdown region: events around every kernel (shares and per-kernel GB/s; not used for value)
-    sim.reset_kernel_times()
-    sim.set_profiling(1)
-    sim.synchronize()
-    sim.timer_record(2)
-    for _ in range(args.steps):
-        sim.dynamic_step()
-    sim.timer_record(3)
-    ms_b = sim.timer_elapsed_ms(2, 3)
-    sim.synchronize()
-    sim.set_profiling(False)
-    kb = sim.kernel_times()
+    ms_b, _, _, kb = timed_steps(sim, args.steps, level=1)
 
     # roofline of the dominant kernel (timed live in the value region)
     dname, d = max(kt.items(), key=lambda kv: kv[1]["total_ms"])
     avg_ms = d["total_ms"] / max(1, d["launches"])
-    bytes_per_launch = d["bytes"] / max(1, d["launches"])
-    achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9
-    peak, peak_src = measured_peak_hbm()
     traffic = ncu_traffic(s.name, dname)
-    # whole-step roofline in the metric's own terms (BASELINE metric "% of HBM roofline"):
-    # B_step = B_F + B_D + k B_CG + B_int with k the measured CG iterations, over the measured step time
+    if dname == "pcg":
+        pr = pcg_roofline(models, cg_iters, d["total_ms"], l2_roof, peak)
+        l2b = pr["bound"] == "l2"
+        per_launch = (models["l2_bytes_per_iter"] if l2b else models["hbm_bytes_per_iter"]) * cg_iters / d["launches"]
+        achieved = per_launch / (avg_ms / 1e3) / 1e9
+        roof = l2_roof if l2b else peak
+        roofline = {"bound": "l2" if l2b else "hbm", "kernel": dname, "achieved": achieved, "peak": roof,
+                    "unit": "GB/s", "frac": achieved / roof, "traffic": traffic,
+                    "peak_source": ("measured live: L2-resident 16-byte reads of a 64 MB buffer from every SM "
+                                    "(gf_measure_bandwidth kind 0)") if l2b else peak_src,
+                    "algorithmic_bytes_per_launch": per_launch, "avg_launch_ms": avg_ms,
+                    "note": ("PCG bytes = the symmetric SELL-32 format's per-iteration traffic x measured iterations: "
+                             "72 B per block of the full matrix (an upper block serves its row and, transposed, its "
+                             "column's row), 4 B per slot word, z gathered + written; the solver state stays on chip. "
+                             "The matrix (~62 MB) is L2-resident during the solve, so the roof is the measured L2 read "
+                             "bandwidth; traffic = ncu DRAM bytes per launch (committed capture)"),
+                    "pcg": pr}
+    else:
+        achieved = d["bytes"] / max(1, d["launches"]) / (avg_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": d["bytes"] / max(1, d["launches"]), "avg_launch_ms": avg_ms}
+    roofline["share_of_step"] = d["total_ms"] / ms
+    roofline["l2_roof_GBps"] = l2_roof
+    roofline["hbm_copy_live_GBps"] = hbm_copy_live
+    roofline["kernels_region"] = {"steps": args.steps, "ms_per_step": ms_b / args.steps,
+                                  "note": "second timed region with CUDA events around every kernel"}
+    roofline["kernels"] = {}
+    for k, v in sorted(kb.items(), key=lambda kv: -kv[1]["total_ms"]):
+        gbps = (v["bytes"] / v["total_ms"] / 1e6) if v["total_ms"] > 0 and v["bytes"] > 0 else None
+        roofline["kernels"][k] = {"launches": v["launches"], "avg_ms": v["total_ms"] / max(1, v["launches"]),
+                                  "share": v["total_ms"] / ms_b, "GBps": gbps,
+                                  "hbm_frac": gbps / peak if gbps else None, "traffic": ncu_traffic(s.name, k)}
+    # whole-step roofline in the metric's own terms (BASELINE metric "% of HBM roofline"): algorithmic bytes per step
+    # (B_F + B_D + B_int of SURVEY §8(d) and the PCG's format bytes per iteration x measured iterations) over the
+    # measured step time; the SURVEY scalar-CSR PCG model is reported alongside (it overstates the format's bytes)
     b_step = sum(v["bytes"] for v in kt.values()) / args.steps
     step_gbs = b_step / (ms_max / args.steps / 1e3) / 1e9
+    pcg_b = kt.get("pcg", {}).get("bytes", 0.0)
+    b_survey = (sum(v["bytes"] for v in kt.values()) - pcg_b + models["survey_bytes_per_iter"] * cg_iters) / args.steps
     step_roofline = {"algorithmic_bytes_per_step": b_step, "achieved": step_gbs, "unit": "GB/s", "peak": peak,
                      "frac": step_gbs / peak, "frac_of_8TBps": step_gbs / 8000.0,
-                     "note": "SURVEY §8(d) B_step = B_F + B_D + k B_CG + B_int (k = measured CG iterations per step); "
-                             "B_CG counts the reference's scalar-CSR SpMV bytes, so the L2-resident symmetric "
-                             "matrix of the PCG lifts the fraction"}
-    roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
-                "note": ("pcg algorithmic bytes = SURVEY §8(d) B_CG per iteration (the reference's scalar CSR: "
-                         "12Z + 4(n+1) + 56n) x iterations; the symmetric SELL matrix and the solver state stay "
-                         "L2-/register-resident during the solve (traffic = ncu DRAM bytes per launch), so frac > 1 "
-                         "is the format + residency gain over that byte model, not an HBM rate") if dname == "pcg" else None,
-                "share_of_step": d["total_ms"] / ms,
-                "kernels_region": {"steps": args.steps, "ms_per_step": ms_b / args.steps,
-                                   "note": "second timed region with CUDA events around every kernel"},
-                "kernels": {k: {"launches": v["launches"], "avg_ms": v["total_ms"] / max(1, v["launches"]),
-                                "share": v["total_ms"] / ms_b,
-                                "GBps": (v["bytes"] / v["total_ms"] / 1e6) if v["total_ms"] > 0 and v["bytes"] > 0 else None}
-                            for k, v in sorted(kb.items(), key=lambda kv: -kv[1]["total_ms"])}}
+                     "survey_model": {"bytes_per_step": b_survey,
+                                      "GBps": b_survey / (ms_max / args.steps / 1e3) / 1e9,
+                                      "note": "SURVEY §8(d) B_step with the reference's scalar-CSR B_CG (12Z + 4(n+1) + 56n); "
+                                              "not an HBM rate: the symmetric L2-resident format moves far fewer bytes"},
+                     "note": "B_F + B_D (12 S for the non-local table) + B_int + PCG format bytes per iteration x measured "
+                             "iterations, over the measured step time"}
+    setup = dict(info["setup_s"], wall_incl_mesh=setup_wall)
 
-    # ---------------- e2e: public API with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        nd = 3 * N
-        pu, pv = g.host_alloc(8 * nd), g.host_alloc(8 * nd)
-        pz, pc = g.host_alloc(E), g.host_alloc(8 * T)
-        sim.get_state_into(pu, pv, pz, pc)
-        e_steps = max(1, args.steps // 2)
-        dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(e_steps):
-            sim.set_state_from(pu, pv)              # H2D: caller-owned state (u, v)
-            sim.dynamic_step()
-            sim.get_state_into(pu, pv, pz, pc)      # D2H: the step's result (u, v, labels, chi)
-        el = dist.max(time.perf_counter() - t0)
-        e2e = {"value": n * T * e_steps / el, "unit": UNIT, "h2d_bytes_per_step": 16 * nd,
-               "d2h_bytes_per_step": 16 * nd + E + 8 * T, "steps": e_steps, "timing": "host wall clock, max over ranks"}
-        for p in (pu, pv, pz, pc):
-            g.host_free(p)
+        e2e = e2e_steps(g, sim, max(1, args.steps // 2), N, T, E, dist, n)
+    sim.close()
+    sub = None
+    if rank == 0 and world == 1 and not args.no_sub:
+        sub = {}
+        for name in [x for x in args.sub.split(",") if x]:
+            try:
+                if name == "c3-general":
+                    sub[name] = sub_record(g, cf, "c3", args.steps, args.warmup, peak, l2_roof,
+                                           env={"GF_NL_LAYOUT": "general"})
+                elif name == "c4":
+                    sub[name] = sub_record(g, cf, "c4", min(args.steps, 10), min(args.warmup, 3), peak, l2_roof, e2e=True)
+                else:
+                    sub[name] = sub_record(g, cf, name, args.steps, args.warmup, peak, l2_roof)
+            except Exception as ex:  # a sub-record never hides the headline line
+                sub[name] = {"error": f"{type(ex).__name__}: {ex}"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -344,10 +471,11 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded jittered box mesh, BASELINE configs[2] shapes)",
-            "config": config_dict(s, f"replicas x{n}" if n > 1 else "single GPU"),
+            "config": config_dict(s, note),
             "roofline": roofline, "step_roofline": step_roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches,
-            "clocks": clk, "cg_iterations_per_step": cg_iters / args.steps, "newly_broken_in_region": newly}
+            "gpu_launches": launches, "setup_s": setup,
+            "clocks": clk, "cg_iterations_per_step": cg_iters / args.steps, "newly_broken_in_region": newly,
+            "sub": sub}
     print(json.dumps(line), flush=True)
 
 

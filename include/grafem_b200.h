@@ -186,6 +186,11 @@ int gf_sim_eval_screening(gf_sim* s, double* screening, double* sigma_f6, uint8_
 int gf_sim_last_system(gf_sim* s, double* vals, double* rhs);
 /* y = A x with the current system matrix (FixedPatternSparse::multiply, sparse.cpp:49-60) */
 int gf_sim_spmv(gf_sim* s, const double* x, double* y);
+/* cg_solve (sparse.cpp:129-188) with the PRODUCTION solver (the persistent PCG on the symmetric SELL-32 matrix) on a
+ * caller-provided matrix with this simulation's pattern: vals in the scalar-CSR order of gf_sim_eval_stiffness,
+ * symmetric (the upper blocks are used); x0 NULL = zero guess. Replaces the simulation's current system. */
+int gf_sim_solve_system(gf_sim* s, const double* vals, const double* b, const double* x0, double tol,
+                        int32_t max_iters, double* x, gf_cg_result* res);
 /* cg_solve (sparse.cpp:129-188) on a caller-provided scalar CSR, on the device */
 int gf_cg_solve_csr(int32_t n, const int32_t* row_ptr, const int32_t* cols, const double* vals, const double* b,
                     double* x, double tol, int32_t max_iters, gf_cg_result* res);
@@ -239,6 +244,27 @@ int gf_viz_export_frame(const gf_viz* v, const char* path, const double* displac
 /* VizMesh::fragment_volumes (viz.cpp:333-412) */
 int gf_viz_fragment_volumes(const gf_viz* v, int32_t tet, const double* displacements, const uint8_t* edge_damage,
                             double out[4]);
+
+/* storage sizes and setup time of one simulation (roofline byte models). Runtime utility, no
+ * reference counterpart: the reference's setup is Simulation::Simulation (solver.cpp:31-60). */
+typedef struct {
+  int64_t nodes, tets, edges;
+  int64_t node_blocks;        /* 3x3 blocks of the full pattern (scalar nonzeros / 9) */
+  int64_t upper_blocks;       /* blocks stored by the symmetric format: (node_blocks + nodes) / 2 */
+  int64_t upper_block_slots;  /* stored block slots incl. SELL-32 padding (32 per slice slot) */
+  int64_t spmv_slots;         /* 4-byte SpMV slot words incl. padding (32 per slice slot) */
+  int64_t nl_entries;         /* non-local table entries S (T when r_d = 0) */
+  int64_t nl_slots;           /* device table slots x 32 lanes (template or sliced-ELL, padding included); 0 local */
+  int32_t nl_layout;          /* as gf_sim_nonlocal_layout */
+  int32_t pcg_dynamic_units;  /* PCG slices handed out by ticket: 0 = solver state on chip for the whole solve */
+  double setup_s[4];          /* wall seconds: [0] pattern + incidence + assembly lists + SELL layout,
+                                 [1] non-local table (grid-binned build), [2] device layout + uploads, [3] ctor total */
+} gf_sim_info;
+int gf_sim_info_get(const gf_sim* s, gf_sim_info* out);
+/* measured device bandwidth in GB/s on the current device: kind 0 = reads of an L2-resident buffer of `bytes`
+ * (16-byte ld.global.cg from every SM, L1 bypassed, `reps` passes after one warm pass); kind 1 = HBM copy of
+ * `bytes` (read + write bytes counted, like MEASURED_PEAKS.json). Roofline denominators for bench.py. */
+int gf_measure_bandwidth(int32_t kind, int64_t bytes, int32_t reps, double* gbps);
 
 /* select the CUDA device for subsequently created simulations (one process per GPU) */
 int gf_set_device(int32_t device);

@@ -23,3 +23,15 @@ def build_oracle(s):
     if s.initial_velocity is not None:
         sim.set_state(v=np.tile(np.asarray(s.initial_velocity, np.float64), (mesh.num_nodes, 1)))
     return sim, mesh
+
+
+def near_threshold_flips(om, mat, u_pre, r_d, thres, edges, tol):
+    """Label-sync acceptance rule (SURVEY §7 hard part 7): a label that differs between the GPU and the oracle after
+    a step is legitimate only if the oracle's screening value of that edge, computed from the PRE-step state the
+    damage pass saw, lies within tol * thres of the threshold (a rounding-level decision). Returns
+    (all_ok, max relative distance |s - thres| / thres over the differing edges)."""
+    sig = om.per_tet_cauchy(mat, u_pre)
+    scr = om.nonlocal_screen(u_pre, sig, r_d)[0]
+    dist = np.abs(scr[np.asarray(edges)] - thres) / thres
+    worst = float(dist.max()) if len(dist) else 0.0
+    return bool(worst <= tol), worst

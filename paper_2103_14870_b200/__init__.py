@@ -95,6 +95,13 @@ class _CgResult(C.Structure):
                 ("_pad", C.c_int32), ("relative_residual", C.c_double)]
 
 
+class _SimInfo(C.Structure):
+    _fields_ = [("nodes", C.c_int64), ("tets", C.c_int64), ("edges", C.c_int64), ("node_blocks", C.c_int64),
+                ("upper_blocks", C.c_int64), ("upper_block_slots", C.c_int64), ("spmv_slots", C.c_int64),
+                ("nl_entries", C.c_int64), ("nl_slots", C.c_int64), ("nl_layout", C.c_int32),
+                ("pcg_dynamic_units", C.c_int32), ("setup_s", C.c_double * 4)]
+
+
 class KernelTime(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("total_ms", C.c_double), ("bytes", C.c_double)]
 
@@ -549,6 +556,19 @@ class Simulation:
         _check(lib().gf_sim_spmv(self._h, px, _p(y, F64P)))
         return y
 
+    def solve_system(self, vals, b, x0=None, tol=1e-8, max_iters=4000):
+        """The production PCG (k_pcg_sell) on a symmetric matrix with this simulation's pattern (scalar-CSR values
+        as eval_stiffness returns them): cg_solve (sparse.cpp:129-188). Replaces the current system."""
+        v, pv = _f64(vals)
+        bb, pb = _f64(np.asarray(b).reshape(-1))
+        xx = None if x0 is None else _f64(np.asarray(x0).reshape(-1))
+        x = np.zeros(3 * self.N)
+        r = _CgResult()
+        _check(lib().gf_sim_solve_system(self._h, pv, pb, None if xx is None else xx[1], C.c_double(tol),
+                                         C.c_int32(max_iters), _p(x, F64P), C.byref(r)))
+        return x, dict(iterations=r.iterations, converged=bool(r.converged),
+                       negative_curvature=bool(r.negative_curvature), relative_residual=r.relative_residual)
+
     # runtime utilities
     def set_profiling(self, level):
         """0 / False off, 1 / True events around every kernel, 2 events around the PCG solve only."""
@@ -566,6 +586,15 @@ class Simulation:
 
     def synchronize(self):
         _check(lib().gf_sim_synchronize(self._h))
+
+    def info(self) -> dict:
+        """gf_sim_info: storage sizes of the device formats (roofline byte models) and the setup wall times."""
+        i = _SimInfo()
+        _check(lib().gf_sim_info_get(self._h, C.byref(i)))
+        out = {k: getattr(i, k) for k, _ in _SimInfo._fields_ if k != "setup_s"}
+        out["setup_s"] = dict(pattern_and_layouts=i.setup_s[0], nonlocal_table=i.setup_s[1],
+                              device_layout_and_upload=i.setup_s[2], total=i.setup_s[3])
+        return out
 
     def timer_record(self, slot: int):
         _check(lib().gf_sim_timer_record(self._h, C.c_int32(slot)))
@@ -679,6 +708,14 @@ def host_alloc(nbytes: int) -> int:
 
 def host_free(p: int):
     lib().gf_host_free(C.c_void_p(p))
+
+
+def measure_bandwidth(kind: str, nbytes: int, reps: int = 20) -> float:
+    """GB/s of the current device: kind "l2" = reads of an L2-resident buffer, "hbm" = copy (read + write)."""
+    out = C.c_double()
+    _check(lib().gf_measure_bandwidth(C.c_int32({"l2": 0, "hbm": 1}[kind]), C.c_int64(int(nbytes)),
+                                      C.c_int32(reps), C.byref(out)))
+    return out.value
 
 
 def device_info():

@@ -27,6 +27,7 @@ CU_SOURCES = {  # file -> extra flags
     "cg.cu": [],
     "cg_sell.cu": [],
     "sim.cu": [],
+    "probe.cu": [],
 }
 CPP_SOURCES = ["host_mesh.cpp", "host_viz.cpp", "capi.cpp"]
 

@@ -233,6 +233,10 @@ int gf_sim_last_system(gf_sim* s, double* vals, double* rhs) {
 int gf_sim_spmv(gf_sim* s, const double* x, double* y) {
   return guard([&] { s->s->spmv(x, y); });
 }
+int gf_sim_solve_system(gf_sim* s, const double* vals, const double* b, const double* x0, double tol,
+                        int32_t max_iters, double* x, gf_cg_result* res) {
+  return guard([&] { s->s->solve_system(vals, b, x0, tol, max_iters, x, res); });
+}
 int gf_cg_solve_csr(int32_t n, const int32_t* row_ptr, const int32_t* cols, const double* vals, const double* b,
                     double* x, double tol, int32_t max_iters, gf_cg_result* res) {
   return guard([&] { cg_solve_csr(n, row_ptr, cols, vals, b, x, tol, max_iters, res); });
@@ -272,6 +276,12 @@ int gf_sim_timer_elapsed(gf_sim* s, int32_t a, int32_t b, double* ms) {
 }
 int gf_sim_cg_trace(gf_sim* s, uint64_t* out) {
   return guard([&] { s->s->cg_trace(reinterpret_cast<unsigned long long*>(out)); });
+}
+int gf_sim_info_get(const gf_sim* s, gf_sim_info* out) {
+  return guard([&] { *out = s->s->info(); });
+}
+int gf_measure_bandwidth(int32_t kind, int64_t bytes, int32_t reps, double* gbps) {
+  return guard([&] { *gbps = measure_bandwidth(kind, bytes, reps); });
 }
 int gf_set_device(int32_t device) {
   return guard([&] {

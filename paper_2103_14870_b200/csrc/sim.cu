@@ -13,6 +13,7 @@
 #include "sim.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -162,6 +163,9 @@ bool Simulation::build_template_layout(const NonlocalTable& tb, Up&& up) {
 Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_solver_config& cfg,
                        const gf_boundary_condition* bcs, int32_t n_bcs, const gf_collider* cols, int32_t n_cols)
     : mesh_(mesh), mat_(mat), cfg_(cfg) {
+  using clk = std::chrono::steady_clock;
+  const auto t_ctor = clk::now();
+  auto secs = [](clk::time_point a) { return std::chrono::duration<double>(clk::now() - a).count(); };
   // validation in the reference's order (material.cpp:37-43, solver.cpp:10-20, collision.cpp:32-40, 46-56)
   if (!(mat.youngs > 0.0)) throw FormatError("youngs modulus must be positive");
   if (!(mat.poisson >= 0.0 && mat.poisson < 0.5)) throw FormatError("poisson ratio must be in [0, 0.5)");
@@ -235,6 +239,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   if (major < 10) throw CudaError("device is not sm_100 class (Blackwell); this build targets sm_100a only");
 
   // host setup: pattern, incidence, table, mass (fem.cpp:140-179, fracture.cpp:32-54)
+  auto t_phase = clk::now();
   pat_ = make_node_pattern(mesh_);
   if (pat_.max_degree > 64) throw GeometryError("node rows with more than 64 neighbour blocks are not supported by the assembly kernel");
   const NodeTets ntets = make_node_tets(mesh_, pat_);
@@ -393,8 +398,11 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     d_.sell_slot = (const uint32_t*)up(slot.data(), 4 * slot.size());
     GF_CUDA(cudaStreamSynchronize(stream_));
   }
+  setup_s_[0] = secs(t_phase);
   if (mat.r_d > 0.0) {
+    t_phase = clk::now();
     const NonlocalTable tb = make_nonlocal_table(mesh_, mat.r_d);
+    setup_s_[1] = secs(t_phase);
     nl_entries_ = (int64_t)tb.ids.size();
     const char* nl_env = std::getenv("GF_NL_LAYOUT");  // "general" forces the sliced-ELL table
     if (!(nl_env && std::string(nl_env) == "general") && build_template_layout(tb, up)) {
@@ -422,6 +430,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     d_.nl_len = (const int32_t*)up(len.data(), 4 * len.size());
     d_.nl_ids = (const int32_t*)up(ids.data(), 4 * ids.size());
     d_.nl_w = (const double*)up(w.data(), 8 * w.size());
+    nl_ell_slots_ = 32 * sptr[ns];
     GF_CUDA(cudaStreamSynchronize(stream_));  // host staging goes out of scope
     }
   } else {
@@ -549,6 +558,25 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   cg_.tol = cfg.cg_tol;
   GF_CUDA(cudaStreamSynchronize(stream_));
   GF_CUDA(cudaGetLastError());
+  setup_s_[3] = secs(t_ctor);
+  setup_s_[2] = setup_s_[3] - setup_s_[0] - setup_s_[1];
+}
+
+gf_sim_info Simulation::info() const {
+  gf_sim_info o{};
+  o.nodes = mesh_.nn;
+  o.tets = mesh_.nt;
+  o.edges = mesh_.ne;
+  o.node_blocks = (int64_t)pat_.cols.size();
+  o.upper_blocks = (o.node_blocks + o.nodes) / 2;
+  o.upper_block_slots = 32 * (int64_t)usp_[d_.nslices];
+  o.spmv_slots = 32 * sell_slots_;
+  o.nl_entries = nl_entries_;
+  o.nl_slots = mat_.r_d <= 0.0 ? 0 : d_.nl_tpl ? 32 * nl_tpl_slots_ : nl_ell_slots_;
+  o.nl_layout = nonlocal_layout();
+  o.pcg_dynamic_units = cg_ndyn_;
+  for (int k = 0; k < 4; ++k) o.setup_s[k] = setup_s_[k];
+  return o;
 }
 
 Simulation::~Simulation() {
@@ -812,8 +840,13 @@ gf_step_stats Simulation::dynamic_step() {
   launch("integrate", 40 * n, [&] { launch_integrate(d_, dt, stream_); });  // B_int = 40n; no-op if not converged
   GF_CUDA(cudaMemcpyAsync(h_stats_, d_stats_, 48, cudaMemcpyDeviceToHost, stream_));  // cg_out, load, newly
   synchronize();
-  // SURVEY.md §8(d) B_CG = 12Z + 4(n+1) + 56n per PCG iteration (the reference's scalar-CSR SpMV + vectors)
-  const double cg_bytes_per_iter = 12 * Z + 4 * (n + 1) + 56 * n;
+  // PCG algorithmic bytes per iteration for THIS format: every stored upper block and slot word
+  // once, plus the vectors that leave the chip -- z gathered and written (24 B per node each) when the solver
+  // state stays on chip (one slice per warp); p, q, x, r, D^-1 traffic as well when it does not (large
+  // matrices). The reference's scalar-CSR model (SURVEY §8(d) B_CG = 12Z + 4(n+1) + 56n) is reported by bench.py
+  // next to it.
+  const double cg_bytes_per_iter = 72.0 * ((double)pat_.cols.size() + mesh_.nn) / 2.0 + 4.0 * 32.0 * (double)sell_slots_ +
+                                   (cg_ndyn_ ? 312.0 : 48.0) * mesh_.nn;
   auto account = [&](double iters) {
     if (profiling_) ktimes_["pcg"].bytes += iters * cg_bytes_per_iter;
   };
@@ -1078,6 +1111,49 @@ void Simulation::spmv(const double* x, double* y) {
   launch("spmv", 0.0, [&] { launch_spmv_sym(cg_, d_.z, d_.Ap, stream_); });
   GF_CUDA(cudaMemcpyAsync(y, d_.Ap, 8 * nd, cudaMemcpyDeviceToHost, stream_));
   synchronize();
+}
+
+// the production PCG (k_pcg_sell) on a caller-provided matrix with the mesh's pattern (scalar-CSR order, symmetric:
+// the upper blocks are stored, the lower ones implied) -- cg_solve (sparse.cpp:129-188) as a parity hook. Replaces
+// the simulation's current system; D^-1 from the diagonal as sparse.cpp:133-136.
+void Simulation::solve_system(const double* vals, const double* b, const double* x0, double tol, int32_t max_iters,
+                              double* x, gf_cg_result* res) {
+  if (max_iters < 0) throw FormatError("max_iters must be non-negative");
+  const size_t nd = 3 * (size_t)mesh_.nn;
+  std::vector<double> bv(bval_doubles_, 0.0), dinv(nd, 1.0);
+  for (int32_t i = 0; i < mesh_.nn; ++i) {
+    const int32_t r0 = pat_.row_ptr[i], deg = pat_.row_ptr[i + 1] - r0;
+    for (int32_t q = 0; q < deg; ++q) {
+      const int32_t j = pat_.cols[r0 + q];
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) {
+          const double v = vals[9 * (size_t)r0 + 3 * (size_t)a * deg + 3 * q + c];
+          if (j >= i) bv[sell_addr(usp_.data(), i, uslot_[r0 + q], 3 * a + c)] = v;
+          if (j == i && a == c) dinv[3 * (size_t)i + a] = std::fabs(v) > 1e-300 ? 1.0 / v : 1.0;
+        }
+    }
+  }
+  GF_CUDA(cudaMemcpyAsync(d_.bval, bv.data(), 8 * bv.size(), cudaMemcpyHostToDevice, stream_));
+  GF_CUDA(cudaMemcpyAsync(d_.dinv, dinv.data(), 8 * nd, cudaMemcpyHostToDevice, stream_));
+  GF_CUDA(cudaMemcpyAsync(d_.rhs, b, 8 * nd, cudaMemcpyHostToDevice, stream_));
+  if (x0) GF_CUDA(cudaMemcpyAsync(d_.x, x0, 8 * nd, cudaMemcpyHostToDevice, stream_));
+  else GF_CUDA(cudaMemsetAsync(d_.x, 0, 8 * nd, stream_));
+  const double tol0 = cg_.tol;
+  cg_.tol = tol;
+  cg_.x0_identity = 0;
+  try {
+    run_cg(max_iters);
+  } catch (...) {
+    cg_.tol = tol0;
+    throw;
+  }
+  cg_.tol = tol0;
+  GF_CUDA(cudaMemcpyAsync(x, d_.x, 8 * nd, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  res->iterations = (int32_t)h_stats_[0];
+  res->converged = h_stats_[1] != 0.0;
+  res->negative_curvature = h_stats_[2] != 0.0;
+  res->relative_residual = h_stats_[3];
 }
 
 double Simulation::reaction_load(const int32_t* nodes, int32_t n, const double axis[3]) {  // solver.cpp:335-340

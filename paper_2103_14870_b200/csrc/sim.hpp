@@ -55,6 +55,7 @@ class Simulation {
   void set_state(const double* u, const double* v, const uint8_t* zeta, const double* chi, const double* time,
                  bool async = false);
   void set_external_forces(const double* f3n);
+  gf_sim_info info() const;
   uint64_t pattern_hash() const { return hash_; }
   int32_t dof_count() const { return 3 * mesh_.nn; }
   int64_t broken_edge_count();
@@ -69,6 +70,8 @@ class Simulation {
   void eval_screening(double* screening, double* sigma_f6, uint8_t* degenerate);
   void last_system(double* vals, double* rhs);
   void spmv(const double* x, double* y);
+  void solve_system(const double* vals, const double* b, const double* x0, double tol, int32_t max_iters, double* x,
+                    gf_cg_result* res);
 
   // 0 off; 1 CUDA events around every kernel; 2 events around the PCG solve only (the dominant kernel), launch
   // counts and algorithmic bytes for all -- per-kernel events cost ~3 % of the step at c3
@@ -116,6 +119,8 @@ class Simulation {
   uint64_t hash_ = 0;
   int64_t nl_entries_ = 0;
   int64_t nl_tpl_slots_ = 0;
+  int64_t nl_ell_slots_ = 0;
+  double setup_s_[4] = {0, 0, 0, 0};
   double time_ = 0.0, last_load_ = 0.0;
   double newton_tol_ = 0.0, quasi_time_ = 0.0;
   double* d_usave_ = nullptr;    // line-search base displacements (quasi-static only, allocated on first use)
@@ -150,6 +155,8 @@ class Simulation {
   std::map<std::string, gf_kernel_time> ktimes_;
   cudaEvent_t timers_[8] = {};
 };
+
+double measure_bandwidth(int kind, int64_t bytes, int reps);
 
 void cg_solve_csr(int32_t n, const int32_t* row_ptr, const int32_t* cols, const double* vals, const double* b,
                   double* x, double tol, int32_t max_iters, gf_cg_result* res);

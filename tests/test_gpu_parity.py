@@ -11,7 +11,7 @@ import pytest
 import paper_2103_14870_b200 as g
 from paper_2103_14870_b200 import configs as cf
 from oracle import oracle as o
-from oracle.scenario import build_oracle
+from oracle.scenario import build_oracle, near_threshold_flips
 
 pytestmark = pytest.mark.gpu
 
@@ -118,6 +118,17 @@ def rel_err(a, b):
     return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300)
 
 
+ENTRY_FLOOR = 1e-6  # entries below 1e-6 of the array's largest are held to 1e-9 of that floor (absolute 1e-15 x max)
+
+
+def entry_err(a, b, floor=ENTRY_FLOOR):
+    """entrywise relative error: max |a - b| / max(|b|, floor * max|b|) -- every entry held to 1e-9 of itself, except
+    entries that are pure cancellation residue (below floor * max|b|), which are held to 1e-9 of that floor"""
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    ref = np.maximum(np.abs(b), floor * max(np.abs(b).max(), 1e-300))
+    return float((np.abs(a - b) / ref).max())
+
+
 @pytest.mark.parametrize("s", SMALL, ids=lambda s: s.name)
 @pytest.mark.parametrize("model", [0, 1])
 def test_forces_and_stiffness_within_1e9(s, model):
@@ -126,9 +137,9 @@ def test_forces_and_stiffness_within_1e9(s, model):
     gs, os_, gm, om = pair(s, rng, disp=0.2, chi_random=True)
     st = os_.get_state()
     f_ref = om.assemble_forces(os_.mat, st["u"], st["chi"])
-    assert rel_err(gs.eval_forces(), f_ref) < FORCE_TOL
+    assert entry_err(gs.eval_forces(), f_ref) < FORCE_TOL
     k_ref = om.assemble_stiffness(os_.mat, st["u"], st["chi"])
-    assert rel_err(gs.eval_stiffness(), k_ref) < FORCE_TOL
+    assert entry_err(gs.eval_stiffness(), k_ref) < FORCE_TOL
 
 
 @pytest.mark.parametrize("s", SMALL, ids=lambda s: s.name)
@@ -139,8 +150,8 @@ def test_system_matrix_and_rhs_within_1e9(s):
     gs.dynamic_step()
     a_ref, r_ref = os_.last_system()
     a_got, r_got = gs.last_system()
-    assert rel_err(a_got, a_ref) < FORCE_TOL
-    assert rel_err(r_got, r_ref) < FORCE_TOL
+    assert entry_err(a_got, a_ref) < FORCE_TOL
+    assert entry_err(r_got, r_ref) < FORCE_TOL
 
 
 def test_pattern_hash_matches():
@@ -203,7 +214,89 @@ def test_spmv_matches_oracle_multiply():
     a_ref, _ = os_.last_system()
     rp, cols, _ = om.pattern()
     x = rng.uniform(-1, 1, 3 * om.num_nodes)
-    assert rel_err(gs.spmv(x), o.spmv_csr(rp, cols, a_ref, x)) < FORCE_TOL
+    assert entry_err(gs.spmv(x), o.spmv_csr(rp, cols, a_ref, x)) < FORCE_TOL
+
+
+# ---------------------------------------------------------------- the production PCG (k_pcg_sell) on given systems
+def _pcg_setup(cells=(4, 4, 4)):
+    s = cf.scaled("c2", cells)
+    gs, os_, gm, om = pair(s)
+    rp, cols, _ = om.pattern()
+    rows = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
+    return gs, os_, om, np.asarray(rp), np.asarray(cols), rows
+
+
+def test_production_pcg_identity_system():  # test_sparse.cpp:20-32 on k_pcg_sell
+    gs, _, om, rp, cols, rows = _pcg_setup()
+    n = len(rp) - 1
+    vals = (rows == cols).astype(np.float64)
+    b = np.random.default_rng(71).uniform(-1, 1, n)
+    x, r = gs.solve_system(vals, b, tol=1e-12, max_iters=100)
+    xo, ro = o.cg_solve_csr(rp, cols, vals, b, np.zeros(n), 1e-12, 100)
+    assert r["converged"] and r["iterations"] == ro["iterations"] == 1 and not r["negative_curvature"]
+    assert np.array_equal(x, b) and np.array_equal(xo, b)
+
+
+def test_production_pcg_zero_rhs():  # sparse.cpp:145-150: b = 0 -> x = 0, converged, no iteration
+    gs, _, om, rp, cols, rows = _pcg_setup()
+    n = len(rp) - 1
+    vals = (rows == cols) * 2.0
+    x, r = gs.solve_system(vals, np.zeros(n), x0=np.ones(n), tol=1e-10, max_iters=50)
+    xo, ro = o.cg_solve_csr(rp, cols, vals, np.zeros(n), np.ones(n), 1e-10, 50)
+    assert r["converged"] and ro["converged"] and r["iterations"] == ro["iterations"] == 0
+    assert np.all(x == 0.0) and np.all(xo == 0.0)
+
+
+def test_production_pcg_negative_curvature():  # test_sparse.cpp:74-84 / sparse.cpp:160-168 on k_pcg_sell
+    gs, _, om, rp, cols, rows = _pcg_setup()
+    n = len(rp) - 1
+    d = np.where(np.arange(n) % 3 == 0, -1.0, 1.0)  # indefinite Jacobi-scaled system: p.Ap < 0 at the first step
+    vals = np.where(rows == cols, d[rows], 0.0)
+    b = np.where(np.arange(n) % 3 == 0, 1.0, 0.1)
+    x, r = gs.solve_system(vals, b, tol=1e-10, max_iters=50)
+    xo, ro = o.cg_solve_csr(rp, cols, vals, b, np.zeros(n), 1e-10, 50)
+    assert ro["negative_curvature"] and not ro["converged"]
+    assert r["negative_curvature"] and not r["converged"] and r["iterations"] == ro["iterations"] == 0
+    assert r["relative_residual"] == pytest.approx(ro["relative_residual"], rel=1e-12)
+
+
+def test_production_pcg_matches_oracle_on_the_step_system():
+    """the implicit-Euler system of a loaded step, random rhs, tight tolerance: same iteration count within 2, same
+    solution within 1e-9; the A-norm error of the production solver never grows (test_sparse.cpp:86-110)"""
+    gs, os_, om, rp, cols, rows = _pcg_setup((5, 4, 6))
+    rng = np.random.default_rng(72)
+    u = rng.uniform(-0.05 * cf.H, 0.05 * cf.H, (om.num_nodes, 3))
+    os_.set_state(u=u)
+    os_.dynamic_step()
+    A, _ = os_.last_system()
+    n = len(rp) - 1
+    b = rng.uniform(-1, 1, n)
+    x, r = gs.solve_system(A, b, tol=1e-13, max_iters=2000)
+    xo, ro = o.cg_solve_csr(rp, cols, A, b, np.zeros(n), 1e-13, 2000)
+    assert r["converged"] and ro["converged"] and abs(r["iterations"] - ro["iterations"]) <= 2
+    assert np.abs(x - xo).max() <= 1e-9 * np.abs(xo).max()
+    Ad = np.zeros((n, n))
+    Ad[rows, cols] = A
+    ex = np.linalg.solve(Ad, b)
+    prev = np.inf
+    for it in range(1, 30, 3):
+        xi, _ = gs.solve_system(A, b, tol=0.0, max_iters=it)
+        e = xi - ex
+        an = e @ Ad @ e
+        assert an <= prev * (1 + 1e-9) + 1e-30
+        prev = an
+
+
+def test_c4_physics_scaled_impact_breaks_edges_bit_exact():
+    """c4 physics (halfspace impact at 5 m/s) on 10^3 cells with sigma_thres lowered below the impact stress
+    (~rho c v = 66 MPa): the collider, relabel and chi run together; labels and newly-broken counts must match the
+    oracle every step, positions within 1e-6."""
+    s = cf.scaled("c4", (10, 10, 10), steps=25)
+    s.sigma_thres = 2.0e7
+    worst, resyncs, broken = run_pair(s, s.steps)
+    assert broken > 0, "the lowered threshold must break edges"
+    assert resyncs == 0
+    assert worst < TRAJ_TOL
 
 
 # ---------------------------------------------------------------- dynamics KATs (test_solver.cpp) on the GPU
@@ -297,21 +390,25 @@ def test_gpu_collider_load_matches_oracle():
 
 # ---------------------------------------------------------------- trajectories
 def run_pair(s, steps, resync_tol=1e-6):
-    """Step both paths; labels must agree (if a label differs, its screening value must sit within
-    resync_tol of the threshold — a legitimate roundoff flip — and the GPU is re-seeded from the oracle:
-    the 'label-sync' mode of SURVEY §7 hard part 7). Returns max relative position error and #resyncs."""
+    """Step both paths; labels must agree. A differing label is accepted only if the oracle's screening value of that
+    edge, from the pre-step state the damage pass saw, sits within resync_tol * sigma_thres of the threshold (a
+    legitimate roundoff flip); the GPU is then re-seeded from the oracle (the 'label-sync' mode of SURVEY §7 hard
+    part 7). Any other flip fails the test. Returns max relative position error, #resyncs and #broken edges."""
     gs, os_, gm, om = pair(s)
     X = om.arrays()["rest"]
     scale = np.abs(X).max()
     worst, resyncs, broken = 0.0, 0, 0
     for _ in range(steps):
+        u_pre = os_.get_state()["u"]
         os_.dynamic_step()
         gs.dynamic_step()
         ost, gst = os_.get_state(), gs.state()
         if not np.array_equal(gst.edge_damage, ost["zeta"]):
             diff = np.nonzero(gst.edge_damage != ost["zeta"])[0]
+            ok, dist = near_threshold_flips(om, os_.mat, u_pre, s.r_d, s.sigma_thres, diff, resync_tol)
+            assert ok, f"{len(diff)} label(s) differ, screening {dist:.3e} x sigma_thres from the threshold"
             resyncs += 1
-            assert resyncs <= 3, f"labels diverged at {len(diff)} edges"
+            assert resyncs <= 3, f"labels diverged {resyncs} times"
             gs.set_state(ost["u"], ost["v"], ost["zeta"], ost["chi"])
             continue
         worst = max(worst, np.abs(gst.displacements - ost["u"]).max() / scale)
@@ -711,15 +808,15 @@ def test_high_valence_rows_match_oracle(model):
     chi = rng.uniform(0.3, 1.0, len(tets))
     gs.set_state(displacements=u, element_chi=chi)
     os_.set_state(u=u, chi=chi)
-    assert rel_err(gs.eval_forces(), om.assemble_forces(os_.mat, u, chi)) < FORCE_TOL
-    assert rel_err(gs.eval_stiffness(), om.assemble_stiffness(os_.mat, u, chi)) < FORCE_TOL
+    assert entry_err(gs.eval_forces(), om.assemble_forces(os_.mat, u, chi)) < FORCE_TOL
+    assert entry_err(gs.eval_stiffness(), om.assemble_stiffness(os_.mat, u, chi)) < FORCE_TOL
     for _ in range(5):
         a = os_.dynamic_step()
         b = gs.dynamic_step()
         assert abs(a.cg_iterations - b.cg_iterations) <= 2
     a_ref, r_ref = os_.last_system()
     a_got, r_got = gs.last_system()
-    assert rel_err(a_got, a_ref) < FORCE_TOL and rel_err(r_got, r_ref) < FORCE_TOL
+    assert entry_err(a_got, a_ref) < FORCE_TOL and entry_err(r_got, r_ref) < FORCE_TOL
     assert np.abs(gs.state().displacements - os_.get_state()["u"]).max() / 0.1 < TRAJ_TOL
 
 

@@ -844,3 +844,43 @@ def test_quasi_static_pull_breaks_edges():  # test_solver.cpp:70-87
     for k in range(1, 11):
         last = s.quasi_static_step(k / 10)
     assert s.get_state()["zeta"].sum() > 0 and last.residual <= s.newton_tolerance()
+
+
+def test_backward_euler_energy_ratio_independent_dense():
+    """Independent check of the 0.9078 bound used above: numpy only -- the small-strain element stiffness
+    V [lambda g_a g_b^T + mu (g_a . g_b) I + mu g_b g_a^T] (= StVK's tangent at rest, test_fem.cpp:184-229), the
+    lumped mass rho V / 4 (fem.cpp:171-179), and the semi-implicit backward Euler of solver.cpp:275-297 with linear
+    forces, (M + dt^2 K) dv = -dt K u - dt^2 K v on the free dofs, integrated densely for 100 steps."""
+    m = o.Mesh.make_box((0.1, 0.05, 0.05), (4, 2, 2))
+    a = m.arrays()
+    X, tets, vol, binv = a["rest"], a["tets"], a["vol"], a["binv"].reshape(-1, 3, 3)
+    E, nu, rho, dt = 1e6, 0.3, 1000.0, 2e-5
+    mu, lam = E / (2 * (1 + nu)), E * nu / ((1 + nu) * (1 - 2 * nu))
+    n = 3 * len(X)
+    K = np.zeros((n, n))
+    M = np.zeros(n)
+    for e, t in enumerate(tets):
+        g = np.vstack([-binv[e].sum(0), binv[e]])  # rows: shape gradients of the 4 nodes (F = I + Du B^-1)
+        for i in range(4):
+            M[3 * t[i]:3 * t[i] + 3] += rho * vol[e] / 4
+            for j in range(4):
+                blk = lam * np.outer(g[i], g[j]) + mu * (g[i] @ g[j]) * np.eye(3) + mu * np.outer(g[j], g[i])
+                K[3 * t[i]:3 * t[i] + 3, 3 * t[j]:3 * t[j] + 3] += vol[e] * blk
+    free = np.ones(n, bool)
+    for node in np.nonzero(X[:, 0] <= 1e-9)[0]:
+        free[3 * node:3 * node + 3] = False
+    Kf, Mf = K[np.ix_(free, free)], M[free]
+    u = np.zeros((len(X), 3))
+    u[:, 0] = 1e-4 * X[:, 0]
+    u = u.reshape(-1)[free]
+    v = np.zeros_like(u)
+    A = np.diag(Mf) + dt * dt * Kf
+    energy = lambda: 0.5 * u @ Kf @ u + 0.5 * v @ (Mf * v)
+    e0 = prev = energy()
+    for _ in range(100):
+        v = v + np.linalg.solve(A, -dt * (Kf @ u) - dt * dt * (Kf @ v))
+        u = u + dt * v
+        e = energy()
+        assert e <= prev * (1 + 1e-12)
+        prev = e
+    assert prev / e0 == pytest.approx(0.9078, abs=0.002)
