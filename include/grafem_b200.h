@@ -173,8 +173,17 @@ double gf_sim_last_collider_load(const gf_sim* s);             /* solver.hpp:87 
 int gf_sim_mass(const gf_sim* s, double* mass3n);              /* Simulation::mass (solver.hpp:82) */
 /* Simulation::reaction_load (solver.cpp:335-340) */
 int gf_sim_reaction_load(gf_sim* s, const int32_t* nodes, int32_t n_nodes, const double axis[3], double* out);
-/* total_strain_energy (fem.cpp:190-199) + kinetic_energy (fem.cpp:201-206) of the current state */
+/* total_strain_energy (fem.cpp:190-199) + kinetic_energy (fem.cpp:201-206) of the current state (device reductions) */
 int gf_sim_energies(gf_sim* s, double* strain, double* kinetic);
+/* the run loop's per-step row and damage-log statistics (run_scenario make_row / log_damage, scenario.cpp:640-672)
+ * of the current state, computed on the device and read back as one record */
+typedef struct {
+  double strain_energy, kinetic_energy; /* total_strain_energy (fem.cpp:190-199), kinetic_energy (fem.cpp:201-206) */
+  double chi_min, chi_mean;             /* log_damage's chi_min / chi_mean */
+  int64_t broken_edges;                 /* SimState::broken_edge_count */
+  double time;
+} gf_step_metrics;
+int gf_sim_step_metrics(gf_sim* s, gf_step_metrics* out);
 
 /* ---------------------------------------------------------------- parity / microbench hooks */
 int gf_sim_eval_forces(gf_sim* s, double* f3n);      /* assemble_forces (fem.cpp:96-108) */
@@ -186,6 +195,16 @@ int gf_sim_eval_screening(gf_sim* s, double* screening, double* sigma_f6, uint8_
 int gf_sim_last_system(gf_sim* s, double* vals, double* rhs);
 /* y = A x with the current system matrix (FixedPatternSparse::multiply, sparse.cpp:49-60) */
 int gf_sim_spmv(gf_sim* s, const double* x, double* y);
+/* edge_decomposed_forces (fem.cpp:57-94) of every tet on the current state, from the edge-length element kernel:
+ * coeff6[6 t + k] = magnitude of local edge k's force (f_i = sum_k c_k s_ik dir_k, s = +1 where the edge leaves node
+ * i; rest volume, no chi -- the reference's convention), ok[t] = 0 on a current edge shorter than 1e-14 or a
+ * degenerate (det C <= 0) element. */
+int gf_sim_edge_forces(gf_sim* s, double* coeff6, uint8_t* ok);
+/* element form of the assembly: 0 = F-based closed-form rows, 1 = edge-length form (GF_ELEMENT=edge at create) */
+int32_t gf_sim_element_form(const gf_sim* s);
+/* total_strain_energy (fem.cpp:190-199) of the state the last assembly evaluated (the step-start state of the last
+ * dynamic_step), the fused by-product of the edge-length kernel (GF_FORMAT_ERROR for the F-based form) */
+int gf_sim_assembly_energy(gf_sim* s, double* energy);
 /* cg_solve (sparse.cpp:129-188) with the PRODUCTION solver (the persistent PCG on the symmetric SELL-32 matrix) on a
  * caller-provided matrix with this simulation's pattern: vals in the scalar-CSR order of gf_sim_eval_stiffness,
  * symmetric (the upper blocks are used); x0 NULL = zero guess. Replaces the simulation's current system. */

@@ -601,6 +601,113 @@ static NodalForces element_internal_force(const Mesh& m, const State& s, const M
   return forces_from_gradient(g);
 }
 
+// pinv_small (sparse.cpp:190-204): pseudo-inverse through an SVD with the 1e-12 * sigma_max cutoff. Eigen's JacobiSVD
+// is restated as a one-sided (Hestenes) Jacobi SVD: column pairs of A (m x n, m >= n) are rotated until mutually
+// orthogonal, V accumulates the rotations, sigma_j = |a_j|, U = a_j / sigma_j. Bits may differ from Eigen's two-sided
+// sweep; the reference pins this path to tolerance only (test_fem.cpp:98-139: 1e-8, 1e-12).
+static std::vector<double> pinv_small(const std::vector<double>& a_in, int m, int n, bool* rank_deficient) {
+  std::vector<double> a(a_in), v((size_t)n * n, 0.0);  // a row-major m x n
+  for (int j = 0; j < n; ++j) v[(size_t)j * n + j] = 1.0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        double alpha = 0.0, beta = 0.0, gamma = 0.0;
+        for (int i = 0; i < m; ++i) {
+          const double ap = a[(size_t)i * n + p], aq = a[(size_t)i * n + q];
+          alpha += ap * ap;
+          beta += aq * aq;
+          gamma += ap * aq;
+        }
+        if (gamma == 0.0) continue;
+        off = std::max(off, std::abs(gamma) / std::sqrt(alpha * beta));
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+        for (int i = 0; i < m; ++i) {
+          const double ap = a[(size_t)i * n + p], aq = a[(size_t)i * n + q];
+          a[(size_t)i * n + p] = c * ap - sn * aq;
+          a[(size_t)i * n + q] = sn * ap + c * aq;
+        }
+        for (int i = 0; i < n; ++i) {
+          const double vp = v[(size_t)i * n + p], vq = v[(size_t)i * n + q];
+          v[(size_t)i * n + p] = c * vp - sn * vq;
+          v[(size_t)i * n + q] = sn * vp + c * vq;
+        }
+      }
+    if (off < 1e-15) break;
+  }
+  std::vector<double> sig(n);
+  double smax = 0.0;
+  for (int j = 0; j < n; ++j) {
+    double ss = 0.0;
+    for (int i = 0; i < m; ++i) ss += a[(size_t)i * n + j] * a[(size_t)i * n + j];
+    sig[j] = std::sqrt(ss);
+    smax = std::max(smax, sig[j]);
+  }
+  const double cutoff = 1e-12 * smax;
+  int rank = 0;
+  std::vector<double> out((size_t)n * m, 0.0);  // n x m
+  for (int j = 0; j < n; ++j) {
+    if (!(sig[j] > cutoff && sig[j] > 0.0)) continue;
+    ++rank;
+    for (int r = 0; r < n; ++r)
+      for (int i = 0; i < m; ++i) out[(size_t)r * m + i] += v[(size_t)r * n + j] * (a[(size_t)i * n + j] / sig[j]) / sig[j];
+  }
+  if (rank_deficient) *rank_deficient = rank < std::min(m, n);
+  return out;
+}
+
+struct EdgeDecomposition {  // EdgeForceDecomposition (fem.hpp:44-48)
+  std::array<double, 6> coeff{};
+  double residual = 0.0;
+  bool ok = false;
+};
+
+// edge_decomposed_forces (fem.cpp:57-94): least-squares edge-force magnitudes of the element's nodal forces (rest
+// volume, no chi), f_i = sum_k c_k s_ik dir_k (s = +1 where the edge leaves node i); ok = false on a current edge
+// shorter than 1e-14 or a rank-deficient system
+static EdgeDecomposition edge_decomposed_forces(const Mesh& m, const State& s, const Material& p, int tet) {
+  EdgeDecomposition out;
+  const auto& t = m.tets[tet];
+  const M3 F = deformation_gradient(m, s.u, tet);
+  const M3 g = prod_r1_bt(scale3(m.vol[tet], pk1(F, p)), m.binv[tet]);
+  const NodalForces f = forces_from_gradient(g);
+  std::array<V3, 6> dir;
+  for (int k = 0; k < 6; ++k) {
+    const int a = kLocalEdges[k][0], b = kLocalEdges[k][1];
+    const V3 xa = add3(m.X[t[a]], s.u[t[a]]), xb = add3(m.X[t[b]], s.u[t[b]]);
+    const V3 d = sub3(xb, xa);
+    const double len = std::sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+    if (len < 1e-14) return out;
+    dir[k] = {d[0] / len, d[1] / len, d[2] / len};
+  }
+  std::vector<double> A(12 * 6, 0.0), b(12);
+  for (int i = 0; i < 4; ++i)
+    for (int a = 0; a < 3; ++a) b[3 * i + a] = f[i][a];
+  for (int k = 0; k < 6; ++k)
+    for (int a = 0; a < 3; ++a) {
+      A[(size_t)(3 * kLocalEdges[k][0] + a) * 6 + k] = dir[k][a];
+      A[(size_t)(3 * kLocalEdges[k][1] + a) * 6 + k] = -dir[k][a];
+    }
+  bool deficient = false;
+  const std::vector<double> Ai = pinv_small(A, 12, 6, &deficient);
+  double res = 0.0;
+  for (int k = 0; k < 6; ++k) {
+    double c = 0.0;
+    for (int i = 0; i < 12; ++i) c += Ai[(size_t)k * 12 + i] * b[i];
+    out.coeff[k] = c;
+  }
+  for (int i = 0; i < 12; ++i) {
+    double r = -b[i];
+    for (int k = 0; k < 6; ++k) r += A[(size_t)i * 6 + k] * out.coeff[k];
+    res += r * r;
+  }
+  out.residual = std::sqrt(res);
+  out.ok = !deficient;
+  return out;
+}
+
 static std::vector<double> assemble_forces(const Mesh& m, const State& s, const Material& p) {  // fem.cpp:96-108
   const int nt = m.nt();
   std::vector<NodalForces> per(nt);
@@ -1639,6 +1746,14 @@ void or_element_internal_force(const or_mesh* m, const double* u, const double* 
   const auto nf = element_internal_force(m->m, s, mat_from(p), tet);
   for (int i = 0; i < 4; ++i)
     for (int a = 0; a < 3; ++a) f[3 * i + a] = nf[i][a];
+}
+int or_edge_decomposed_forces(const or_mesh* m, const double* u, const or_material* p, int32_t tet, double coeff[6],
+                              double* residual) {
+  const State s = state_from(m->m, u, nullptr);
+  const EdgeDecomposition d = edge_decomposed_forces(m->m, s, mat_from(p), tet);
+  for (int k = 0; k < 6; ++k) coeff[k] = d.coeff[k];
+  if (residual) *residual = d.residual;
+  return d.ok ? 1 : 0;
 }
 void or_element_stiffness(const or_mesh* m, const double* u, const double* chi, const or_material* p,
                           int32_t tet, double k[144]) {

@@ -106,6 +106,9 @@ int or_cauchy_sixvector(const double F[9], const or_material* p, double out[6]);
 void or_deformation_gradient(const or_mesh* m, const double* u, int32_t tet, double F[9]);
 void or_element_internal_force(const or_mesh* m, const double* u, const double* chi, const or_material* p,
                                int32_t tet, double f[12]);
+/* edge_decomposed_forces (fem.cpp:57-94): returns ok (1/0); coeff[6], residual */
+int or_edge_decomposed_forces(const or_mesh* m, const double* u, const or_material* p, int32_t tet, double coeff[6],
+                              double* residual);
 void or_element_stiffness(const or_mesh* m, const double* u, const double* chi, const or_material* p,
                           int32_t tet, double k[144]);
 void or_assemble_forces(const or_mesh* m, const double* u, const double* chi, const or_material* p, double* f);

@@ -256,6 +256,14 @@ class Mesh:
         lib().or_element_internal_force(self._h, pu, pc, C.byref(mat), C.c_int32(tet), _p(f, F64P))
         return f
 
+    def edge_decomposed_forces(self, mat, tet, u=None):
+        """edge_decomposed_forces (fem.cpp:57-94): (coeff[6], residual, ok)"""
+        (u, pu), _ = self._uchi(u, None)
+        c = np.zeros(6)
+        r = C.c_double()
+        ok = lib().or_edge_decomposed_forces(self._h, pu, C.byref(mat), C.c_int32(tet), _p(c, F64P), C.byref(r))
+        return c, r.value, bool(ok)
+
     def element_stiffness(self, mat, tet, u=None, chi=None):
         (u, pu), (chi, pc) = self._uchi(u, chi)
         k = np.zeros((12, 12))

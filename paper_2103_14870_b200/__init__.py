@@ -102,6 +102,12 @@ class _SimInfo(C.Structure):
                 ("pcg_dynamic_units", C.c_int32), ("setup_s", C.c_double * 4)]
 
 
+class StepMetrics(C.Structure):
+    """gf_step_metrics: run_scenario's make_row + log_damage values (scenario.cpp:640-672), device reductions"""
+    _fields_ = [("strain_energy", C.c_double), ("kinetic_energy", C.c_double), ("chi_min", C.c_double),
+                ("chi_mean", C.c_double), ("broken_edges", C.c_int64), ("time", C.c_double)]
+
+
 class KernelTime(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("total_ms", C.c_double), ("bytes", C.c_double)]
 
@@ -523,6 +529,11 @@ class Simulation:
         _check(lib().gf_sim_energies(self._h, C.byref(s), C.byref(k)))
         return s.value, k.value
 
+    def step_metrics(self) -> StepMetrics:
+        m = StepMetrics()
+        _check(lib().gf_sim_step_metrics(self._h, C.byref(m)))
+        return m
+
     # parity / microbench hooks
     def eval_forces(self) -> np.ndarray:
         f = np.zeros(3 * self.N)
@@ -555,6 +566,20 @@ class Simulation:
         y = np.zeros(3 * self.N)
         _check(lib().gf_sim_spmv(self._h, px, _p(y, F64P)))
         return y
+
+    def edge_forces(self):
+        """edge_decomposed_forces (fem.cpp:57-94) of every tet: (coeff[T, 6], ok[T])"""
+        c, ok = np.zeros((self.T, 6)), np.zeros(self.T, np.uint8)
+        _check(lib().gf_sim_edge_forces(self._h, _p(c, F64P), _p(ok, U8P)))
+        return c, ok.astype(bool)
+
+    def element_form(self) -> str:
+        return "edge" if lib().gf_sim_element_form(self._h) else "F"
+
+    def assembly_energy(self) -> float:
+        e = C.c_double()
+        _check(lib().gf_sim_assembly_energy(self._h, C.byref(e)))
+        return e.value
 
     def solve_system(self, vals, b, x0=None, tol=1e-8, max_iters=4000):
         """The production PCG (k_pcg_sell) on a symmetric matrix with this simulation's pattern (scalar-CSR values

@@ -28,6 +28,7 @@ CU_SOURCES = {  # file -> extra flags
     "cg_sell.cu": [],
     "sim.cu": [],
     "probe.cu": [],
+    "metrics.cu": [],
 }
 CPP_SOURCES = ["host_mesh.cpp", "host_viz.cpp", "capi.cpp"]
 

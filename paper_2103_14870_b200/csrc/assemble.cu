@@ -129,6 +129,143 @@ __device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, i
   }
 }
 
+// ---------------------------------------------------------------- edge-length form (north_star (1))
+// The element's energy as a function of its six squared edge lengths l2_k: C = I + 2E with
+//   2E = sum_k dl2_k N_k,  N_k = -sym(g_a x g_b)  (edge k = (a, b), g = shape gradients from B^-1),
+// the polarization identity G_ij = (l2_0i + l2_0j - l2_ij) / 2 pushed through C = B^-T G B^-1. dl2_k = l2_k - L2_k is
+// formed cancellation-free as (u_b - u_a).(2 (X_b - X_a) + (u_b - u_a)), so a rest state has E = 0 exactly. Then
+//   t_k = dPsi/dl2_k = -1/2 g_a^T S g_b                (S = 2 dPsi/dC)
+//   M_kk' = d2Psi/dl2_k dl2_k' = N_k : (d2Psi/dC2) : N_k', in Gram form over the rest gradients
+//     gamma_ab = g_a.g_b and eta_ab = g_a^T C^-1 g_b (stable NH) -- see k_tet_edge;
+//   forces  f_n  = -chi V sum_k t_k 2 s_nk d_k            (d_k current edge vector, s_nk = +1 / -1 at b / a)
+//   Hessian K_nm = chi V [sum_kk' M_kk' 4 s_nk s_mk' d_k d_k'^T + sum_k 2 t_k s_nk s_mk I].
+// Stable NH needs the SIGNED J: J = sign(det[d_01 d_02 d_03]) sqrt(det C) (edge lengths alone give |J|).
+// k_tet_edge evaluates t (6) and M (21) once per tet into a 224-byte record (x chi V) plus the tet's energy
+// (deterministic reduction); the row kernel expands each incident tet's record with the current edge vectors.
+// local edge k = (kEA(k), kEB(k)): 01 02 03 12 13 23 (mesh.hpp:41-42)
+__host__ __device__ constexpr int kEA(int k) { return k < 3 ? 0 : (k < 5 ? 1 : 2); }
+__host__ __device__ constexpr int kEB(int k) { return k < 3 ? k + 1 : (k == 3 ? 2 : 3); }
+constexpr int kRec = 28;  // t[6], packed M[21], fallback slot
+__host__ __device__ constexpr int pidx(int k, int kp) {
+  return k <= kp ? k * 6 - k * (k - 1) / 2 + (kp - k) : kp * 6 - kp * (kp - 1) / 2 + (k - kp);
+}
+__host__ __device__ constexpr int er(int q) { return q < 3 ? q : (q == 5 ? 1 : 0); }  // E entries 00 11 22 01 02 12
+__host__ __device__ constexpr int ec(int q) { return q < 3 ? q : (q == 3 ? 1 : 2); }
+__host__ __device__ constexpr int sgn(int n, int k) { return n == kEB(k) ? 1 : (n == kEA(k) ? -1 : 0); }
+
+// one lane's contribution of an edge-record tet to node row li: force on li, diagonal block, the three
+// off-diagonal blocks into shared memory (slot lj < li ? lj : lj - 1)
+template <bool kBlocks>
+__device__ __forceinline__ void element_row_edge(const DevData& d, int e, int4 t, int li, double f[3], double* blk,
+                                                 double dg[9]) {
+  const int id[4] = {t.x, t.y, t.z, t.w};
+  double x[4][3];
+#pragma unroll
+  for (int n = 0; n < 4; ++n)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) x[n][a] = __ldg(d.X + 3 * (size_t)id[n] + a) + __ldg(d.u + 3 * (size_t)id[n] + a);
+  double dc[6][3], sk[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) dc[k][a] = x[kEB(k)][a] - x[kEA(k)][a];
+    sk[k] = (li == kEB(k)) ? 1.0 : (li == kEA(k)) ? -1.0 : 0.0;
+  }
+  const double* rec = d.erec + (size_t)kRec * e;
+  double tau[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) tau[k] = __ldg(rec + k);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) acc = fma(sk[k] * tau[k], dc[k][a], acc);
+    f[a] = -2.0 * acc;
+  }
+  if (!kBlocks) return;
+  double y[6][3];
+#pragma unroll
+  for (int kp = 0; kp < 6; ++kp)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) y[kp][a] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k)
+#pragma unroll
+    for (int kp = k; kp < 6; ++kp) {
+      const double mkk = 4.0 * __ldg(rec + 6 + pidx(k, kp));
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        y[kp][a] = fma(sk[k] * mkk, dc[k][a], y[kp][a]);
+        if (kp != k) y[k][a] = fma(sk[kp] * mkk, dc[kp][a], y[k][a]);
+      }
+    }
+#pragma unroll
+  for (int lj = 0; lj < 4; ++lj) {
+    double ci = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+      if (sgn(lj, k) != 0) ci = fma(2.0 * sgn(lj, k) * sk[k], tau[k], ci);
+    double K[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double v = r == c ? ci : 0.0;
+#pragma unroll
+        for (int kp = 0; kp < 6; ++kp)
+          if (sgn(lj, kp) != 0) v = fma((double)sgn(lj, kp) * y[kp][r], dc[kp][c], v);
+        K[3 * r + c] = v;
+      }
+    if (lj == li) {
+#pragma unroll
+      for (int q = 0; q < 9; ++q) dg[q] = K[q];
+    } else {
+      double* o = blk + 9 * (lj < li ? lj : lj - 1);
+#pragma unroll
+      for (int q = 0; q < 9; ++q) o[q] = K[q];
+    }
+  }
+}
+
+// lane work of the row kernels: tet e's contribution to node row li (F-based closed form or edge record)
+template <bool kEdge, bool kBlocks>
+__device__ __forceinline__ void lane_element(const DevData& d, const MatDev& m, int e, int4 t, int li, double f[3],
+                                             double* blk, double dg[9]) {
+  if (kEdge) {
+    const uint8_t fl = __ldg(d.eflag + e);
+    if (fl == 0) {
+      element_row_edge<kBlocks>(d, e, t, li, f, blk, dg);
+      return;
+    }
+    if (fl == 1) {  // degenerate for the edge form: the F-based rows precomputed by k_tet_edge_fallback
+      const int slot = (int)__ldg(d.erec + (size_t)kRec * e + 27);
+      const double* r = d.efall + ((size_t)slot * 4 + li) * 39;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) f[a] = r[a];
+      if (kBlocks) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) dg[q] = r[3 + q];
+#pragma unroll
+        for (int q = 0; q < 27; ++q) blk[q] = r[12 + q];
+      }
+      return;
+    }
+    if (kBlocks)  // chi V = 0 (fem.cpp:51 / fem.cpp:114)
+#pragma unroll
+      for (int r = 0; r < 27; ++r) blk[r] = 0.0;
+    return;
+  }
+  double B[9], vol;
+  load_rest(d, e, B, vol);
+  const double scale = d.chi[e] * vol;
+  if (scale != 0.0) {  // fem.cpp:51 / fem.cpp:114 early-out
+    element_row<kBlocks>(d, m, t, B, li, scale, f, blk, dg);
+  } else if (kBlocks) {
+#pragma unroll
+    for (int r = 0; r < 27; ++r) blk[r] = 0.0;
+  }
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -246,7 +383,7 @@ __device__ __forceinline__ void finish_row(const DevData& d, const StepCoeffs& s
 #ifndef GF_ASM_MINB
 #define GF_ASM_MINB 4
 #endif
-template <int kMode>
+template <int kMode, bool kEdge>
 __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d, MatDev m, StepCoeffs sc) {
   constexpr bool kBlocks = kMode != kAssembleForcesOnly;
   extern __shared__ double s_dyn[];  // kBlocks: s_blk[kWarps][32 * 27 + 9] (dynamic: > 48 KB static limit)
@@ -266,16 +403,8 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
     const int e = __ldg(d.nt_tet + p0 + lane);
     const int4 t = __ldg(d.tets + e);
     const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
-    double B[9], vol;
-    load_rest(d, e, B, vol);
-    const double scale = d.chi[e] * vol;
     double* blk = kBlocks ? &s_blk[w][27 * lane] : nullptr;
-    if (scale != 0.0) {  // fem.cpp:51 / fem.cpp:114 early-out
-      element_row<kBlocks>(d, m, t, B, li, scale, f, blk, dg);
-    } else if (kBlocks) {
-#pragma unroll
-      for (int r = 0; r < 27; ++r) blk[r] = 0.0;
-    }
+    lane_element<kEdge, kBlocks>(d, m, e, t, li, f, blk, dg);
   }
   // the row's force (fem.cpp:104-106) and its diagonal block (every incident tet contributes) are fixed
   // butterfly sums over the lanes; only the off-diagonal blocks (the ~5 tets around each edge) go through
@@ -334,7 +463,7 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
 // shared memory and every output adds the items of its (padded, ascending) list that fall in the chunk; forces
 // and diagonal blocks accumulate per lane across chunks, then one butterfly. Items are 3 l + s (l < 85), 255 pads.
 constexpr int kBigDeg = 64;
-template <int kMode>
+template <int kMode, bool kEdge>
 __global__ void __launch_bounds__(32 * kWarps) k_assemble_big(DevData d, MatDev m, StepCoeffs sc) {
   constexpr bool kBlocks = kMode != kAssembleForcesOnly;
   extern __shared__ double s_dyn[];
@@ -365,13 +494,8 @@ __global__ void __launch_bounds__(32 * kWarps) k_assemble_big(DevData d, MatDev 
       const int e = __ldg(d.nt_tet + p0 + l);
       const int4 t = __ldg(d.tets + e);
       const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
-      double B[9], vol;
-      load_rest(d, e, B, vol);
-      const double scale = d.chi[e] * vol;
-      if (scale != 0.0) {
-        element_row<kBlocks>(d, m, t, B, li, scale, f, blk, dg);
-        wrote = true;
-      }
+      lane_element<kEdge, kBlocks>(d, m, e, t, li, f, blk, dg);
+      wrote = true;
     }
     if (kBlocks && !wrote)
 #pragma unroll
@@ -434,79 +558,272 @@ __global__ void __launch_bounds__(32 * kWarps) k_assemble_big(DevData d, MatDev 
   finish_row<kMode>(d, sc, i, lane, fsum, fixed_i, kv[lane < 3 ? lane : 0], corr[lane < 3 ? lane : 0]);
 }
 
-// per-tet strain energy chi*V*Psi(F) (fem.cpp:190-199), block partial sums (deterministic order)
-__global__ void __launch_bounds__(256) k_energy(DevData d, MatDev m, double* partials) {
-  __shared__ double s[256];
-  double acc = 0.0;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d.nt; e += gridDim.x * blockDim.x) {
-    double B[9], vol;
-    load_rest(d, e, B, vol);
-    const double scale = d.chi[e] * vol;
-    if (scale == 0.0) continue;
-    const int4 t = d.tets[e];
-    const int id[4] = {t.x, t.y, t.z, t.w};
-    double du[9], F[9];
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int r = 0; r < 3; ++r) du[3 * r + c] = d.u[3 * (size_t)id[c + 1] + r] - d.u[3 * (size_t)id[0] + r];
-    def_grad(du, B, F);
-    double psi;
-    if (m.model == 1) {
-      double Cm[9];
-      for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) Cm[3 * r + c] = F[r] * F[c] + F[3 + r] * F[3 + c] + F[6 + r] * F[6 + c];
-      const double ic = Cm[0] + Cm[4] + Cm[8];
-      double iic = 0.0;
-      for (int q = 0; q < 9; ++q) iic += Cm[q] * Cm[q];
-      psi = 0.125 * m.lambda * (ic - 3.0) * (ic - 3.0) + 0.25 * m.mu * (iic - 2.0 * ic + 3.0);
-    } else {
-      const double ic = sqnorm9(F);
-      const double j = det3(F);
-      psi = 0.5 * m.mu * (ic - 3.0) + 0.5 * m.lambda * (j - m.alpha_nh) * (j - m.alpha_nh) - 0.5 * m.mu * log(ic + 1.0);
-    }
-    acc += scale * psi;
-  }
-  s[threadIdx.x] = acc;
+// ---------------------------------------------------------------- per-tet edge-length kernel
+constexpr int kTetTpb = 256;
+__device__ __forceinline__ double block_sum256(double v, double* sm) {
+  sm[threadIdx.x] = v;
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+  for (int o = kTetTpb / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) partials[blockIdx.x] = s[0];
+  return sm[0];
+}
+
+// mode 0: per-tet record (chi V t, chi V M) for the row kernel + the tet energies chi V Psi summed into
+//         *d.eng_out (deterministic: block tree, then the last block sums the block partials in block order);
+//         tets the edge form cannot evaluate (stable NH with det C <= 1e-12: J -> 0, C^-1 unbounded) are listed for
+//         k_tet_edge_fallback (F-based rows); chi V = 0 tets are flagged and skipped (fem.cpp:51, 114, 194).
+// mode 1: edge_decomposed_forces (fem.cpp:57-94) -- c_k = 2 V t_k |d_k| (rest volume, no chi: the reference's
+//         convention); ok = 0 on a current edge shorter than 1e-14 or det C <= 0.
+__global__ void __launch_bounds__(kTetTpb) k_tet_edge(DevData d, MatDev m, int mode) {
+  __shared__ double s_red[kTetTpb];
+  __shared__ bool s_last;
+  const int e = blockIdx.x * kTetTpb + threadIdx.x;
+  double energy = 0.0;
+  if (e < d.nt) {
+    const int4 t = __ldg(d.tets + e);
+    const int id[4] = {t.x, t.y, t.z, t.w};
+    double B[9], vol;
+    load_rest(d, e, B, vol);
+    const double scale = mode == 0 ? d.chi[e] * vol : vol;
+    if (mode == 0 && scale == 0.0) {
+      d.eflag[e] = 2;
+    } else {
+      double X[4][3], U[4][3];
+#pragma unroll
+      for (int n = 0; n < 4; ++n)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          X[n][a] = __ldg(d.X + 3 * (size_t)id[n] + a);
+          U[n][a] = __ldg(d.u + 3 * (size_t)id[n] + a);
+        }
+      double g[4][3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        g[1][a] = B[a];
+        g[2][a] = B[3 + a];
+        g[3][a] = B[6 + a];
+        g[0][a] = -((B[a] + B[3 + a]) + B[6 + a]);
+      }
+      double dl2[6], len[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        double q = 0.0, l2 = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double D = X[kEB(k)][a] - X[kEA(k)][a], del = U[kEB(k)][a] - U[kEA(k)][a];
+          q = fma(del, 2.0 * D + del, q);
+          l2 = fma(D + del, D + del, l2);
+        }
+        dl2[k] = q;
+        len[k] = sqrt(l2);
+      }
+      // E = -1/4 sum_k dl2_k (g_a g_b^T + g_b g_a^T): entries 00 11 22 01 02 12
+      
+      double E[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+          acc = fma(dl2[k], g[kEA(k)][er(q)] * g[kEB(k)][ec(q)] + g[kEB(k)][er(q)] * g[kEA(k)][ec(q)], acc);
+        E[q] = -0.25 * acc;
+      }
+      double gam[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = a; b < 4; ++b) {
+          gam[a][b] = g[a][0] * g[b][0] + g[a][1] * g[b][1] + g[a][2] * g[b][2];
+          gam[b][a] = gam[a][b];
+        }
+      const double trE = E[0] + E[1] + E[2];
+      double tk[6], Mk[21];
+      bool ok = true;
+      double psi = 0.0;
+      if (m.model == 1) {  // StVK: Psi = lambda/2 tr(E)^2 + mu E:E, S = lambda tr(E) I + 2 mu E
+        psi = 0.5 * m.lambda * trE * trE +
+              m.mu * ((E[0] * E[0] + E[1] * E[1] + E[2] * E[2]) + 2.0 * (E[3] * E[3] + E[4] * E[4] + E[5] * E[5]));
+        const double S[9] = {m.lambda * trE + 2.0 * m.mu * E[0], 2.0 * m.mu * E[3], 2.0 * m.mu * E[4],
+                             2.0 * m.mu * E[3], m.lambda * trE + 2.0 * m.mu * E[1], 2.0 * m.mu * E[5],
+                             2.0 * m.mu * E[4], 2.0 * m.mu * E[5], m.lambda * trE + 2.0 * m.mu * E[2]};
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          const int a = kEA(k), b = kEB(k);
+          double v = 0.0;
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+            v = fma(g[a][r], S[3 * r] * g[b][0] + S[3 * r + 1] * g[b][1] + S[3 * r + 2] * g[b][2], v);
+          tk[k] = -0.5 * v;
+        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+#pragma unroll
+          for (int kp = k; kp < 6; ++kp) {
+            const int a = kEA(k), b = kEB(k), c = kEA(kp), dd = kEB(kp);
+            Mk[pidx(k, kp)] = 0.25 * m.lambda * gam[a][b] * gam[c][dd] +
+                              0.25 * m.mu * (gam[a][c] * gam[b][dd] + gam[a][dd] * gam[b][c]);
+          }
+      } else {  // stable NH: S = mu (1 - 1/(I_C + 1)) I + lambda (J - alpha) J C^-1
+        const double C[9] = {1.0 + 2.0 * E[0], 2.0 * E[3], 2.0 * E[4], 2.0 * E[3], 1.0 + 2.0 * E[1], 2.0 * E[5],
+                             2.0 * E[4], 2.0 * E[5], 1.0 + 2.0 * E[2]};
+        const double detC = det3(C);
+        ok = detC > 1e-12;
+        if (ok) {
+          double dcur[3][3];  // current edge vectors 01, 02, 03 (columns) for the orientation sign
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) dcur[a][c] = (X[c + 1][a] + U[c + 1][a]) - (X[0][a] + U[0][a]);
+          const double ds[9] = {dcur[0][0], dcur[0][1], dcur[0][2], dcur[1][0], dcur[1][1], dcur[1][2],
+                                dcur[2][0], dcur[2][1], dcur[2][2]};
+          const double J = (det3(ds) < 0.0 ? -1.0 : 1.0) * sqrt(detC);
+          double Ci[9];
+          cofactor(C, Ci);  // C symmetric: adj(C) = cof(C)^T = cof(C)
+          const double inv = 1.0 / detC;
+#pragma unroll
+          for (int q = 0; q < 9; ++q) Ci[q] *= inv;
+          const double ic = 3.0 + 2.0 * trE, ip1 = ic + 1.0;
+          const double jm = J - m.alpha_nh;
+          psi = m.mu * trE + 0.5 * m.lambda * jm * jm - 0.5 * m.mu * log(ip1);
+          const double c1 = m.mu * (1.0 - 1.0 / ip1), c2 = m.lambda * jm * J;
+          double eta[4][4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            double h[3];
+#pragma unroll
+            for (int r = 0; r < 3; ++r) h[r] = Ci[3 * r] * g[a][0] + Ci[3 * r + 1] * g[a][1] + Ci[3 * r + 2] * g[a][2];
+#pragma unroll
+            for (int b = a; b < 4; ++b) {
+              eta[a][b] = h[0] * g[b][0] + h[1] * g[b][1] + h[2] * g[b][2];
+              eta[b][a] = eta[a][b];
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 6; ++k) tk[k] = -0.5 * (c1 * gam[kEA(k)][kEB(k)] + c2 * eta[kEA(k)][kEB(k)]);
+          const double a1 = m.mu / (2.0 * ip1 * ip1), a2 = 0.25 * m.lambda * J * (2.0 * J - m.alpha_nh),
+                       a3 = -0.25 * m.lambda * jm * J;
+#pragma unroll
+          for (int k = 0; k < 6; ++k)
+#pragma unroll
+            for (int kp = k; kp < 6; ++kp) {
+              const int a = kEA(k), b = kEB(k), c = kEA(kp), dd = kEB(kp);
+              Mk[pidx(k, kp)] = a1 * gam[a][b] * gam[c][dd] + a2 * eta[a][b] * eta[c][dd] +
+                                a3 * (eta[a][c] * eta[b][dd] + eta[a][dd] * eta[b][c]);
+            }
+        }
+      }
+      if (mode == 1) {
+        bool lok = ok;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) lok = lok && !(len[k] < 1e-14);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) d.ecoef[6 * (size_t)e + k] = lok ? 2.0 * scale * tk[k] * len[k] : 0.0;
+        d.eok[e] = lok ? 1 : 0;
+      } else if (ok) {
+        double* rec = d.erec + (size_t)kRec * e;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) rec[k] = scale * tk[k];
+#pragma unroll
+        for (int q = 0; q < 21; ++q) rec[6 + q] = scale * Mk[q];
+        d.eflag[e] = 0;
+        energy = scale * psi;
+      } else {  // F-based rows by k_tet_edge_fallback; the energy through F (material.cpp:71-84)
+        const int slot = atomicAdd(d.efall_count, 1);
+        if (slot < d.efall_cap) {
+          d.efall_tet[slot] = e;
+          d.erec[(size_t)kRec * e + 27] = (double)slot;
+          d.eflag[e] = 1;
+        } else {
+          d.eflag[e] = 2;  // capacity exceeded: reported through the step's stats record (SolveError on the host)
+        }
+        double du[9], F[9];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int r = 0; r < 3; ++r) du[3 * r + c] = U[c + 1][r] - U[0][r];
+        def_grad(du, B, F);
+        energy = scale * energy_density(F, m);
+      }
+    }
+  }
+  if (mode != 0) return;
+  const double bs = block_sum256(energy, s_red);
+  if (threadIdx.x == 0) d.eng_part[blockIdx.x] = bs;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(d.eng_ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += kTetTpb) acc += __ldcg(d.eng_part + b);
+  __syncthreads();
+  const double tot = block_sum256(acc, s_red);
+  if (threadIdx.x == 0) {
+    *d.eng_out = tot;
+    *d.eng_ticket = 0u;
+  }
+}
+
+// the F-based rows (element_row) of the tets k_tet_edge could not evaluate in the edge form, per slot:
+// 4 rows x [force 3, diagonal block 9, off-diagonal blocks 27]
+__global__ void __launch_bounds__(128) k_tet_edge_fallback(DevData d, MatDev m) {
+  const int n = min(*d.efall_count, d.efall_cap);
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 4 * n; q += gridDim.x * blockDim.x) {
+    const int slot = q >> 2, li = q & 3;
+    const int e = d.efall_tet[slot];
+    const int4 t = __ldg(d.tets + e);
+    double B[9], vol;
+    load_rest(d, e, B, vol);
+    double* r = d.efall + ((size_t)slot * 4 + li) * 39;
+    double f[3], dg[9];
+    element_row<true>(d, m, t, B, li, d.chi[e] * vol, f, r + 12, dg);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) r[a] = f[a];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) r[3 + k] = dg[k];
+  }
+}
+
+template <bool kEdge>
+void launch_assemble_t(const DevData& d, const MatDev& m, const StepCoeffs& c, int mode, cudaStream_t s) {
+  const int grid = (d.nn + kWarps - 1) / kWarps;
+  constexpr int kDyn = kWarps * kBlkStride * sizeof(double);
+  static bool attr = [] {
+    cudaFuncSetAttribute(k_assemble<kAssembleSystem, kEdge>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+    cudaFuncSetAttribute(k_assemble<kAssembleRawK, kEdge>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+    cudaFuncSetAttribute(k_assemble_big<kAssembleSystem, kEdge>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+    cudaFuncSetAttribute(k_assemble_big<kAssembleRawK, kEdge>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+    cudaFuncSetAttribute(k_assemble_big<kAssembleForcesOnly, kEdge>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+    return true;
+  }();
+  (void)attr;
+  if (mode == kAssembleSystem) k_assemble<kAssembleSystem, kEdge><<<grid, 32 * kWarps, kDyn, s>>>(d, m, c);
+  else if (mode == kAssembleRawK) k_assemble<kAssembleRawK, kEdge><<<grid, 32 * kWarps, kDyn, s>>>(d, m, c);
+  else k_assemble<kAssembleForcesOnly, kEdge><<<grid, 32 * kWarps, 0, s>>>(d, m, c);
+  if (d.n_big > 0) {
+    const int bg = (d.n_big + kWarps - 1) / kWarps;
+    if (mode == kAssembleSystem) k_assemble_big<kAssembleSystem, kEdge><<<bg, 32 * kWarps, kDyn, s>>>(d, m, c);
+    else if (mode == kAssembleRawK) k_assemble_big<kAssembleRawK, kEdge><<<bg, 32 * kWarps, kDyn, s>>>(d, m, c);
+    else k_assemble_big<kAssembleForcesOnly, kEdge><<<bg, 32 * kWarps, kDyn, s>>>(d, m, c);
+  }
 }
 
 }  // namespace
 
 void launch_assemble(const DevData& d, const MatDev& m, const StepCoeffs& c, int mode, cudaStream_t s) {
-  const int grid = (d.nn + kWarps - 1) / kWarps;
-  constexpr int kDyn = kWarps * kBlkStride * sizeof(double);
-  static bool attr = [] {
-    cudaFuncSetAttribute(k_assemble<kAssembleSystem>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
-    cudaFuncSetAttribute(k_assemble<kAssembleRawK>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
-    return true;
-  }();
-  (void)attr;
-  if (mode == kAssembleSystem) k_assemble<kAssembleSystem><<<grid, 32 * kWarps, kDyn, s>>>(d, m, c);
-  else if (mode == kAssembleRawK) k_assemble<kAssembleRawK><<<grid, 32 * kWarps, kDyn, s>>>(d, m, c);
-  else k_assemble<kAssembleForcesOnly><<<grid, 32 * kWarps, 0, s>>>(d, m, c);
-  if (d.n_big > 0) {
-    static bool big_attr = [] {
-      cudaFuncSetAttribute(k_assemble_big<kAssembleSystem>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
-      cudaFuncSetAttribute(k_assemble_big<kAssembleRawK>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
-      cudaFuncSetAttribute(k_assemble_big<kAssembleForcesOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
-      return true;
-    }();
-    (void)big_attr;
-    const int bg = (d.n_big + kWarps - 1) / kWarps;
-    if (mode == kAssembleSystem) k_assemble_big<kAssembleSystem><<<bg, 32 * kWarps, kDyn, s>>>(d, m, c);
-    else if (mode == kAssembleRawK) k_assemble_big<kAssembleRawK><<<bg, 32 * kWarps, kDyn, s>>>(d, m, c);
-    else k_assemble_big<kAssembleForcesOnly><<<bg, 32 * kWarps, kDyn, s>>>(d, m, c);
-  }
+  if (d.erec) launch_assemble_t<true>(d, m, c, mode, s);
+  else launch_assemble_t<false>(d, m, c, mode, s);
 }
 
-void launch_energy(const DevData& d, const MatDev& m, double* partials, int nblocks, cudaStream_t s) {
-  k_energy<<<nblocks, 256, 0, s>>>(d, m, partials);
+int tet_edge_blocks(int nt) { return (nt + kTetTpb - 1) / kTetTpb; }
+
+void launch_tet_edge(const DevData& d, const MatDev& m, int mode, cudaStream_t s) {
+  if (mode == 0) cudaMemsetAsync(d.efall_count, 0, sizeof(int32_t), s);
+  k_tet_edge<<<tet_edge_blocks(d.nt), kTetTpb, 0, s>>>(d, m, mode);
+  if (mode == 0) k_tet_edge_fallback<<<32, 128, 0, s>>>(d, m);
 }
+
 
 }  // namespace gfb

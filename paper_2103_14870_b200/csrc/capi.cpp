@@ -277,6 +277,16 @@ int gf_sim_timer_elapsed(gf_sim* s, int32_t a, int32_t b, double* ms) {
 int gf_sim_cg_trace(gf_sim* s, uint64_t* out) {
   return guard([&] { s->s->cg_trace(reinterpret_cast<unsigned long long*>(out)); });
 }
+int gf_sim_edge_forces(gf_sim* s, double* coeff6, uint8_t* ok) {
+  return guard([&] { s->s->edge_forces(coeff6, ok); });
+}
+int gf_sim_assembly_energy(gf_sim* s, double* energy) {
+  return guard([&] { *energy = s->s->assembly_energy(); });
+}
+int32_t gf_sim_element_form(const gf_sim* s) { return s->s->edge_form() ? 1 : 0; }
+int gf_sim_step_metrics(gf_sim* s, gf_step_metrics* out) {
+  return guard([&] { *out = s->s->step_metrics(); });
+}
 int gf_sim_info_get(const gf_sim* s, gf_sim_info* out) {
   return guard([&] { *out = s->s->info(); });
 }

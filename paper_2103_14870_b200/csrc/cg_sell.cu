@@ -60,12 +60,13 @@ __device__ __forceinline__ double lane_sum(double v) {  // fixed butterfly: same
 #ifndef GF_GATHER_L1
 #define GF_GATHER_L1 1
 #endif
-// Vectors written in the previous phase are read through L1 (ld.global.nc): safe because every phase boundary
-// is a cooperative-groups grid barrier, whose gpu-scope fence invalidates L1 (CCTL.IVALL), and within a phase
-// the gathered vectors are read-only (phase A writes only the owner rows of p and q, z is written in phase B).
+// Vectors written earlier in the same kernel are gathered with coherent L1-cached loads (ld.global.ca, not the
+// read-only .nc path: the data changes during the kernel). Safe because every phase boundary is a cooperative-groups
+// grid barrier, whose gpu-scope fence invalidates L1 (CCTL.IVALL), and within a phase the gathered vector is
+// read-only (the pipelined solver double-buffers it).
 __device__ __forceinline__ double ldv(const double* p) {
 #if GF_GATHER_L1
-  return __ldg(p);
+  return __ldca(p);
 #else
   return __ldcg(p);
 #endif
@@ -601,6 +602,197 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
   }
 }
 
+// Pipelined PCG (Ghysels & Vanroose 2014, preconditioned pipelined CG) for matrices of at most one slice per warp:
+// ONE grid barrier per iteration. The recurrences carry s = A p, q = D^-1 s and z = A q next to x, r, u = D^-1 r and
+// w = A u, so the only SpMV of an iteration is n = A m with m = D^-1 w -- and m is known at the END of the previous
+// iteration, before alpha and beta are. The iteration's reduction (gamma = r.u, delta = w.u, r.r) is published at
+// the same barrier as m, loaded before the SpMV and reduced after it:
+//   [barrier] load partials -> n = A m (gather m) -> gamma, delta, r.r -> stop tests -> beta, alpha
+//             -> z = n + beta z, q = m + beta q, s = w + beta s, p = u + beta p
+//             -> x += alpha p, r -= alpha s, u -= alpha q, w -= alpha z, m' = D^-1 w, partials -> [barrier]
+// Equivalent to the reference's PCG (sparse.cpp:129-188) in exact arithmetic, with its decisions mapped one to one:
+// p.Ap = delta - beta gamma / alpha_prev (<= 0: negative curvature exit, sparse.cpp:160-168), ||r||/||b|| <= tol
+// tested on every updated r (sparse.cpp:172-178), bnorm = 0 -> x = 0 (sparse.cpp:145-150), max_iters updates.
+// Solver state (x, r, D^-1, u, w, p, s, q, z) lives in shared memory for the whole solve; m is double-buffered in
+// global memory (a slow warp may still gather m_i while a fast one writes m_{i+1}); deterministic fixed-order
+// reductions as in k_pcg_sell.
+constexpr int kPipeFields = 9;
+__global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
+  cg::grid_group grid = cg::this_grid();
+  const CgLaunch& a = sa.a;
+  const int nrows = a.nrows, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int G = (int)gridDim.x;
+  const int u0 = __ldg(a.cta_first + blockIdx.x) + w;
+  const bool has = u0 < __ldg(a.cta_first + blockIdx.x + 1);
+  const int row = u0 * 32 + lane;
+  const bool live = has && row < nrows;
+  extern __shared__ double s_state[];
+  enum { X = 0, R = 1, D = 2, U = 3, W = 4, P = 5, S = 6, Q = 7, Z = 8 };
+#define PV(f, c) s_state[((w * kPipeFields + (f)) * 3 + (c)) * 32 + lane]
+  __shared__ double s_acc[kWarpsPerCta][4];
+  // double-buffered gathered vector (u during setup, then m): buffer k is a.z (k = 0) or a.p0 (k = 1)
+  auto gm = [&](int k) { return k ? a.p0 : a.z; };
+  auto part = [&](int parity, int q) { return sa.cta_part + ((size_t)parity * 4 + q) * kMaxGrid; };
+  // CTA partials of NV warp values (one slice per warp): warp sums in lane order, CTA sum in warp order
+  auto publish = [&](const double* v, int nv, int parity) {
+    if (lane == 0)
+      for (int q = 0; q < nv; ++q) s_acc[w][q] = v[q];
+    __syncthreads();
+    if ((int)threadIdx.x < nv) {
+      double x = 0.0;
+      for (int k = 0; k < kWarpsPerCta; ++k) x += s_acc[k][threadIdx.x];
+      part(parity, threadIdx.x)[blockIdx.x] = x;
+    }
+  };
+
+  // setup 1 (sparse.cpp:145-157): r = b - A x0, u = D^-1 r (gathered next), partial b.b
+  double acc[3] = {0.0, 0.0, 0.0};
+  if (has) {
+    if (a.x0_identity) {  // A x0 = x0 (see CgLaunch::x0_identity): no SpMV
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[c] = row < nrows ? a.x[3 * (size_t)row + c] : 0.0;
+    } else {
+      slice_spmv_sym_g(a, u0, GatherX{a.x}, acc);
+    }
+  }
+  double bb = 0.0;
+  if (live) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const size_t dof = 3 * (size_t)row + c;
+      const double bi = a.b[dof], ri = bi - acc[c], di = __ldg(a.dinv + dof), ui = di * ri;
+      PV(X, c) = a.x[dof];
+      PV(R, c) = ri;
+      PV(D, c) = di;
+      PV(U, c) = ui;
+      PV(P, c) = PV(S, c) = PV(Q, c) = PV(Z, c) = 0.0;
+      gm(0)[dof] = ui;
+      bb = __fma_rn(bi, bi, bb);
+    }
+  }
+  bb = lane_sum(bb);
+  publish(&bb, 1, 0);
+  grid.sync();
+  double tot[1];
+  {
+    double x[1] = {(int)threadIdx.x < G ? __ldcg(part(0, 0) + threadIdx.x) : 0.0};
+    cta_tree<1>(x, tot);
+  }
+  const double bnorm = sqrt(tot[0]);
+  int iterations = 0, converged = 0, negcurv = 0;
+  double relres = 0.0;
+  if (bnorm == 0.0) {  // sparse.cpp:145-150
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * (size_t)nrows; i += (size_t)gridDim.x * blockDim.x)
+      a.x[i] = 0.0;
+    converged = 1;
+  } else {
+    // setup 2: w = A u, m = D^-1 w (gathered by iteration 0), partials gamma_0, delta_0, r.r
+    acc[0] = acc[1] = acc[2] = 0.0;
+    if (has) slice_spmv_sym_g(a, u0, GatherZ{gm(0)}, acc);
+    double v3[3] = {0.0, 0.0, 0.0};
+    if (live) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const size_t dof = 3 * (size_t)row + c;
+        PV(W, c) = acc[c];
+        gm(1)[dof] = PV(D, c) * acc[c];
+        v3[0] = __fma_rn(PV(R, c), PV(U, c), v3[0]);
+        v3[1] = __fma_rn(acc[c], PV(U, c), v3[1]);
+        v3[2] = __fma_rn(PV(R, c), PV(R, c), v3[2]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) v3[q] = lane_sum(v3[q]);
+    __syncthreads();  // s_acc reuse
+    publish(v3, 3, 1);
+    grid.sync();
+    int pp = 1, cur = 1;
+    double gam_prev = 1.0, alpha_prev = 1.0;
+    for (int it = 0;; ++it) {
+      SELL_STAMP(it, 0);
+      double pb[3] = {0.0, 0.0, 0.0};
+      if ((int)threadIdx.x < G) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) pb[q] = __ldcg(part(pp, q) + threadIdx.x);
+      }
+      double n3[3] = {0.0, 0.0, 0.0};
+      if (has && it < a.max_iters) slice_spmv_sym_g(a, u0, GatherZ{gm(cur)}, n3);
+      SELL_STAMP(it, 1);
+      SELL_BLOCK_STAMP(it, 3000);
+      double red[3];
+      cta_tree<3>(pb, red);  // gamma_it, delta_it, r_it.r_it
+      const double gam = red[0], del = red[1];
+      relres = sqrt(red[2]) / bnorm;
+      if (it > 0 && relres <= a.tol) {  // sparse.cpp:172-178 on the residual of update it
+        iterations = it;
+        converged = 1;
+        break;
+      }
+      if (it >= a.max_iters) {
+        iterations = it;
+        converged = relres <= a.tol;
+        break;
+      }
+      const double beta = it > 0 ? gam / gam_prev : 0.0;
+      const double pap = it > 0 ? del - beta * gam / alpha_prev : del;  // = p.Ap
+      if (pap <= 0.0) {  // sparse.cpp:160-168
+        negcurv = pap < 0.0;
+        iterations = it;
+        converged = relres <= a.tol;
+        break;
+      }
+      const double alpha = gam / pap;
+      gam_prev = gam;
+      alpha_prev = alpha;
+      double v[3] = {0.0, 0.0, 0.0};
+      if (live) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const size_t dof = 3 * (size_t)row + c;
+          const double mi = PV(D, c) * PV(W, c);  // m_it of this row (the value gathered this iteration)
+          const double zi = __fma_rn(beta, PV(Z, c), n3[c]);
+          const double qi = __fma_rn(beta, PV(Q, c), mi);
+          const double si = __fma_rn(beta, PV(S, c), PV(W, c));
+          const double pi = __fma_rn(beta, PV(P, c), PV(U, c));
+          PV(Z, c) = zi;
+          PV(Q, c) = qi;
+          PV(S, c) = si;
+          PV(P, c) = pi;
+          PV(X, c) = __fma_rn(alpha, pi, PV(X, c));
+          const double ri = __fma_rn(-alpha, si, PV(R, c));
+          const double ui = __fma_rn(-alpha, qi, PV(U, c));
+          const double wi = __fma_rn(-alpha, zi, PV(W, c));
+          PV(R, c) = ri;
+          PV(U, c) = ui;
+          PV(W, c) = wi;
+          gm(cur ^ 1)[dof] = PV(D, c) * wi;
+          v[0] = __fma_rn(ri, ui, v[0]);
+          v[1] = __fma_rn(wi, ui, v[1]);
+          v[2] = __fma_rn(ri, ri, v[2]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) v[q] = lane_sum(v[q]);
+      publish(v, 3, pp ^ 1);
+      SELL_STAMP(it, 3);
+      SELL_BLOCK_STAMP(it, 2000);
+      pp ^= 1;
+      cur ^= 1;
+      grid.sync();
+    }
+    if (live)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) a.x[3 * (size_t)row + c] = PV(X, c);
+  }
+#undef PV
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.out[0] = iterations;
+    a.out[1] = converged;
+    a.out[2] = negcurv;
+    a.out[3] = relres;
+  }
+}
+
 // y = A x on the symmetric format (the FixedPatternSparse::multiply parity hook, sparse.cpp:49-58)
 __global__ void __launch_bounds__(kThreads) k_spmv_sym(CgLaunch a, const double* xin, double* y) {
   const int lane = threadIdx.x & 31;
@@ -617,15 +809,38 @@ __global__ void __launch_bounds__(kThreads) k_spmv_sym(CgLaunch a, const double*
 
 int g_grid = 0;
 
+constexpr size_t kSellSmem = GF_CG_SMEM ? (size_t)kWarpsPerCta * 6 * 3 * 32 * sizeof(double) : 0;
+constexpr size_t kPipeSmem = (size_t)kWarpsPerCta * kPipeFields * 3 * 32 * sizeof(double);
+
+void set_smem_attributes() {
+  static bool done = [] {
+    cudaFuncSetAttribute((const void*)k_pcg_sell<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellSmem);
+    cudaFuncSetAttribute((const void*)k_pcg_sell<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellSmem);
+    cudaFuncSetAttribute((const void*)k_pcg_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
+    return true;
+  }();
+  (void)done;
+}
+
 }  // namespace
 
+// co-resident CTAs of the cooperative solvers: the occupancy of every instance WITH its dynamic shared memory (the
+// pipelined solver's 166 KB bounds it), one CTA per SM at 768 threads
 int pcg_sell_grid() {
   if (g_grid == 0) {
-    int dev = 0, sms = 0, per = 0;
+    set_smem_attributes();
+    int dev = 0, sms = 0, per = 1 << 30;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg_sell<true>, kThreads, 0);
-    g_grid = std::min(kMaxGrid, sms * (per > 0 ? per : 1));
+    int q = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_sell<true>, kThreads, kSellSmem);
+    per = std::min(per, q);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_sell<false>, kThreads, kSellSmem);
+    per = std::min(per, q);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_pipe, kThreads, kPipeSmem);
+    per = std::min(per, q);
+    if (per < 1) throw std::runtime_error("cooperative PCG kernels cannot be resident (occupancy 0)");
+    g_grid = std::min(kMaxGrid, sms * per);
   }
   return g_grid;
 }
@@ -633,21 +848,21 @@ int pcg_sell_grid() {
 size_t pcg_sell_part_doubles(int ndyn) { return 2 * 4 * ((size_t)kMaxGrid + (size_t)std::max(1, ndyn)); }
 int pcg_sell_warps_per_cta() { return kWarpsPerCta; }
 
+int pcg_pipelined_default() {
+  const char* e = std::getenv("GF_CG_PIPE");
+  return e ? std::atoi(e) != 0 : 1;
+}
+
 void launch_pcg_sell(const CgLaunch& a, double* part, int ndyn, unsigned long long* ctr, cudaStream_t s) {
   SellArgs sa{a, part, part + 2 * 4 * (size_t)kMaxGrid, ctr};
   if (ndyn > 0) cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), s);
   void* args[] = {&sa};
-  const void* fn = ndyn > 0 ? (const void*)k_pcg_sell<true> : (const void*)k_pcg_sell<false>;
-  const size_t smem = GF_CG_SMEM ? (size_t)kWarpsPerCta * 6 * 3 * 32 * sizeof(double) : 0;
-  if (GF_CG_SMEM) {
-    static bool attr = [&] {
-      cudaFuncSetAttribute((const void*)k_pcg_sell<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaFuncSetAttribute((const void*)k_pcg_sell<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      return true;
-    }();
-    (void)attr;
-  }
-  const cudaError_t err = cudaLaunchCooperativeKernel(fn, pcg_sell_grid(), kThreads, args, smem, s);
+  set_smem_attributes();
+  const bool pipe = ndyn == 0 && a.pipelined;
+  const void* fn = pipe ? (const void*)k_pcg_pipe : ndyn > 0 ? (const void*)k_pcg_sell<true> : (const void*)k_pcg_sell<false>;
+  const size_t smem = pipe ? kPipeSmem : kSellSmem;
+  const int grid = a.grid > 0 ? a.grid : pcg_sell_grid();
+  const cudaError_t err = cudaLaunchCooperativeKernel(fn, grid, kThreads, args, smem, s);
   if (err != cudaSuccess) {
     cudaGetLastError();
     throw std::runtime_error(std::string("cooperative CG launch failed: ") + cudaGetErrorString(err));

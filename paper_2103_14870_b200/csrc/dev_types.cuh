@@ -135,6 +135,18 @@ struct DevData {
   double* p0;
   double* Ap;
   double* cg_out;           // [iterations, converged, negcurv, relres]
+  // edge-length element form (assemble.cu k_tet_edge; null = F-based row kernel)
+  double* erec;             // 28 nt: chi V t_k (6), chi V M_kk' packed upper (21), fallback slot
+  uint8_t* eflag;           // nt: 0 edge record, 1 F-based fallback rows, 2 no contribution (chi V = 0)
+  double* efall;            // efall_cap x 4 rows x 39: F-based rows of the fallback tets
+  int32_t* efall_tet;       // efall_cap
+  int32_t* efall_count;     // 1 (device counter; the host reads it with the step's stats)
+  int32_t efall_cap;
+  double* eng_part;         // tet_edge_blocks(nt) block partials of the fused energy
+  unsigned* eng_ticket;
+  double* eng_out;          // total strain energy of the state the last edge-form assembly evaluated
+  double* ecoef;            // 6 nt edge decomposition coefficients (parity hook)
+  uint8_t* eok;             // nt
   // misc
   const BcStep* bcstep;
   const ColliderDev* colliders;
@@ -151,7 +163,9 @@ void launch_reset_keys(const DevData& d, cudaStream_t s);
 // ---- assemble.cu ----
 enum AssembleMode { kAssembleSystem = 0, kAssembleRawK = 1, kAssembleForcesOnly = 2 };
 void launch_assemble(const DevData& d, const MatDev& m, const StepCoeffs& c, int mode, cudaStream_t s);
-void launch_energy(const DevData& d, const MatDev& m, double* out_partials, int nblocks, cudaStream_t s);
+int tet_edge_blocks(int nt);
+// mode 0: edge records + fused energy (+ F-based fallback rows); mode 1: edge decomposition (ecoef, eok)
+void launch_tet_edge(const DevData& d, const MatDev& m, int mode, cudaStream_t s);
 // ---- cg.cu ----
 struct CgLaunch {
   int32_t nrows;          // node rows (cg_sell.cu) or scalar rows (cg.cu)
@@ -175,6 +189,8 @@ struct CgLaunch {
   // zero elsewhere): those rows are identity rows and their columns are zero, so A x0 = x0 exactly (up to the
   // sign of zero) and the setup's SpMV is skipped. The solve_linear retries start from a solve's result: 0.
   int32_t x0_identity;
+  int32_t pipelined;  // cg_sell.cu: 1 = the single-barrier pipelined solver (k_pcg_pipe) when the state fits on chip
+  int32_t grid;       // cg_sell.cu: CTAs of the cooperative launch (0 = all co-resident)
 };
 int cg_csr_grid();
 void launch_pcg_csr(const CgLaunch& a, cudaStream_t s);  // scalar CSR (gf_cg_solve_csr)
@@ -182,6 +198,7 @@ void launch_pcg_csr(const CgLaunch& a, cudaStream_t s);  // scalar CSR (gf_cg_so
 int pcg_sell_grid();
 size_t pcg_sell_part_doubles(int ndyn);  // size of the partial work array (ndyn dynamic units)
 int pcg_sell_warps_per_cta();
+int pcg_pipelined_default();  // GF_CG_PIPE (default 1)
 void launch_pcg_sell(const CgLaunch& a, double* part, int ndyn, unsigned long long* ctr, cudaStream_t s);
 void launch_spmv_sym(const CgLaunch& a, const double* xin, double* y, cudaStream_t s);
 // ---- misc.cu ----
@@ -196,7 +213,12 @@ void launch_bsr_dinv(const DevData& d, cudaStream_t s);
 void launch_fill(double* p, double v, int64_t n, cudaStream_t s);
 void launch_qs_bc(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, cudaStream_t s);
 void launch_qs_update(double* u, const double* saved, const double* dx, double step, int64_t n, cudaStream_t s);
-void launch_dot(const double* a, const double* b, int64_t n, double* partials, int nblocks, cudaStream_t s);
+// ---- metrics.cu (device reductions; the last block writes the result) ----
+size_t metrics_partial_doubles();
+// out[0..4] = strain energy, kinetic energy, chi sum, broken edges, chi min
+void launch_metrics(const DevData& d, const MatDev& m, double* partials, unsigned* ticket, double* out, cudaStream_t s);
+void launch_dot(const double* a, const double* b, int64_t n, double* partials, unsigned* ticket, double* out,
+                cudaStream_t s);
 
 #ifdef __CUDACC__
 // the tet's rest record: B^-1 (row-major) and volume V

@@ -85,6 +85,25 @@ GF_HD double pk1(const double F[9], const MatDev& p, double P[9]) {
   return J;
 }
 
+// energy_density (material.cpp:71-84): StVK invariants of C = F^T F; stable NH with log(I_C + 1)
+GF_HD double energy_density(const double F[9], const MatDev& m) {
+  if (m.model == 1) {
+    double Cm[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) Cm[3 * r + c] = F[r] * F[c] + F[3 + r] * F[3 + c] + F[6 + r] * F[6 + c];
+    const double ic = Cm[0] + Cm[4] + Cm[8];
+    double iic = 0.0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) iic += Cm[q] * Cm[q];
+    return 0.125 * m.lambda * (ic - 3.0) * (ic - 3.0) + 0.25 * m.mu * (iic - 2.0 * ic + 3.0);
+  }
+  const double ic = sqnorm9(F);
+  const double j = det3(F);
+  return 0.5 * m.mu * (ic - 3.0) + 0.5 * m.lambda * (j - m.alpha_nh) * (j - m.alpha_nh) - 0.5 * m.mu * log(ic + 1.0);
+}
+
 // cartesian_stress_sixvector (material.cpp:121-135): sigma = P F^T / J (R1), then the Release-build
 // in-place column-major symmetrisation of material.cpp:128; det F <= 0 falls back to sym(P).
 GF_HD void cauchy6(const double F[9], const double P[9], double J, double c6[6]) {

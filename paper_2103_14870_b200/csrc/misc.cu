@@ -4,7 +4,7 @@
 //   k_collide     per-vertex penalty + impulse + Coulomb response (detect_and_respond, collision.cpp:49-111)
 //                 on the substep probe u + tau v (solver.cpp:233-249), block partials for the load
 //   k_integrate   v += dv, u += dt v, then pin BC nodes (solver.cpp:296-328); no-op unless the PCG converged
-//   k_qs_bc / k_qs_update / k_dot  quasi-static Newton helpers (solver.cpp:138-217)
+//   k_qs_bc / k_qs_update  quasi-static Newton helpers (solver.cpp:138-217; the dots are in metrics.cu)
 //   k_shift_diag  shift_diagonal on the node-block matrix (solver.cpp:119-129 ladder)
 #include "device_math.cuh"
 
@@ -244,20 +244,6 @@ __global__ void k_qs_update(double* u, const double* saved, const double* dx, do
 }
 
 // per-block partial dot products a.b (fixed grid, deterministic order; summed on the host)
-__global__ void __launch_bounds__(kTpb) k_dot(const double* a, const double* b, int64_t n, double* partials) {
-  __shared__ double s[kTpb];
-  double acc = 0.0;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
-    acc += a[k] * b[k];
-  s[threadIdx.x] = acc;
-  __syncthreads();
-  for (int o = kTpb / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) partials[blockIdx.x] = s[0];
-}
-
 __global__ void k_fill(double* p, double v, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -291,9 +277,6 @@ void launch_qs_bc(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes,
 }
 void launch_qs_update(double* u, const double* saved, const double* dx, double step, int64_t n, cudaStream_t s) {
   if (n > 0) k_qs_update<<<nblk(n), kTpb, 0, s>>>(u, saved, dx, step, n);
-}
-void launch_dot(const double* a, const double* b, int64_t n, double* partials, int nblocks, cudaStream_t s) {
-  k_dot<<<nblocks, kTpb, 0, s>>>(a, b, n, partials);
 }
 void launch_fill(double* p, double v, int64_t n, cudaStream_t s) {
   if (n > 0) k_fill<<<(int)((n + kTpb - 1) / kTpb), kTpb, 0, s>>>(p, v, n);

@@ -484,7 +484,24 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     GF_CUDA(cudaMallocHost(&h_cols_, sizeof(ColliderDev) * cols_.size() * nsub));
   }
   d_load_ = d_stats_ + 4;
-  d_energy_partials_ = (double*)zeros(8 * 1024);
+  {  // element form: GF_ELEMENT=edge selects the edge-length kernels (k_tet_edge + edge row kernel)
+    const char* ef = std::getenv("GF_ELEMENT");
+    edge_form_ = ef ? std::string(ef) == "edge" : kEdgeFormDefault;
+    if (edge_form_) {
+      d_.erec = (double*)zeros(8 * 28 * (size_t)nt);
+      d_.eflag = (uint8_t*)zeros((size_t)nt);
+      d_.efall_cap = std::max<int32_t>(1024, nt / 64);
+      d_.efall = (double*)zeros(8 * 156 * (size_t)d_.efall_cap);
+      d_.efall_tet = (int32_t*)zeros(4 * (size_t)d_.efall_cap);
+      d_.efall_count = reinterpret_cast<int32_t*>(d_stats_ + 6);
+      d_.eng_part = (double*)zeros(8 * (size_t)tet_edge_blocks(nt));
+      d_.eng_ticket = (unsigned*)zeros(64);
+      d_.eng_out = d_stats_ + 7;
+    }
+  }
+  d_energy_partials_ = (double*)zeros(8 * metrics_partial_doubles());
+  d_red_ticket_ = (unsigned*)zeros(64);
+  d_red_out_ = (double*)zeros(64);
   if (!bcs_.empty()) {
     d_bcstep_ = (BcStep*)dalloc(sizeof(BcStep) * bcs_.size());
     d_.bcstep = d_bcstep_;
@@ -496,7 +513,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   n_fixed_ = (int32_t)fixed.size();
   d_fixed_nodes_ = (int32_t*)up(fixed.data(), 4 * fixed.size());
   GF_CUDA(cudaMallocHost(&h_stats_, 8 * 8));
-  GF_CUDA(cudaMallocHost(&h_partials_, 8 * 1024));
+  GF_CUDA(cudaMallocHost(&h_partials_, 64));
   newton_tol_ = cfg_.newton_tol > 0.0 ? cfg_.newton_tol : 1e-6 * mat_.sigma_thres * mesh_.mean_face_area();  // solver.cpp:57-59
   // static external force: m g (solver.cpp:230-231)
   std::vector<double> fext(nd);
@@ -521,7 +538,16 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
      // slices' slot counts (interior slices carry ~1.5x the slots of boundary ones): the smallest per-CTA slot
      // budget that places the static slices. One slice per warp covers the matrix while it fits (c3: no
      // dynamic units); a larger matrix places one slice per warp statically and hands out the rest by ticket.
-    const int G = pcg_sell_grid(), W = pcg_sell_warps_per_cta(), ns = d_.nslices;
+    const int Gfull = pcg_sell_grid(), W = pcg_sell_warps_per_cta(), ns = d_.nslices;
+    // CTAs of the cooperative solve: all co-resident ones by default; GF_CG_GRID=<n> asks for fewer (cheaper grid
+    // barriers for small matrices), never fewer than one slice per warp needs
+    int G = Gfull;
+    if (const char* e = std::getenv("GF_CG_GRID")) {
+      const int want = std::atoi(e);
+      if (want > 0) G = std::min(Gfull, std::max(want, (ns + W - 1) / W));
+    }
+    cg_.grid = G;
+    cg_.pipelined = pcg_pipelined_default();
     const int64_t gw = (int64_t)G * W;
     double frac = 0.0;  // measured at c4 (28k slices): all-dynamic tail 22.5 ms, 50 % static 23.0, 80 % 26.2
     if (const char* e = std::getenv("GF_CG_STATIC")) frac = std::atof(e);  // static share of a large matrix
@@ -780,6 +806,45 @@ void Simulation::solve_ladder(bool ok, int32_t* iters, Acc&& account) {
   }
 }
 
+// force + stiffness assembly (fem.cpp:96-169 fused with solver.cpp:275-295): the F-based row kernel, or the
+// edge-length form (k_tet_edge once per tet -> records + fused energy, then the edge row kernel)
+void Simulation::assemble(const StepCoeffs& c, int mode, const char* name, double bytes) {
+  if (edge_form_) {
+    const double T = mesh_.nt, N = mesh_.nn;
+    // reads conn 16, rest record 80, chi 8 per tet and X, u once (48 per node); writes the 224-byte record
+    launch("tet_edge", 328.0 * T + 48.0 * N, [&] { launch_tet_edge(d_, md_, 0, stream_); });
+  }
+  launch(name, bytes, [&] { launch_assemble(d_, md_, c, mode, stream_); });
+}
+
+void Simulation::check_edge_fallback() {  // h_stats_ holds the step's record
+  if (!edge_form_) return;
+  int32_t nf = 0;
+  std::memcpy(&nf, h_stats_ + 6, 4);
+  if (nf > d_.efall_cap)
+    throw GeometryError("edge-length element form: " + std::to_string(nf) + " degenerate tets exceed the fallback capacity " +
+                        std::to_string(d_.efall_cap) + " (use GF_ELEMENT=F)");
+}
+
+double Simulation::assembly_energy() {
+  if (!edge_form_) throw FormatError("the fused assembly energy needs the edge-length element form (GF_ELEMENT=edge)");
+  GF_CUDA(cudaMemcpyAsync(h_partials_, d_.eng_out, 8, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  return h_partials_[0];
+}
+
+void Simulation::edge_forces(double* coeff6, uint8_t* ok) {  // edge_decomposed_forces (fem.cpp:57-94), every tet
+  const size_t nt = (size_t)mesh_.nt;
+  if (!d_.ecoef) {
+    d_.ecoef = (double*)dalloc(48 * nt);
+    d_.eok = (uint8_t*)dalloc(nt);
+  }
+  launch("edge_decomposition", 0.0, [&] { launch_tet_edge(d_, md_, 1, stream_); });
+  GF_CUDA(cudaMemcpyAsync(coeff6, d_.ecoef, 48 * nt, cudaMemcpyDeviceToHost, stream_));
+  GF_CUDA(cudaMemcpyAsync(ok, d_.eok, nt, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+}
+
 gf_step_stats Simulation::dynamic_step() {
   gf_step_stats st{};
   const double t = time_, dt = cfg_.dt;
@@ -830,7 +895,7 @@ gf_step_stats Simulation::dynamic_step() {
   // algorithmic bytes: SURVEY.md §8(d) B_F = 16n + 104T + 8Z (n = 3N dofs, Z scalar nonzeros)
   const double n = 3.0 * mesh_.nn, T = mesh_.nt, Z = 9.0 * pat_.cols.size();
   d_.fint_out = nullptr;
-  launch("assemble", 16 * n + 104 * T + 8 * Z, [&] { launch_assemble(d_, md_, c, kAssembleSystem, stream_); });
+  assemble(c, kAssembleSystem, "assemble", 16 * n + 104 * T + 8 * Z);
 
   // solve_linear (solver.cpp:105-136): first attempt, 4x retry, then cumulative diagonal shifts
   cg_.max_iters = cfg_.cg_max_iters;
@@ -838,7 +903,8 @@ gf_step_stats Simulation::dynamic_step() {
   launch("pcg", 0.0, [&] { launch_cg(); });
   cg_.x0_identity = 0;
   launch("integrate", 40 * n, [&] { launch_integrate(d_, dt, stream_); });  // B_int = 40n; no-op if not converged
-  GF_CUDA(cudaMemcpyAsync(h_stats_, d_stats_, 48, cudaMemcpyDeviceToHost, stream_));  // cg_out, load, newly
+  // cg_out, load, newly broken, edge-form fallback count, assembled-state energy
+  GF_CUDA(cudaMemcpyAsync(h_stats_, d_stats_, 64, cudaMemcpyDeviceToHost, stream_));
   synchronize();
   // PCG algorithmic bytes per iteration for THIS format: every stored upper block and slot word
   // once, plus the vectors that leave the chip -- z gathered and written (24 B per node each) when the solver
@@ -850,6 +916,7 @@ gf_step_stats Simulation::dynamic_step() {
   auto account = [&](double iters) {
     if (profiling_) ktimes_["pcg"].bytes += iters * cg_bytes_per_iter;
   };
+  check_edge_fallback();
   int32_t newly = 0;
   std::memcpy(&newly, h_stats_ + 5, 4);
   st.newly_broken = newly;
@@ -873,23 +940,24 @@ gf_step_stats Simulation::dynamic_step() {
 
 // ---------------------------------------------------------------- quasi-static step (solver.cpp:138-217)
 double Simulation::device_dot(const double* a, const double* b, int64_t n) {
-  constexpr int nblocks = 1024;
-  launch("dot", 16.0 * n, [&] { launch_dot(a, b, n, d_energy_partials_, nblocks, stream_); });
-  GF_CUDA(cudaMemcpyAsync(h_partials_, d_energy_partials_, 8 * nblocks, cudaMemcpyDeviceToHost, stream_));
+  launch("dot", 16.0 * n, [&] { launch_dot(a, b, n, d_energy_partials_, d_red_ticket_, d_red_out_, stream_); });
+  GF_CUDA(cudaMemcpyAsync(h_partials_, d_red_out_, 8, cudaMemcpyDeviceToHost, stream_));
   synchronize();
-  double s = 0.0;
-  for (int k = 0; k < nblocks; ++k) s += h_partials_[k];
-  return s;
+  return h_partials_[0];
+}
+
+// k_metrics: [strain energy, kinetic energy, chi sum, broken edges, chi min] of the current state, one 40-byte read
+void Simulation::device_metrics(double out[5]) {
+  launch("metrics", 0.0, [&] { launch_metrics(d_, md_, d_energy_partials_, d_red_ticket_, d_red_out_, stream_); });
+  GF_CUDA(cudaMemcpyAsync(h_partials_, d_red_out_, 40, cudaMemcpyDeviceToHost, stream_));
+  synchronize();
+  for (int k = 0; k < 5; ++k) out[k] = h_partials_[k];
 }
 
 double Simulation::device_strain_energy() {
-  constexpr int nblocks = 1024;
-  launch("energy", 0.0, [&] { launch_energy(d_, md_, d_energy_partials_, nblocks, stream_); });
-  GF_CUDA(cudaMemcpyAsync(h_partials_, d_energy_partials_, 8 * nblocks, cudaMemcpyDeviceToHost, stream_));
-  synchronize();
-  double s = 0.0;
-  for (int k = 0; k < nblocks; ++k) s += h_partials_[k];
-  return s;
+  double m[5];
+  device_metrics(m);
+  return m[0];
 }
 
 void Simulation::apply_boundary_displacements(double t) {  // solver.cpp:74-77, plus zero Newton increments
@@ -910,7 +978,7 @@ bool Simulation::newton_solve(gf_step_stats& st) {
   d_.fint_out = nullptr;
   auto account = [](double) {};
   for (int it = 0; it <= cfg_.newton_max_iters; ++it) {
-    launch("assemble", 16 * n + 104 * T + 8 * Z, [&] { launch_assemble(d_, md_, c, kAssembleSystem, stream_); });
+    assemble(c, kAssembleSystem, "assemble", 16 * n + 104 * T + 8 * Z);
     const double rr = device_dot(d_.rhs, d_.rhs, (int64_t)nd);
     st.residual = std::sqrt(rr);
     st.newton_iterations = it;
@@ -1018,12 +1086,10 @@ void Simulation::set_external_forces(const double* f3n) {
   synchronize();
 }
 
-int64_t Simulation::broken_edge_count() {
-  std::vector<uint8_t> z(mesh_.ne);
-  get_state(nullptr, nullptr, z.data(), nullptr, nullptr);
-  int64_t n = 0;
-  for (uint8_t b : z) n += b;
-  return n;
+int64_t Simulation::broken_edge_count() {  // SimState::broken_edge_count, a device reduction
+  double m[5];
+  device_metrics(m);
+  return (int64_t)m[3];
 }
 
 void Simulation::mass(double* m3n) const {
@@ -1036,7 +1102,7 @@ void Simulation::eval_forces(double* f3n) {
   const size_t nd = 3 * (size_t)mesh_.nn;
   StepCoeffs c{};
   d_.fint_out = d_.r;  // scratch
-  launch("forces", 0.0, [&] { launch_assemble(d_, md_, c, kAssembleForcesOnly, stream_); });
+  assemble(c, kAssembleForcesOnly, "forces", 0.0);
   d_.fint_out = nullptr;
   GF_CUDA(cudaMemcpyAsync(f3n, d_.r, 8 * nd, cudaMemcpyDeviceToHost, stream_));
   synchronize();
@@ -1064,7 +1130,7 @@ void Simulation::bsr_to_csr(const std::vector<double>& bval, double* vals) const
 
 void Simulation::eval_stiffness(double* vals) {
   StepCoeffs c{};
-  launch("stiffness", 0.0, [&] { launch_assemble(d_, md_, c, kAssembleRawK, stream_); });
+  assemble(c, kAssembleRawK, "stiffness", 0.0);
   std::vector<double> b(bval_doubles_);
   GF_CUDA(cudaMemcpyAsync(b.data(), d_.bval, 8 * b.size(), cudaMemcpyDeviceToHost, stream_));
   synchronize();
@@ -1165,22 +1231,24 @@ double Simulation::reaction_load(const int32_t* nodes, int32_t n, const double a
   return -((tot[0] * axis[0] + tot[1] * axis[1]) + tot[2] * axis[2]);
 }
 
-void Simulation::energies(double* strain, double* kinetic) {
-  const int nblocks = 1024;
-  launch("energy", 0.0, [&] { launch_energy(d_, md_, d_energy_partials_, nblocks, stream_); });
-  std::vector<double> part(nblocks), v(3 * (size_t)mesh_.nn);
-  GF_CUDA(cudaMemcpyAsync(part.data(), d_energy_partials_, 8 * nblocks, cudaMemcpyDeviceToHost, stream_));
-  GF_CUDA(cudaMemcpyAsync(v.data(), d_.v, 8 * v.size(), cudaMemcpyDeviceToHost, stream_));
-  synchronize();
-  double s = 0.0;
-  for (double p : part) s += p;
-  double k = 0.0;  // kinetic_energy (fem.cpp:201-206)
-  for (int32_t i = 0; i < mesh_.nn; ++i) {
-    const double* vi = &v[3 * (size_t)i];
-    k += 0.5 * mass_[i] * ((vi[0] * vi[0] + vi[1] * vi[1]) + vi[2] * vi[2]);
-  }
-  if (strain) *strain = s;
-  if (kinetic) *kinetic = k;
+void Simulation::energies(double* strain, double* kinetic) {  // total_strain_energy + kinetic_energy (fem.cpp:190-206)
+  double m[5];
+  device_metrics(m);
+  if (strain) *strain = m[0];
+  if (kinetic) *kinetic = m[1];
+}
+
+gf_step_metrics Simulation::step_metrics() {  // run_scenario's make_row + log_damage (scenario.cpp:640-672)
+  double m[5];
+  device_metrics(m);
+  gf_step_metrics r{};
+  r.strain_energy = m[0];
+  r.kinetic_energy = m[1];
+  r.chi_mean = m[2] / (double)mesh_.nt;
+  r.broken_edges = (int64_t)m[3];
+  r.chi_min = m[4];
+  r.time = time_;
+  return r;
 }
 
 }  // namespace gfb

@@ -63,6 +63,7 @@ class Simulation {
   void mass(double* m3n) const;
   double reaction_load(const int32_t* nodes, int32_t n, const double axis[3]);
   void energies(double* strain, double* kinetic);
+  gf_step_metrics step_metrics();
 
   void eval_forces(double* f3n);
   void eval_stiffness(double* vals);
@@ -70,6 +71,9 @@ class Simulation {
   void eval_screening(double* screening, double* sigma_f6, uint8_t* degenerate);
   void last_system(double* vals, double* rhs);
   void spmv(const double* x, double* y);
+  void edge_forces(double* coeff6, uint8_t* ok);
+  double assembly_energy();
+  bool edge_form() const { return edge_form_; }
   void solve_system(const double* vals, const double* b, const double* x0, double tol, int32_t max_iters, double* x,
                     gf_cg_result* res);
 
@@ -96,12 +100,17 @@ class Simulation {
   void solve_ladder(bool ok, int32_t* iters, Acc&& account);
   double device_dot(const double* a, const double* b, int64_t n);
   double device_strain_energy();
+  void device_metrics(double out[5]);
   void apply_boundary_displacements(double t);
   bool newton_solve(gf_step_stats& st);
   void launch_cg();
+  void assemble(const StepCoeffs& c, int mode, const char* name, double bytes);
+  void check_edge_fallback();
   template <class Up>
   bool build_template_layout(const NonlocalTable& tb, Up&& up);
 
+  static constexpr bool kEdgeFormDefault = false;
+  bool edge_form_ = false;
   HostMesh mesh_;
   NodePattern pat_;
   std::vector<int32_t> sell_ptr_;
@@ -125,7 +134,7 @@ class Simulation {
   double newton_tol_ = 0.0, quasi_time_ = 0.0;
   double* d_usave_ = nullptr;    // line-search base displacements (quasi-static only, allocated on first use)
   double* d_ubackup_ = nullptr;  // last converged load increment
-  double* h_partials_ = nullptr; // pinned, 1024 block partials
+  double* h_partials_ = nullptr; // pinned, 8 doubles: reduction results read back
   int32_t n_fixed_ = 0;
 
   cudaStream_t stream_ = nullptr;
@@ -139,7 +148,9 @@ class Simulation {
   BcStep* d_bcstep_ = nullptr;
   ColliderDev* d_cols_ = nullptr;
   double* d_load_ = nullptr;
-  double* d_energy_partials_ = nullptr;
+  double* d_energy_partials_ = nullptr;  // block partials of the device reductions (metrics.cu)
+  unsigned* d_red_ticket_ = nullptr;
+  double* d_red_out_ = nullptr;
   // pinned staging
   BcStep* h_bcstep_ = nullptr;
   ColliderDev* h_cols_ = nullptr;

@@ -217,6 +217,125 @@ def test_spmv_matches_oracle_multiply():
     assert entry_err(gs.spmv(x), o.spmv_csr(rp, cols, a_ref, x)) < FORCE_TOL
 
 
+# ---------------------------------------------------------------- edge-length element form (north_star (1))
+@pytest.fixture
+def edge_form(monkeypatch):
+    monkeypatch.setenv("GF_ELEMENT", "edge")
+
+
+@pytest.mark.parametrize("s", SMALL, ids=lambda s: s.name)
+@pytest.mark.parametrize("model", [0, 1])
+def test_edge_form_forces_stiffness_system_within_1e9(s, model, edge_form):
+    """the edge-length kernels (k_tet_edge records + edge row kernel): forces, K, the step's A and rhs against the
+    oracle's F-based assembly, entrywise within 1e-9; the fused energy equals total_strain_energy of the assembled
+    state within 1e-9"""
+    s.model = model
+    rng = np.random.default_rng(14)
+    gs, os_, gm, om = pair(s, rng, disp=0.2, chi_random=True)
+    assert gs.element_form() == "edge"
+    st = os_.get_state()
+    assert entry_err(gs.eval_forces(), om.assemble_forces(os_.mat, st["u"], st["chi"])) < FORCE_TOL
+    assert entry_err(gs.eval_stiffness(), om.assemble_stiffness(os_.mat, st["u"], st["chi"])) < FORCE_TOL
+    e_ref = om.total_strain_energy(os_.mat, st["u"], st["chi"])
+    assert abs(gs.assembly_energy() - e_ref) <= 1e-9 * abs(e_ref)
+    os_.dynamic_step()
+    gs.dynamic_step()
+    a_ref, r_ref = os_.last_system()
+    a_got, r_got = gs.last_system()
+    assert entry_err(a_got, a_ref) < FORCE_TOL and entry_err(r_got, r_ref) < FORCE_TOL
+
+
+def test_edge_form_rest_is_exact(edge_form):  # test_solver.cpp:89-98 with the edge form: dl2 = 0 -> no force at all
+    for model in (g.STVK, g.STABLE_NEO_HOOKEAN):
+        m = g.make_box_mesh((0.1, 0.1, 0.1), (2, 2, 2))
+        s = g.Simulation(m, g.MaterialParams.from_youngs(1e6, 0.3, 1000, 1e9, 0, model), g.SolverConfig(dt=1e-3))
+        assert s.element_form() == "edge"
+        s.dynamic_step()
+        s.dynamic_step()
+        st = s.state()
+        if model == g.STVK:
+            assert np.all(st.displacements == 0) and np.all(st.velocities == 0)
+        else:  # the stable NH rest stress is zero only up to rounding of alpha (material.cpp:65-67)
+            assert np.abs(st.displacements).max() < 1e-15
+
+
+def test_edge_form_degenerate_tets_fall_back(edge_form):
+    """a collapsed tet (det C = 0) cannot be written in edge lengths: k_tet_edge_fallback assembles its F-based rows;
+    forces and K still match the oracle"""
+    s = cf.scaled("c1", (3, 3, 3))
+    gs, os_, gm, om = pair(s)
+    X = om.arrays()["rest"]
+    u = np.random.default_rng(5).uniform(-1e-4, 1e-4, X.shape)
+    u[5] = X[6] - X[5]
+    os_.set_state(u=u)
+    gs.set_state(u)
+    f_ref = om.assemble_forces(os_.mat, u, os_.get_state()["chi"])
+    assert entry_err(gs.eval_forces(), f_ref) < FORCE_TOL
+    k_ref = om.assemble_stiffness(os_.mat, u, os_.get_state()["chi"])
+    assert entry_err(gs.eval_stiffness(), k_ref) < FORCE_TOL
+
+
+@pytest.mark.parametrize("model", [0, 1])
+def test_edge_decomposition_matches_oracle(model):
+    """gf_sim_edge_forces (the edge kernel's t_k: c_k = 2 V t_k |d_k|) against the oracle's edge_decomposed_forces
+    (fem.cpp:57-94, least squares through an SVD pseudo-inverse) on every tet of a loaded state, within 1e-8 of the
+    tet's largest coefficient; a collapsed edge flags !ok on both sides (test_fem.cpp:141-150)"""
+    s = cf.scaled("c2", (3, 3, 3))
+    s.model = model
+    rng = np.random.default_rng(91)
+    gs, os_, gm, om = pair(s, rng, disp=0.2)
+    X = om.arrays()["rest"]
+    u = os_.get_state()["u"]
+    u[5] = X[6] - X[5] + u[6]  # collapse edge (5, 6): its tets are flagged
+    gs.set_state(u)
+    c, ok = gs.edge_forces()
+    flagged = 0
+    for e in range(om.num_tets):
+        cr, res, okr = om.edge_decomposed_forces(os_.mat, e, u)
+        assert ok[e] == okr, e
+        if okr:
+            assert np.abs(c[e] - cr).max() <= 1e-8 * np.abs(cr).max(), e
+        else:
+            flagged += 1
+    assert flagged > 0
+
+
+def test_edge_form_trajectory_c3_scaled(edge_form):
+    s = cf.scaled("c3", (10, 10, 9), steps=40)
+    worst, resyncs, broken = run_pair(s, s.steps)
+    assert broken > 0
+    assert worst < TRAJ_TOL
+
+
+# ---------------------------------------------------------------- per-step metrics on the device (SURVEY §8(f)-2)
+@pytest.mark.parametrize("model", [0, 1])
+def test_step_metrics_match_oracle(model):
+    """gf_sim_step_metrics (k_metrics) against the reference's total_strain_energy / kinetic_energy / broken-edge count
+    and log_damage's chi statistics (fem.cpp:190-206, scenario.cpp:660-672) from an identical state: energies within
+    1e-9 relative, counts and chi_min exact."""
+    s = cf.scaled("c3", (8, 8, 7))
+    s.model = model
+    rng = np.random.default_rng(81)
+    gs, os_, gm, om = pair(s, rng, disp=0.1, damage=0.1, chi_random=True)
+    chi = os_.get_state()["chi"]
+    chi[::7] = 0.0  # chi V = 0 tets are skipped (fem.cpp:194)
+    os_.set_state(chi=chi)
+    gs.set_state(element_chi=chi)
+    st = os_.get_state()
+    m = gs.step_metrics()
+    e_ref = om.total_strain_energy(os_.mat, st["u"], st["chi"])
+    mass = om.lumped_mass(os_.mat)[::3]
+    ke_ref = float(np.sum(0.5 * mass * (st["v"] ** 2).sum(1)))
+    assert abs(m.strain_energy - e_ref) <= 1e-9 * abs(e_ref)
+    assert abs(m.kinetic_energy - ke_ref) <= 1e-9 * abs(ke_ref)
+    assert m.broken_edges == int(st["zeta"].sum())
+    assert m.chi_min == st["chi"].min()
+    assert m.chi_mean == pytest.approx(st["chi"].mean(), rel=1e-12)
+    e, k = gs.energies()
+    assert e == m.strain_energy and k == m.kinetic_energy
+    assert gs.broken_fraction() == pytest.approx(m.broken_edges / om.num_edges, rel=0, abs=0)
+
+
 # ---------------------------------------------------------------- the production PCG (k_pcg_sell) on given systems
 def _pcg_setup(cells=(4, 4, 4)):
     s = cf.scaled("c2", cells)
@@ -226,13 +345,19 @@ def _pcg_setup(cells=(4, 4, 4)):
     return gs, os_, om, np.asarray(rp), np.asarray(cols), rows
 
 
+def _oracle_cg(rp, cols, vals, b, x0, tol, max_iters):
+    x, r = o.cg_solve_csr(rp, cols, vals, b, x0, tol, max_iters)
+    return x, dict(iterations=r.iterations, converged=bool(r.converged),
+                   negative_curvature=bool(r.negative_curvature), relative_residual=r.relative_residual)
+
+
 def test_production_pcg_identity_system():  # test_sparse.cpp:20-32 on k_pcg_sell
     gs, _, om, rp, cols, rows = _pcg_setup()
     n = len(rp) - 1
     vals = (rows == cols).astype(np.float64)
     b = np.random.default_rng(71).uniform(-1, 1, n)
     x, r = gs.solve_system(vals, b, tol=1e-12, max_iters=100)
-    xo, ro = o.cg_solve_csr(rp, cols, vals, b, np.zeros(n), 1e-12, 100)
+    xo, ro = _oracle_cg(rp, cols, vals, b, np.zeros(n), 1e-12, 100)
     assert r["converged"] and r["iterations"] == ro["iterations"] == 1 and not r["negative_curvature"]
     assert np.array_equal(x, b) and np.array_equal(xo, b)
 
@@ -242,7 +367,7 @@ def test_production_pcg_zero_rhs():  # sparse.cpp:145-150: b = 0 -> x = 0, conve
     n = len(rp) - 1
     vals = (rows == cols) * 2.0
     x, r = gs.solve_system(vals, np.zeros(n), x0=np.ones(n), tol=1e-10, max_iters=50)
-    xo, ro = o.cg_solve_csr(rp, cols, vals, np.zeros(n), np.ones(n), 1e-10, 50)
+    xo, ro = _oracle_cg(rp, cols, vals, np.zeros(n), np.ones(n), 1e-10, 50)
     assert r["converged"] and ro["converged"] and r["iterations"] == ro["iterations"] == 0
     assert np.all(x == 0.0) and np.all(xo == 0.0)
 
@@ -254,7 +379,7 @@ def test_production_pcg_negative_curvature():  # test_sparse.cpp:74-84 / sparse.
     vals = np.where(rows == cols, d[rows], 0.0)
     b = np.where(np.arange(n) % 3 == 0, 1.0, 0.1)
     x, r = gs.solve_system(vals, b, tol=1e-10, max_iters=50)
-    xo, ro = o.cg_solve_csr(rp, cols, vals, b, np.zeros(n), 1e-10, 50)
+    xo, ro = _oracle_cg(rp, cols, vals, b, np.zeros(n), 1e-10, 50)
     assert ro["negative_curvature"] and not ro["converged"]
     assert r["negative_curvature"] and not r["converged"] and r["iterations"] == ro["iterations"] == 0
     assert r["relative_residual"] == pytest.approx(ro["relative_residual"], rel=1e-12)
@@ -272,7 +397,7 @@ def test_production_pcg_matches_oracle_on_the_step_system():
     n = len(rp) - 1
     b = rng.uniform(-1, 1, n)
     x, r = gs.solve_system(A, b, tol=1e-13, max_iters=2000)
-    xo, ro = o.cg_solve_csr(rp, cols, A, b, np.zeros(n), 1e-13, 2000)
+    xo, ro = _oracle_cg(rp, cols, A, b, np.zeros(n), 1e-13, 2000)
     assert r["converged"] and ro["converged"] and abs(r["iterations"] - ro["iterations"]) <= 2
     assert np.abs(x - xo).max() <= 1e-9 * np.abs(xo).max()
     Ad = np.zeros((n, n))

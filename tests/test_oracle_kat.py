@@ -884,3 +884,51 @@ def test_backward_euler_energy_ratio_independent_dense():
         assert e <= prev * (1 + 1e-12)
         prev = e
     assert prev / e0 == pytest.approx(0.9078, abs=0.002)
+
+
+# ------------------------------------------------------------------ edge force decomposition (test_fem.cpp:98-150)
+def _one_tet(nodes):
+    return o.Mesh.create(np.asarray(nodes, float), np.array([[0, 1, 2, 3]], np.int32))
+
+
+EDGES = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
+
+
+def _rebuild(m, u, coeff):
+    x = m.arrays()["rest"] + u
+    f = np.zeros((4, 3))
+    for k, (a, b) in enumerate(EDGES):
+        d = x[b] - x[a]
+        d = d / np.linalg.norm(d)
+        f[a] += coeff[k] * d
+        f[b] -= coeff[k] * d
+    return f
+
+
+def test_edge_decomposition_rest_and_uniform_expansion():  # test_fem.cpp:98-113
+    m = _one_tet([[0, 0, 0], [1, 0, 0], [0.5, np.sqrt(3) / 2, 0], [0.5, np.sqrt(3) / 6, np.sqrt(6) / 3]])
+    p = o.material_from_youngs(1e6, 0.3, 1000.0, 1e5, 0.0, STVK)
+    c, res, ok = m.edge_decomposed_forces(p, 0)
+    assert ok and np.all(np.abs(c) < 1e-12)
+    c, res, ok = m.edge_decomposed_forces(p, 0, 0.2 * m.arrays()["rest"])
+    assert ok and res < 1e-8
+    assert np.all(np.abs(c[1:] - c[0]) <= 1e-8 * abs(c[0]))
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_edge_decomposition_rebuilds_forces(seed):  # test_fem.cpp:115-139, tools/main.cpp:99-127
+    m = _one_tet([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])
+    p = o.material_from_youngs(1e6, 0.3, 1000.0, 1e5, 0.0, STVK)
+    u = np.random.default_rng(seed).uniform(-0.15, 0.15, (4, 3))
+    c, res, ok = m.edge_decomposed_forces(p, 0, u)
+    assert ok
+    f = m.element_internal_force(p, 0, u)
+    assert np.linalg.norm(_rebuild(m, u, c) - f, axis=1).max() < 1e-8
+
+
+def test_edge_decomposition_degenerate_flags():  # test_fem.cpp:141-150
+    m = _one_tet([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])
+    p = o.material_from_youngs(1e6, 0.3, 1000.0, 1e5, 0.0, STVK)
+    u = np.zeros((4, 3))
+    u[3] = [0, 0, -1]
+    assert not m.edge_decomposed_forces(p, 0, u)[2]
