@@ -202,8 +202,8 @@ int gf_sim_spmv(gf_sim* s, const double* x, double* y);
 int gf_sim_edge_forces(gf_sim* s, double* coeff6, uint8_t* ok);
 /* element form of the assembly: 0 = F-based closed-form rows, 1 = edge-length form (GF_ELEMENT=edge at create) */
 int32_t gf_sim_element_form(const gf_sim* s);
-/* total_strain_energy (fem.cpp:190-199) of the state the last assembly evaluated (the step-start state of the last
- * dynamic_step), the fused by-product of the edge-length kernel (GF_FORMAT_ERROR for the F-based form) */
+/* total_strain_energy (fem.cpp:190-199) of the state the last system assembly evaluated (the step-start state of the
+ * last dynamic_step / Newton iterate), the fused by-product of the force pass (either element form) */
 int gf_sim_assembly_energy(gf_sim* s, double* energy);
 /* cg_solve (sparse.cpp:129-188) with the PRODUCTION solver (the persistent PCG on the symmetric SELL-32 matrix) on a
  * caller-provided matrix with this simulation's pattern: vals in the scalar-CSR order of gf_sim_eval_stiffness,

@@ -1,10 +1,14 @@
 // grafem_b200.hpp — header-only C++ facade over the C ABI (grafem_b200.h) with the shape of the reference's
-// grafem::Simulation API (/root/reference/proj/include/grafem/solver.hpp:60-118): same class and method
-// names, same exception types (types.hpp:17-29), AoS std::array<double,3> node vectors like the reference's
-// Eigen::Vector3d (solver.cpp:62-72 dof order). A reference caller switches by replacing
+// grafem API (/root/reference/proj/include/grafem): the value types MaterialParams / EnergyModel (material.hpp:10-31),
+// SolverConfig, BoundaryCondition, StepStats (solver.hpp:15-55), Schedule3 and Collider (collision.hpp:10-34),
+// TetMesh / SimState, the Simulation class (solver.hpp:60-118) with the same method names and accessors, and the
+// same exception types (types.hpp:17-29). Vec3 is a 3-double value with Eigen::Vector3d's constructor and
+// Zero()/UnitX()/UnitZ() spellings; node vectors are AoS in dof order 3 node + axis (solver.cpp:62-72). A reference
+// caller switches by replacing
 //   #include "grafem/solver.hpp"     ->  #include "grafem_b200.hpp"
-//   grafem::Simulation sim(...)      ->  grafem_b200::Simulation sim(...)
-// and linking libgrafem_b200.so.
+//   namespace grafem                 ->  namespace grafem_b200
+// and linking libgrafem_b200.so. The one semantic difference: state() returns a copy of the
+// device-resident SimState; the reference's mutable state() reference becomes set_state(SimState).
 #pragma once
 
 #include <array>
@@ -35,7 +39,19 @@ inline void check(int rc) {
   }
 }
 
-using Vec3 = std::array<double, 3>;
+// Eigen::Vector3d stand-in: Vec3(x, y, z), Vec3::Zero(), UnitX/Y/Z(), x()/y()/z(); contiguous (24 bytes)
+struct Vec3 : std::array<double, 3> {
+  Vec3() : std::array<double, 3>{{0.0, 0.0, 0.0}} {}
+  Vec3(double x, double y, double z) : std::array<double, 3>{{x, y, z}} {}
+  static Vec3 Zero() { return Vec3(); }
+  static Vec3 UnitX() { return Vec3(1.0, 0.0, 0.0); }
+  static Vec3 UnitY() { return Vec3(0.0, 1.0, 0.0); }
+  static Vec3 UnitZ() { return Vec3(0.0, 0.0, 1.0); }
+  double x() const { return (*this)[0]; }
+  double y() const { return (*this)[1]; }
+  double z() const { return (*this)[2]; }
+};
+static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 must stay a packed triple (AoS node vectors)");
 
 // TetMesh (mesh.hpp:15-43)
 class TetMesh {
@@ -79,7 +95,132 @@ class TetMesh {
   std::shared_ptr<gf_mesh> m_;
 };
 
-// MaterialParams::from_youngs (material.hpp:14-31); energy model 0 stable_neo_hookean, 1 stvk
+// free-function construction, as mesh.hpp:55-61 and primitives.hpp:12-13 declare it
+inline TetMesh make_mesh(const std::vector<Vec3>& nodes, const std::vector<std::array<int, 4>>& tets) {
+  return TetMesh::make_mesh(nodes, tets);
+}
+inline TetMesh make_box_mesh(const Vec3& size, const std::array<int, 3>& cells, const Vec3& origin = Vec3::Zero()) {
+  return TetMesh::make_box_mesh(size, cells, origin);
+}
+inline TetMesh load_tetgen(const std::string& node_text, const std::string& ele_text) {
+  return TetMesh::load_tetgen(node_text, ele_text);
+}
+
+// EnergyModel / MaterialParams (material.hpp:10-31)
+enum class EnergyModel : int { stable_neo_hookean = 0, stvk = 1 };
+
+struct MaterialParams {
+  double youngs = 1e6, poisson = 0.3, density = 1000.0;
+  double mu = 0.0, lambda = 0.0;
+  double sigma_thres = 1e5, r_d = 0.0;
+  double damp_mass_coeff = 0.0, damp_stiff_coeff = 0.0;
+  EnergyModel energy_model = EnergyModel::stable_neo_hookean;
+  // MaterialParams::from_youngs (material.cpp:17-30): Lame parameters derived, ranges validated (FormatError)
+  static MaterialParams from_youngs(double youngs, double poisson, double density, double sigma_thres,
+                                    double r_d = 0.0, EnergyModel model = EnergyModel::stable_neo_hookean) {
+    gf_material g;
+    check(gf_material_from_youngs(youngs, poisson, density, sigma_thres, r_d, (int32_t)model, &g));
+    return from_raw(g);
+  }
+  static MaterialParams from_raw(const gf_material& g) {
+    MaterialParams p;
+    p.youngs = g.youngs;
+    p.poisson = g.poisson;
+    p.density = g.density;
+    p.mu = g.mu;
+    p.lambda = g.lambda;
+    p.sigma_thres = g.sigma_thres;
+    p.r_d = g.r_d;
+    p.damp_mass_coeff = g.damp_mass_coeff;
+    p.damp_stiff_coeff = g.damp_stiff_coeff;
+    p.energy_model = (EnergyModel)g.energy_model;
+    return p;
+  }
+  gf_material raw() const {
+    gf_material g{};
+    g.youngs = youngs;
+    g.poisson = poisson;
+    g.density = density;
+    g.mu = mu;
+    g.lambda = lambda;
+    g.sigma_thres = sigma_thres;
+    g.r_d = r_d;
+    g.damp_mass_coeff = damp_mass_coeff;
+    g.damp_stiff_coeff = damp_stiff_coeff;
+    g.energy_model = (int32_t)energy_model;
+    return g;
+  }
+};
+
+// SolverConfig (solver.hpp:15-31), the reference's defaults
+struct SolverConfig {
+  double dt = 1e-3;
+  double newton_tol = 0.0;
+  int newton_max_iters = 40;
+  double cg_tol = 1e-8;
+  int cg_max_iters = 4000;
+  double ls_backtrack = 0.5;
+  double ls_sufficient_decrease = 1e-4;
+  int ls_max_halvings = 40;
+  Vec3 gravity = Vec3::Zero();
+  bool dynamic_full_newton = false;
+  int collision_substeps = 1;
+  gf_solver_config raw() const {
+    gf_solver_config c;
+    gf_solver_config_default(&c);
+    c.dt = dt;
+    c.newton_tol = newton_tol;
+    c.newton_max_iters = newton_max_iters;
+    c.cg_tol = cg_tol;
+    c.cg_max_iters = cg_max_iters;
+    c.ls_backtrack = ls_backtrack;
+    c.ls_sufficient_decrease = ls_sufficient_decrease;
+    c.ls_max_halvings = ls_max_halvings;
+    for (int a = 0; a < 3; ++a) c.gravity[a] = gravity[a];
+    c.dynamic_full_newton = dynamic_full_newton ? 1 : 0;
+    c.collision_substeps = collision_substeps;
+    return c;
+  }
+};
+
+// Schedule3 (collision.hpp:10-18): piecewise-linear keyframes (evaluated on the device side of the library)
+struct Schedule3 {
+  std::vector<double> times;
+  std::vector<Vec3> values;
+  bool empty() const { return times.empty(); }
+  static Schedule3 constant(const Vec3& v) { return Schedule3{{0.0}, {v}}; }
+};
+
+// BoundaryCondition (solver.hpp:35-47)
+struct BoundaryCondition {
+  enum class Kind { translate, rotate };
+  Kind kind = Kind::translate;
+  std::string name;
+  std::vector<int> nodes;
+  Schedule3 translation;
+  Vec3 axis_point = Vec3::Zero();
+  Vec3 axis_dir = Vec3::UnitX();
+  Schedule3 angle;
+};
+
+// Collider (collision.hpp:20-34)
+struct Collider {
+  enum class Kind { sphere, halfspace };
+  Kind kind = Kind::sphere;
+  Schedule3 center;
+  double radius = 0.0;
+  Vec3 point = Vec3::Zero();
+  Vec3 normal = Vec3::UnitZ();
+  double stiffness = 1e6, restitution = 0.0, friction = 0.0;
+};
+
+// StepStats (solver.hpp:49-55)
+struct StepStats {
+  int newton_iterations = 0, cg_iterations = 0, newly_broken = 0;
+  double residual = 0.0, load = 0.0;
+};
+
+// the C-struct forms (kept for C-ABI callers of the earlier facade)
 inline gf_material material_from_youngs(double E, double nu, double rho, double sigma_thres, double r_d = 0.0,
                                         int model = 0) {
   gf_material p;
@@ -112,21 +253,89 @@ class Simulation {
  public:
   Simulation(const TetMesh& mesh, const gf_material& material, const gf_solver_config& config,
              const std::vector<gf_boundary_condition>& bcs = {}, const std::vector<gf_collider>& colliders = {})
-      : mesh_(mesh) {
+      : mesh_(mesh), material_(MaterialParams::from_raw(material)) {
     gf_sim* s = nullptr;
     check(gf_sim_create(mesh.raw(), &material, &config, bcs.data(), (int32_t)bcs.size(), colliders.data(),
                         (int32_t)colliders.size(), &s));
     s_.reset(s);
+    config_.dt = config.dt;
+    config_.newton_tol = config.newton_tol;
+    config_.newton_max_iters = config.newton_max_iters;
+    config_.cg_tol = config.cg_tol;
+    config_.cg_max_iters = config.cg_max_iters;
+    config_.ls_backtrack = config.ls_backtrack;
+    config_.ls_sufficient_decrease = config.ls_sufficient_decrease;
+    config_.ls_max_halvings = config.ls_max_halvings;
+    config_.gravity = Vec3(config.gravity[0], config.gravity[1], config.gravity[2]);
+    config_.dynamic_full_newton = config.dynamic_full_newton != 0;
+    config_.collision_substeps = config.collision_substeps;
   }
-  gf_step_stats dynamic_step() {  // solver.hpp:71
+  // Simulation(TetMesh, MaterialParams, SolverConfig, vector<BoundaryCondition>, vector<Collider>) (solver.hpp:62-63)
+  Simulation(const TetMesh& mesh, const MaterialParams& material, const SolverConfig& config,
+             const std::vector<BoundaryCondition>& bcs = {}, const std::vector<Collider>& colliders = {})
+      : mesh_(mesh), material_(material), config_(config), colliders_(colliders) {
+    const gf_material m = material.raw();
+    const gf_solver_config c = config.raw();
+    std::vector<gf_boundary_condition> b(bcs.size());
+    std::vector<std::vector<int32_t>> nodes(bcs.size());
+    std::vector<std::vector<double>> kv(bcs.size() + colliders.size());
+    for (size_t i = 0; i < bcs.size(); ++i) {
+      const Schedule3& sc = bcs[i].kind == BoundaryCondition::Kind::translate ? bcs[i].translation : bcs[i].angle;
+      nodes[i].assign(bcs[i].nodes.begin(), bcs[i].nodes.end());
+      for (const Vec3& v : sc.values) kv[i].insert(kv[i].end(), v.begin(), v.end());
+      b[i] = gf_boundary_condition{};
+      b[i].kind = bcs[i].kind == BoundaryCondition::Kind::translate ? 0 : 1;
+      b[i].n_nodes = (int32_t)nodes[i].size();
+      b[i].nodes = nodes[i].data();
+      b[i].n_keys = (int32_t)sc.times.size();
+      b[i].key_times = sc.times.data();
+      b[i].key_values = kv[i].data();
+      for (int a = 0; a < 3; ++a) {
+        b[i].axis_point[a] = bcs[i].axis_point[a];
+        b[i].axis_dir[a] = bcs[i].axis_dir[a];
+      }
+    }
+    std::vector<gf_collider> k(colliders.size());
+    for (size_t i = 0; i < colliders.size(); ++i) {
+      const Collider& q = colliders[i];
+      std::vector<double>& v = kv[bcs.size() + i];
+      for (const Vec3& x : q.center.values) v.insert(v.end(), x.begin(), x.end());
+      k[i] = gf_collider{};
+      k[i].kind = q.kind == Collider::Kind::sphere ? 0 : 1;
+      k[i].n_keys = (int32_t)q.center.times.size();
+      k[i].key_times = q.center.times.data();
+      k[i].key_values = v.data();
+      k[i].radius = q.radius;
+      for (int a = 0; a < 3; ++a) {
+        k[i].point[a] = q.point[a];
+        k[i].normal[a] = q.normal[a];
+      }
+      k[i].stiffness = q.stiffness;
+      k[i].restitution = q.restitution;
+      k[i].friction = q.friction;
+    }
+    gf_sim* s = nullptr;
+    check(gf_sim_create(mesh.raw(), &m, &c, b.data(), (int32_t)b.size(), k.data(), (int32_t)k.size(), &s));
+    s_.reset(s);
+  }
+  StepStats dynamic_step() {  // solver.hpp:71
     gf_step_stats st;
     check(gf_sim_dynamic_step(s_.get(), &st));
-    return st;
+    return to_stats(st);
   }
-  gf_step_stats quasi_static_step(double t_load) {  // solver.hpp:76
+  StepStats quasi_static_step(double t_load) {  // solver.hpp:76
     gf_step_stats st;
     check(gf_sim_quasi_static_step(s_.get(), t_load, &st));
-    return st;
+    return to_stats(st);
+  }
+  const MaterialParams& material() const { return material_; }  // solver.hpp:81
+  const SolverConfig& config() const { return config_; }         // solver.hpp:82
+  const std::vector<Collider>& colliders() const { return colliders_; }
+  // run_scenario's per-step row + damage-log values as device reductions (scenario.cpp:640-672)
+  gf_step_metrics step_metrics() {
+    gf_step_metrics m;
+    check(gf_sim_step_metrics(s_.get(), &m));
+    return m;
   }
   double newton_tolerance() const { return gf_sim_newton_tolerance(s_.get()); }  // solver.hpp:96
   std::vector<int> damage_pass() {  // solver.hpp:67
@@ -174,7 +383,19 @@ class Simulation {
   struct Del {
     void operator()(gf_sim* s) const { gf_sim_destroy(s); }
   };
+  static StepStats to_stats(const gf_step_stats& g) {
+    StepStats s;
+    s.newton_iterations = g.newton_iterations;
+    s.cg_iterations = g.cg_iterations;
+    s.newly_broken = g.newly_broken;
+    s.residual = g.residual;
+    s.load = g.load;
+    return s;
+  }
   TetMesh mesh_;
+  MaterialParams material_;
+  SolverConfig config_;
+  std::vector<Collider> colliders_;
   std::unique_ptr<gf_sim, Del> s_;
   std::unique_ptr<VizMesh> viz_;
 };

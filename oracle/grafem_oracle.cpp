@@ -1510,9 +1510,8 @@ struct Sim {
     return stats;
   }
 
-  or_step_stats dynamic_step() {  // solver.cpp:219-333 (semi-implicit path)
+  or_step_stats dynamic_step() {  // solver.cpp:219-333 (semi-implicit step, or full Newton: solver.cpp:266-313)
     using clk = std::chrono::steady_clock;
-    if (cfg.full_newton) throw FormatError("dynamic_full_newton is outside the ported hot path");
     or_step_stats stats{};
     const double t = st.time, dt = cfg.dt;
     const int nn = mesh.nn(), ndof = 3 * nn;
@@ -1558,34 +1557,72 @@ struct Sim {
       }
     const double alpha = mat.damp_mass, beta = mat.damp_stiff;
 
-    const auto f_int = assemble_forces(mesh, st, mat);
-    assemble_stiffness(mesh, st, mat, K);
-    const auto kv = K.multiply(v);
-    std::vector<double> rhs(ndof);
-    for (int i = 0; i < ndof; ++i) rhs[i] = dt * (f_ext[i] + f_int[i]);
-    if (alpha != 0.0)
-      for (int i = 0; i < ndof; ++i) rhs[i] -= dt * alpha * (mass[i] * v[i]);
-    const double c = dt * beta + dt * dt;
-    for (int i = 0; i < ndof; ++i) rhs[i] -= c * kv[i];
-    const double kscale = dt * beta + dt * dt;
-    for (auto& x : K.val) x *= kscale;
-    std::vector<double> mdiag(ndof);
-    for (int i = 0; i < ndof; ++i) mdiag[i] = (1.0 + dt * alpha) * mass[i];
-    K.shift_diagonal(mdiag, 1.0);
-    auto t2 = clk::now();
+    // solver.cpp:264-313: one Newton iteration on the backward-Euler residual M dv - dt (f_ext + f(u + dt v+) - B v+)
+    // from v+ = v (semi-implicit), or up to newton_max_iters of them (dynamic_full_newton)
+    const int max_outer = cfg.full_newton ? cfg.newton_max_iters : 1;
+    const std::vector<V3> u_start = st.u;
+    std::vector<double> dv_total(ndof, 0.0);
+    auto t2 = clk::now(), t3 = t2;
+    double msum = 0.0;
+    for (double m : mass) msum += m;
+    for (int outer = 0; outer < max_outer; ++outer) {
+      const auto f_int = assemble_forces(mesh, st, mat);
+      assemble_stiffness(mesh, st, mat, K);
+      const auto kv = K.multiply(v);
+      std::vector<double> rhs(ndof);
+      for (int i = 0; i < ndof; ++i) rhs[i] = dt * (f_ext[i] + f_int[i]);
+      if (alpha != 0.0)
+        for (int i = 0; i < ndof; ++i) rhs[i] -= dt * alpha * (mass[i] * v[i]);
+      const double c = dt * beta + (outer == 0 ? dt * dt : 0.0);
+      for (int i = 0; i < ndof; ++i) rhs[i] -= c * kv[i];
+      if (outer > 0)
+        for (int i = 0; i < ndof; ++i) rhs[i] -= mass[i] * dv_total[i];
+      const double kscale = dt * beta + dt * dt;
+      for (auto& x : K.val) x *= kscale;
+      std::vector<double> mdiag(ndof);
+      for (int i = 0; i < ndof; ++i) mdiag[i] = (1.0 + dt * alpha) * mass[i];
+      K.shift_diagonal(mdiag, 1.0);
+      t2 = clk::now();
 
-    std::vector<double> fixed_rhs(ndof, 0.0);
-    for (int d : fixed) fixed_rhs[d] = fixed_dv[d];
-    std::vector<double> dv(ndof, 0.0);
-    std::vector<double> rhs_work = rhs;
-    solve_linear(dv, rhs_work, fixed, fixed_rhs, &stats.cg_iterations);
-    auto t3 = clk::now();
-    for (int i = 0; i < ndof; ++i) v[i] += dv[i];
-    for (int n = 0; n < nn; ++n)
-      for (int a = 0; a < 3; ++a) {
-        st.v[n][a] = v[3 * (size_t)n + a];
-        st.u[n][a] += dt * st.v[n][a];
+      std::vector<double> fixed_rhs(ndof, 0.0);
+      for (int d : fixed) fixed_rhs[d] = outer == 0 ? fixed_dv[d] : 0.0;
+      std::vector<double> dv(ndof, 0.0);
+      std::vector<double> rhs_work = rhs;
+      solve_linear(dv, rhs_work, fixed, fixed_rhs, &stats.cg_iterations);
+      t3 = clk::now();
+      for (int i = 0; i < ndof; ++i) {
+        dv_total[i] += dv[i];
+        v[i] += dv[i];
       }
+      if (!cfg.full_newton) break;
+      // the true residual at the trial state (solver.cpp:298-312)
+      for (int n = 0; n < nn; ++n)
+        for (int a = 0; a < 3; ++a) {
+          st.v[n][a] = v[3 * (size_t)n + a];
+          st.u[n][a] = u_start[n][a] + dt * st.v[n][a];
+        }
+      const auto f_new = assemble_forces(mesh, st, mat);
+      assemble_stiffness(mesh, st, mat, K);
+      std::vector<double> res(ndof);
+      for (int i = 0; i < ndof; ++i) res[i] = mass[i] * dv_total[i] - dt * (f_ext[i] + f_new[i]);
+      if (alpha != 0.0)
+        for (int i = 0; i < ndof; ++i) res[i] += dt * alpha * (mass[i] * v[i]);
+      if (beta != 0.0) {
+        const auto kvn = K.multiply(v);
+        for (int i = 0; i < ndof; ++i) res[i] += dt * beta * kvn[i];
+      }
+      for (int d : fixed) res[d] = 0.0;
+      stats.newton_iterations = outer + 1;
+      double rn = 0.0;
+      for (double x : res) rn += x * x;
+      if (std::sqrt(rn) <= std::max(newton_tol, 1e-12 * msum)) break;
+    }
+    if (!cfg.full_newton)
+      for (int n = 0; n < nn; ++n)
+        for (int a = 0; a < 3; ++a) {
+          st.v[n][a] = v[3 * (size_t)n + a];
+          st.u[n][a] += dt * st.v[n][a];
+        }
     for (const auto& bc : bcs)
       for (int n : bc.nodes) {
         const V3 d1 = bc.displacement_at(mesh, n, t + dt), d0 = bc.displacement_at(mesh, n, t);

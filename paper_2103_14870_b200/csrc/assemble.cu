@@ -27,9 +27,17 @@ constexpr int kBlkStride = 32 * 27 + 9;  // per warp: 27 doubles per lane + the 
 // contribution of tet e to node-row i (local index li): force on i (returned), the diagonal block K(li, li)
 // (returned in dg) and the three off-diagonal blocks K(li, lj), written straight to shared memory at slot
 // s = lj < li ? lj : lj - 1 (blk[9 s + r]) so they never occupy registers together
+// shape gradient of local node l (component a) from B^-1: g_0 = -(row 0 + row 1 + row 2), g_l = row l - 1. The runtime
+// row index keeps B in a 72-byte local-memory array (L1-resident); the select form without a stack frame was measured
+// 23 % slower at c3 (0.482 vs 0.393 ms: more live registers in the block loop)
+__device__ __forceinline__ double shape_grad(const double B[9], int l, int a) {
+  return l == 0 ? -((B[a] + B[3 + a]) + B[6 + a]) : B[3 * (l - 1) + a];
+}
+
 template <bool kBlocks>
 __device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, int4 t, const double B[9], int li,
-                                            double scale, double f[3], double* blk, double dg[9]) {
+                                            double scale, double f[3], double* blk, double dg[9],
+                                            double* psi = nullptr) {
   const int id[4] = {t.x, t.y, t.z, t.w};
   double du[9], F[9];
   {
@@ -45,9 +53,11 @@ __device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, i
   double gi[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
-    gi[a] = (li == 0) ? -((B[a] + B[3 + a]) + B[6 + a]) : B[3 * (li - 1) + a];
+    gi[a] = shape_grad(B, li, a);
   double P[9];
   const double J = pk1(F, m, P);
+  // the tet's strain energy chi V Psi(F) (fem.cpp:190-199), fused: evaluated by the lane of its local node 0 only
+  if (psi && li == 0) *psi += scale * energy_density(F, m);
 #pragma unroll
   for (int a = 0; a < 3; ++a) f[a] = -scale * ((P[3 * a] * gi[0] + P[3 * a + 1] * gi[1]) + P[3 * a + 2] * gi[2]);
   if (!kBlocks) return;
@@ -73,7 +83,7 @@ __device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, i
     for (int lj = 0; lj < 4; ++lj) {
       double gj[3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) gj[a] = (lj == 0) ? -((B[a] + B[3 + a]) + B[6 + a]) : B[3 * (lj - 1) + a];
+      for (int a = 0; a < 3; ++a) gj[a] = shape_grad(B, lj, a);
       double aj[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) aj[a] = F[3 * a] * gj[0] + F[3 * a + 1] * gj[1] + F[3 * a + 2] * gj[2];
@@ -103,7 +113,7 @@ __device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, i
     for (int lj = 0; lj < 4; ++lj) {
       double gj[3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) gj[a] = (lj == 0) ? -((B[a] + B[3 + a]) + B[6 + a]) : B[3 * (lj - 1) + a];
+      for (int a = 0; a < 3; ++a) gj[a] = shape_grad(B, lj, a);
       double aj[3], bj[3], cr[3], w[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
@@ -230,7 +240,7 @@ __device__ __forceinline__ void element_row_edge(const DevData& d, int e, int4 t
 // lane work of the row kernels: tet e's contribution to node row li (F-based closed form or edge record)
 template <bool kEdge, bool kBlocks>
 __device__ __forceinline__ void lane_element(const DevData& d, const MatDev& m, int e, int4 t, int li, double f[3],
-                                             double* blk, double dg[9]) {
+                                             double* blk, double dg[9], double* psi = nullptr) {
   if (kEdge) {
     const uint8_t fl = __ldg(d.eflag + e);
     if (fl == 0) {
@@ -259,7 +269,7 @@ __device__ __forceinline__ void lane_element(const DevData& d, const MatDev& m, 
   load_rest(d, e, B, vol);
   const double scale = d.chi[e] * vol;
   if (scale != 0.0) {  // fem.cpp:51 / fem.cpp:114 early-out
-    element_row<kBlocks>(d, m, t, B, li, scale, f, blk, dg);
+    element_row<kBlocks>(d, m, t, B, li, scale, f, blk, dg, psi);
   } else if (kBlocks) {
 #pragma unroll
     for (int r = 0; r < 27; ++r) blk[r] = 0.0;
@@ -331,7 +341,7 @@ __device__ __forceinline__ void finish_column(const DevData& d, const StepCoeffs
   } else if (__ldg(d.node_bc + j) >= 0) {  // fixed column: move A_ij * dv_j to the rhs, zero it
     double fj[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) fj[a] = d.fv[3 * (size_t)j + a];
+    for (int a = 0; a < 3; ++a) fj[a] = sc.fixed_zero ? 0.0 : d.fv[3 * (size_t)j + a];
 #pragma unroll
     for (int a = 0; a < 3; ++a) corr[a] += A[3 * a] * fj[0] + A[3 * a + 1] * fj[1] + A[3 * a + 2] * fj[2];
 #pragma unroll
@@ -359,14 +369,16 @@ __device__ __forceinline__ void finish_row(const DevData& d, const StepCoeffs& s
   if (d.fint_out) d.fint_out[dof] = fsum;
   if (kMode == kAssembleSystem) {
     if (fixed_i) {
-      d.rhs[dof] = d.fv[dof];
-      d.x[dof] = d.fv[dof];
+      const double fv = sc.fixed_zero ? 0.0 : d.fv[dof];
+      d.rhs[dof] = fv;
+      d.x[dof] = fv;
     } else {
       const double mv = __ldg(d.mass + i) * d.v[dof];
       const double fe = sc.use_ext ? d.fext[dof] + d.fcoll[dof] : 0.0;
       double r = sc.rhs_fint_scale * (fe + fsum);
       r -= sc.rhs_mv_scale * mv;
       r -= sc.rhs_kv_scale * kva;
+      if (sc.mdv) r -= __ldg(d.mass + i) * sc.mdv[dof];
       r -= corra;
       d.rhs[dof] = r;
       d.x[dof] = 0.0;
@@ -380,6 +392,9 @@ __device__ __forceinline__ void finish_row(const DevData& d, const StepCoeffs& s
 //  2. the row's 9*deg outputs (column c, entry q) are spread over the 32 lanes; each sums its precomputed
 //     contribution list (ascending tet order, deterministic) from s_blk into s_row
 //  3. lane c finishes column block c: K v, A = kscale K + mscale M, Dirichlet projection, SELL-32 store
+#ifndef GF_ASM_FUSED_ENERGY
+#define GF_ASM_FUSED_ENERGY 1  // the tet energies of the assembled state as a by-product of the force pass
+#endif
 #ifndef GF_ASM_MINB
 #define GF_ASM_MINB 4
 #endif
@@ -399,12 +414,18 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
 
   double f[3] = {0.0, 0.0, 0.0};
   double dg[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  constexpr bool kFusedEnergy = kMode == kAssembleSystem && !kEdge && GF_ASM_FUSED_ENERGY;  // edge form: k_tet_edge
+  double psi = 0.0;
   if (lane < np) {
     const int e = __ldg(d.nt_tet + p0 + lane);
     const int4 t = __ldg(d.tets + e);
     const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
     double* blk = kBlocks ? &s_blk[w][27 * lane] : nullptr;
-    lane_element<kEdge, kBlocks>(d, m, e, t, li, f, blk, dg);
+    lane_element<kEdge, kBlocks>(d, m, e, t, li, f, blk, dg, kFusedEnergy ? &psi : nullptr);
+  }
+  if (kFusedEnergy) {  // per-row sum of the energies of the tets whose local node 0 is this row (fixed butterfly)
+    const double ps = warp_sum(psi);
+    if (lane == 0) d.eng_row[i] = ps;
   }
   // the row's force (fem.cpp:104-106) and its diagonal block (every incident tet contributes) are fixed
   // butterfly sums over the lanes; only the off-diagonal blocks (the ~5 tets around each edge) go through
@@ -485,6 +506,8 @@ __global__ void __launch_bounds__(32 * kWarps) k_assemble_big(DevData d, MatDev 
     __syncwarp();
   }
   double facc[3] = {0.0, 0.0, 0.0}, dacc[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  constexpr bool kFusedEnergy = kMode == kAssembleSystem && !kEdge && GF_ASM_FUSED_ENERGY;
+  double psi = 0.0;  // accumulated per lane across chunks (each tet's energy added by one lane, once)
   for (int ch = 0; ch < np; ch += 32) {
     const int l = ch + lane;
     double f[3] = {0.0, 0.0, 0.0}, dg[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -494,7 +517,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_assemble_big(DevData d, MatDev 
       const int e = __ldg(d.nt_tet + p0 + l);
       const int4 t = __ldg(d.tets + e);
       const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
-      lane_element<kEdge, kBlocks>(d, m, e, t, li, f, blk, dg);
+      lane_element<kEdge, kBlocks>(d, m, e, t, li, f, blk, dg, kFusedEnergy ? &psi : nullptr);
       wrote = true;
     }
     if (kBlocks && !wrote)
@@ -525,6 +548,10 @@ __global__ void __launch_bounds__(32 * kWarps) k_assemble_big(DevData d, MatDev 
   for (int a = 0; a < 3; ++a) {
     const double t = warp_sum(facc[a]);
     if (lane == a) fsum = t;
+  }
+  if (kFusedEnergy) {
+    const double ps = warp_sum(psi);
+    if (lane == 0) d.eng_row[i] = ps;
   }
   const bool fixed_i = __ldg(d.node_bc + i) >= 0;
   double kv[3] = {0.0, 0.0, 0.0}, corr[3] = {0.0, 0.0, 0.0};
@@ -572,7 +599,7 @@ __device__ __forceinline__ double block_sum256(double v, double* sm) {
 
 // mode 0: per-tet record (chi V t, chi V M) for the row kernel + the tet energies chi V Psi summed into
 //         *d.eng_out (deterministic: block tree, then the last block sums the block partials in block order);
-//         tets the edge form cannot evaluate (stable NH with det C <= 1e-12: J -> 0, C^-1 unbounded) are listed for
+//         tets the edge form cannot evaluate accurately (stable NH with |J| < 0.05, see below) are listed for
 //         k_tet_edge_fallback (F-based rows); chi V = 0 tets are flagged and skipped (fem.cpp:51, 114, 194).
 // mode 1: edge_decomposed_forces (fem.cpp:57-94) -- c_k = 2 V t_k |d_k| (rest volume, no chi: the reference's
 //         convention); ok = 0 on a current edge shorter than 1e-14 or det C <= 0.
@@ -669,7 +696,10 @@ __global__ void __launch_bounds__(kTetTpb) k_tet_edge(DevData d, MatDev m, int m
         const double C[9] = {1.0 + 2.0 * E[0], 2.0 * E[3], 2.0 * E[4], 2.0 * E[3], 1.0 + 2.0 * E[1], 2.0 * E[5],
                              2.0 * E[4], 2.0 * E[5], 1.0 + 2.0 * E[2]};
         const double detC = det3(C);
-        ok = detC > 1e-12;
+        // conditioning: the edge form's Hessian loses ~1e-16 / |J|^3 of relative accuracy (C^-1 terms of size 1/J^2
+        // cancel against the rank-1 edge products): measured 5e-11 at |J| = 0.01, 3e-6 at 2e-4. Below |J| = 0.05
+        // (error < 1e-12) the tet takes the F-based rows instead (k_tet_edge_fallback).
+        ok = mode == 1 ? detC > 0.0 : detC > 0.0025;
         if (ok) {
           double dcur[3][3];  // current edge vectors 01, 02, 03 (columns) for the orientation sign
 #pragma unroll

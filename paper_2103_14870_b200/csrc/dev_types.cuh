@@ -29,7 +29,8 @@ struct StepCoeffs {  // per-step scalars of solver.cpp:279-289
   double kscale;          // dt*beta + dt*dt
   double mscale;          // 1 + dt*alpha
   int32_t use_ext;        // 1: rhs includes f_ext + f_coll (dynamic); 0: internal forces only (quasi-static)
-  int32_t _pad;
+  int32_t fixed_zero;     // 1: Dirichlet rows prescribe 0 instead of fv (full-Newton iterations > 0, solver.cpp:291)
+  const double* mdv;      // non-null: rhs -= M dv_total (full-Newton iterations > 0, solver.cpp:282)
 };
 
 // one entry per boundary condition, evaluated by the host each step (solver.cpp:22-29)
@@ -144,7 +145,9 @@ struct DevData {
   int32_t efall_cap;
   double* eng_part;         // tet_edge_blocks(nt) block partials of the fused energy
   unsigned* eng_ticket;
-  double* eng_out;          // total strain energy of the state the last edge-form assembly evaluated
+  double* eng_out;          // total strain energy of the state the last assembly evaluated (both element forms)
+  double* eng_row;          // nn: F-based form, per-row sums of the energies of the tets whose local node 0 is the row
+  int32_t eng_sum;          // 1: k_integrate reduces eng_row into eng_out (F-based form's dynamic step)
   double* ecoef;            // 6 nt edge decomposition coefficients (parity hook)
   uint8_t* eok;             // nt
   // misc
@@ -213,6 +216,9 @@ void launch_bsr_dinv(const DevData& d, cudaStream_t s);
 void launch_fill(double* p, double v, int64_t n, cudaStream_t s);
 void launch_qs_bc(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, cudaStream_t s);
 void launch_qs_update(double* u, const double* saved, const double* dx, double step, int64_t n, cudaStream_t s);
+// dynamic_full_newton (solver.cpp:296-303): dv_total += dv, v += dv, u = u_start + dt v; and the final BC pinning
+void launch_newton_update(const DevData& d, double* dv_total, const double* u_start, double dt, cudaStream_t s);
+void launch_pin_bc(const DevData& d, cudaStream_t s);
 // ---- metrics.cu (device reductions; the last block writes the result) ----
 size_t metrics_partial_doubles();
 // out[0..4] = strain energy, kinetic energy, chi sum, broken edges, chi min

@@ -5,7 +5,8 @@
 //             total_strain_energy (fem.cpp:190-199: chi V Psi(F) of every tet with chi V != 0), kinetic_energy
 //             (fem.cpp:201-206: 1/2 m |v|^2 per node), broken-edge count (SimState::broken_edge_count), chi min and
 //             chi sum (log_damage's chi_min / chi_mean).
-//  k_dot      a . b (the quasi-static Newton residual norm and line-search slope, solver.cpp:148, 168).
+//  k_dot      a . b (the quasi-static Newton residual norm and line-search slope, solver.cpp:148, 168), or sum a
+//             (b = null: the fused assembly energy's per-row partials).
 // Deterministic: a fixed partition of kBlocks blocks (independent of the device), per-block fixed trees, and the
 // last block to finish (ticket) sums the block partials in block order and writes the result, so the values are
 // bit-reproducible run to run. They differ from the reference's serial ascending sums at rounding level only.
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(kTpb) k_dot(const double* a, const double* b, 
                                               unsigned* ticket, double* out) {
   __shared__ double s[kTpb];
   double acc = 0.0;
-  for (int64_t k = (int64_t)blockIdx.x * kTpb + threadIdx.x; k < n; k += (int64_t)kBlocks * kTpb) acc += a[k] * b[k];
+  for (int64_t k = (int64_t)blockIdx.x * kTpb + threadIdx.x; k < n; k += (int64_t)kBlocks * kTpb) acc += b ? a[k] * b[k] : a[k];
   const double r = block_tree(acc, s, false);
   if (threadIdx.x == 0) partials[blockIdx.x] = r;
   if (!last_block(ticket)) return;

@@ -164,22 +164,51 @@ __global__ void k_collide_load(const double* partials, int nblocks, int nc, int 
 
 // enqueued right behind the PCG: it commits the step only when the solve converged (cg_out[1]), so the host
 // needs no round trip before it; after a failed solve the host runs the ladder and enqueues it again
-__global__ void k_integrate(DevData d, double dt) {
-  if (d.cg_out[1] == 0.0) return;
+// also finishes the F-based assembly's fused energy (d.eng_sum): the per-row partials of the step's assembled state are
+// summed by a fixed block tree, and the last block sums the block partials in block order (deterministic)
+__global__ void __launch_bounds__(kTpb) k_integrate(DevData d, double dt) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= d.nn) return;
-  const bool fixed = d.node_bc[i] >= 0;
+  if (d.cg_out[1] != 0.0 && i < d.nn) {
+    const bool fixed = d.node_bc[i] >= 0;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const size_t k = 3 * (size_t)i + a;
-    if (fixed) {
-      d.u[k] = d.utgt[k];
-      d.v[k] = d.vtgt[k];
-    } else {
-      const double v = d.v[k] + d.x[k];
-      d.v[k] = v;
-      d.u[k] = d.u[k] + dt * v;
+    for (int a = 0; a < 3; ++a) {
+      const size_t k = 3 * (size_t)i + a;
+      if (fixed) {
+        d.u[k] = d.utgt[k];
+        d.v[k] = d.vtgt[k];
+      } else {
+        const double v = d.v[k] + d.x[k];
+        d.v[k] = v;
+        d.u[k] = d.u[k] + dt * v;
+      }
     }
+  }
+  if (!d.eng_sum) return;
+  __shared__ double s[kTpb];
+  __shared__ bool s_last;
+  s[threadIdx.x] = i < d.nn ? d.eng_row[i] : 0.0;
+  __syncthreads();
+  for (int o = kTpb / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) s[threadIdx.x] = s[threadIdx.x] + s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) d.eng_part[blockIdx.x] = s[0];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(d.eng_ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += kTpb) acc = acc + __ldcg(d.eng_part + b);
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = kTpb / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) s[threadIdx.x] = s[threadIdx.x] + s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *d.eng_out = s[0];
+    *d.eng_ticket = 0u;
   }
 }
 
@@ -249,6 +278,28 @@ __global__ void k_fill(double* p, double v, int64_t n) {
   if (i < n) p[i] = v;
 }
 
+// dynamic_full_newton update after each Newton solve (solver.cpp:296-303): dv_total += dv, v += dv on every dof
+// (fixed dofs carry their prescribed dv), u = u_start + dt v
+__global__ void k_newton_update(DevData d, double* dv_total, const double* u_start, double dt) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= 3 * (int64_t)d.nn) return;
+  const double dv = d.x[k];
+  dv_total[k] = dv_total[k] + dv;
+  const double v = d.v[k] + dv;
+  d.v[k] = v;
+  d.u[k] = u_start[k] + dt * v;
+}
+
+__global__ void k_pin_bc(DevData d) {  // solver.cpp:322-328
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d.nn || d.node_bc[i] < 0) return;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    d.u[3 * (size_t)i + a] = d.utgt[3 * (size_t)i + a];
+    d.v[3 * (size_t)i + a] = d.vtgt[3 * (size_t)i + a];
+  }
+}
+
 }  // namespace
 
 void launch_bc_targets(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, double dt, cudaStream_t s) {
@@ -265,6 +316,10 @@ void launch_collide_load(const DevData& d, int nsub, double* out, cudaStream_t s
   const int nc = d.n_colliders < 8 ? d.n_colliders : 8;
   k_collide_load<<<1, 256, 0, s>>>(d.coll_partials, nblk(d.nn), nc, nsub, out);
 }
+void launch_newton_update(const DevData& d, double* dv_total, const double* u_start, double dt, cudaStream_t s) {
+  k_newton_update<<<nblk(3 * (int64_t)d.nn), kTpb, 0, s>>>(d, dv_total, u_start, dt);
+}
+void launch_pin_bc(const DevData& d, cudaStream_t s) { k_pin_bc<<<nblk(d.nn), kTpb, 0, s>>>(d); }
 void launch_integrate(const DevData& d, double dt, cudaStream_t s) { k_integrate<<<nblk(d.nn), kTpb, 0, s>>>(d, dt); }
 void launch_shift_diag(const DevData& d, double shift, cudaStream_t s) {
   k_shift_diag<<<nblk(d.nn), kTpb, 0, s>>>(d, shift);

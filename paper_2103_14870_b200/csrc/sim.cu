@@ -180,7 +180,6 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   if (!(cfg.ls_sufficient_decrease > 0.0 && cfg.ls_sufficient_decrease < 1.0))
     throw FormatError("line-search sufficient-decrease constant must be in (0, 1)");
   if (cfg.collision_substeps < 1) throw FormatError("collision_substeps must be >= 1");
-  if (cfg.dynamic_full_newton) throw FormatError("dynamic_full_newton is outside the B200 hot path");
   for (int c = 0; c < n_cols; ++c) {
     const gf_collider& k = cols[c];
     const double nn = std::sqrt((k.normal[0] * k.normal[0] + k.normal[1] * k.normal[1]) + k.normal[2] * k.normal[2]);
@@ -496,7 +495,12 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
       d_.efall_count = reinterpret_cast<int32_t*>(d_stats_ + 6);
       d_.eng_part = (double*)zeros(8 * (size_t)tet_edge_blocks(nt));
       d_.eng_ticket = (unsigned*)zeros(64);
-      d_.eng_out = d_stats_ + 7;
+    }
+    d_.eng_out = d_stats_ + 7;
+    d_.eng_row = (double*)zeros(8 * (size_t)nn);
+    if (!edge_form_) {  // the F-based form's energy partials are reduced by k_integrate (misc.cu)
+      d_.eng_part = (double*)zeros(8 * (size_t)((nn + 255) / 256));
+      d_.eng_ticket = (unsigned*)zeros(64);
     }
   }
   d_energy_partials_ = (double*)zeros(8 * metrics_partial_doubles());
@@ -581,6 +585,9 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     cg_.cta_first = (const int32_t*)up(first.data(), 4 * first.size());
   }
   if (std::getenv("GF_CG_TRACE")) cg_.trace = (unsigned long long*)zeros(8 * 5000);
+  if (const char* e = std::getenv("GF_GRAPH")) graphs_enabled_ = std::atoi(e) != 0;
+  GF_CUDA(cudaEventCreate(&pcg_ev_[0]));
+  GF_CUDA(cudaEventCreate(&pcg_ev_[1]));
   cg_.tol = cfg.cg_tol;
   GF_CUDA(cudaStreamSynchronize(stream_));
   GF_CUDA(cudaGetLastError());
@@ -607,6 +614,10 @@ gf_sim_info Simulation::info() const {
 
 Simulation::~Simulation() {
   if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& e : step_exec_)
+    if (e) cudaGraphExecDestroy(e);
+  for (auto e : pcg_ev_)
+    if (e) cudaEventDestroy(e);
   for (auto& p : pending_) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
@@ -625,6 +636,15 @@ Simulation::~Simulation() {
 // ---------------------------------------------------------------- launch bookkeeping / profiling
 template <class F>
 void Simulation::launch(const char* name, double bytes, F&& f) {
+  if (capturing_) {  // recorded into the step graph; counted at replay (dynamic_step)
+    capture_list_.emplace_back(name, bytes);
+    const bool ev = profiling_ == 2 && std::strcmp(name, "pcg") == 0;
+    if (ev) GF_CUDA(cudaEventRecordWithFlags(pcg_ev_[0], stream_, cudaEventRecordExternal));  // an event node
+    f();
+    GF_CUDA(cudaGetLastError());
+    if (ev) GF_CUDA(cudaEventRecordWithFlags(pcg_ev_[1], stream_, cudaEventRecordExternal));
+    return;
+  }
   if (!profiling_) {
     f();
     GF_CUDA(cudaGetLastError());
@@ -771,7 +791,7 @@ double Simulation::run_cg(int max_iters) {
   const double N = mesh_.nn, NB = pat_.cols.size();
   // bytes are filled in after the run from the iteration count (see dynamic_step)
   launch("pcg", 0.0 * (N + NB), [&] { launch_cg(); });
-  GF_CUDA(cudaMemcpyAsync(h_stats_, d_.cg_out, 32, cudaMemcpyDeviceToHost, stream_));
+  GF_CUDA(cudaMemcpyAsync(h_stats_, d_stats_, 64, cudaMemcpyDeviceToHost, stream_));  // the whole stats record
   synchronize();
   return h_stats_[0];
 }
@@ -808,13 +828,18 @@ void Simulation::solve_ladder(bool ok, int32_t* iters, Acc&& account) {
 
 // force + stiffness assembly (fem.cpp:96-169 fused with solver.cpp:275-295): the F-based row kernel, or the
 // edge-length form (k_tet_edge once per tet -> records + fused energy, then the edge row kernel)
-void Simulation::assemble(const StepCoeffs& c, int mode, const char* name, double bytes) {
+void Simulation::assemble(const StepCoeffs& c, int mode, const char* name, double bytes, bool energy_in_integrate) {
   if (edge_form_) {
     const double T = mesh_.nt, N = mesh_.nn;
     // reads conn 16, rest record 80, chi 8 per tet and X, u once (48 per node); writes the 224-byte record
     launch("tet_edge", 328.0 * T + 48.0 * N, [&] { launch_tet_edge(d_, md_, 0, stream_); });
   }
   launch(name, bytes, [&] { launch_assemble(d_, md_, c, mode, stream_); });
+  // the F-based form's fused energy: per-row partials -> one deterministic sum, folded into the step's k_integrate
+  // (dynamic_step) or a separate reduction (quasi-static Newton)
+  if (!edge_form_ && mode == kAssembleSystem && !energy_in_integrate)
+    launch("energy_sum", 8.0 * mesh_.nn,
+           [&] { launch_dot(d_.eng_row, nullptr, mesh_.nn, d_energy_partials_, d_red_ticket_, d_.eng_out, stream_); });
 }
 
 void Simulation::check_edge_fallback() {  // h_stats_ holds the step's record
@@ -827,7 +852,6 @@ void Simulation::check_edge_fallback() {  // h_stats_ holds the step's record
 }
 
 double Simulation::assembly_energy() {
-  if (!edge_form_) throw FormatError("the fused assembly energy needs the edge-length element form (GF_ELEMENT=edge)");
   GF_CUDA(cudaMemcpyAsync(h_partials_, d_.eng_out, 8, cudaMemcpyDeviceToHost, stream_));
   synchronize();
   return h_partials_[0];
@@ -845,34 +869,49 @@ void Simulation::edge_forces(double* coeff6, uint8_t* ok) {  // edge_decomposed_
   synchronize();
 }
 
-gf_step_stats Simulation::dynamic_step() {
-  gf_step_stats st{};
-  const double t = time_, dt = cfg_.dt;
-  run_damage(true, false, true);
+// host-side per-step parameters (pinned records, read by the step's H2D copies): collider states at each substep
+// probe time (solver.cpp:233-249, Schedule3 eval/rate) and the boundary-condition displacements at t and t + dt
+// (solver.cpp:22-29, 255-262)
+void Simulation::fill_step_params(double t, double dt) {
+  const int nsub = cfg_.collision_substeps;
+  const size_t nc = cols_.size();
+  for (int s = 0; s < nsub && nc; ++s) {
+    const double tau = dt * (double)s / (double)nsub;
+    for (size_t c = 0; c < nc; ++c) {
+      ColliderDev& k = h_cols_[s * nc + c];
+      std::memset(&k, 0, sizeof k);
+      k.kind = cols_[c].kind;
+      if (k.kind == 0) {
+        cols_[c].center.eval(t + tau, k.center);
+        cols_[c].center.rate(t + tau, k.cvel);
+      }
+      k.radius = cols_[c].radius;
+      for (int a = 0; a < 3; ++a) {
+        k.point[a] = cols_[c].point[a];
+        k.normal[a] = cols_[c].normal[a];
+      }
+      k.stiffness = cols_[c].stiffness;
+      k.restitution = cols_[c].restitution;
+      k.friction = cols_[c].friction;
+    }
+  }
+  for (size_t b = 0; b < bcs_.size(); ++b) {
+    BcStep& q = h_bcstep_[b];
+    std::memset(&q, 0, sizeof q);
+    q.kind = bcs_[b].kind;
+    bcs_[b].displacement_params(t, q.d0, q.R0);
+    bcs_[b].displacement_params(t + dt, q.d1, q.R1);
+    for (int a = 0; a < 3; ++a) q.axis_point[a] = bcs_[b].axis_point[a];
+  }
+}
 
+// the device work of one dynamic_step, enqueued on the stream (or captured into the step graph): no host decision
+// inside, the only read-back is the 64-byte stats record at the end
+void Simulation::enqueue_prologue(double dt) {  // damage pass, collider forces, BC targets (solver.cpp:225-262)
+  run_damage(true, false, true);
   const int nsub = cfg_.collision_substeps;
   if (!cols_.empty()) {
     const size_t nc = cols_.size();
-    for (int s = 0; s < nsub; ++s) {
-      const double tau = dt * (double)s / (double)nsub;
-      for (size_t c = 0; c < nc; ++c) {
-        ColliderDev& k = h_cols_[s * nc + c];
-        std::memset(&k, 0, sizeof k);
-        k.kind = cols_[c].kind;
-        if (k.kind == 0) {
-          cols_[c].center.eval(t + tau, k.center);
-          cols_[c].center.rate(t + tau, k.cvel);
-        }
-        k.radius = cols_[c].radius;
-        for (int a = 0; a < 3; ++a) {
-          k.point[a] = cols_[c].point[a];
-          k.normal[a] = cols_[c].normal[a];
-        }
-        k.stiffness = cols_[c].stiffness;
-        k.restitution = cols_[c].restitution;
-        k.friction = cols_[c].friction;
-      }
-    }
     GF_CUDA(cudaMemcpyAsync(d_cols_, h_cols_, sizeof(ColliderDev) * nc * nsub, cudaMemcpyHostToDevice, stream_));
     for (int s = 0; s < nsub; ++s) {
       const double tau = dt * (double)s / (double)nsub;
@@ -881,9 +920,13 @@ gf_step_stats Simulation::dynamic_step() {
     launch("collide_load", 0.0, [&] { launch_collide_load(d_, nsub, d_load_, stream_); });
   }
   if (!bcs_.empty()) {
-    upload_bc_step(t, dt);
+    GF_CUDA(cudaMemcpyAsync(d_bcstep_, h_bcstep_, sizeof(BcStep) * bcs_.size(), cudaMemcpyHostToDevice, stream_));
     launch("bc_targets", 96.0 * n_fixed_, [&] { launch_bc_targets(d_, n_fixed_, d_fixed_nodes_, dt, stream_); });
   }
+}
+
+void Simulation::enqueue_step(double dt) {
+  enqueue_prologue(dt);
   StepCoeffs c{};
   c.use_ext = 1;
   c.dt = dt;
@@ -895,17 +938,145 @@ gf_step_stats Simulation::dynamic_step() {
   // algorithmic bytes: SURVEY.md §8(d) B_F = 16n + 104T + 8Z (n = 3N dofs, Z scalar nonzeros)
   const double n = 3.0 * mesh_.nn, T = mesh_.nt, Z = 9.0 * pat_.cols.size();
   d_.fint_out = nullptr;
-  assemble(c, kAssembleSystem, "assemble", 16 * n + 104 * T + 8 * Z);
-
-  // solve_linear (solver.cpp:105-136): first attempt, 4x retry, then cumulative diagonal shifts
+  assemble(c, kAssembleSystem, "assemble", 16 * n + 104 * T + 8 * Z, true);
+  // solve_linear (solver.cpp:105-136): first attempt here; the 4x retry and the diagonal shifts run on the host
+  // only when the stats record says this one failed
   cg_.max_iters = cfg_.cg_max_iters;
   cg_.x0_identity = 1;  // x0 from the assembly's epilogue (fixed rows: prescribed values, identity rows)
   launch("pcg", 0.0, [&] { launch_cg(); });
   cg_.x0_identity = 0;
+  d_.eng_sum = edge_form_ ? 0 : 1;
   launch("integrate", 40 * n, [&] { launch_integrate(d_, dt, stream_); });  // B_int = 40n; no-op if not converged
+  d_.eng_sum = 0;
   // cg_out, load, newly broken, edge-form fallback count, assembled-state energy
   GF_CUDA(cudaMemcpyAsync(h_stats_, d_stats_, 64, cudaMemcpyDeviceToHost, stream_));
+}
+
+// CUDA-graph step orchestration: the step's ~10 launches and copies are captured once per
+// profiling level (0: none; 2: events around the PCG solve) and replayed; the per-step host parameters travel
+// through pinned records that the graph's copy nodes read at replay time. Falls back to direct launches when the
+// capture fails (GF_GRAPH=0 disables it).
+bool Simulation::launch_step_graph(double dt) {
+  if (!graphs_enabled_ || profiling_ == 1) return false;
+  const int lvl = profiling_ == 2 ? 1 : 0;
+  if (!step_exec_[lvl]) {
+    capture_list_.clear();
+    capturing_ = true;
+    cudaGraph_t gr = nullptr;
+    bool ok = cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      try {
+        enqueue_step(dt);
+      } catch (...) {
+        ok = false;
+      }
+      ok = (cudaStreamEndCapture(stream_, &gr) == cudaSuccess) && ok;
+    }
+    capturing_ = false;
+    if (ok) ok = cudaGraphInstantiate(&step_exec_[lvl], gr, 0) == cudaSuccess;
+    if (gr) cudaGraphDestroy(gr);
+    if (!ok) {
+      cudaGetLastError();
+      step_exec_[lvl] = nullptr;
+      graphs_enabled_ = false;
+      return false;
+    }
+    step_list_[lvl] = capture_list_;
+  }
+  GF_CUDA(cudaGraphLaunch(step_exec_[lvl], stream_));
+  replayed_ = lvl + 1;
+  return true;
+}
+
+// dynamic_full_newton (solver.cpp:264-313): Newton iterations on the backward-Euler residual
+// M dv - dt (f_ext + f(u_start + dt v+) - B v+), each a fused assembly + PCG solve. The system assembled at a trial
+// state is exactly the next iteration's (its rhs is -residual, fixed rows 0), so the residual norm is taken from it and
+// it is reused -- one assembly per iteration where the reference assembles twice.
+gf_step_stats Simulation::dynamic_step_full_newton() {
+  gf_step_stats st{};
+  const double t = time_, dt = cfg_.dt;
+  const size_t nd = 3 * (size_t)mesh_.nn;
+  if (!d_usave_) {
+    d_usave_ = (double*)dalloc(8 * nd);
+    d_ubackup_ = (double*)dalloc(8 * nd);
+  }
+  double* dv_total = d_ubackup_;
+  fill_step_params(t, dt);
+  enqueue_prologue(dt);
+  GF_CUDA(cudaMemcpyAsync(d_usave_, d_.u, 8 * nd, cudaMemcpyDeviceToDevice, stream_));
+  GF_CUDA(cudaMemsetAsync(dv_total, 0, 8 * nd, stream_));
+  const double n = (double)nd, T = mesh_.nt, Z = 9.0 * pat_.cols.size();
+  double msum = 0.0;
+  for (double m : mass_) msum += 3.0 * m;
+  const double tol = std::max(newton_tol_, 1e-12 * msum);
+  auto coeffs = [&](int outer) {
+    StepCoeffs c{};
+    c.use_ext = 1;
+    c.dt = dt;
+    c.rhs_fint_scale = dt;
+    c.rhs_mv_scale = dt * mat_.damp_mass_coeff;
+    c.rhs_kv_scale = dt * mat_.damp_stiff_coeff + (outer == 0 ? dt * dt : 0.0);
+    c.kscale = dt * mat_.damp_stiff_coeff + dt * dt;
+    c.mscale = 1.0 + dt * mat_.damp_mass_coeff;
+    c.fixed_zero = outer > 0;
+    c.mdv = outer > 0 ? dv_total : nullptr;
+    return c;
+  };
+  d_.fint_out = nullptr;
+  assemble(coeffs(0), kAssembleSystem, "assemble", 16 * n + 104 * T + 8 * Z);
+  for (int outer = 0; outer < cfg_.newton_max_iters; ++outer) {
+    cg_.x0_identity = 1;
+    st.cg_iterations += (int32_t)run_cg(cfg_.cg_max_iters);
+    cg_.x0_identity = 0;
+    if (outer == 0) {
+      check_edge_fallback();
+      int32_t newly = 0;
+      std::memcpy(&newly, h_stats_ + 5, 4);
+      st.newly_broken = newly;
+      last_load_ = cols_.empty() ? 0.0 : h_stats_[4];
+      st.load = last_load_;
+    }
+    solve_ladder(h_stats_[1] != 0.0, &st.cg_iterations, [](double) {});
+    launch("newton_update", 56.0 * n, [&] { launch_newton_update(d_, dv_total, d_usave_, dt, stream_); });
+    // the residual at the trial state = -(the next iteration's rhs), fixed dofs 0 (solver.cpp:298-312)
+    assemble(coeffs(outer + 1), kAssembleSystem, "assemble", 16 * n + 104 * T + 8 * Z);
+    st.newton_iterations = outer + 1;
+    if (std::sqrt(device_dot(d_.rhs, d_.rhs, (int64_t)nd)) <= tol) break;
+  }
+  if (!bcs_.empty()) launch("pin_bc", 96.0 * n_fixed_, [&] { launch_pin_bc(d_, stream_); });
+  if (viz_ && st.newly_broken > 0) {
+    std::vector<int32_t> ids(st.newly_broken);
+    GF_CUDA(cudaMemcpyAsync(ids.data(), d_.newly, 4 * (size_t)st.newly_broken, cudaMemcpyDeviceToHost, stream_));
+    feed_viz(std::move(ids));
+  }
   synchronize();
+  time_ = t + dt;
+  st.residual = 0.0;
+  return st;
+}
+
+gf_step_stats Simulation::dynamic_step() {
+  if (cfg_.dynamic_full_newton) return dynamic_step_full_newton();
+  gf_step_stats st{};
+  const double t = time_, dt = cfg_.dt;
+  fill_step_params(t, dt);
+  replayed_ = 0;
+  if (!launch_step_graph(dt)) enqueue_step(dt);
+  synchronize();
+  if (replayed_ && profiling_) {  // launch counts, bytes and the PCG's event time of the replayed step
+    for (const auto& it : step_list_[replayed_ - 1]) {
+      auto& k = ktimes_[it.first];
+      std::strncpy(k.name, it.first.c_str(), sizeof(k.name) - 1);
+      k.launches += 1;
+      k.bytes += it.second;
+    }
+    if (replayed_ == 2) {
+      float ms = 0.f;
+      GF_CUDA(cudaEventElapsedTime(&ms, pcg_ev_[0], pcg_ev_[1]));
+      ktimes_["pcg"].total_ms += ms;
+    }
+  }
+  const double n = 3.0 * mesh_.nn;
   // PCG algorithmic bytes per iteration for THIS format: every stored upper block and slot word
   // once, plus the vectors that leave the chip -- z gathered and written (24 B per node each) when the solver
   // state stays on chip (one slice per warp); p, q, x, r, D^-1 traffic as well when it does not (large

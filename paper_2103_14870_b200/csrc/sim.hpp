@@ -104,7 +104,12 @@ class Simulation {
   void apply_boundary_displacements(double t);
   bool newton_solve(gf_step_stats& st);
   void launch_cg();
-  void assemble(const StepCoeffs& c, int mode, const char* name, double bytes);
+  void assemble(const StepCoeffs& c, int mode, const char* name, double bytes, bool energy_in_integrate = false);
+  void fill_step_params(double t, double dt);
+  void enqueue_step(double dt);
+  void enqueue_prologue(double dt);
+  gf_step_stats dynamic_step_full_newton();
+  bool launch_step_graph(double dt);
   void check_edge_fallback();
   template <class Up>
   bool build_template_layout(const NonlocalTable& tb, Up&& up);
@@ -165,6 +170,13 @@ class Simulation {
   std::vector<cudaEvent_t> event_pool_;
   std::map<std::string, gf_kernel_time> ktimes_;
   cudaEvent_t timers_[8] = {};
+  // CUDA-graph step (dynamic_step): one executable per profiling level (0, 2), the captured (name, bytes) list
+  bool graphs_enabled_ = true;
+  bool capturing_ = false;
+  int replayed_ = 0;
+  cudaGraphExec_t step_exec_[2] = {nullptr, nullptr};
+  std::vector<std::pair<std::string, double>> capture_list_, step_list_[2];
+  cudaEvent_t pcg_ev_[2] = {nullptr, nullptr};
 };
 
 double measure_bandwidth(int kind, int64_t bytes, int reps);

@@ -121,15 +121,18 @@ def test_config_selections():
     assert cf.get("c4").num_tets == 5308416
 
 
-def test_cpp_facade_compiles_and_links(tmp_path):
-    """include/grafem_b200.hpp (reference-shaped C++ API) builds against the library; on a CPU-only host the
-    Simulation constructor must raise CudaError (exit 10), on a GPU host the 3 steps must run (exit 0)."""
+@pytest.mark.parametrize("src", ["facade_smoke.cpp", "facade_reference_style.cpp"])
+def test_cpp_facade_compiles_and_links(tmp_path, src):
+    """include/grafem_b200.hpp (reference-shaped C++ API: MaterialParams, SolverConfig, BoundaryCondition, Schedule3,
+    Collider, StepStats, Simulation with material()/config()) builds against the library -- facade_reference_style.cpp
+    is a reference call site with only the include and namespace changed; on a CPU-only host the Simulation
+    constructor must raise CudaError (exit 10), on a GPU host the steps must run (exit 0)."""
     import subprocess
     from paper_2103_14870_b200 import build as b
     exe = tmp_path / "facade"
     libdir = os.path.dirname(g.library_path())
-    subprocess.run([b._host_cxx(), "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
-                    os.path.join(ROOT, "tests", "cpp", "facade_smoke.cpp"), "-L", libdir, "-lgrafem_b200",
+    subprocess.run([b._host_cxx(), "-std=c++17", "-O1", "-Wall", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", src), "-L", libdir, "-lgrafem_b200",
                     f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == (0 if gpu_available() else 10), r.stdout + r.stderr

@@ -236,13 +236,33 @@ def test_edge_form_forces_stiffness_system_within_1e9(s, model, edge_form):
     st = os_.get_state()
     assert entry_err(gs.eval_forces(), om.assemble_forces(os_.mat, st["u"], st["chi"])) < FORCE_TOL
     assert entry_err(gs.eval_stiffness(), om.assemble_stiffness(os_.mat, st["u"], st["chi"])) < FORCE_TOL
-    e_ref = om.total_strain_energy(os_.mat, st["u"], st["chi"])
-    assert abs(gs.assembly_energy() - e_ref) <= 1e-9 * abs(e_ref)
+    gs.set_state(displacements=0.05 * st["u"], velocities=st["v"])  # a step from a milder state (StVK stays SPD)
+    os_.set_state(u=0.05 * st["u"])
+    st = os_.get_state()
     os_.dynamic_step()
     gs.dynamic_step()
+    # the fused energy of the step's assembled state: the pre-step u with the chi of the step's damage pass
+    e_ref = om.total_strain_energy(os_.mat, st["u"], os_.get_state()["chi"])
+    assert abs(gs.assembly_energy() - e_ref) <= 1e-9 * abs(e_ref)
     a_ref, r_ref = os_.last_system()
     a_got, r_got = gs.last_system()
     assert entry_err(a_got, a_ref) < FORCE_TOL and entry_err(r_got, r_ref) < FORCE_TOL
+
+
+@pytest.mark.parametrize("model", [0, 1])
+def test_fused_assembly_energy_f_form(model):
+    """the F-based assembly's fused energy (the lane of each tet's local node 0, per-row sums, one deterministic
+    reduction) equals total_strain_energy (fem.cpp:190-199) of the step's assembled state within 1e-9"""
+    s = cf.scaled("c3", (8, 8, 7))
+    s.model = model
+    rng = np.random.default_rng(17)
+    gs, os_, gm, om = pair(s, rng, disp=0.01, chi_random=True)
+    assert gs.element_form() == "F"
+    st = os_.get_state()
+    gs.dynamic_step()
+    os_.dynamic_step()
+    e_ref = om.total_strain_energy(os_.mat, st["u"], os_.get_state()["chi"])  # chi after the step's damage pass
+    assert abs(gs.assembly_energy() - e_ref) <= 1e-9 * abs(e_ref)
 
 
 def test_edge_form_rest_is_exact(edge_form):  # test_solver.cpp:89-98 with the edge form: dl2 = 0 -> no force at all
@@ -839,6 +859,38 @@ def test_gpu_quasi_static_fixed_load_and_halving_match_oracle():  # solver.cpp:1
         assert a.newton_iterations == b.newton_iterations == 0
 
 
+# ---------------------------------------------------------------- dynamic_full_newton (solver.cpp:264-313)
+def _newton_pair(full=True, max_iters=40, model=g.STABLE_NEO_HOOKEAN):
+    om_tmp = o.Mesh.make_box((0.2, 0.05, 0.05), (8, 2, 2))
+    X = om_tmp.arrays()["rest"]
+    bcs = [dict(nodes=np.nonzero(X[:, 0] <= 1e-9)[0], times=[0, 1], values=[[0, 0, 0], [0, 0, 0]])]
+    cfg = dict(dt=2e-3, cg_tol=1e-12, dynamic_full_newton=1 if full else 0, newton_max_iters=max_iters,
+               newton_tol=1e-9, gravity=(0.0, -9.81, 0.0))
+    u0 = np.zeros_like(X)
+    u0[:, 1] = -0.02 * X[:, 0]
+    return _pair_custom(((0.2, 0.05, 0.05), (8, 2, 2)), (1e6, 0.3, 1000, 1e9, 0, model), cfg, bcs=bcs, u0=u0)
+
+
+@pytest.mark.parametrize("model", [g.STABLE_NEO_HOOKEAN, g.STVK])
+def test_full_newton_matches_oracle(model):
+    gs, os_, om = _newton_pair(model=model)
+    scale = np.abs(om.arrays()["rest"]).max()
+    for _ in range(4):
+        a, b = os_.dynamic_step(), gs.dynamic_step()
+        assert a.newton_iterations >= 2 and abs(a.newton_iterations - b.newton_iterations) <= 1
+    ost, gst = os_.get_state(), gs.state()
+    assert np.abs(gst.displacements - ost["u"]).max() / scale < TRAJ_TOL
+    assert np.abs(gst.velocities - ost["v"]).max() <= TRAJ_TOL * max(1.0, np.abs(ost["v"]).max())
+
+
+def test_full_newton_one_iteration_equals_the_semi_implicit_step():
+    a, _, _ = _newton_pair(full=False)
+    b, _, _ = _newton_pair(full=True, max_iters=1)
+    sa, sb = a.dynamic_step(), b.dynamic_step()
+    assert sb.newton_iterations == 1 and sa.cg_iterations == sb.cg_iterations
+    assert np.abs(a.state().displacements - b.state().displacements).max() <= 1e-15 * 0.2
+
+
 # ---------------------------------------------------------------- non-local table layouts
 @pytest.mark.parametrize("layout", ["template", "general"])
 @pytest.mark.parametrize("cells,rd_h", [((8, 8, 7), 2.0), ((7, 5, 9), 1.5), ((6, 9, 5), 3.1)])
@@ -989,6 +1041,33 @@ def test_render_companion_follows_the_gpu_damage_passes(tmp_path):
     v = np.array([[float(x) for x in l.split()[1:]] for l in lines if l.startswith("v ")])
     f = np.array([[int(x) for x in l.split()[1:]] for l in lines if l.startswith("f ")]) - 1
     assert np.array_equal(v, vg) and np.array_equal(f, tg)
+
+
+# ---------------------------------------------------------------- CUDA-graph step orchestration
+@pytest.mark.parametrize("name,cells", [("c3", (8, 8, 7)), ("c4", (6, 6, 6))])
+def test_graph_step_equals_direct_launches(name, cells, monkeypatch):
+    """dynamic_step replayed from the captured CUDA graph is bit-identical to direct launches (same kernels, same
+    order; the per-step BC / collider parameters reach the graph through its pinned copy nodes)"""
+    s = cf.scaled(name, cells)
+    if name == "c3":
+        s.sigma_thres = 500.0
+    else:
+        s.sigma_thres = 2.0e7
+    rng = np.random.default_rng(3)
+    runs = []
+    for graph in ("1", "0"):
+        monkeypatch.setenv("GF_GRAPH", graph)
+        gs, _ = cf.build_gpu(s)
+        u = rng.uniform(-0.02 * cf.H, 0.02 * cf.H, (gs.N, 3)) if not runs else runs[0][1]
+        gs.set_state(displacements=u)
+        stats = [gs.dynamic_step() for _ in range(6)]
+        st = gs.state()
+        runs.append((st, u, [(x.cg_iterations, x.newly_broken, x.load) for x in stats]))
+    (a, _, sa), (b, _, sb) = runs
+    assert sa == sb
+    assert np.array_equal(bits(a.displacements), bits(b.displacements))
+    assert np.array_equal(bits(a.velocities), bits(b.velocities))
+    assert np.array_equal(a.edge_damage, b.edge_damage) and np.array_equal(bits(a.element_chi), bits(b.element_chi))
 
 
 # ---------------------------------------------------------------- timing plumbing of bench.py (DESIGN.md §4)

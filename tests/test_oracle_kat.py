@@ -932,3 +932,35 @@ def test_edge_decomposition_degenerate_flags():  # test_fem.cpp:141-150
     u = np.zeros((4, 3))
     u[3] = [0, 0, -1]
     assert not m.edge_decomposed_forces(p, 0, u)[2]
+
+
+# ------------------------------------------------------------------ dynamic_full_newton (solver.cpp:266-313)
+def _bar_sim(full, max_iters=40, dt=2e-3):
+    m = o.Mesh.make_box((0.2, 0.05, 0.05), (8, 2, 2))
+    X = m.arrays()["rest"]
+    p = o.material_from_youngs(1e6, 0.3, 1000, 1e9, 0, 0)
+    cfg = o.solver_config(dt=dt, cg_tol=1e-12, dynamic_full_newton=1 if full else 0, newton_max_iters=max_iters,
+                          newton_tol=1e-9, gravity=(0.0, -9.81, 0.0))
+    s = o.Sim(m, p, cfg, [dict(nodes=_slab(X, -1.0, 1e-9))])
+    u = np.zeros_like(X)
+    u[:, 1] = -0.02 * X[:, 0]  # bent start: a nonlinear first step
+    s.set_state(u=u)
+    return s
+
+
+def test_full_newton_one_iteration_equals_semi_implicit():
+    a, b = _bar_sim(False), _bar_sim(True, max_iters=1)
+    sa, sb = a.dynamic_step(), b.dynamic_step()
+    assert sb.newton_iterations == 1 and sa.newton_iterations == 0
+    assert np.array_equal(a.get_state()["u"], b.get_state()["u"])
+    assert np.array_equal(a.get_state()["v"], b.get_state()["v"])
+
+
+def test_full_newton_converges_on_the_backward_euler_residual():
+    s = _bar_sim(True)
+    st = s.dynamic_step()
+    assert 2 <= st.newton_iterations < 40
+    semi = _bar_sim(False)
+    semi.dynamic_step()
+    # the Newton-converged step differs from the single linearised step by the nonlinearity
+    assert np.abs(s.get_state()["u"] - semi.get_state()["u"]).max() > 1e-9
