@@ -31,6 +31,11 @@ namespace {
 
 constexpr int kThreads = GF_SELL_THREADS;
 constexpr int kWarpsPerCta = kThreads / 32;
+#ifndef GF_DYN_THREADS
+#define GF_DYN_THREADS 512  // large-matrix instance: 16 warps x 128 registers -- deeper SpMV pipelines, no spills
+#endif
+constexpr int kDynThreads = GF_DYN_THREADS;
+constexpr int kDynWarps = kDynThreads / 32;
 
 struct SellArgs {
   CgLaunch a;
@@ -64,8 +69,13 @@ __device__ __forceinline__ double lane_sum(double v) {  // fixed butterfly: same
 // read-only .nc path: the data changes during the kernel). Safe because every phase boundary is a cooperative-groups
 // grid barrier, whose gpu-scope fence invalidates L1 (CCTL.IVALL), and within a phase the gathered vector is
 // read-only (the pipelined solver double-buffers it).
+#ifndef GF_GATHER_NC
+#define GF_GATHER_NC 0  // A/B only: the read-only (.nc) path, outside its contract for data written in-kernel
+#endif
 __device__ __forceinline__ double ldv(const double* p) {
-#if GF_GATHER_L1
+#if GF_GATHER_NC
+  return __ldg(p);
+#elif GF_GATHER_L1
   return __ldca(p);
 #else
   return __ldcg(p);
@@ -178,9 +188,9 @@ struct Phase {
   // warp w of the CTA takes static units first + w, first + w + W, ... (consecutive warps on consecutive
   // slices), then dynamic units by ticket (requested one unit ahead). Static unit values are summed per warp in
   // unit order and per CTA in warp order (one partial per CTA); dynamic units keep one partial each.
-  template <bool kDyn, int NV, class Body>
+  template <bool kDyn, int NV, int W = kWarpsPerCta, class Body>
   __device__ __forceinline__ void run(double* const (&cta)[NV], double* const (&dyn)[NV], Body&& body) {
-    __shared__ double s_acc[kWarpsPerCta][4];
+    __shared__ double s_acc[W][4];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nst = kDyn ? __ldg(cta_first + gridDim.x) : n;
     const unsigned long long nd = (unsigned long long)(n - nst);
@@ -190,7 +200,7 @@ struct Phase {
     unsigned long long tk = 0;
     if (kDyn && lane == 0) tk = atomicAdd(ctr, 1ull);
     const int u1 = __ldg(cta_first + blockIdx.x + 1);
-    for (int u = __ldg(cta_first + blockIdx.x) + w; u < u1; u += kWarpsPerCta) {
+    for (int u = __ldg(cta_first + blockIdx.x) + w; u < u1; u += W) {
       double v[NV];
       body(u, v);
 #pragma unroll
@@ -215,16 +225,16 @@ struct Phase {
     __syncthreads();
     if (threadIdx.x < NV) {
       double x = 0.0;
-      for (int k = 0; k < kWarpsPerCta; ++k) x += s_acc[k][threadIdx.x];
+      for (int k = 0; k < W; ++k) x += s_acc[k][threadIdx.x];
       cta[threadIdx.x][blockIdx.x] = x;
     }
   }
 };
 
 // fixed lane and warp trees over the CTA's per-thread values; every thread gets the same totals
-template <int NV>
+template <int NV, int W = kWarpsPerCta>
 __device__ __forceinline__ void cta_tree(const double (&x)[NV], double (&out)[NV]) {
-  __shared__ double s_w[kWarpsPerCta][4];
+  __shared__ double s_w[W][4];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
@@ -234,14 +244,14 @@ __device__ __forceinline__ void cta_tree(const double (&x)[NV], double (&out)[NV
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
-    const double t = (lane < kWarpsPerCta) ? s_w[lane][q] : 0.0;
+    const double t = (lane < W) ? s_w[lane][q] : 0.0;
     out[q] = lane_sum(t);  // every warp computes the same total
   }
   __syncthreads();
 }
 
 // sum of [CTA partials, dynamic-unit partials] in one fixed order (thread stride, fixed lane and warp trees)
-template <bool kDyn, int NV>
+template <bool kDyn, int NV, int W = kWarpsPerCta>
 __device__ __forceinline__ void sum_phase(double* const (&cta)[NV], double* const (&dyn)[NV], int G, int nd,
                                           double (&out)[NV]) {
   double x[NV];
@@ -266,13 +276,14 @@ __device__ __forceinline__ void sum_phase(double* const (&cta)[NV], double* cons
         for (int b = 0; b < kB; ++b) x[q] += v[b];
       }
   }
-  cta_tree<NV>(x, out);
+  cta_tree<NV, W>(x, out);
 }
 
 constexpr int kMaxGrid = 1024;  // CTA partial slots per value
 
 template <bool kDyn>
-__global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
+__global__ void __launch_bounds__(kDyn ? kDynThreads : kThreads) k_pcg_sell(SellArgs sa) {
+  constexpr int W = kDyn ? kDynWarps : kWarpsPerCta;
   cg::grid_group grid = cg::this_grid();
   const CgLaunch& a = sa.a;
   const int ns = a.nslices, nrows = a.nrows, lane = threadIdx.x & 31;
@@ -311,7 +322,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
   {
     double *c3[3], *d3[3];
     ptrs(c3, d3);
-    ph.run<kDyn, 3>(c3, d3, [&](int sl, double (&v)[3]) {
+    ph.run<kDyn, 3, W>(c3, d3, [&](int sl, double (&v)[3]) {
       double acc[3];
       const int row = sl * 32 + lane;
       if (a.x0_identity) {  // A x0 = x0 (see CgLaunch::x0_identity): no SpMV
@@ -354,7 +365,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       v[2] = lane_sum(rr);
     });
     grid.sync();
-    sum_phase<kDyn, 3>(c3, d3, G, nd, tot3);
+    sum_phase<kDyn, 3, W>(c3, d3, G, nd, tot3);
     parity ^= 1;
   }
   const double bnorm = sqrt(tot3[0]);
@@ -388,7 +399,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
         if (has && it < a.max_iters) slice_spmv_sym_g(a, u0, GatherZ{a.z}, acc);
         if (it > 0) {  // previous iteration's phase-B totals
           double red2[2];
-          cta_tree<2>(pb, red2);
+          cta_tree<2, W>(pb, red2);
           rr = red2[0];
           iterations = it;
           const double rnorm = sqrt(rr);
@@ -407,7 +418,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
         const bool fused = it > 0;
         double *cA[1], *dA[1];
         ptrs(cA, dA);
-        ph.run<false, 1>(cA, dA, [&](int sl, double (&v)[1]) {
+        ph.run<false, 1, W>(cA, dA, [&](int sl, double (&v)[1]) {
           const int row = sl * 32 + lane;
           double pq = 0.0;
           if (row < nrows) {
@@ -428,7 +439,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
         double pap[1];
         grid.sync();
         SELL_STAMP(it, 5);
-        sum_phase<false, 1>(cA, dA, G, 0, pap);
+        sum_phase<false, 1, W>(cA, dA, G, 0, pap);
         parity ^= 1;
         SELL_STAMP(it, 2);
         if (pap[0] <= 0.0) {  // sparse.cpp:160-168
@@ -442,7 +453,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
         const double alpha = rz / pap[0];
         double *cB[2], *dB[2];
         ptrs(cB, dB);
-        ph.run<false, 2>(cB, dB, [&](int sl, double (&v)[2]) {
+        ph.run<false, 2, W>(cB, dB, [&](int sl, double (&v)[2]) {
           double r2 = 0.0, rzp = 0.0;
           const int row = sl * 32 + lane;
           if (row < nrows) {
@@ -482,7 +493,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       // traffic of the L2-bound phase); q and p are then updated in place by their row owner
       double *cA[1], *dA[1];
       ptrs(cA, dA);
-      ph.run<kDyn, 1>(cA, dA, [&](int sl, double (&v)[1]) {
+      ph.run<kDyn, 1, W>(cA, dA, [&](int sl, double (&v)[1]) {
         double acc[3];
         slice_spmv_sym_g<GatherZ, kDyn ? GF_SELL_GROUP_DYN : GF_SELL_GROUP>(a, sl, GatherZ{a.z}, acc);
         const int row = sl * 32 + lane;
@@ -498,9 +509,10 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
               GF_SV(4, c) = qr;
               pq = __fma_rn(pr, qr, pq);
             } else {
-              const double zi = ldv(a.z + dof);
-              const double pr = fused ? __fma_rn(beta, ldv(p + dof), zi) : zi;
-              const double qr = fused ? __fma_rn(beta, ldv(a.Ap + dof), acc[c]) : acc[c];
+              // own rows, read once per phase: through L2 only (no L1 allocation competing with the z gathers)
+              const double zi = __ldcg(a.z + dof);
+              const double pr = fused ? __fma_rn(beta, __ldcg(p + dof), zi) : zi;
+              const double qr = fused ? __fma_rn(beta, __ldcg(a.Ap + dof), acc[c]) : acc[c];
               p[dof] = pr;
               a.Ap[dof] = qr;
               pq = __fma_rn(pr, qr, pq);
@@ -515,7 +527,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       double pap[1];
       grid.sync();
       SELL_STAMP(it, 5);
-      sum_phase<kDyn, 1>(cA, dA, G, nd, pap);
+      sum_phase<kDyn, 1, W>(cA, dA, G, nd, pap);
       parity ^= 1;
       SELL_STAMP(it, 2);
       if (pap[0] <= 0.0) {  // sparse.cpp:160-168
@@ -530,7 +542,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
       double *cB[2], *dB[2];
       ptrs(cB, dB);
-      ph.run<kDyn, 2>(cB, dB, [&](int sl, double (&v)[2]) {
+      ph.run<kDyn, 2, W>(cB, dB, [&](int sl, double (&v)[2]) {
         double r2 = 0.0, rzp = 0.0;
         if (kRegs) {
           const int row = sl * 32 + lane;
@@ -571,7 +583,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
       double red2[2];
       grid.sync();
       SELL_STAMP(it, 6);
-      sum_phase<kDyn, 2>(cB, dB, G, nd, red2);
+      sum_phase<kDyn, 2, W>(cB, dB, G, nd, red2);
       parity ^= 1;
       SELL_STAMP(it, 4);
       rr = red2[0];
@@ -616,7 +628,10 @@ __global__ void __launch_bounds__(kThreads) k_pcg_sell(SellArgs sa) {
 // Solver state (x, r, D^-1, u, w, p, s, q, z) lives in shared memory for the whole solve; m is double-buffered in
 // global memory (a slow warp may still gather m_i while a fast one writes m_{i+1}); deterministic fixed-order
 // reductions as in k_pcg_sell.
-constexpr int kPipeFields = 9;
+#ifndef GF_PIPE_XG
+#define GF_PIPE_XG 0  // 1: x stays in global memory (updated in place each iteration): 8 fields of shared memory, more L1
+#endif
+constexpr int kPipeFields = GF_PIPE_XG ? 8 : 9;
 __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
   cg::grid_group grid = cg::this_grid();
   const CgLaunch& a = sa.a;
@@ -627,7 +642,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
   const int row = u0 * 32 + lane;
   const bool live = has && row < nrows;
   extern __shared__ double s_state[];
-  enum { X = 0, R = 1, D = 2, U = 3, W = 4, P = 5, S = 6, Q = 7, Z = 8 };
+  enum { R = 0, D = 1, U = 2, W = 3, P = 4, S = 5, Q = 6, Z = 7, X = 8 };  // X last: absent when GF_PIPE_XG
 #define PV(f, c) s_state[((w * kPipeFields + (f)) * 3 + (c)) * 32 + lane]
   __shared__ double s_acc[kWarpsPerCta][4];
   // double-buffered gathered vector (u during setup, then m): buffer k is a.z (k = 0) or a.p0 (k = 1)
@@ -661,7 +676,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
     for (int c = 0; c < 3; ++c) {
       const size_t dof = 3 * (size_t)row + c;
       const double bi = a.b[dof], ri = bi - acc[c], di = __ldg(a.dinv + dof), ui = di * ri;
-      PV(X, c) = a.x[dof];
+      if (!GF_PIPE_XG) PV(X, c) = a.x[dof];
       PV(R, c) = ri;
       PV(D, c) = di;
       PV(U, c) = ui;
@@ -758,7 +773,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
           PV(Q, c) = qi;
           PV(S, c) = si;
           PV(P, c) = pi;
-          PV(X, c) = __fma_rn(alpha, pi, PV(X, c));
+          if (GF_PIPE_XG) a.x[dof] = __fma_rn(alpha, pi, a.x[dof]);
+          else PV(X, c) = __fma_rn(alpha, pi, PV(X, c));
           const double ri = __fma_rn(-alpha, si, PV(R, c));
           const double ui = __fma_rn(-alpha, qi, PV(U, c));
           const double wi = __fma_rn(-alpha, zi, PV(W, c));
@@ -782,7 +798,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
     }
     if (live)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) a.x[3 * (size_t)row + c] = PV(X, c);
+      for (int c = 0; c < 3; ++c)
+        if (!GF_PIPE_XG) a.x[3 * (size_t)row + c] = PV(X, c);
   }
 #undef PV
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -807,7 +824,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv_sym(CgLaunch a, const double*
   }
 }
 
-int g_grid = 0;
+int g_grid = 0, g_dyn_per = 0;
 
 constexpr size_t kSellSmem = GF_CG_SMEM ? (size_t)kWarpsPerCta * 6 * 3 * 32 * sizeof(double) : 0;
 constexpr size_t kPipeSmem = (size_t)kWarpsPerCta * kPipeFields * 3 * 32 * sizeof(double);
@@ -833,8 +850,8 @@ int pcg_sell_grid() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int q = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_sell<true>, kThreads, kSellSmem);
-    per = std::min(per, q);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_sell<true>, kDynThreads, 0);
+    g_dyn_per = q;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_sell<false>, kThreads, kSellSmem);
     per = std::min(per, q);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_pipe, kThreads, kPipeSmem);
@@ -847,6 +864,15 @@ int pcg_sell_grid() {
 
 size_t pcg_sell_part_doubles(int ndyn) { return 2 * 4 * ((size_t)kMaxGrid + (size_t)std::max(1, ndyn)); }
 int pcg_sell_warps_per_cta() { return kWarpsPerCta; }
+int pcg_dyn_warps_per_cta() { return kDynWarps; }
+int pcg_dyn_grid() {  // co-resident CTAs of the large-matrix instance (its own block size, no dynamic smem)
+  pcg_sell_grid();
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (g_dyn_per < 1) throw std::runtime_error("large-matrix PCG kernel cannot be resident (occupancy 0)");
+  return std::min(kMaxGrid, sms * g_dyn_per);
+}
 
 int pcg_pipelined_default() {
   const char* e = std::getenv("GF_CG_PIPE");
@@ -860,9 +886,9 @@ void launch_pcg_sell(const CgLaunch& a, double* part, int ndyn, unsigned long lo
   set_smem_attributes();
   const bool pipe = ndyn == 0 && a.pipelined;
   const void* fn = pipe ? (const void*)k_pcg_pipe : ndyn > 0 ? (const void*)k_pcg_sell<true> : (const void*)k_pcg_sell<false>;
-  const size_t smem = pipe ? kPipeSmem : kSellSmem;
-  const int grid = a.grid > 0 ? a.grid : pcg_sell_grid();
-  const cudaError_t err = cudaLaunchCooperativeKernel(fn, grid, kThreads, args, smem, s);
+  const size_t smem = pipe ? kPipeSmem : ndyn > 0 ? 0 : kSellSmem;
+  const int grid = a.grid > 0 ? a.grid : ndyn > 0 ? pcg_dyn_grid() : pcg_sell_grid();
+  const cudaError_t err = cudaLaunchCooperativeKernel(fn, grid, ndyn > 0 ? kDynThreads : kThreads, args, smem, s);
   if (err != cudaSuccess) {
     cudaGetLastError();
     throw std::runtime_error(std::string("cooperative CG launch failed: ") + cudaGetErrorString(err));

@@ -201,6 +201,8 @@ void launch_pcg_csr(const CgLaunch& a, cudaStream_t s);  // scalar CSR (gf_cg_so
 int pcg_sell_grid();
 size_t pcg_sell_part_doubles(int ndyn);  // size of the partial work array (ndyn dynamic units)
 int pcg_sell_warps_per_cta();
+int pcg_dyn_warps_per_cta();  // the large-matrix instance's warps per CTA and co-resident CTAs
+int pcg_dyn_grid();
 int pcg_pipelined_default();  // GF_CG_PIPE (default 1)
 void launch_pcg_sell(const CgLaunch& a, double* part, int ndyn, unsigned long long* ctr, cudaStream_t s);
 void launch_spmv_sym(const CgLaunch& a, const double* xin, double* y, cudaStream_t s);

@@ -542,7 +542,11 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
      // slices' slot counts (interior slices carry ~1.5x the slots of boundary ones): the smallest per-CTA slot
      // budget that places the static slices. One slice per warp covers the matrix while it fits (c3: no
      // dynamic units); a larger matrix places one slice per warp statically and hands out the rest by ticket.
-    const int Gfull = pcg_sell_grid(), W = pcg_sell_warps_per_cta(), ns = d_.nslices;
+    const int ns = d_.nslices;
+    // a matrix of at most one slice per resident warp keeps the solver state on chip (k_pcg_pipe / k_pcg_sell<false>);
+    // a larger one runs the large-matrix instance with its own block size (k_pcg_sell<true>)
+    const bool dyn = ns > pcg_sell_grid() * pcg_sell_warps_per_cta();
+    const int Gfull = dyn ? pcg_dyn_grid() : pcg_sell_grid(), W = dyn ? pcg_dyn_warps_per_cta() : pcg_sell_warps_per_cta();
     // CTAs of the cooperative solve: all co-resident ones by default; GF_CG_GRID=<n> asks for fewer (cheaper grid
     // barriers for small matrices), never fewer than one slice per warp needs
     int G = Gfull;
