@@ -32,7 +32,7 @@ namespace {
 constexpr int kThreads = GF_SELL_THREADS;
 constexpr int kWarpsPerCta = kThreads / 32;
 #ifndef GF_DYN_THREADS
-#define GF_DYN_THREADS 512  // large-matrix instance: 16 warps x 128 registers -- deeper SpMV pipelines, no spills
+#define GF_DYN_THREADS 768  // large-matrix instance block size (measured at c4: 768 23.0 ms, 512 26.9, 384 + 12-deep 23.6)
 #endif
 constexpr int kDynThreads = GF_DYN_THREADS;
 constexpr int kDynWarps = kDynThreads / 32;
@@ -176,6 +176,17 @@ struct GatherX {
 struct GatherZ {
   const double* z;
   __device__ __forceinline__ double3 operator()(size_t j) const {
+    return make_double3(ldv(z + 3 * j), ldv(z + 3 * j + 1), ldv(z + 3 * j + 2));
+  }
+};
+
+// gathers of the pipelined solver's m (and u): L1-cached after the grid barrier's invalidation; inside a cluster
+// (whose barrier orders memory at cluster scope only) through L2
+template <bool kL2>
+struct GatherM {
+  const double* z;
+  __device__ __forceinline__ double3 operator()(size_t j) const {
+    if (kL2) return make_double3(__ldcg(z + 3 * j), __ldcg(z + 3 * j + 1), __ldcg(z + 3 * j + 2));
     return make_double3(ldv(z + 3 * j), ldv(z + 3 * j + 1), ldv(z + 3 * j + 2));
   }
 };
@@ -509,10 +520,11 @@ __global__ void __launch_bounds__(kDyn ? kDynThreads : kThreads) k_pcg_sell(Sell
               GF_SV(4, c) = qr;
               pq = __fma_rn(pr, qr, pq);
             } else {
-              // own rows, read once per phase: through L2 only (no L1 allocation competing with the z gathers)
-              const double zi = __ldcg(a.z + dof);
-              const double pr = fused ? __fma_rn(beta, __ldcg(p + dof), zi) : zi;
-              const double qr = fused ? __fma_rn(beta, __ldcg(a.Ap + dof), acc[c]) : acc[c];
+              // own rows through L1: z_i was just gathered by this warp's SpMV (the diagonal slot), an L1 hit
+              // (measured: L2-only loads here cost c4 9 %)
+              const double zi = ldv(a.z + dof);
+              const double pr = fused ? __fma_rn(beta, ldv(p + dof), zi) : zi;
+              const double qr = fused ? __fma_rn(beta, ldv(a.Ap + dof), acc[c]) : acc[c];
               p[dof] = pr;
               a.Ap[dof] = qr;
               pq = __fma_rn(pr, qr, pq);
@@ -631,9 +643,24 @@ __global__ void __launch_bounds__(kDyn ? kDynThreads : kThreads) k_pcg_sell(Sell
 #ifndef GF_PIPE_XG
 #define GF_PIPE_XG 0  // 1: x stays in global memory (updated in place each iteration): 8 fields of shared memory, more L1
 #endif
-constexpr int kPipeFields = GF_PIPE_XG ? 8 : 9;
+#ifndef GF_PIPE_EXPLICIT
+#define GF_PIPE_EXPLICIT 0  // 1: u = D^-1 r and q = D^-1 s evaluated explicitly instead of carried (7 shared fields)
+#endif
+constexpr int kPipeFields = (GF_PIPE_EXPLICIT ? 7 : 9) - (GF_PIPE_XG ? 1 : 0);
+// kCluster: the whole solve inside ONE thread-block cluster (small matrices, <= 16 x 24 slices): the grid barrier
+// becomes the hardware cluster barrier and the CTA partials are exchanged through distributed shared memory
+template <bool kCluster>
 __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
-  cg::grid_group grid = cg::this_grid();
+  __shared__ double s_part[2][4];  // kCluster: this CTA's published partials, read by the cluster through DSMEM
+  auto gsync = [&] {
+    if constexpr (kCluster) cg::this_cluster().sync();
+    else cg::this_grid().sync();
+  };
+  // a published CTA partial (CTA k, parity, value q)
+  auto read_part = [&](int parity, int q, int k) -> double {
+    if constexpr (kCluster) return *cg::this_cluster().map_shared_rank(&s_part[parity][q], k);
+    else return __ldcg(sa.cta_part + ((size_t)parity * 4 + q) * kMaxGrid + k);
+  };
   const CgLaunch& a = sa.a;
   const int nrows = a.nrows, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int G = (int)gridDim.x;
@@ -642,12 +669,16 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
   const int row = u0 * 32 + lane;
   const bool live = has && row < nrows;
   extern __shared__ double s_state[];
+#if GF_PIPE_EXPLICIT
+  enum { R = 0, D = 1, W = 2, P = 3, S = 4, Z = 5, X = 6, U = 7, Q = 8 };  // U, Q never stored
+#else
   enum { R = 0, D = 1, U = 2, W = 3, P = 4, S = 5, Q = 6, Z = 7, X = 8 };  // X last: absent when GF_PIPE_XG
+#endif
 #define PV(f, c) s_state[((w * kPipeFields + (f)) * 3 + (c)) * 32 + lane]
   __shared__ double s_acc[kWarpsPerCta][4];
   // double-buffered gathered vector (u during setup, then m): buffer k is a.z (k = 0) or a.p0 (k = 1)
   auto gm = [&](int k) { return k ? a.p0 : a.z; };
-  auto part = [&](int parity, int q) { return sa.cta_part + ((size_t)parity * 4 + q) * kMaxGrid; };
+
   // CTA partials of NV warp values (one slice per warp): warp sums in lane order, CTA sum in warp order
   auto publish = [&](const double* v, int nv, int parity) {
     if (lane == 0)
@@ -656,7 +687,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
     if ((int)threadIdx.x < nv) {
       double x = 0.0;
       for (int k = 0; k < kWarpsPerCta; ++k) x += s_acc[k][threadIdx.x];
-      part(parity, threadIdx.x)[blockIdx.x] = x;
+      if constexpr (kCluster) s_part[parity][threadIdx.x] = x;
+      else sa.cta_part[((size_t)parity * 4 + threadIdx.x) * kMaxGrid + blockIdx.x] = x;
     }
   };
 
@@ -679,18 +711,19 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
       if (!GF_PIPE_XG) PV(X, c) = a.x[dof];
       PV(R, c) = ri;
       PV(D, c) = di;
-      PV(U, c) = ui;
-      PV(P, c) = PV(S, c) = PV(Q, c) = PV(Z, c) = 0.0;
+      if (!GF_PIPE_EXPLICIT) PV(U, c) = ui;
+      PV(P, c) = PV(S, c) = PV(Z, c) = 0.0;
+      if (!GF_PIPE_EXPLICIT) PV(Q, c) = 0.0;
       gm(0)[dof] = ui;
       bb = __fma_rn(bi, bi, bb);
     }
   }
   bb = lane_sum(bb);
   publish(&bb, 1, 0);
-  grid.sync();
+  gsync();
   double tot[1];
   {
-    double x[1] = {(int)threadIdx.x < G ? __ldcg(part(0, 0) + threadIdx.x) : 0.0};
+    double x[1] = {(int)threadIdx.x < G ? read_part(0, 0, threadIdx.x) : 0.0};
     cta_tree<1>(x, tot);
   }
   const double bnorm = sqrt(tot[0]);
@@ -703,7 +736,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
   } else {
     // setup 2: w = A u, m = D^-1 w (gathered by iteration 0), partials gamma_0, delta_0, r.r
     acc[0] = acc[1] = acc[2] = 0.0;
-    if (has) slice_spmv_sym_g(a, u0, GatherZ{gm(0)}, acc);
+    if (has) slice_spmv_sym_g(a, u0, GatherM<kCluster>{gm(0)}, acc);
     double v3[3] = {0.0, 0.0, 0.0};
     if (live) {
 #pragma unroll
@@ -711,8 +744,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
         const size_t dof = 3 * (size_t)row + c;
         PV(W, c) = acc[c];
         gm(1)[dof] = PV(D, c) * acc[c];
-        v3[0] = __fma_rn(PV(R, c), PV(U, c), v3[0]);
-        v3[1] = __fma_rn(acc[c], PV(U, c), v3[1]);
+        const double uc = GF_PIPE_EXPLICIT ? PV(D, c) * PV(R, c) : PV(U, c);
+        v3[0] = __fma_rn(PV(R, c), uc, v3[0]);
+        v3[1] = __fma_rn(acc[c], uc, v3[1]);
         v3[2] = __fma_rn(PV(R, c), PV(R, c), v3[2]);
       }
     }
@@ -720,7 +754,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
     for (int q = 0; q < 3; ++q) v3[q] = lane_sum(v3[q]);
     __syncthreads();  // s_acc reuse
     publish(v3, 3, 1);
-    grid.sync();
+    gsync();
     int pp = 1, cur = 1;
     double gam_prev = 1.0, alpha_prev = 1.0;
     for (int it = 0;; ++it) {
@@ -728,10 +762,10 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
       double pb[3] = {0.0, 0.0, 0.0};
       if ((int)threadIdx.x < G) {
 #pragma unroll
-        for (int q = 0; q < 3; ++q) pb[q] = __ldcg(part(pp, q) + threadIdx.x);
+        for (int q = 0; q < 3; ++q) pb[q] = read_part(pp, q, threadIdx.x);
       }
       double n3[3] = {0.0, 0.0, 0.0};
-      if (has && it < a.max_iters) slice_spmv_sym_g(a, u0, GatherZ{gm(cur)}, n3);
+      if (has && it < a.max_iters) slice_spmv_sym_g(a, u0, GatherM<kCluster>{gm(cur)}, n3);
       SELL_STAMP(it, 1);
       SELL_BLOCK_STAMP(it, 3000);
       double red[3];
@@ -766,20 +800,31 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
           const size_t dof = 3 * (size_t)row + c;
           const double mi = PV(D, c) * PV(W, c);  // m_it of this row (the value gathered this iteration)
           const double zi = __fma_rn(beta, PV(Z, c), n3[c]);
-          const double qi = __fma_rn(beta, PV(Q, c), mi);
           const double si = __fma_rn(beta, PV(S, c), PV(W, c));
+#if GF_PIPE_EXPLICIT
+          const double di = PV(D, c);
+          const double qi = di * si;             // q = D^-1 s (carried as m + beta q in the recurrence form)
+          const double pi = __fma_rn(beta, PV(P, c), di * PV(R, c));  // u = D^-1 r
+#else
+          const double qi = __fma_rn(beta, PV(Q, c), mi);
           const double pi = __fma_rn(beta, PV(P, c), PV(U, c));
-          PV(Z, c) = zi;
           PV(Q, c) = qi;
+#endif
+          PV(Z, c) = zi;
           PV(S, c) = si;
           PV(P, c) = pi;
           if (GF_PIPE_XG) a.x[dof] = __fma_rn(alpha, pi, a.x[dof]);
           else PV(X, c) = __fma_rn(alpha, pi, PV(X, c));
           const double ri = __fma_rn(-alpha, si, PV(R, c));
+#if GF_PIPE_EXPLICIT
+          const double ui = di * ri;
+          (void)qi;
+#else
           const double ui = __fma_rn(-alpha, qi, PV(U, c));
+          PV(U, c) = ui;
+#endif
           const double wi = __fma_rn(-alpha, zi, PV(W, c));
           PV(R, c) = ri;
-          PV(U, c) = ui;
           PV(W, c) = wi;
           gm(cur ^ 1)[dof] = PV(D, c) * wi;
           v[0] = __fma_rn(ri, ui, v[0]);
@@ -794,7 +839,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
       SELL_BLOCK_STAMP(it, 2000);
       pp ^= 1;
       cur ^= 1;
-      grid.sync();
+      gsync();
     }
     if (live)
 #pragma unroll
@@ -802,6 +847,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
         if (!GF_PIPE_XG) a.x[3 * (size_t)row + c] = PV(X, c);
   }
 #undef PV
+  // no CTA of a cluster may exit while another can still read its shared memory (the last partial reads)
+  if constexpr (kCluster) cg::this_cluster().sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.out[0] = iterations;
     a.out[1] = converged;
@@ -833,7 +880,9 @@ void set_smem_attributes() {
   static bool done = [] {
     cudaFuncSetAttribute((const void*)k_pcg_sell<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellSmem);
     cudaFuncSetAttribute((const void*)k_pcg_sell<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellSmem);
-    cudaFuncSetAttribute((const void*)k_pcg_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
+    cudaFuncSetAttribute((const void*)k_pcg_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
+    cudaFuncSetAttribute((const void*)k_pcg_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
+    cudaFuncSetAttribute((const void*)k_pcg_pipe<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return true;
   }();
   (void)done;
@@ -854,7 +903,7 @@ int pcg_sell_grid() {
     g_dyn_per = q;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_sell<false>, kThreads, kSellSmem);
     per = std::min(per, q);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_pipe, kThreads, kPipeSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_pipe<false>, kThreads, kPipeSmem);
     per = std::min(per, q);
     if (per < 1) throw std::runtime_error("cooperative PCG kernels cannot be resident (occupancy 0)");
     g_grid = std::min(kMaxGrid, sms * per);
@@ -874,6 +923,32 @@ int pcg_dyn_grid() {  // co-resident CTAs of the large-matrix instance (its own 
   return std::min(kMaxGrid, sms * g_dyn_per);
 }
 
+// the largest cluster k_pcg_pipe<true> can be launched with on this device (0: clusters unavailable)
+int pcg_max_cluster() {
+  static int cached = -1;
+  if (cached < 0) {
+    set_smem_attributes();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = kPipeSmem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 16;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxPotentialClusterSize(&n, (const void*)k_pcg_pipe<true>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    cached = std::min(n, 16);
+  }
+  return cached;
+}
+
 int pcg_pipelined_default() {
   const char* e = std::getenv("GF_CG_PIPE");
   return e ? std::atoi(e) != 0 : 1;
@@ -885,7 +960,27 @@ void launch_pcg_sell(const CgLaunch& a, double* part, int ndyn, unsigned long lo
   void* args[] = {&sa};
   set_smem_attributes();
   const bool pipe = ndyn == 0 && a.pipelined;
-  const void* fn = pipe ? (const void*)k_pcg_pipe : ndyn > 0 ? (const void*)k_pcg_sell<true> : (const void*)k_pcg_sell<false>;
+  if (pipe && a.cluster > 0) {  // one thread-block cluster of a.grid CTAs (small matrices)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.grid, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = kPipeSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = a.grid;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t err = cudaLaunchKernelEx(&cfg, k_pcg_pipe<true>, sa);
+    if (err != cudaSuccess) {
+      cudaGetLastError();
+      throw std::runtime_error(std::string("cluster CG launch failed: ") + cudaGetErrorString(err));
+    }
+    return;
+  }
+  const void* fn = pipe ? (const void*)k_pcg_pipe<false> : ndyn > 0 ? (const void*)k_pcg_sell<true> : (const void*)k_pcg_sell<false>;
   const size_t smem = pipe ? kPipeSmem : ndyn > 0 ? 0 : kSellSmem;
   const int grid = a.grid > 0 ? a.grid : ndyn > 0 ? pcg_dyn_grid() : pcg_sell_grid();
   const cudaError_t err = cudaLaunchCooperativeKernel(fn, grid, ndyn > 0 ? kDynThreads : kThreads, args, smem, s);

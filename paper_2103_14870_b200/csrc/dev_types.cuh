@@ -194,6 +194,7 @@ struct CgLaunch {
   int32_t x0_identity;
   int32_t pipelined;  // cg_sell.cu: 1 = the single-barrier pipelined solver (k_pcg_pipe) when the state fits on chip
   int32_t grid;       // cg_sell.cu: CTAs of the cooperative launch (0 = all co-resident)
+  int32_t cluster;    // cg_sell.cu: 1 = the pipelined solve runs in ONE thread-block cluster of `grid` CTAs
 };
 int cg_csr_grid();
 void launch_pcg_csr(const CgLaunch& a, cudaStream_t s);  // scalar CSR (gf_cg_solve_csr)
@@ -204,6 +205,7 @@ int pcg_sell_warps_per_cta();
 int pcg_dyn_warps_per_cta();  // the large-matrix instance's warps per CTA and co-resident CTAs
 int pcg_dyn_grid();
 int pcg_pipelined_default();  // GF_CG_PIPE (default 1)
+int pcg_max_cluster();        // largest launchable cluster of the pipelined solver (0: none)
 void launch_pcg_sell(const CgLaunch& a, double* part, int ndyn, unsigned long long* ctr, cudaStream_t s);
 void launch_spmv_sym(const CgLaunch& a, const double* xin, double* y, cudaStream_t s);
 // ---- misc.cu ----

@@ -554,8 +554,16 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
       const int want = std::atoi(e);
       if (want > 0) G = std::min(Gfull, std::max(want, (ns + W - 1) / W));
     }
-    cg_.grid = G;
     cg_.pipelined = pcg_pipelined_default();
+    // small matrices (c1): the whole pipelined solve in one thread-block cluster -- hardware cluster barriers and
+    // DSMEM partial exchange instead of grid barriers through global memory (GF_CG_CLUSTER=0 disables)
+    const char* ce = std::getenv("GF_CG_CLUSTER");
+    const int cmax = (ce && std::atoi(ce) == 0) || !cg_.pipelined || dyn ? 0 : pcg_max_cluster();
+    if (cmax > 0 && ns <= cmax * W) {
+      G = cmax;
+      cg_.cluster = 1;
+    }
+    cg_.grid = G;
     const int64_t gw = (int64_t)G * W;
     double frac = 0.0;  // measured at c4 (28k slices): all-dynamic tail 22.5 ms, 50 % static 23.0, 80 % 26.2
     if (const char* e = std::getenv("GF_CG_STATIC")) frac = std::atof(e);  // static share of a large matrix

@@ -357,6 +357,14 @@ def test_step_metrics_match_oracle(model):
 
 
 # ---------------------------------------------------------------- the production PCG (k_pcg_sell) on given systems
+@pytest.fixture(params=["cluster", "grid", "two-barrier"])
+def pcg_mode(request, monkeypatch):
+    """the production solver's on-chip instances: pipelined in one cluster / on the grid, and the two-barrier one"""
+    monkeypatch.setenv("GF_CG_CLUSTER", "1" if request.param == "cluster" else "0")
+    monkeypatch.setenv("GF_CG_PIPE", "0" if request.param == "two-barrier" else "1")
+    return request.param
+
+
 def _pcg_setup(cells=(4, 4, 4)):
     s = cf.scaled("c2", cells)
     gs, os_, gm, om = pair(s)
@@ -371,7 +379,7 @@ def _oracle_cg(rp, cols, vals, b, x0, tol, max_iters):
                    negative_curvature=bool(r.negative_curvature), relative_residual=r.relative_residual)
 
 
-def test_production_pcg_identity_system():  # test_sparse.cpp:20-32 on k_pcg_sell
+def test_production_pcg_identity_system(pcg_mode):  # test_sparse.cpp:20-32 on k_pcg_sell
     gs, _, om, rp, cols, rows = _pcg_setup()
     n = len(rp) - 1
     vals = (rows == cols).astype(np.float64)
@@ -382,7 +390,7 @@ def test_production_pcg_identity_system():  # test_sparse.cpp:20-32 on k_pcg_sel
     assert np.array_equal(x, b) and np.array_equal(xo, b)
 
 
-def test_production_pcg_zero_rhs():  # sparse.cpp:145-150: b = 0 -> x = 0, converged, no iteration
+def test_production_pcg_zero_rhs(pcg_mode):  # sparse.cpp:145-150: b = 0 -> x = 0, converged, no iteration
     gs, _, om, rp, cols, rows = _pcg_setup()
     n = len(rp) - 1
     vals = (rows == cols) * 2.0
@@ -392,7 +400,7 @@ def test_production_pcg_zero_rhs():  # sparse.cpp:145-150: b = 0 -> x = 0, conve
     assert np.all(x == 0.0) and np.all(xo == 0.0)
 
 
-def test_production_pcg_negative_curvature():  # test_sparse.cpp:74-84 / sparse.cpp:160-168 on k_pcg_sell
+def test_production_pcg_negative_curvature(pcg_mode):  # test_sparse.cpp:74-84 / sparse.cpp:160-168 on k_pcg_sell
     gs, _, om, rp, cols, rows = _pcg_setup()
     n = len(rp) - 1
     d = np.where(np.arange(n) % 3 == 0, -1.0, 1.0)  # indefinite Jacobi-scaled system: p.Ap < 0 at the first step
@@ -405,7 +413,7 @@ def test_production_pcg_negative_curvature():  # test_sparse.cpp:74-84 / sparse.
     assert r["relative_residual"] == pytest.approx(ro["relative_residual"], rel=1e-12)
 
 
-def test_production_pcg_matches_oracle_on_the_step_system():
+def test_production_pcg_matches_oracle_on_the_step_system(pcg_mode):
     """the implicit-Euler system of a loaded step, random rhs, tight tolerance: same iteration count within 2, same
     solution within 1e-9; the A-norm error of the production solver never grows (test_sparse.cpp:86-110)"""
     gs, os_, om, rp, cols, rows = _pcg_setup((5, 4, 6))
@@ -561,14 +569,21 @@ def run_pair(s, steps, resync_tol=1e-6):
     return worst, resyncs, broken
 
 
-def test_trajectory_c1_scaled():
+@pytest.mark.parametrize("cluster", ["1", "0"])
+def test_trajectory_c1_scaled(cluster, monkeypatch):
+    """small matrix: the pipelined PCG inside one thread-block cluster (default) and on the cooperative grid"""
+    monkeypatch.setenv("GF_CG_CLUSTER", cluster)
     s = cf.scaled("c1", (4, 4, 16), steps=60)
     s.point_load = (s.point_load[0], (0.0, -500.0 / 8, 0.0))  # same bending stress as the 8x8 section
     worst, resyncs, _ = run_pair(s, s.steps)
     assert worst < TRAJ_TOL
 
 
-def test_trajectory_c3_scaled_with_fracture():
+@pytest.mark.parametrize("solver", ["cluster", "grid", "two-barrier"])
+def test_trajectory_c3_scaled_with_fracture(solver, monkeypatch):
+    """the three on-chip-state PCG instances: k_pcg_pipe in one cluster, k_pcg_pipe on the grid, k_pcg_sell"""
+    monkeypatch.setenv("GF_CG_CLUSTER", "1" if solver == "cluster" else "0")
+    monkeypatch.setenv("GF_CG_PIPE", "0" if solver == "two-barrier" else "1")
     s = cf.scaled("c3", (10, 10, 9), steps=60)
     worst, resyncs, broken = run_pair(s, s.steps)
     assert broken > 0
