@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
   extern __shared__ double s_dyn[];  // kBlocks: s_blk[kWarps][32 * 27 + 9] (dynamic: > 48 KB static limit)
   double(*s_blk)[kBlkStride] = reinterpret_cast<double(*)[kBlkStride]>(s_dyn);
   __shared__ double s_row[kBlocks ? kWarps : 1][kMaxDeg * 9];
-  __shared__ uint8_t s_item[kBlocks ? kWarps : 1][16 * kMaxDeg];
+  __shared__ __align__(16) uint8_t s_item[kBlocks ? kWarps : 1][16 * kMaxDeg];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kWarps + w;
   if (i >= d.nn) return;
@@ -443,9 +443,13 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
     const double dsum = __shfl_sync(0xffffffffu, rsum, 2 * (lane < 9 ? 3 + lane : 3));  // lane q < 9: entry q
     // the row's padded contribution lists (mx <= 16 items per column) staged in shared memory, so
     // the reduction below touches only shared memory with a uniform trip count
+    // lists padded to whole 4-item words by the host: staged and read 32 bits (4 items) at a time, so an output's
+    // block loads issue together (the sum stays sequential in item order)
     const int ib0 = __ldg(d.contrib_ptr + i), nitems = __ldg(d.contrib_ptr + i + 1) - ib0;
-    const int mx = nitems / deg;
-    for (int k = lane; k < nitems; k += 32) s_item[w][k] = __ldg(d.contrib_item + ib0 + k);
+    const int mx4 = nitems / (4 * deg);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(d.contrib_item + ib0);
+    uint32_t* s_item4 = reinterpret_cast<uint32_t*>(&s_item[w][0]);
+    for (int k = lane; k < nitems / 4; k += 32) s_item4[k] = __ldg(src + k);
     if (lane < 9) s_blk[w][32 * 27 + lane] = 0.0;  // the zero block padding items point at
     __syncwarp();
     // off-diagonal outputs (column c != cdiag, entry q), 9 (deg - 1) of them spread over the lanes
@@ -453,9 +457,17 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
       int c = o / 9;
       const int q = o - 9 * c;
       c += (c >= cdiag) ? 1 : 0;
-      const uint8_t* it = &s_item[w][c * mx];
+      const uint32_t* it4 = s_item4 + c * mx4;
       double sum = 0.0;
-      for (int t = 0; t < mx; ++t) sum += s_blk[w][9 * (int)it[t] + q];
+      for (int t = 0; t < mx4; ++t) {
+        const uint32_t wv = it4[t];
+        const double v0 = s_blk[w][9 * (int)(wv & 0xffu) + q], v1 = s_blk[w][9 * (int)((wv >> 8) & 0xffu) + q];
+        const double v2 = s_blk[w][9 * (int)((wv >> 16) & 0xffu) + q], v3 = s_blk[w][9 * (int)(wv >> 24) + q];
+        sum += v0;
+        sum += v1;
+        sum += v2;
+        sum += v3;
+      }
       s_row[w][9 * c + q] = sum;
     }
     if (lane < 9) s_row[w][9 * cdiag + lane] = dsum;

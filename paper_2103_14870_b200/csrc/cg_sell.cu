@@ -119,11 +119,28 @@ __device__ __forceinline__ double ldmat(const double* p) {
 #endif
 }
 
+#ifndef GF_L1_HINTS
+#define GF_L1_HINTS 0  // 1: matrix blocks with no later reader on this SM are loaded without L1 allocation; 2: + m/z gathers evict_last
+#endif
+// a block read for the last time on this SM (a transposed read, or a direct read whose transposed reader sits in
+// another CTA): no L1 allocation, so L1 keeps the blocks the CTA's sibling warps will read transposed, and the gathers
+__device__ __forceinline__ double ldmat_dead(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ldv_keep(const double* p) {
+  double v;
+  asm volatile("ld.global.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 #ifndef GF_SELL_GROUP_DYN
 #define GF_SELL_GROUP_DYN 8  // the large-matrix (HBM-streaming) instance: more block loads in flight (c4: -0.8 %)
 #endif
-template <class G, int kGroup = GF_SELL_GROUP>
-__device__ __forceinline__ void slice_spmv_sym_g(const CgLaunch& a, int sl, const G& gat, double acc[3]) {
+template <class G, int kGroup = GF_SELL_GROUP, bool kHints = false>
+__device__ __forceinline__ void slice_spmv_sym_g(const CgLaunch& a, int sl, const G& gat, double acc[3],
+                                                 int cta_s0 = 0, int cta_s1 = 0) {
   const int lane = threadIdx.x & 31;
   const int row = sl * 32 + lane;
   const int k0 = __ldg(a.row_ptr + sl), k1 = __ldg(a.row_ptr + sl + 1);
@@ -148,8 +165,13 @@ __device__ __forceinline__ void slice_spmv_sym_g(const CgLaunch& a, int sl, cons
         const double3 p = gat((size_t)j);
         const double* v = a.vals + base;
         double m[9];
+        if (kHints && (tr || (j >> 5) < cta_s0 || (j >> 5) >= cta_s1)) {
 #pragma unroll
-        for (int q = 0; q < 9; ++q) m[q] = ldmat(v + 32 * q);
+          for (int q = 0; q < 9; ++q) m[q] = ldmat_dead(v + 32 * q);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 9; ++q) m[q] = ldmat(v + 32 * q);
+        }
         if (!tr) {
           acc[0] = __fma_rn(m[0], p.x, acc[0]); acc[0] = __fma_rn(m[1], p.y, acc[0]); acc[0] = __fma_rn(m[2], p.z, acc[0]);
           acc[1] = __fma_rn(m[3], p.x, acc[1]); acc[1] = __fma_rn(m[4], p.y, acc[1]); acc[1] = __fma_rn(m[5], p.z, acc[1]);
@@ -187,6 +209,7 @@ struct GatherM {
   const double* z;
   __device__ __forceinline__ double3 operator()(size_t j) const {
     if (kL2) return make_double3(__ldcg(z + 3 * j), __ldcg(z + 3 * j + 1), __ldcg(z + 3 * j + 2));
+    if (GF_L1_HINTS >= 2) return make_double3(ldv_keep(z + 3 * j), ldv_keep(z + 3 * j + 1), ldv_keep(z + 3 * j + 2));
     return make_double3(ldv(z + 3 * j), ldv(z + 3 * j + 1), ldv(z + 3 * j + 2));
   }
 };
@@ -644,7 +667,7 @@ __global__ void __launch_bounds__(kDyn ? kDynThreads : kThreads) k_pcg_sell(Sell
 #define GF_PIPE_XG 0  // 1: x stays in global memory (updated in place each iteration): 8 fields of shared memory, more L1
 #endif
 #ifndef GF_PIPE_EXPLICIT
-#define GF_PIPE_EXPLICIT 0  // 1: u = D^-1 r and q = D^-1 s evaluated explicitly instead of carried (7 shared fields)
+#define GF_PIPE_EXPLICIT 1  // u = D^-1 r and q = D^-1 s evaluated, not carried: 7 shared fields (more L1), -8 % at c3
 #endif
 constexpr int kPipeFields = (GF_PIPE_EXPLICIT ? 7 : 9) - (GF_PIPE_XG ? 1 : 0);
 // kCluster: the whole solve inside ONE thread-block cluster (small matrices, <= 16 x 24 slices): the grid barrier
@@ -664,8 +687,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
   const CgLaunch& a = sa.a;
   const int nrows = a.nrows, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int G = (int)gridDim.x;
-  const int u0 = __ldg(a.cta_first + blockIdx.x) + w;
-  const bool has = u0 < __ldg(a.cta_first + blockIdx.x + 1);
+  const int cta_s0 = __ldg(a.cta_first + blockIdx.x), cta_s1 = __ldg(a.cta_first + blockIdx.x + 1);
+  const int u0 = cta_s0 + w;
+  const bool has = u0 < cta_s1;
   const int row = u0 * 32 + lane;
   const bool live = has && row < nrows;
   extern __shared__ double s_state[];
@@ -765,7 +789,9 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
         for (int q = 0; q < 3; ++q) pb[q] = read_part(pp, q, threadIdx.x);
       }
       double n3[3] = {0.0, 0.0, 0.0};
-      if (has && it < a.max_iters) slice_spmv_sym_g(a, u0, GatherM<kCluster>{gm(cur)}, n3);
+      if (has && it < a.max_iters)
+        slice_spmv_sym_g<GatherM<kCluster>, GF_SELL_GROUP, (GF_L1_HINTS > 0)>(a, u0, GatherM<kCluster>{gm(cur)}, n3,
+                                                                        cta_s0, cta_s1);
       SELL_STAMP(it, 1);
       SELL_BLOCK_STAMP(it, 3000);
       double red[3];

@@ -315,6 +315,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
       int32_t mx = 0;
       for (int32_t b = pat_.row_ptr[i]; b < pat_.row_ptr[i + 1]; ++b) mx = std::max(mx, cnt[b + 1] - cnt[b]);
       if (mx > 16) throw GeometryError("more than 16 tets around an edge are not supported by the assembly kernel");
+      mx = (mx + 3) & ~3;  // lists padded to whole 4-item words (the kernel reads them as 32-bit words)
       rptr[i + 1] = rptr[i] + mx * (pat_.row_ptr[i + 1] - pat_.row_ptr[i]);
     }
     // rows beyond one warp's lanes (> 32 incident tets or > 32 neighbour blocks) go to k_assemble_big, whose
