@@ -34,20 +34,28 @@ __device__ __forceinline__ double shape_grad(const double B[9], int l, int a) {
   return l == 0 ? -((B[a] + B[3 + a]) + B[6 + a]) : B[3 * (l - 1) + a];
 }
 
+// du[3r+c] = (u_{c+1} - u_0)_r of tet t
+__device__ __forceinline__ void tet_du(const DevData& d, int4 t, double du[9]) {
+  const int id[4] = {t.x, t.y, t.z, t.w};
+  double u0[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) u0[a] = __ldg(d.u + 3 * (size_t)id[0] + a);
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) du[3 * r + c] = __ldg(d.u + 3 * (size_t)id[c + 1] + r) - u0[r];
+}
+
 template <bool kBlocks>
 __device__ __forceinline__ void element_row(const DevData& d, const MatDev& m, int4 t, const double B[9], int li,
                                             double scale, double f[3], double* blk, double dg[9],
-                                            double* psi = nullptr) {
-  const int id[4] = {t.x, t.y, t.z, t.w};
+                                            double* psi = nullptr, const double* du_in = nullptr) {
   double du[9], F[9];
-  {
-    double u0[3];
+  if (du_in) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) u0[a] = __ldg(d.u + 3 * (size_t)id[0] + a);
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int r = 0; r < 3; ++r) du[3 * r + c] = __ldg(d.u + 3 * (size_t)id[c + 1] + r) - u0[r];
+    for (int q = 0; q < 9; ++q) du[q] = du_in[q];
+  } else {
+    tet_du(d, t, du);
   }
   def_grad(du, B, F);
   double gi[3];
@@ -265,11 +273,15 @@ __device__ __forceinline__ void lane_element(const DevData& d, const MatDev& m, 
       for (int r = 0; r < 27; ++r) blk[r] = 0.0;
     return;
   }
+  // the displacement gathers, the rest record and chi are independent loads: issued together, before the
+  // chi V = 0 early-out that would otherwise make the gathers wait for chi
+  double du[9];
+  tet_du(d, t, du);
   double B[9], vol;
   load_rest(d, e, B, vol);
   const double scale = d.chi[e] * vol;
   if (scale != 0.0) {  // fem.cpp:51 / fem.cpp:114 early-out
-    element_row<kBlocks>(d, m, t, B, li, scale, f, blk, dg, psi);
+    element_row<kBlocks>(d, m, t, B, li, scale, f, blk, dg, psi, du);
   } else if (kBlocks) {
 #pragma unroll
     for (int r = 0; r < 27; ++r) blk[r] = 0.0;
@@ -418,7 +430,7 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
   double psi = 0.0;
   if (lane < np) {
     const int e = __ldg(d.nt_tet + p0 + lane);
-    const int4 t = __ldg(d.tets + e);
+    const int4 t = __ldg(d.nt_nodes + p0 + lane);  // not tets[e]: no dependence on e
     const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
     double* blk = kBlocks ? &s_blk[w][27 * lane] : nullptr;
     lane_element<kEdge, kBlocks>(d, m, e, t, li, f, blk, dg, kFusedEnergy ? &psi : nullptr);
@@ -527,7 +539,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_assemble_big(DevData d, MatDev 
     bool wrote = false;
     if (l < np) {
       const int e = __ldg(d.nt_tet + p0 + l);
-      const int4 t = __ldg(d.tets + e);
+      const int4 t = __ldg(d.nt_nodes + p0 + l);
       const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
       lane_element<kEdge, kBlocks>(d, m, e, t, li, f, blk, dg, kFusedEnergy ? &psi : nullptr);
       wrote = true;

@@ -119,6 +119,9 @@ __device__ __forceinline__ double ldmat(const double* p) {
 #endif
 }
 
+#ifndef GF_CARVEOUT
+#define GF_CARVEOUT 0
+#endif
 #ifndef GF_L1_HINTS
 #define GF_L1_HINTS 0  // 1: matrix blocks with no later reader on this SM are loaded without L1 allocation; 2: + m/z gathers evict_last
 #endif
@@ -669,7 +672,11 @@ __global__ void __launch_bounds__(kDyn ? kDynThreads : kThreads) k_pcg_sell(Sell
 #ifndef GF_PIPE_EXPLICIT
 #define GF_PIPE_EXPLICIT 1  // u = D^-1 r and q = D^-1 s evaluated, not carried: 7 shared fields (more L1), -8 % at c3
 #endif
-constexpr int kPipeFields = (GF_PIPE_EXPLICIT ? 7 : 9) - (GF_PIPE_XG ? 1 : 0);
+#ifndef GF_PIPE_DIAG
+#define GF_PIPE_DIAG 0  // 1 (with GF_PIPE_EXPLICIT): D^-1 recomputed from the diagonal block each iteration, not stored
+#endif
+constexpr bool kPipeDiag = GF_PIPE_DIAG && GF_PIPE_EXPLICIT;
+constexpr int kPipeFields = (GF_PIPE_EXPLICIT ? 7 : 9) - (GF_PIPE_XG ? 1 : 0) - (kPipeDiag ? 1 : 0);
 // kCluster: the whole solve inside ONE thread-block cluster (small matrices, <= 16 x 24 slices): the grid barrier
 // becomes the hardware cluster barrier and the CTA partials are exchanged through distributed shared memory
 template <bool kCluster>
@@ -693,12 +700,25 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
   const int row = u0 * 32 + lane;
   const bool live = has && row < nrows;
   extern __shared__ double s_state[];
-#if GF_PIPE_EXPLICIT
+#if GF_PIPE_EXPLICIT && GF_PIPE_DIAG
+  enum { R = 0, W = 1, P = 2, S = 3, Z = 4, X = 5, D = 6, U = 7, Q = 8 };  // D, U, Q never stored
+#elif GF_PIPE_EXPLICIT
   enum { R = 0, D = 1, W = 2, P = 3, S = 4, Z = 5, X = 6, U = 7, Q = 8 };  // U, Q never stored
 #else
   enum { R = 0, D = 1, U = 2, W = 3, P = 4, S = 5, Q = 6, Z = 7, X = 8 };  // X last: absent when GF_PIPE_XG
 #endif
 #define PV(f, c) s_state[((w * kPipeFields + (f)) * 3 + (c)) * 32 + lane]
+  // D^-1 of this row: stored, or (kPipeDiag) recomputed from the diagonal block -- the first upper block of the row
+  // (ordinal 0), entries 0, 4, 8 -- with the assembly's formula (sparse.cpp:133-136), so the bits are the same
+  const double* diag = a.vals + (size_t)__ldg(a.usp + (u0 < a.nslices ? u0 : 0)) * 288 + lane;
+  auto DV = [&](int c) -> double {
+    if constexpr (kPipeDiag) {
+      const double dd = diag[32 * 4 * c];
+      return (fabs(dd) > 1e-300) ? 1.0 / dd : 1.0;
+    } else {
+      return PV(D, c);
+    }
+  };
   __shared__ double s_acc[kWarpsPerCta][4];
   // double-buffered gathered vector (u during setup, then m): buffer k is a.z (k = 0) or a.p0 (k = 1)
   auto gm = [&](int k) { return k ? a.p0 : a.z; };
@@ -734,7 +754,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
       const double bi = a.b[dof], ri = bi - acc[c], di = __ldg(a.dinv + dof), ui = di * ri;
       if (!GF_PIPE_XG) PV(X, c) = a.x[dof];
       PV(R, c) = ri;
-      PV(D, c) = di;
+      if (!kPipeDiag) PV(D, c) = di;
       if (!GF_PIPE_EXPLICIT) PV(U, c) = ui;
       PV(P, c) = PV(S, c) = PV(Z, c) = 0.0;
       if (!GF_PIPE_EXPLICIT) PV(Q, c) = 0.0;
@@ -767,8 +787,8 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
       for (int c = 0; c < 3; ++c) {
         const size_t dof = 3 * (size_t)row + c;
         PV(W, c) = acc[c];
-        gm(1)[dof] = PV(D, c) * acc[c];
-        const double uc = GF_PIPE_EXPLICIT ? PV(D, c) * PV(R, c) : PV(U, c);
+        gm(1)[dof] = DV(c) * acc[c];
+        const double uc = GF_PIPE_EXPLICIT ? DV(c) * PV(R, c) : PV(U, c);
         v3[0] = __fma_rn(PV(R, c), uc, v3[0]);
         v3[1] = __fma_rn(acc[c], uc, v3[1]);
         v3[2] = __fma_rn(PV(R, c), PV(R, c), v3[2]);
@@ -824,11 +844,12 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const size_t dof = 3 * (size_t)row + c;
-          const double mi = PV(D, c) * PV(W, c);  // m_it of this row (the value gathered this iteration)
+          const double dvc = DV(c);
+          const double mi = dvc * PV(W, c);  // m_it of this row (the value gathered this iteration)
           const double zi = __fma_rn(beta, PV(Z, c), n3[c]);
           const double si = __fma_rn(beta, PV(S, c), PV(W, c));
 #if GF_PIPE_EXPLICIT
-          const double di = PV(D, c);
+          const double di = dvc;
           const double qi = di * si;             // q = D^-1 s (carried as m + beta q in the recurrence form)
           const double pi = __fma_rn(beta, PV(P, c), di * PV(R, c));  // u = D^-1 r
 #else
@@ -852,7 +873,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
           const double wi = __fma_rn(-alpha, zi, PV(W, c));
           PV(R, c) = ri;
           PV(W, c) = wi;
-          gm(cur ^ 1)[dof] = PV(D, c) * wi;
+          gm(cur ^ 1)[dof] = dvc * wi;
           v[0] = __fma_rn(ri, ui, v[0]);
           v[1] = __fma_rn(wi, ui, v[1]);
           v[2] = __fma_rn(ri, ri, v[2]);
@@ -909,6 +930,12 @@ void set_smem_attributes() {
     cudaFuncSetAttribute((const void*)k_pcg_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
     cudaFuncSetAttribute((const void*)k_pcg_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
     cudaFuncSetAttribute((const void*)k_pcg_pipe<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+#if GF_CARVEOUT
+    // one CTA per SM: the smallest shared-memory configuration that holds the solver state, the rest as L1
+    for (const void* f : {(const void*)k_pcg_pipe<false>, (const void*)k_pcg_pipe<true>, (const void*)k_pcg_sell<false>,
+                          (const void*)k_pcg_sell<true>})
+      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxL1);
+#endif
     return true;
   }();
   (void)done;

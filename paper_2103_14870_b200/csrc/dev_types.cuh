@@ -66,6 +66,8 @@ struct DevData {
   // node -> tet incidence (ascending tet) with packed column slots
   const int32_t* nt_ptr;
   const int32_t* nt_tet;
+  const int4* nt_nodes;     // per incidence entry: the tet's 4 node ids (a copy of tets[nt_tet]), so the assembly's
+                            // displacement gathers issue with the tet's rest-record loads, one dependent round trip less
   // per block (CSR order) the contributions (pair l, local node k) as items l*4+k, ascending tet order
   const int32_t* contrib_ptr;  // nn+1: padded contribution items of row i start here (mx per column)
   const int32_t* big_rows;     // rows with > 32 incident tets or > 32 neighbour blocks (k_assemble_big)

@@ -283,6 +283,13 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   d_.node_bc = (const int32_t*)up(node_bc.data(), 4 * node_bc.size());
   d_.nt_ptr = (const int32_t*)up(ntets.ptr.data(), 4 * ntets.ptr.size());
   d_.nt_tet = (const int32_t*)up(ntets.tet.data(), 4 * ntets.tet.size());
+  {
+    std::vector<int32_t> nodes(4 * ntets.tet.size());
+    for (size_t q = 0; q < ntets.tet.size(); ++q)
+      for (int k = 0; k < 4; ++k) nodes[4 * q + k] = mesh_.tets[4 * (size_t)ntets.tet[q] + k];
+    d_.nt_nodes = (const int4*)up(nodes.data(), 4 * nodes.size());
+    GF_CUDA(cudaStreamSynchronize(stream_));  // host staging goes out of scope
+  }
   {  // contribution lists of the assembly reduction (assemble.cu): per off-diagonal block, items 3 l + s
      // (lane l = incident tet, s = its off-diagonal block slot), ascending l; diagonal blocks are warp sums
     auto col_of = [&](int32_t q, int k) { return (int32_t)((ntets.slot[q] >> (8 * k)) & 0xff); };
