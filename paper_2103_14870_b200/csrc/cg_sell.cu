@@ -69,13 +69,8 @@ __device__ __forceinline__ double lane_sum(double v) {  // fixed butterfly: same
 // read-only .nc path: the data changes during the kernel). Safe because every phase boundary is a cooperative-groups
 // grid barrier, whose gpu-scope fence invalidates L1 (CCTL.IVALL), and within a phase the gathered vector is
 // read-only (the pipelined solver double-buffers it).
-#ifndef GF_GATHER_NC
-#define GF_GATHER_NC 0  // A/B only: the read-only (.nc) path, outside its contract for data written in-kernel
-#endif
 __device__ __forceinline__ double ldv(const double* p) {
-#if GF_GATHER_NC
-  return __ldg(p);
-#elif GF_GATHER_L1
+#if GF_GATHER_L1
   return __ldca(p);
 #else
   return __ldcg(p);
@@ -119,31 +114,11 @@ __device__ __forceinline__ double ldmat(const double* p) {
 #endif
 }
 
-#ifndef GF_CARVEOUT
-#define GF_CARVEOUT 0
-#endif
-#ifndef GF_L1_HINTS
-#define GF_L1_HINTS 0  // 1: matrix blocks with no later reader on this SM are loaded without L1 allocation; 2: + m/z gathers evict_last
-#endif
-// a block read for the last time on this SM (a transposed read, or a direct read whose transposed reader sits in
-// another CTA): no L1 allocation, so L1 keeps the blocks the CTA's sibling warps will read transposed, and the gathers
-__device__ __forceinline__ double ldmat_dead(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ double ldv_keep(const double* p) {
-  double v;
-  asm volatile("ld.global.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
-
 #ifndef GF_SELL_GROUP_DYN
 #define GF_SELL_GROUP_DYN 8  // the large-matrix (HBM-streaming) instance: more block loads in flight (c4: -0.8 %)
 #endif
-template <class G, int kGroup = GF_SELL_GROUP, bool kHints = false>
-__device__ __forceinline__ void slice_spmv_sym_g(const CgLaunch& a, int sl, const G& gat, double acc[3],
-                                                 int cta_s0 = 0, int cta_s1 = 0) {
+template <class G, int kGroup = GF_SELL_GROUP>
+__device__ __forceinline__ void slice_spmv_sym_g(const CgLaunch& a, int sl, const G& gat, double acc[3]) {
   const int lane = threadIdx.x & 31;
   const int row = sl * 32 + lane;
   const int k0 = __ldg(a.row_ptr + sl), k1 = __ldg(a.row_ptr + sl + 1);
@@ -168,13 +143,8 @@ __device__ __forceinline__ void slice_spmv_sym_g(const CgLaunch& a, int sl, cons
         const double3 p = gat((size_t)j);
         const double* v = a.vals + base;
         double m[9];
-        if (kHints && (tr || (j >> 5) < cta_s0 || (j >> 5) >= cta_s1)) {
 #pragma unroll
-          for (int q = 0; q < 9; ++q) m[q] = ldmat_dead(v + 32 * q);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 9; ++q) m[q] = ldmat(v + 32 * q);
-        }
+        for (int q = 0; q < 9; ++q) m[q] = ldmat(v + 32 * q);
         if (!tr) {
           acc[0] = __fma_rn(m[0], p.x, acc[0]); acc[0] = __fma_rn(m[1], p.y, acc[0]); acc[0] = __fma_rn(m[2], p.z, acc[0]);
           acc[1] = __fma_rn(m[3], p.x, acc[1]); acc[1] = __fma_rn(m[4], p.y, acc[1]); acc[1] = __fma_rn(m[5], p.z, acc[1]);
@@ -212,7 +182,6 @@ struct GatherM {
   const double* z;
   __device__ __forceinline__ double3 operator()(size_t j) const {
     if (kL2) return make_double3(__ldcg(z + 3 * j), __ldcg(z + 3 * j + 1), __ldcg(z + 3 * j + 2));
-    if (GF_L1_HINTS >= 2) return make_double3(ldv_keep(z + 3 * j), ldv_keep(z + 3 * j + 1), ldv_keep(z + 3 * j + 2));
     return make_double3(ldv(z + 3 * j), ldv(z + 3 * j + 1), ldv(z + 3 * j + 2));
   }
 };
@@ -666,17 +635,9 @@ __global__ void __launch_bounds__(kDyn ? kDynThreads : kThreads) k_pcg_sell(Sell
 // Solver state (x, r, D^-1, u, w, p, s, q, z) lives in shared memory for the whole solve; m is double-buffered in
 // global memory (a slow warp may still gather m_i while a fast one writes m_{i+1}); deterministic fixed-order
 // reductions as in k_pcg_sell.
-#ifndef GF_PIPE_XG
-#define GF_PIPE_XG 0  // 1: x stays in global memory (updated in place each iteration): 8 fields of shared memory, more L1
-#endif
-#ifndef GF_PIPE_EXPLICIT
-#define GF_PIPE_EXPLICIT 1  // u = D^-1 r and q = D^-1 s evaluated, not carried: 7 shared fields (more L1), -8 % at c3
-#endif
-#ifndef GF_PIPE_DIAG
-#define GF_PIPE_DIAG 0  // 1 (with GF_PIPE_EXPLICIT): D^-1 recomputed from the diagonal block each iteration, not stored
-#endif
-constexpr bool kPipeDiag = GF_PIPE_DIAG && GF_PIPE_EXPLICIT;
-constexpr int kPipeFields = (GF_PIPE_EXPLICIT ? 7 : 9) - (GF_PIPE_XG ? 1 : 0) - (kPipeDiag ? 1 : 0);
+// solver state per lane in shared memory: x, r, D^-1, w, p, s, z (u = D^-1 r and q = D^-1 s are evaluated where
+// needed instead of carried: the same quantities, and 37 KB more L1 per SM than 9 carried fields -- DESIGN.md §7)
+constexpr int kPipeFields = 7;
 // kCluster: the whole solve inside ONE thread-block cluster (small matrices, <= 16 x 24 slices): the grid barrier
 // becomes the hardware cluster barrier and the CTA partials are exchanged through distributed shared memory
 template <bool kCluster>
@@ -700,39 +661,49 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
   const int row = u0 * 32 + lane;
   const bool live = has && row < nrows;
   extern __shared__ double s_state[];
-#if GF_PIPE_EXPLICIT && GF_PIPE_DIAG
-  enum { R = 0, W = 1, P = 2, S = 3, Z = 4, X = 5, D = 6, U = 7, Q = 8 };  // D, U, Q never stored
-#elif GF_PIPE_EXPLICIT
-  enum { R = 0, D = 1, W = 2, P = 3, S = 4, Z = 5, X = 6, U = 7, Q = 8 };  // U, Q never stored
-#else
-  enum { R = 0, D = 1, U = 2, W = 3, P = 4, S = 5, Q = 6, Z = 7, X = 8 };  // X last: absent when GF_PIPE_XG
-#endif
+  enum { R = 0, D = 1, W = 2, P = 3, S = 4, Z = 5, X = 6 };
 #define PV(f, c) s_state[((w * kPipeFields + (f)) * 3 + (c)) * 32 + lane]
-  // D^-1 of this row: stored, or (kPipeDiag) recomputed from the diagonal block -- the first upper block of the row
-  // (ordinal 0), entries 0, 4, 8 -- with the assembly's formula (sparse.cpp:133-136), so the bits are the same
-  const double* diag = a.vals + (size_t)__ldg(a.usp + (u0 < a.nslices ? u0 : 0)) * 288 + lane;
-  auto DV = [&](int c) -> double {
-    if constexpr (kPipeDiag) {
-      const double dd = diag[32 * 4 * c];
-      return (fabs(dd) > 1e-300) ? 1.0 / dd : 1.0;
-    } else {
-      return PV(D, c);
-    }
-  };
+  auto DV = [&](int c) -> double { return PV(D, c); };
   __shared__ double s_acc[kWarpsPerCta][4];
   // double-buffered gathered vector (u during setup, then m): buffer k is a.z (k = 0) or a.p0 (k = 1)
   auto gm = [&](int k) { return k ? a.p0 : a.z; };
 
   // CTA partials of NV warp values (one slice per warp): warp sums in lane order, CTA sum in warp order
+  // the CTA's partial of NV warp values: warp 0 reduces the warps' values with one fixed butterfly (not a serial
+  // 24-term loop), lane q < NV publishes value q
   auto publish = [&](const double* v, int nv, int parity) {
     if (lane == 0)
       for (int q = 0; q < nv; ++q) s_acc[w][q] = v[q];
     __syncthreads();
-    if ((int)threadIdx.x < nv) {
-      double x = 0.0;
-      for (int k = 0; k < kWarpsPerCta; ++k) x += s_acc[k][threadIdx.x];
-      if constexpr (kCluster) s_part[parity][threadIdx.x] = x;
-      else sa.cta_part[((size_t)parity * 4 + threadIdx.x) * kMaxGrid + blockIdx.x] = x;
+    if (w == 0) {
+      double x[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) x[q] = (q < nv && lane < kWarpsPerCta) ? s_acc[lane][q] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) x[q] = lane_sum(x[q]);
+      const double xl = lane == 0 ? x[0] : lane == 1 ? x[1] : x[2];
+      if (lane < nv) {
+        if constexpr (kCluster) s_part[parity][lane] = xl;
+        else sa.cta_part[((size_t)parity * 4 + lane) * kMaxGrid + blockIdx.x] = xl;
+      }
+    }
+  };
+  // totals of the published partials of all G CTAs: fixed lane and warp trees with ONE block barrier (the next
+  // writer of s_tot is separated from these reads by the publish barrier and the grid / cluster barrier)
+  __shared__ double s_tot[kWarpsPerCta][4];
+  auto totals3 = [&](const double (&pbv)[3], double (&out)[3]) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double t = lane_sum(pbv[q]);
+      if (lane == 0) s_tot[w][q] = t;
+    }
+    __syncthreads();
+    const int nw = (G + 31) >> 5;  // warps holding partials (threads < G)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      double t = 0.0;
+      for (int k = 0; k < nw; ++k) t += s_tot[k][q];
+      out[q] = t;
     }
   };
 
@@ -752,12 +723,10 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
     for (int c = 0; c < 3; ++c) {
       const size_t dof = 3 * (size_t)row + c;
       const double bi = a.b[dof], ri = bi - acc[c], di = __ldg(a.dinv + dof), ui = di * ri;
-      if (!GF_PIPE_XG) PV(X, c) = a.x[dof];
+      PV(X, c) = a.x[dof];
       PV(R, c) = ri;
-      if (!kPipeDiag) PV(D, c) = di;
-      if (!GF_PIPE_EXPLICIT) PV(U, c) = ui;
+      PV(D, c) = di;
       PV(P, c) = PV(S, c) = PV(Z, c) = 0.0;
-      if (!GF_PIPE_EXPLICIT) PV(Q, c) = 0.0;
       gm(0)[dof] = ui;
       bb = __fma_rn(bi, bi, bb);
     }
@@ -788,7 +757,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
         const size_t dof = 3 * (size_t)row + c;
         PV(W, c) = acc[c];
         gm(1)[dof] = DV(c) * acc[c];
-        const double uc = GF_PIPE_EXPLICIT ? DV(c) * PV(R, c) : PV(U, c);
+        const double uc = DV(c) * PV(R, c);  // u_0 = D^-1 r_0
         v3[0] = __fma_rn(PV(R, c), uc, v3[0]);
         v3[1] = __fma_rn(acc[c], uc, v3[1]);
         v3[2] = __fma_rn(PV(R, c), PV(R, c), v3[2]);
@@ -809,13 +778,11 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
         for (int q = 0; q < 3; ++q) pb[q] = read_part(pp, q, threadIdx.x);
       }
       double n3[3] = {0.0, 0.0, 0.0};
-      if (has && it < a.max_iters)
-        slice_spmv_sym_g<GatherM<kCluster>, GF_SELL_GROUP, (GF_L1_HINTS > 0)>(a, u0, GatherM<kCluster>{gm(cur)}, n3,
-                                                                        cta_s0, cta_s1);
+      if (has && it < a.max_iters) slice_spmv_sym_g(a, u0, GatherM<kCluster>{gm(cur)}, n3);
       SELL_STAMP(it, 1);
       SELL_BLOCK_STAMP(it, 3000);
       double red[3];
-      cta_tree<3>(pb, red);  // gamma_it, delta_it, r_it.r_it
+      totals3(pb, red);  // gamma_it, delta_it, r_it.r_it
       const double gam = red[0], del = red[1];
       relres = sqrt(red[2]) / bnorm;
       if (it > 0 && relres <= a.tol) {  // sparse.cpp:172-178 on the residual of update it
@@ -845,32 +812,16 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
         for (int c = 0; c < 3; ++c) {
           const size_t dof = 3 * (size_t)row + c;
           const double dvc = DV(c);
-          const double mi = dvc * PV(W, c);  // m_it of this row (the value gathered this iteration)
-          const double zi = __fma_rn(beta, PV(Z, c), n3[c]);
-          const double si = __fma_rn(beta, PV(S, c), PV(W, c));
-#if GF_PIPE_EXPLICIT
-          const double di = dvc;
-          const double qi = di * si;             // q = D^-1 s (carried as m + beta q in the recurrence form)
-          const double pi = __fma_rn(beta, PV(P, c), di * PV(R, c));  // u = D^-1 r
-#else
-          const double qi = __fma_rn(beta, PV(Q, c), mi);
-          const double pi = __fma_rn(beta, PV(P, c), PV(U, c));
-          PV(Q, c) = qi;
-#endif
+          const double zi = __fma_rn(beta, PV(Z, c), n3[c]);   // z = A q  = n + beta z
+          const double si = __fma_rn(beta, PV(S, c), PV(W, c));  // s = A p  = w + beta s
+          const double pi = __fma_rn(beta, PV(P, c), dvc * PV(R, c));  // p = u + beta p, u = D^-1 r
           PV(Z, c) = zi;
           PV(S, c) = si;
           PV(P, c) = pi;
-          if (GF_PIPE_XG) a.x[dof] = __fma_rn(alpha, pi, a.x[dof]);
-          else PV(X, c) = __fma_rn(alpha, pi, PV(X, c));
+          PV(X, c) = __fma_rn(alpha, pi, PV(X, c));
           const double ri = __fma_rn(-alpha, si, PV(R, c));
-#if GF_PIPE_EXPLICIT
-          const double ui = di * ri;
-          (void)qi;
-#else
-          const double ui = __fma_rn(-alpha, qi, PV(U, c));
-          PV(U, c) = ui;
-#endif
-          const double wi = __fma_rn(-alpha, zi, PV(W, c));
+          const double ui = dvc * ri;                              // u = D^-1 r (q = D^-1 s is implied)
+          const double wi = __fma_rn(-alpha, zi, PV(W, c));        // w -= alpha z
           PV(R, c) = ri;
           PV(W, c) = wi;
           gm(cur ^ 1)[dof] = dvc * wi;
@@ -890,8 +841,7 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
     }
     if (live)
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-        if (!GF_PIPE_XG) a.x[3 * (size_t)row + c] = PV(X, c);
+      for (int c = 0; c < 3; ++c) a.x[3 * (size_t)row + c] = PV(X, c);
   }
 #undef PV
   // no CTA of a cluster may exit while another can still read its shared memory (the last partial reads)
@@ -930,12 +880,6 @@ void set_smem_attributes() {
     cudaFuncSetAttribute((const void*)k_pcg_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
     cudaFuncSetAttribute((const void*)k_pcg_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
     cudaFuncSetAttribute((const void*)k_pcg_pipe<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-#if GF_CARVEOUT
-    // one CTA per SM: the smallest shared-memory configuration that holds the solver state, the rest as L1
-    for (const void* f : {(const void*)k_pcg_pipe<false>, (const void*)k_pcg_pipe<true>, (const void*)k_pcg_sell<false>,
-                          (const void*)k_pcg_sell<true>})
-      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxL1);
-#endif
     return true;
   }();
   (void)done;

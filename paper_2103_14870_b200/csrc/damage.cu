@@ -169,13 +169,7 @@ constexpr int kNlTpb = GF_NL_TPB;
 #ifndef GF_NL_PRED
 #define GF_NL_PRED 1
 #endif
-#ifndef GF_NL_EARLY
-#define GF_NL_EARLY 0  // 1: sigma gather addresses independent of the streamed weight: measured 0.430 vs 0.418 ms (absent slots then load real sigma records)
-#endif
-#ifndef GF_NL_UNROLL
-#define GF_NL_UNROLL 4
-#endif
-constexpr int kNlUnroll = GF_NL_UNROLL;  // template warps per CTA x 32
+  // template warps per CTA x 32
 __global__ void __launch_bounds__(kNlTpb, (GF_NL_MINB * 256) / kNlTpb) k_nonlocal_tpl(DevData d) {
   const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (wid >= d.nl_nwarps) return;
@@ -187,22 +181,14 @@ __global__ void __launch_bounds__(kNlTpb, (GF_NL_MINB * 256) / kNlTpb) k_nonloca
   const double2* s2 = reinterpret_cast<const double2*>(d.sigc);
   const size_t plane = (size_t)d.nt;
   double avg[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  // loads are unconditional and their addresses do not depend on the weight: an absent slot reads the (clamped)
-  // template position anyway, so the sigma gathers issue together with the weight stream instead of waiting for
-  // it (the weight is an HBM load; its first use was 44 % of this kernel's stall samples); an absent slot leaves
-  // avg untouched (a predicated add, not a multiply-add: exact whatever it read)
-  [[maybe_unused]] const int pmax = d.nt - 1;
-#pragma unroll kNlUnroll
+  // loads are unconditional (absent slots read lane 0's record of plane position 0, one L1 line) so consecutive
+  // slots pipeline; an absent slot leaves avg untouched (a predicated add, not a multiply-add: exact whatever it read).
+  // Gathering at the template position regardless of the weight was measured slower.
+#pragma unroll 4
   for (int j = j0; j < j1; ++j) {
     const double w = __ldcs(d.nl_tw + (size_t)j * 32 + lane);
     const bool present = w != 0.0;
-#if GF_NL_EARLY
-    int pi = __ldg(d.nl_spos + j) + lane;
-    pi = pi < 0 ? 0 : (pi > pmax ? pmax : pi);
-    const size_t pos = (size_t)pi;
-#else
     const size_t pos = present ? (size_t)__ldg(d.nl_spos + j) + lane : 0;
-#endif
     const double2 s01 = __ldg(s2 + pos), s23 = __ldg(s2 + plane + pos), s45 = __ldg(s2 + 2 * plane + pos);
 #if GF_NL_PRED
     if (present) {  // predicated adds: half the instructions of per-component selects
@@ -311,23 +297,7 @@ inline int nblk(int64_t n) { return (int)((n + kTpb - 1) / kTpb); }
 
 }  // namespace
 
-#ifndef GF_CARVEOUT
-#define GF_CARVEOUT 0  // 1: prefer the maximum L1 (no shared memory) for the L1-bound damage kernels
-#endif
-static void damage_carveout() {
-  [[maybe_unused]] static bool done = [] {
-    if (GF_CARVEOUT) {
-      cudaFuncSetAttribute(k_tet_stress, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxL1);
-      cudaFuncSetAttribute(k_nonlocal_tpl, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxL1);
-      cudaFuncSetAttribute(k_nonlocal, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxL1);
-    }
-    return true;
-  }();
-  (void)done;
-}
-
 void launch_tet_stress(const DevData& d, const MatDev& m, bool local_screen, cudaStream_t s) {
-  damage_carveout();
   k_tet_stress<<<nblk(d.nt), kTpb, 0, s>>>(d, m, local_screen ? 1 : 0);
 }
 void launch_nonlocal(const DevData& d, cudaStream_t s) {
