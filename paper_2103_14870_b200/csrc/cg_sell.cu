@@ -781,6 +781,12 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
       if (has && it < a.max_iters) slice_spmv_sym_g(a, u0, GatherM<kCluster>{gm(cur)}, n3);
       SELL_STAMP(it, 1);
       SELL_BLOCK_STAMP(it, 3000);
+      SELL_BLOCK_STAMP_AT(it, 20, 4000);
+      if (a.trace && it == 10 && threadIdx.x == 0) {  // the SM each CTA runs on (imbalance diagnostics)
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.trace[1600 + blockIdx.x] = smid;
+      }
       double red[3];
       totals3(pb, red);  // gamma_it, delta_it, r_it.r_it
       const double gam = red[0], del = red[1];

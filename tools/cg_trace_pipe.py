@@ -26,3 +26,16 @@ print(json.dumps({"config": s.name, "iterations": int(st.cg_iterations), "us_per
                   "cta0_spmv_us": us(0, 1), "cta0_reduce_update_publish_us": us(1, 3), "cta0_barrier_wait_us": wait,
                   "ctas": nb, "spmv_end_spread_us": float((spmv.max() - t0) / 1e3),
                   "publish_end_spread_us": float((pub.max() - pub.min()) / 1e3)}))
+# per-CTA SpMV-end offsets at iterations 10 and 20 with the SM each CTA ran on: is the spread the same CTAs / SMs?
+s10 = buf[3000:3000 + nb].astype(np.float64)
+s20 = buf[4000:4000 + nb].astype(np.float64)
+sm = buf[1600:1600 + nb].astype(np.int64)
+if (s20 > 0).all():
+    d10 = (s10 - s10.min()) / 1e3
+    d20 = (s20 - s20.min()) / 1e3
+    slow = np.argsort(-d10)[:10]
+    print(json.dumps({"corr_spmv_end_it10_it20": float(np.corrcoef(d10, d20)[0, 1]),
+                      "slowest_ctas_it10": [int(x) for x in slow], "their_sm": [int(sm[x]) for x in slow],
+                      "their_delay_us_it10": [round(float(d10[x]), 2) for x in slow],
+                      "their_delay_us_it20": [round(float(d20[x]), 2) for x in slow],
+                      "median_delay_us": float(np.median(d10))}))
