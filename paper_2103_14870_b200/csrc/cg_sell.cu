@@ -114,14 +114,26 @@ __device__ __forceinline__ double ldmat(const double* p) {
 #endif
 }
 
+#ifndef GF_CG_TRACE_SM
+#define GF_CG_TRACE_SM 0  // diagnostics build (tools/cg_trace_pipe.py imbalance section): per-CTA stamps + %smid
+#endif
+
 #ifndef GF_SELL_GROUP_DYN
 #define GF_SELL_GROUP_DYN 8  // the large-matrix (HBM-streaming) instance: more block loads in flight (c4: -0.8 %)
 #endif
+// part / split: this warp takes the part-th of `split` contiguous chunks of the slice's slots (small matrices whose
+// slices are shared by several warps, k_pcg_pipe<true>); the owner adds the chunks' sums in chunk order
 template <class G, int kGroup = GF_SELL_GROUP>
-__device__ __forceinline__ void slice_spmv_sym_g(const CgLaunch& a, int sl, const G& gat, double acc[3]) {
+__device__ __forceinline__ void slice_spmv_sym_g(const CgLaunch& a, int sl, const G& gat, double acc[3], int part = 0,
+                                                 int split = 1) {
   const int lane = threadIdx.x & 31;
   const int row = sl * 32 + lane;
-  const int k0 = __ldg(a.row_ptr + sl), k1 = __ldg(a.row_ptr + sl + 1);
+  int k0 = __ldg(a.row_ptr + sl), k1 = __ldg(a.row_ptr + sl + 1);
+  if (split > 1) {
+    const int per = (k1 - k0 + split - 1) / split;
+    k0 += part * per;
+    k1 = min(k1, k0 + per);
+  }
   const uint32_t* slots = reinterpret_cast<const uint32_t*>(a.cols);
   const int own_base = __ldg(a.usp + sl) * 288 + lane;
   const int zero_base = a.zero_base + lane;
@@ -655,14 +667,30 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
   const CgLaunch& a = sa.a;
   const int nrows = a.nrows, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int G = (int)gridDim.x;
+  // kCluster: `split` warps share a slice (part 0 owns its state; the others SpMV a chunk of its slots)
+  const int split = kCluster ? a.split : 1;
+  const int ws = kCluster ? w / split : w, part = kCluster ? w - ws * split : 0;
   const int cta_s0 = __ldg(a.cta_first + blockIdx.x), cta_s1 = __ldg(a.cta_first + blockIdx.x + 1);
-  const int u0 = cta_s0 + w;
+  const int u0 = cta_s0 + ws;
   const bool has = u0 < cta_s1;
   const int row = u0 * 32 + lane;
-  const bool live = has && row < nrows;
+  const bool live = has && part == 0 && row < nrows;
   extern __shared__ double s_state[];
+  double* const s_split = s_state + kWarpsPerCta * kPipeFields * 96;  // kCluster, split > 1: chunk sums
+  // the chunk sums of a shared slice, added by the owner in chunk order (deterministic)
+  auto combine = [&](double (&v)[3]) {
+    if (split == 1) return;
+    if (has && part > 0)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) s_split[((ws * (split - 1) + part - 1) * 3 + c) * 32 + lane] = v[c];
+    __syncthreads();
+    if (has && part == 0)
+      for (int q = 1; q < split; ++q)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] += s_split[((ws * (split - 1) + q - 1) * 3 + c) * 32 + lane];
+  };
   enum { R = 0, D = 1, W = 2, P = 3, S = 4, Z = 5, X = 6 };
-#define PV(f, c) s_state[((w * kPipeFields + (f)) * 3 + (c)) * 32 + lane]
+#define PV(f, c) s_state[((ws * kPipeFields + (f)) * 3 + (c)) * 32 + lane]
   auto DV = [&](int c) -> double { return PV(D, c); };
   __shared__ double s_acc[kWarpsPerCta][4];
   // double-buffered gathered vector (u during setup, then m): buffer k is a.z (k = 0) or a.p0 (k = 1)
@@ -675,16 +703,21 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
     if (lane == 0)
       for (int q = 0; q < nv; ++q) s_acc[w][q] = v[q];
     __syncthreads();
-    if (w == 0) {
-      double x[3];
+    if constexpr (kCluster) {  // latency-bound small solves: one warp butterfly instead of a serial 24-term loop
+      if (w == 0) {
+        double x[3];
 #pragma unroll
-      for (int q = 0; q < 3; ++q) x[q] = (q < nv && lane < kWarpsPerCta) ? s_acc[lane][q] : 0.0;
+        for (int q = 0; q < 3; ++q) x[q] = (q < nv && lane < kWarpsPerCta) ? s_acc[lane][q] : 0.0;
 #pragma unroll
-      for (int q = 0; q < 3; ++q) x[q] = lane_sum(x[q]);
-      const double xl = lane == 0 ? x[0] : lane == 1 ? x[1] : x[2];
-      if (lane < nv) {
-        if constexpr (kCluster) s_part[parity][lane] = xl;
-        else sa.cta_part[((size_t)parity * 4 + lane) * kMaxGrid + blockIdx.x] = xl;
+        for (int q = 0; q < 3; ++q) x[q] = lane_sum(x[q]);
+        const double xl = lane == 0 ? x[0] : lane == 1 ? x[1] : x[2];
+        if (lane < nv) s_part[parity][lane] = xl;
+      }
+    } else {  // (the butterfly costs the grid instance a register spill: measured neutral-to-worse at c3)
+      if ((int)threadIdx.x < nv) {
+        double x = 0.0;
+        for (int k = 0; k < kWarpsPerCta; ++k) x += s_acc[k][threadIdx.x];
+        sa.cta_part[((size_t)parity * 4 + threadIdx.x) * kMaxGrid + blockIdx.x] = x;
       }
     }
   };
@@ -714,9 +747,11 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) acc[c] = row < nrows ? a.x[3 * (size_t)row + c] : 0.0;
     } else {
-      slice_spmv_sym_g(a, u0, GatherX{a.x}, acc);
+      if constexpr (kCluster) slice_spmv_sym_g(a, u0, GatherX{a.x}, acc, part, split);
+      else slice_spmv_sym_g(a, u0, GatherX{a.x}, acc);
     }
   }
+  if (!a.x0_identity) combine(acc);
   double bb = 0.0;
   if (live) {
 #pragma unroll
@@ -749,7 +784,11 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
   } else {
     // setup 2: w = A u, m = D^-1 w (gathered by iteration 0), partials gamma_0, delta_0, r.r
     acc[0] = acc[1] = acc[2] = 0.0;
-    if (has) slice_spmv_sym_g(a, u0, GatherM<kCluster>{gm(0)}, acc);
+    if (has) {
+      if constexpr (kCluster) slice_spmv_sym_g(a, u0, GatherM<kCluster>{gm(0)}, acc, part, split);
+      else slice_spmv_sym_g(a, u0, GatherM<kCluster>{gm(0)}, acc);
+    }
+    combine(acc);
     double v3[3] = {0.0, 0.0, 0.0};
     if (live) {
 #pragma unroll
@@ -778,17 +817,24 @@ __global__ void __launch_bounds__(kThreads) k_pcg_pipe(SellArgs sa) {
         for (int q = 0; q < 3; ++q) pb[q] = read_part(pp, q, threadIdx.x);
       }
       double n3[3] = {0.0, 0.0, 0.0};
-      if (has && it < a.max_iters) slice_spmv_sym_g(a, u0, GatherM<kCluster>{gm(cur)}, n3);
+      if (has && it < a.max_iters) {
+        if constexpr (kCluster) slice_spmv_sym_g(a, u0, GatherM<kCluster>{gm(cur)}, n3, part, split);
+        else slice_spmv_sym_g(a, u0, GatherM<kCluster>{gm(cur)}, n3);
+      }
+      combine(n3);
       SELL_STAMP(it, 1);
       SELL_BLOCK_STAMP(it, 3000);
+#if GF_CG_TRACE_SM
       SELL_BLOCK_STAMP_AT(it, 20, 4000);
       if (a.trace && it == 10 && threadIdx.x == 0) {  // the SM each CTA runs on (imbalance diagnostics)
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         a.trace[1600 + blockIdx.x] = smid;
       }
+#endif
       double red[3];
-      totals3(pb, red);  // gamma_it, delta_it, r_it.r_it
+      if constexpr (kCluster) totals3(pb, red);  // gamma_it, delta_it, r_it.r_it
+      else cta_tree<3>(pb, red);
       const double gam = red[0], del = red[1];
       relres = sqrt(red[2]) / bnorm;
       if (it > 0 && relres <= a.tol) {  // sparse.cpp:172-178 on the residual of update it
@@ -878,13 +924,15 @@ int g_grid = 0, g_dyn_per = 0;
 
 constexpr size_t kSellSmem = GF_CG_SMEM ? (size_t)kWarpsPerCta * 6 * 3 * 32 * sizeof(double) : 0;
 constexpr size_t kPipeSmem = (size_t)kWarpsPerCta * kPipeFields * 3 * 32 * sizeof(double);
+constexpr size_t kSplitSmem = (size_t)1728 * sizeof(double);  // chunk sums of shared slices (split <= 4: 24 warps)
 
 void set_smem_attributes() {
   static bool done = [] {
     cudaFuncSetAttribute((const void*)k_pcg_sell<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellSmem);
     cudaFuncSetAttribute((const void*)k_pcg_sell<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellSmem);
     cudaFuncSetAttribute((const void*)k_pcg_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
-    cudaFuncSetAttribute((const void*)k_pcg_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem);
+    cudaFuncSetAttribute((const void*)k_pcg_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(kPipeSmem + kSplitSmem));
     cudaFuncSetAttribute((const void*)k_pcg_pipe<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return true;
   }();
@@ -934,7 +982,7 @@ int pcg_max_cluster() {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(16, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = kPipeSmem;
+    cfg.dynamicSmemBytes = kPipeSmem + kSplitSmem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 16;
@@ -967,7 +1015,7 @@ void launch_pcg_sell(const CgLaunch& a, double* part, int ndyn, unsigned long lo
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.grid, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = kPipeSmem;
+    cfg.dynamicSmemBytes = kPipeSmem + kSplitSmem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;

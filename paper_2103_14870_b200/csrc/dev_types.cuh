@@ -197,6 +197,7 @@ struct CgLaunch {
   int32_t pipelined;  // cg_sell.cu: 1 = the single-barrier pipelined solver (k_pcg_pipe) when the state fits on chip
   int32_t grid;       // cg_sell.cu: CTAs of the cooperative launch (0 = all co-resident)
   int32_t cluster;    // cg_sell.cu: 1 = the pipelined solve runs in ONE thread-block cluster of `grid` CTAs
+  int32_t split;      // cg_sell.cu (cluster): warps sharing one slice's SpMV (1, 2, 3 or 4)
 };
 int cg_csr_grid();
 void launch_pcg_csr(const CgLaunch& a, cudaStream_t s);  // scalar CSR (gf_cg_solve_csr)

@@ -567,16 +567,23 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     // DSMEM partial exchange instead of grid barriers through global memory (GF_CG_CLUSTER=0 disables)
     const char* ce = std::getenv("GF_CG_CLUSTER");
     const int cmax = (ce && std::atoi(ce) == 0) || !cg_.pipelined || dyn ? 0 : pcg_max_cluster();
+    int Weff = W;
     if (cmax > 0 && ns <= cmax * W) {
       G = cmax;
       cg_.cluster = 1;
+      // warps to spare: up to 4 warps share a slice's SpMV (shorter latency chains)
+      int split = 4;
+      if (const char* se = std::getenv("GF_CG_SPLIT")) split = std::max(1, std::min(4, std::atoi(se)));
+      while (split > 1 && ns > cmax * (W / split)) --split;
+      cg_.split = split;
+      Weff = W / split;
     }
     cg_.grid = G;
-    const int64_t gw = (int64_t)G * W;
+    const int64_t gw = (int64_t)G * Weff;
     double frac = 0.0;  // measured at c4 (28k slices): all-dynamic tail 22.5 ms, 50 % static 23.0, 80 % 26.2
     if (const char* e = std::getenv("GF_CG_STATIC")) frac = std::atof(e);  // static share of a large matrix
     const int32_t nstat = ns <= gw ? ns : (int32_t)std::min<int64_t>(ns, std::max<int64_t>(gw, (int64_t)(frac * ns)));
-    const int64_t cap_n = (int64_t)W * std::max<int64_t>(1, (nstat + gw - 1) / gw);
+    const int64_t cap_n = (int64_t)Weff * std::max<int64_t>(1, (nstat + gw - 1) / gw);
     std::vector<int32_t> first(G + 1, 0);
     auto fill = [&](int64_t cap, bool write) {
       int32_t sl = 0;
