@@ -278,6 +278,9 @@ typedef struct {
   int32_t pcg_dynamic_units;  /* PCG slices handed out by ticket: 0 = solver state on chip for the whole solve */
   double setup_s[4];          /* wall seconds: [0] pattern + incidence + assembly lists + SELL layout,
                                  [1] non-local table (grid-binned build), [2] device layout + uploads, [3] ctor total */
+  int32_t pcg_solver;         /* production PCG instance: 0 k_pcg_sell (two barriers), 1 k_pcg_pipe (grid), 2 k_pcg_pipe
+                                 (one cluster), 3 k_pcg_onchip (matrix in TMEM + shared memory), 4 k_pcg_sell large-matrix */
+  int32_t _pad0;
 } gf_sim_info;
 int gf_sim_info_get(const gf_sim* s, gf_sim_info* out);
 /* measured device bandwidth in GB/s on the current device: kind 0 = reads of an L2-resident buffer of `bytes`

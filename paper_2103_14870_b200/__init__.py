@@ -95,11 +95,15 @@ class _CgResult(C.Structure):
                 ("_pad", C.c_int32), ("relative_residual", C.c_double)]
 
 
+PCG_SOLVERS = ("two-barrier", "grid", "cluster", "onchip", "large-matrix")  # gf_sim_info.pcg_solver
+
+
 class _SimInfo(C.Structure):
     _fields_ = [("nodes", C.c_int64), ("tets", C.c_int64), ("edges", C.c_int64), ("node_blocks", C.c_int64),
                 ("upper_blocks", C.c_int64), ("upper_block_slots", C.c_int64), ("spmv_slots", C.c_int64),
                 ("nl_entries", C.c_int64), ("nl_slots", C.c_int64), ("nl_layout", C.c_int32),
-                ("pcg_dynamic_units", C.c_int32), ("setup_s", C.c_double * 4)]
+                ("pcg_dynamic_units", C.c_int32), ("setup_s", C.c_double * 4), ("pcg_solver", C.c_int32),
+                ("_pad0", C.c_int32)]
 
 
 class StepMetrics(C.Structure):
@@ -616,7 +620,8 @@ class Simulation:
         """gf_sim_info: storage sizes of the device formats (roofline byte models) and the setup wall times."""
         i = _SimInfo()
         _check(lib().gf_sim_info_get(self._h, C.byref(i)))
-        out = {k: getattr(i, k) for k, _ in _SimInfo._fields_ if k != "setup_s"}
+        out = {k: getattr(i, k) for k, _ in _SimInfo._fields_ if k not in ("setup_s", "_pad0")}
+        out["pcg_solver_name"] = PCG_SOLVERS[i.pcg_solver]
         out["setup_s"] = dict(pattern_and_layouts=i.setup_s[0], nonlocal_table=i.setup_s[1],
                               device_layout_and_upload=i.setup_s[2], total=i.setup_s[3])
         return out

@@ -26,6 +26,7 @@ CU_SOURCES = {  # file -> extra flags
     "assemble.cu": [],
     "cg.cu": [],
     "cg_sell.cu": [],
+    "cg_onchip.cu": [],
     "sim.cu": [],
     "probe.cu": [],
     "metrics.cu": [],

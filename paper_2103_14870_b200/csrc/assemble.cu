@@ -321,7 +321,17 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&v)[N], int lane) 
 // diagonal; kv and corr accumulate
 template <int kMode>
 __device__ __forceinline__ void finish_column(const DevData& d, const StepCoeffs& sc, int i, int row0, int c, int j,
-                                              const double K[9], bool fixed_i, double kv[3], double corr[3]) {
+                                              const double Kin[9], bool fixed_i, double kv[3], double corr[3]) {
+  // the diagonal block is symmetric up to rounding ((c2 a_r) a_c vs (c2 a_c) a_r): its upper triangle is mirrored so
+  // that the stored block is exactly symmetric (the on-chip solver, cg_onchip.cu, keeps 6 of its 9 values)
+  double K[9];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) K[r] = Kin[r];
+  if (j == i) {
+    K[3] = K[1];
+    K[6] = K[2];
+    K[7] = K[5];
+  }
   // destination: the upper block in SELL-32 (entry r at out[32 r]); lower blocks of the symmetric format are
   // not stored (row j writes (j,i) = (i,j)^T)
   const int cu = __ldg(d.uslot + row0 + c);

@@ -198,6 +198,7 @@ struct CgLaunch {
   int32_t grid;       // cg_sell.cu: CTAs of the cooperative launch (0 = all co-resident)
   int32_t cluster;    // cg_sell.cu: 1 = the pipelined solve runs in ONE thread-block cluster of `grid` CTAs
   int32_t split;      // cg_sell.cu (cluster): warps sharing one slice's SpMV (1, 2, 3 or 4)
+  int32_t onchip;     // cg_onchip.cu: 1 = the pipelined solve with the matrix held in TMEM + shared memory
 };
 int cg_csr_grid();
 void launch_pcg_csr(const CgLaunch& a, cudaStream_t s);  // scalar CSR (gf_cg_solve_csr)
@@ -211,6 +212,17 @@ int pcg_pipelined_default();  // GF_CG_PIPE (default 1)
 int pcg_max_cluster();        // largest launchable cluster of the pipelined solver (0: none)
 void launch_pcg_sell(const CgLaunch& a, double* part, int ndyn, unsigned long long* ctr, cudaStream_t s);
 void launch_spmv_sym(const CgLaunch& a, const double* xin, double* y, cudaStream_t s);
+// ---- cg_onchip.cu (the pipelined solve with the matrix on chip: at most 7 distinct positive column offsets (rows
+// of <= 8 upper blocks), <= 24 slices per CTA, exactly symmetric diagonal blocks) ----
+int pcg_onchip_grid();  // co-resident CTAs (0: not launchable on this device)
+int pcg_onchip_warps_per_cta();
+int pcg_onchip_max_upper();
+int pcg_onchip_npad(int nslices);
+size_t pcg_onchip_t_doubles(int nslices);  // the remote transposed-product buffers (zero-initialized)
+size_t pcg_onchip_m_doubles(int nslices);  // the gathered vector's two buffers (zero-initialized)
+// meta / off: the rows' structure over the matrix's (at most 7) distinct positive column offsets (cg_onchip.cu)
+void launch_pcg_onchip(const CgLaunch& a, double* part, double* tg, double* gm, const uint32_t* meta,
+                       const int32_t off[7], cudaStream_t s);
 // ---- misc.cu ----
 void launch_bc_targets(const DevData& d, int32_t n_fixed, const int32_t* fixed_nodes, double dt, cudaStream_t s);
 int collide_blocks(const DevData& d);

@@ -610,6 +610,33 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     d_slice_part_ = (double*)zeros(8 * pcg_sell_part_doubles(cg_ndyn_));
     d_ctr_ = (unsigned long long*)zeros(64);
     cg_.cta_first = (const int32_t*)up(first.data(), 4 * first.size());
+    // the matrix on chip (cg_onchip.cu) when the pattern has at most 7 distinct positive column offsets (the box
+    // meshes: +1, +nx, +nx+1, +nx ny, ...) and the slices fit one warp each on a grid of one CTA per SM (c2, c3;
+    // GF_CG_ONCHIP=0 disables)
+    std::vector<int32_t> offs;
+    for (int32_t i = 0; i < nn && offs.size() <= 7; ++i)
+      for (int32_t q = pat_.row_ptr[i]; q < pat_.row_ptr[i + 1]; ++q) {
+        const int32_t d = pat_.cols[q] - i;
+        if (d > 0 && std::find(offs.begin(), offs.end(), d) == offs.end()) offs.push_back(d);
+      }
+    const char* oe = std::getenv("GF_CG_ONCHIP");
+    if (!(oe && std::atoi(oe) == 0) && cg_.pipelined && !dyn && !cg_.cluster && offs.size() <= 7 &&
+        pcg_onchip_grid() >= G && W == pcg_onchip_warps_per_cta()) {
+      std::sort(offs.begin(), offs.end());
+      for (size_t b = 0; b < offs.size(); ++b) oc_off_[b] = offs[b];
+      auto bit = [&](int32_t d) { return (int)(std::lower_bound(offs.begin(), offs.end(), d) - offs.begin()); };
+      std::vector<uint32_t> meta(nn, 0u);  // upper slot mask | lower slot mask << 8 (slot b: offset offs[b])
+      for (int32_t i = 0; i < nn; ++i)
+        for (int32_t q = pat_.row_ptr[i]; q < pat_.row_ptr[i + 1]; ++q) {
+          const int32_t j = pat_.cols[q];
+          if (j > i) meta[i] |= 1u << bit(j - i);
+          else if (j < i) meta[i] |= 1u << (8 + bit(i - j));
+        }
+      d_oc_meta_ = (uint32_t*)up(meta.data(), sizeof(uint32_t) * meta.size());
+      cg_.onchip = 1;
+      d_tg_ = (double*)zeros(8 * pcg_onchip_t_doubles(ns));
+      d_ocm_ = (double*)zeros(8 * pcg_onchip_m_doubles(ns));
+    }
   }
   if (std::getenv("GF_CG_TRACE")) cg_.trace = (unsigned long long*)zeros(8 * 5000);
   if (const char* e = std::getenv("GF_GRAPH")) graphs_enabled_ = std::atoi(e) != 0;
@@ -635,6 +662,7 @@ gf_sim_info Simulation::info() const {
   o.nl_slots = mat_.r_d <= 0.0 ? 0 : d_.nl_tpl ? 32 * nl_tpl_slots_ : nl_ell_slots_;
   o.nl_layout = nonlocal_layout();
   o.pcg_dynamic_units = cg_ndyn_;
+  o.pcg_solver = cg_ndyn_ > 0 ? 4 : cg_.onchip ? 3 : !cg_.pipelined ? 0 : cg_.cluster ? 2 : 1;
   for (int k = 0; k < 4; ++k) o.setup_s[k] = setup_s_[k];
   return o;
 }
@@ -810,7 +838,8 @@ void Simulation::upload_bc_step(double t, double dt) {
 }
 
 void Simulation::launch_cg() {
-  launch_pcg_sell(cg_, d_slice_part_, cg_ndyn_, d_ctr_, stream_);
+  if (cg_.onchip) launch_pcg_onchip(cg_, d_slice_part_, d_tg_, d_ocm_, d_oc_meta_, oc_off_, stream_);
+  else launch_pcg_sell(cg_, d_slice_part_, cg_ndyn_, d_ctr_, stream_);
 }
 
 double Simulation::run_cg(int max_iters) {
@@ -1385,6 +1414,7 @@ void Simulation::solve_system(const double* vals, const double* b, const double*
   if (max_iters < 0) throw FormatError("max_iters must be non-negative");
   const size_t nd = 3 * (size_t)mesh_.nn;
   std::vector<double> bv(bval_doubles_, 0.0), dinv(nd, 1.0);
+  bool diag_sym = true;  // the on-chip solver stores the diagonal block's upper triangle only
   for (int32_t i = 0; i < mesh_.nn; ++i) {
     const int32_t r0 = pat_.row_ptr[i], deg = pat_.row_ptr[i + 1] - r0;
     for (int32_t q = 0; q < deg; ++q) {
@@ -1394,9 +1424,16 @@ void Simulation::solve_system(const double* vals, const double* b, const double*
           const double v = vals[9 * (size_t)r0 + 3 * (size_t)a * deg + 3 * q + c];
           if (j >= i) bv[sell_addr(usp_.data(), i, uslot_[r0 + q], 3 * a + c)] = v;
           if (j == i && a == c) dinv[3 * (size_t)i + a] = std::fabs(v) > 1e-300 ? 1.0 / v : 1.0;
+          if (j == i && c < a && v != vals[9 * (size_t)r0 + 3 * (size_t)c * deg + 3 * q + a]) diag_sym = false;
         }
     }
   }
+  struct Restore {  // a caller's matrix with an asymmetric diagonal block takes k_pcg_pipe
+    int32_t& flag;
+    int32_t saved;
+    ~Restore() { flag = saved; }
+  } restore{cg_.onchip, cg_.onchip};
+  if (!diag_sym) cg_.onchip = 0;
   GF_CUDA(cudaMemcpyAsync(d_.bval, bv.data(), 8 * bv.size(), cudaMemcpyHostToDevice, stream_));
   GF_CUDA(cudaMemcpyAsync(d_.dinv, dinv.data(), 8 * nd, cudaMemcpyHostToDevice, stream_));
   GF_CUDA(cudaMemcpyAsync(d_.rhs, b, 8 * nd, cudaMemcpyHostToDevice, stream_));

@@ -148,6 +148,10 @@ class Simulation {
   double* d_slice_part_ = nullptr;
   unsigned long long* d_ctr_ = nullptr;
   int cg_ndyn_ = 0;  // dynamically handed-out PCG slices (cg_sell.cu Phase)
+  double* d_tg_ = nullptr;  // cg_onchip.cu remote transposed products (null: the on-chip solver is not used)
+  double* d_ocm_ = nullptr;  // cg_onchip.cu gathered-vector buffers
+  uint32_t* d_oc_meta_ = nullptr;  // cg_onchip.cu per-row slot masks over oc_off_
+  int32_t oc_off_[7] = {0, 0, 0, 0, 0, 0, 0};
   std::vector<void*> allocs_;
   int32_t* d_fixed_nodes_ = nullptr;
   BcStep* d_bcstep_ = nullptr;

@@ -357,17 +357,28 @@ def test_step_metrics_match_oracle(model):
 
 
 # ---------------------------------------------------------------- the production PCG (k_pcg_sell) on given systems
-@pytest.fixture(params=["cluster", "grid", "two-barrier"])
+def _solver_env(monkeypatch, solver):
+    """cluster: k_pcg_pipe in one thread-block cluster; onchip: k_pcg_onchip (matrix in TMEM + shared memory);
+    grid: k_pcg_pipe on the cooperative grid; two-barrier: k_pcg_sell"""
+    monkeypatch.setenv("GF_CG_CLUSTER", "1" if solver == "cluster" else "0")
+    monkeypatch.setenv("GF_CG_PIPE", "0" if solver == "two-barrier" else "1")
+    monkeypatch.setenv("GF_CG_ONCHIP", "1" if solver == "onchip" else "0")
+
+
+SOLVERS = ["cluster", "onchip", "grid", "two-barrier"]
+
+
+@pytest.fixture(params=SOLVERS)
 def pcg_mode(request, monkeypatch):
-    """the production solver's on-chip instances: pipelined in one cluster / on the grid, and the two-barrier one"""
-    monkeypatch.setenv("GF_CG_CLUSTER", "1" if request.param == "cluster" else "0")
-    monkeypatch.setenv("GF_CG_PIPE", "0" if request.param == "two-barrier" else "1")
+    """the production solver's instances whose state stays on chip"""
+    _solver_env(monkeypatch, request.param)
     return request.param
 
 
-def _pcg_setup(cells=(4, 4, 4)):
+def _pcg_setup(mode, cells=(4, 4, 4)):
     s = cf.scaled("c2", cells)
     gs, os_, gm, om = pair(s)
+    assert gs.info()["pcg_solver_name"] == mode
     rp, cols, _ = om.pattern()
     rows = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
     return gs, os_, om, np.asarray(rp), np.asarray(cols), rows
@@ -380,7 +391,7 @@ def _oracle_cg(rp, cols, vals, b, x0, tol, max_iters):
 
 
 def test_production_pcg_identity_system(pcg_mode):  # test_sparse.cpp:20-32 on k_pcg_sell
-    gs, _, om, rp, cols, rows = _pcg_setup()
+    gs, _, om, rp, cols, rows = _pcg_setup(pcg_mode)
     n = len(rp) - 1
     vals = (rows == cols).astype(np.float64)
     b = np.random.default_rng(71).uniform(-1, 1, n)
@@ -391,7 +402,7 @@ def test_production_pcg_identity_system(pcg_mode):  # test_sparse.cpp:20-32 on k
 
 
 def test_production_pcg_zero_rhs(pcg_mode):  # sparse.cpp:145-150: b = 0 -> x = 0, converged, no iteration
-    gs, _, om, rp, cols, rows = _pcg_setup()
+    gs, _, om, rp, cols, rows = _pcg_setup(pcg_mode)
     n = len(rp) - 1
     vals = (rows == cols) * 2.0
     x, r = gs.solve_system(vals, np.zeros(n), x0=np.ones(n), tol=1e-10, max_iters=50)
@@ -401,7 +412,7 @@ def test_production_pcg_zero_rhs(pcg_mode):  # sparse.cpp:145-150: b = 0 -> x = 
 
 
 def test_production_pcg_negative_curvature(pcg_mode):  # test_sparse.cpp:74-84 / sparse.cpp:160-168 on k_pcg_sell
-    gs, _, om, rp, cols, rows = _pcg_setup()
+    gs, _, om, rp, cols, rows = _pcg_setup(pcg_mode)
     n = len(rp) - 1
     d = np.where(np.arange(n) % 3 == 0, -1.0, 1.0)  # indefinite Jacobi-scaled system: p.Ap < 0 at the first step
     vals = np.where(rows == cols, d[rows], 0.0)
@@ -416,12 +427,18 @@ def test_production_pcg_negative_curvature(pcg_mode):  # test_sparse.cpp:74-84 /
 def test_production_pcg_matches_oracle_on_the_step_system(pcg_mode):
     """the implicit-Euler system of a loaded step, random rhs, tight tolerance: same iteration count within 2, same
     solution within 1e-9; the A-norm error of the production solver never grows (test_sparse.cpp:86-110)"""
-    gs, os_, om, rp, cols, rows = _pcg_setup((5, 4, 6))
+    gs, os_, om, rp, cols, rows = _pcg_setup(pcg_mode, (5, 4, 6))
     rng = np.random.default_rng(72)
     u = rng.uniform(-0.05 * cf.H, 0.05 * cf.H, (om.num_nodes, 3))
     os_.set_state(u=u)
     os_.dynamic_step()
     A, _ = os_.last_system()
+    # the oracle's diagonal blocks are symmetric up to rounding; mirrored, so that k_pcg_onchip (which keeps their
+    # upper triangle, as the GPU assembly writes them) takes this system too -- both solvers get the same matrix
+    diag = (rows // 3 == cols // 3) & (rows % 3 > cols % 3)
+    key = {(int(r), int(c)): k for k, (r, c) in enumerate(zip(rows, cols))}
+    A = A.copy()
+    A[np.nonzero(diag)[0]] = A[[key[(int(c), int(r))] for r, c in zip(rows[diag], cols[diag])]]
     n = len(rp) - 1
     b = rng.uniform(-1, 1, n)
     x, r = gs.solve_system(A, b, tol=1e-13, max_iters=2000)
@@ -438,6 +455,34 @@ def test_production_pcg_matches_oracle_on_the_step_system(pcg_mode):
         an = e @ Ad @ e
         assert an <= prev * (1 + 1e-9) + 1e-30
         prev = an
+
+
+@pytest.mark.parametrize("grid,cells", [("1", (5, 4, 6)), ("2", (8, 8, 8)), ("4", (14, 14, 14))])
+def test_onchip_pcg_many_slices_per_cta(grid, cells, monkeypatch):
+    """k_pcg_onchip with few CTAs (GF_CG_GRID), so that every CTA owns many slices and both rows of its threads: the
+    shared-memory routes of the transposed products (slot 0 across slices, slots 1/2 through the t buffer) and the
+    second row per thread all run; same solution as the oracle's cg_solve within 1e-9, iterations within 2"""
+    _solver_env(monkeypatch, "onchip")
+    monkeypatch.setenv("GF_CG_GRID", grid)
+    s = cf.scaled("c2", cells)
+    gs, os_, gm, om = pair(s)
+    assert gs.info()["pcg_solver_name"] == "onchip"
+    rp, cols, _ = om.pattern()
+    rows = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
+    rng = np.random.default_rng(73)
+    os_.set_state(u=rng.uniform(-0.002 * cf.H, 0.002 * cf.H, (om.num_nodes, 3)))
+    os_.dynamic_step()
+    A, _ = os_.last_system()
+    diag = (rows // 3 == cols // 3) & (rows % 3 > cols % 3)
+    key = {(int(r), int(c)): k for k, (r, c) in enumerate(zip(rows, cols))}
+    A = A.copy()
+    A[np.nonzero(diag)[0]] = A[[key[(int(c), int(r))] for r, c in zip(rows[diag], cols[diag])]]
+    n = len(rp) - 1
+    b = rng.uniform(-1, 1, n)
+    x, r = gs.solve_system(A, b, tol=1e-12, max_iters=3000)
+    xo, ro = _oracle_cg(rp, cols, A, b, np.zeros(n), 1e-12, 3000)
+    assert r["converged"] and ro["converged"] and abs(r["iterations"] - ro["iterations"]) <= 2
+    assert np.abs(x - xo).max() <= 1e-9 * np.abs(xo).max()
 
 
 def test_c4_physics_scaled_impact_breaks_edges_bit_exact():
@@ -569,21 +614,21 @@ def run_pair(s, steps, resync_tol=1e-6):
     return worst, resyncs, broken
 
 
-@pytest.mark.parametrize("cluster", ["1", "0"])
-def test_trajectory_c1_scaled(cluster, monkeypatch):
-    """small matrix: the pipelined PCG inside one thread-block cluster (default) and on the cooperative grid"""
-    monkeypatch.setenv("GF_CG_CLUSTER", cluster)
+@pytest.mark.parametrize("solver", ["cluster", "onchip", "grid"])
+def test_trajectory_c1_scaled(solver, monkeypatch):
+    """small matrix: the pipelined PCG inside one thread-block cluster (default), with the matrix on chip, and on the
+    cooperative grid"""
+    _solver_env(monkeypatch, solver)
     s = cf.scaled("c1", (4, 4, 16), steps=60)
     s.point_load = (s.point_load[0], (0.0, -500.0 / 8, 0.0))  # same bending stress as the 8x8 section
     worst, resyncs, _ = run_pair(s, s.steps)
     assert worst < TRAJ_TOL
 
 
-@pytest.mark.parametrize("solver", ["cluster", "grid", "two-barrier"])
+@pytest.mark.parametrize("solver", SOLVERS)
 def test_trajectory_c3_scaled_with_fracture(solver, monkeypatch):
-    """the three on-chip-state PCG instances: k_pcg_pipe in one cluster, k_pcg_pipe on the grid, k_pcg_sell"""
-    monkeypatch.setenv("GF_CG_CLUSTER", "1" if solver == "cluster" else "0")
-    monkeypatch.setenv("GF_CG_PIPE", "0" if solver == "two-barrier" else "1")
+    """the four on-chip-state PCG instances"""
+    _solver_env(monkeypatch, solver)
     s = cf.scaled("c3", (10, 10, 9), steps=60)
     worst, resyncs, broken = run_pair(s, s.steps)
     assert broken > 0
