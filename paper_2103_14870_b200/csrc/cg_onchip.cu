@@ -62,7 +62,7 @@ struct OcArgs {
   CgLaunch a;
   double* cta_part;       // 2 parities x 4 values x kMaxGridOc
   double* tg;             // remote t: 2 parities x 21 planes (slot b * 3 + component) x npad
-  double* gm;             // the gathered vector m: 2 buffers x 3 npad (row r at 3 r)
+  double* gm;             // the gathered vector m: 2 buffers x 3 component planes x npad
   const uint32_t* meta;   // per row: upper slot mask | lower slot mask << 8
   int32_t npad;           // >= nrows + 1: row index nrows of every plane / buffer is a zero entry (never written)
   int32_t shuf;           // off[0] == 1: slot 0's column is the next row (the shuffle route)
@@ -304,9 +304,9 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
       for (int k = 0; k < 3; ++k) t[k] = __ldcg(tgb + (b * 3 + k) * npad + src);
     };
     auto gather = [&](int h, int b, double (&g)[3]) {  // v at slot b's column (the zero entry when absent)
-      const int j3 = 3 * (up(h, b) ? row[h] + oa.off[b] : ZP);
+      const int j = up(h, b) ? row[h] + oa.off[b] : ZP;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) g[k] = __ldca(vg + j3 + k);
+      for (int k = 0; k < 3; ++k) g[k] = __ldca(vg + k * npad + j);
     };
     auto add3 = [&](int h, const double (&t)[3]) {
 #pragma unroll
@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
     for (int h = 0; h < kRpt; ++h) {
       if (live[h])
 #pragma unroll
-        for (int k = 0; k < 3; ++k) gm1[3 * (size_t)row[h] + k] = X[h][k];
+        for (int k = 0; k < 3; ++k) gm1[k * npad + row[h]] = X[h][k];
       produce(h, X[h], tpar);
     }
     grid.sync();
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
       const double bi = live[h] ? a.b[dof] : 0.0;
       R[h][k] = bi - acc[h][k];
       U[h][k] = Dv(h, k) * R[h][k];
-      if (live[h]) gm0[dof] = U[h][k];
+      if (live[h]) gm0[k * npad + row[h]] = U[h][k];
       bb = __fma_rn(bi, bi, bb);
     }
     produce(h, U[h], tpar);
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
       for (int k = 0; k < 3; ++k) {
         Wv[h][k] = acc[h][k];
         M[k] = Dv(h, k) * acc[h][k];
-        if (live[h]) gm1[3 * (size_t)row[h] + k] = M[k];
+        if (live[h]) gm1[k * npad + row[h]] = M[k];
         v3[0] = __fma_rn(R[h][k], U[h][k], v3[0]);
         v3[1] = __fma_rn(acc[h][k], U[h][k], v3[1]);
         v3[2] = __fma_rn(R[h][k], R[h][k], v3[2]);
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
           const double uk = dk * R[h][k];
           Wv[h][k] = __fma_rn(-alpha, Z[h][k], Wv[h][k]);   // w -= alpha z
           M2[h][k] = dk * Wv[h][k];
-          if (live[h]) gnext[3 * (size_t)row[h] + k] = M2[h][k];
+          if (live[h]) gnext[k * npad + row[h]] = M2[h][k];
           v[0] = __fma_rn(R[h][k], uk, v[0]);
           v[1] = __fma_rn(Wv[h][k], uk, v[1]);
           v[2] = __fma_rn(R[h][k], R[h][k], v[2]);
