@@ -201,7 +201,8 @@ def config_dict(s, scaling_note):
     return {"workload": s.name, "tets": s.num_tets, "cells": list(s.cells), "r_d_m": s.r_d, "dt": s.dt,
             "cg_tol": s.cg_tol, "material": "stable_neo_hookean" if s.model == 0 else "stvk",
             "l2": "inputs larger than L2: non-local table (~1.2 GB) + per-tet data streamed every step; the symmetric "
-                  "system matrix (~62 MB) is rebuilt each step and stays L2-resident only within the PCG",
+                  "system matrix (~62 MB) is rebuilt each step and read once per solve into the SMs' tensor and shared "
+                  "memory (k_pcg_onchip)",
             "parallelism": scaling_note}
 
 
@@ -216,12 +217,24 @@ def pcg_models(info):
     working set: what must stay L2-resident for the solve to run from L2."""
     N = info["nodes"]
     dyn = info["pcg_dynamic_units"] > 0
+    survey = 12 * 9 * info["node_blocks"] + 4 * (3 * N + 1) + 56 * 3 * N  # SURVEY §8(d) B_CG (scalar CSR)
+    if info.get("pcg_solver_name") == "onchip":
+        # k_pcg_onchip: the matrix is loaded ONCE per solve into TMEM + shared memory; per iteration only the column
+        # gathers of slots 1..6 (slot 0 is the next lane's), the remote transposed products of slots 3..6 (written
+        # and read) and m leave the chip -- 24 B each (cg_onchip.cu)
+        sb = info["oc_slot_blocks"]
+        it = 24 * sum(sb[1:]) + 48 * sum(sb[3:]) + 24 * N
+        once = 72 * info["upper_block_slots"]
+        return dict(l2_bytes_per_iter=it, hbm_bytes_per_iter=it, bytes_per_solve=once, working_set_bytes=it,
+                    survey_bytes_per_iter=survey,
+                    format_bytes_per_iter=72 * info["upper_blocks"] + 4 * info["spmv_slots"] + 48 * N,
+                    solver_state="matrix and solver state on chip (TMEM + shared memory + registers)")
     vec = (312 if dyn else 48) * N
     l2 = 72 * info["node_blocks"] + 4 * info["spmv_slots"] + vec
     hbm = 72 * info["upper_blocks"] + 4 * info["spmv_slots"] + vec
     ws = 72 * info["upper_block_slots"] + 4 * info["spmv_slots"] + (144 if dyn else 24) * N
-    survey = 12 * 9 * info["node_blocks"] + 4 * (3 * N + 1) + 56 * 3 * N  # SURVEY §8(d) B_CG (scalar CSR)
-    return dict(l2_bytes_per_iter=l2, hbm_bytes_per_iter=hbm, working_set_bytes=ws, survey_bytes_per_iter=survey,
+    return dict(l2_bytes_per_iter=l2, hbm_bytes_per_iter=hbm, bytes_per_solve=0, working_set_bytes=ws,
+                survey_bytes_per_iter=survey,
                 solver_state="global (large matrix)" if dyn else "on chip (one slice per warp)")
 
 
@@ -267,11 +280,11 @@ def e2e_steps(g, sim, steps, N, T, E, dist=None, n=1):
             "d2h_bytes_per_step": 16 * nd + E + 8 * T, "steps": steps, "timing": "host wall clock, max over ranks"}
 
 
-def pcg_roofline(models, iters, pcg_ms, l2_roof, hbm_peak):
+def pcg_roofline(models, iters, pcg_ms, l2_roof, hbm_peak, solves=1):
     """roofline of the PCG solve over a timed region: bound L2 when its working set fits L2, else HBM."""
     l2_bound = models["working_set_bytes"] <= 100e6
-    b_l2 = models["l2_bytes_per_iter"] * iters
-    b_hbm = models["hbm_bytes_per_iter"] * iters
+    b_l2 = models["l2_bytes_per_iter"] * iters + models["bytes_per_solve"] * solves
+    b_hbm = models["hbm_bytes_per_iter"] * iters + models["bytes_per_solve"] * solves
     out = {"bound": "l2" if l2_bound else "hbm", "iterations": iters, "ms": pcg_ms,
            "l2_GBps": b_l2 / pcg_ms / 1e6, "l2_frac": b_l2 / pcg_ms / 1e6 / l2_roof if l2_roof else None,
            "hbm_GBps": b_hbm / pcg_ms / 1e6, "hbm_frac": b_hbm / pcg_ms / 1e6 / hbm_peak,
@@ -308,7 +321,7 @@ def sub_record(g, cf, name, steps, warmup, hbm_peak, l2_roof, e2e=False, env=Non
            "warmup": warmup, "ms_per_step": ms / steps, "cg_iterations_per_step": iters / steps,
            "newly_broken_in_region": newly, "nonlocal_layout": {0: "local", 1: "general sliced-ELL", 2: "template"}[info["nl_layout"]],
            "setup_s": dict(info["setup_s"], wall_incl_mesh=setup_wall),
-           "pcg": pcg_roofline(pcg_models(info), iters, pcg["total_ms"], l2_roof, hbm_peak),
+           "pcg": pcg_roofline(pcg_models(info), iters, pcg["total_ms"], l2_roof, hbm_peak, steps),
            "step_hbm_GBps": sum(v["bytes"] for v in kt.values()) / ms / 1e6}
     rec["step_hbm_frac"] = rec["step_hbm_GBps"] / hbm_peak
     if e2e:
@@ -394,9 +407,10 @@ def main():
     avg_ms = d["total_ms"] / max(1, d["launches"])
     traffic = ncu_traffic(s.name, dname)
     if dname == "pcg":
-        pr = pcg_roofline(models, cg_iters, d["total_ms"], l2_roof, peak)
+        pr = pcg_roofline(models, cg_iters, d["total_ms"], l2_roof, peak, d["launches"])
         l2b = pr["bound"] == "l2"
-        per_launch = (models["l2_bytes_per_iter"] if l2b else models["hbm_bytes_per_iter"]) * cg_iters / d["launches"]
+        per_launch = ((models["l2_bytes_per_iter"] if l2b else models["hbm_bytes_per_iter"]) * cg_iters / d["launches"]
+                      + models["bytes_per_solve"])
         achieved = per_launch / (avg_ms / 1e3) / 1e9
         roof = l2_roof if l2b else peak
         roofline = {"bound": "l2" if l2b else "hbm", "kernel": dname, "achieved": achieved, "peak": roof,
@@ -404,11 +418,18 @@ def main():
                     "peak_source": ("measured live: L2-resident 16-byte reads of a 64 MB buffer from every SM "
                                     "(gf_measure_bandwidth kind 0)") if l2b else peak_src,
                     "algorithmic_bytes_per_launch": per_launch, "avg_launch_ms": avg_ms,
-                    "note": ("PCG bytes = the symmetric SELL-32 format's per-iteration traffic x measured iterations: "
-                             "72 B per block of the full matrix (an upper block serves its row and, transposed, its "
-                             "column's row), 4 B per slot word, z gathered + written; the solver state stays on chip. "
-                             "The matrix (~62 MB) is L2-resident during the solve, so the roof is the measured L2 read "
-                             "bandwidth; traffic = ncu DRAM bytes per launch (committed capture)"),
+                    "note": (("k_pcg_onchip: the matrix (~62 MB) is read once per solve into TMEM + shared memory; "
+                              "per iteration only the column gathers, the remote transposed products and m cross the "
+                              "L2 (24 B each, ~3.5x fewer bytes than streaming the symmetric format), so the solve is "
+                              "bound by synchronisation latency (grid barrier, dependent L2 round trips; DESIGN.md §7), "
+                              "not by a bandwidth roof: frac is the L2 traffic it does move over the measured L2 read "
+                              "roof. traffic = ncu DRAM bytes per launch (committed capture)")
+                             if models.get("bytes_per_solve") else
+                             ("PCG bytes = the symmetric SELL-32 format's per-iteration traffic x measured iterations: "
+                              "72 B per block of the full matrix (an upper block serves its row and, transposed, its "
+                              "column's row), 4 B per slot word, z gathered + written; the solver state stays on chip. "
+                              "The matrix (~62 MB) is L2-resident during the solve, so the roof is the measured L2 read "
+                              "bandwidth; traffic = ncu DRAM bytes per launch (committed capture)")),
                     "pcg": pr}
     else:
         achieved = d["bytes"] / max(1, d["launches"]) / (avg_ms / 1e3) / 1e9

@@ -281,6 +281,9 @@ typedef struct {
   int32_t pcg_solver;         /* production PCG instance: 0 k_pcg_sell (two barriers), 1 k_pcg_pipe (grid), 2 k_pcg_pipe
                                  (one cluster), 3 k_pcg_onchip (matrix in TMEM + shared memory), 4 k_pcg_sell large-matrix */
   int32_t _pad0;
+  int64_t oc_slot_blocks[7];  /* k_pcg_onchip: upper off-diagonal blocks per slot (column offset oc_offsets[b]) */
+  int32_t oc_offsets[7];      /* k_pcg_onchip: the pattern's positive column offsets (0 when not used) */
+  int32_t _pad1;
 } gf_sim_info;
 int gf_sim_info_get(const gf_sim* s, gf_sim_info* out);
 /* measured device bandwidth in GB/s on the current device: kind 0 = reads of an L2-resident buffer of `bytes`

@@ -103,7 +103,8 @@ class _SimInfo(C.Structure):
                 ("upper_blocks", C.c_int64), ("upper_block_slots", C.c_int64), ("spmv_slots", C.c_int64),
                 ("nl_entries", C.c_int64), ("nl_slots", C.c_int64), ("nl_layout", C.c_int32),
                 ("pcg_dynamic_units", C.c_int32), ("setup_s", C.c_double * 4), ("pcg_solver", C.c_int32),
-                ("_pad0", C.c_int32)]
+                ("_pad0", C.c_int32), ("oc_slot_blocks", C.c_int64 * 7), ("oc_offsets", C.c_int32 * 7),
+                ("_pad1", C.c_int32)]
 
 
 class StepMetrics(C.Structure):
@@ -620,7 +621,10 @@ class Simulation:
         """gf_sim_info: storage sizes of the device formats (roofline byte models) and the setup wall times."""
         i = _SimInfo()
         _check(lib().gf_sim_info_get(self._h, C.byref(i)))
-        out = {k: getattr(i, k) for k, _ in _SimInfo._fields_ if k not in ("setup_s", "_pad0")}
+        out = {k: getattr(i, k) for k, _ in _SimInfo._fields_
+               if k not in ("setup_s", "_pad0", "_pad1", "oc_slot_blocks", "oc_offsets")}
+        out["oc_slot_blocks"] = list(i.oc_slot_blocks)
+        out["oc_offsets"] = list(i.oc_offsets)
         out["pcg_solver_name"] = PCG_SOLVERS[i.pcg_solver]
         out["setup_s"] = dict(pattern_and_layouts=i.setup_s[0], nonlocal_table=i.setup_s[1],
                               device_layout_and_upload=i.setup_s[2], total=i.setup_s[3])

@@ -629,7 +629,10 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
       for (int32_t i = 0; i < nn; ++i)
         for (int32_t q = pat_.row_ptr[i]; q < pat_.row_ptr[i + 1]; ++q) {
           const int32_t j = pat_.cols[q];
-          if (j > i) meta[i] |= 1u << bit(j - i);
+          if (j > i) {
+            meta[i] |= 1u << bit(j - i);
+            ++oc_slot_blocks_[bit(j - i)];
+          }
           else if (j < i) meta[i] |= 1u << (8 + bit(i - j));
         }
       d_oc_meta_ = (uint32_t*)up(meta.data(), sizeof(uint32_t) * meta.size());
@@ -663,6 +666,10 @@ gf_sim_info Simulation::info() const {
   o.nl_layout = nonlocal_layout();
   o.pcg_dynamic_units = cg_ndyn_;
   o.pcg_solver = cg_ndyn_ > 0 ? 4 : cg_.onchip ? 3 : !cg_.pipelined ? 0 : cg_.cluster ? 2 : 1;
+  for (int b = 0; b < 7; ++b) {
+    o.oc_slot_blocks[b] = cg_.onchip ? oc_slot_blocks_[b] : 0;
+    o.oc_offsets[b] = cg_.onchip ? oc_off_[b] : 0;
+  }
   for (int k = 0; k < 4; ++k) o.setup_s[k] = setup_s_[k];
   return o;
 }
@@ -1138,10 +1145,19 @@ gf_step_stats Simulation::dynamic_step() {
   // state stays on chip (one slice per warp); p, q, x, r, D^-1 traffic as well when it does not (large
   // matrices). The reference's scalar-CSR model (SURVEY §8(d) B_CG = 12Z + 4(n+1) + 56n) is reported by bench.py
   // next to it.
-  const double cg_bytes_per_iter = 72.0 * ((double)pat_.cols.size() + mesh_.nn) / 2.0 + 4.0 * 32.0 * (double)sell_slots_ +
-                                   (cg_ndyn_ ? 312.0 : 48.0) * mesh_.nn;
+  double cg_bytes_per_iter = 72.0 * ((double)pat_.cols.size() + mesh_.nn) / 2.0 + 4.0 * 32.0 * (double)sell_slots_ +
+                             (cg_ndyn_ ? 312.0 : 48.0) * mesh_.nn;
+  if (cg_.onchip) {  // the matrix stays on chip: per iteration the column gathers of slots 1..6, the remote t of
+                     // slots 3..6 (written and read) and m (bench.py pcg_models; the one matrix load is not counted)
+    double g = 0.0, t = 0.0;
+    for (int b = 1; b < 7; ++b) g += (double)oc_slot_blocks_[b];
+    for (int b = 3; b < 7; ++b) t += (double)oc_slot_blocks_[b];
+    cg_bytes_per_iter = 24.0 * g + 48.0 * t + 24.0 * mesh_.nn;
+  }
+  // k_pcg_onchip loads the matrix (upper blocks incl. slice padding) once per solve
+  const double cg_bytes_per_solve = cg_.onchip ? 72.0 * 32.0 * (double)usp_[d_.nslices] : 0.0;
   auto account = [&](double iters) {
-    if (profiling_) ktimes_["pcg"].bytes += iters * cg_bytes_per_iter;
+    if (profiling_) ktimes_["pcg"].bytes += iters * cg_bytes_per_iter + cg_bytes_per_solve;
   };
   check_edge_fallback();
   int32_t newly = 0;

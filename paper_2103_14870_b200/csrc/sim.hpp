@@ -152,6 +152,7 @@ class Simulation {
   double* d_ocm_ = nullptr;  // cg_onchip.cu gathered-vector buffers
   uint32_t* d_oc_meta_ = nullptr;  // cg_onchip.cu per-row slot masks over oc_off_
   int32_t oc_off_[7] = {0, 0, 0, 0, 0, 0, 0};
+  int64_t oc_slot_blocks_[7] = {0, 0, 0, 0, 0, 0, 0};
   std::vector<void*> allocs_;
   int32_t* d_fixed_nodes_ = nullptr;
   BcStep* d_bcstep_ = nullptr;

@@ -8,12 +8,12 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv 
 timeout 900 python bench.py > $o/bench_c3.json 2> $o/bench_c3.err; echo "bench c3 rc=$?"
 timeout 900 python bench.py --config c4 --steps 10 --warmup 3 --no-cpu > $o/bench_c4.json 2> $o/bench_c4.err; echo "bench c4 rc=$?"
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $o/bench_reference.json 2> $o/bench_reference.err; echo "reference rc=$?"
-timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > $o/plain.json 2>&1 && \
+timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-sub > $o/plain.json 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $o/launches.csv \
-  python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > $o/ncu_launches.log 2>&1; echo "launches rc=$?"
-for k in k_pcg_sell k_nonlocal_tpl k_assemble; do
+  python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-sub > $o/ncu_launches.log 2>&1; echo "launches rc=$?"
+for k in k_pcg_onchip k_nonlocal_tpl k_assemble; do
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
-    -o $o/ncu_$k -f python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $o/ncu_$k.log 2>&1; echo "ncu $k rc=$?"
+    -o $o/ncu_$k -f python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-sub > $o/ncu_$k.log 2>&1; echo "ncu $k rc=$?"
 done
 for c in c1 c2 c3; do timeout 1500 python tools/trajectory.py $c >> $o/trajectories.jsonl 2>> $o/trajectories.err; echo "traj $c rc=$?"; done
 timeout 900 python tools/trajectory.py c4 --steps 10 >> $o/trajectories.jsonl 2>> $o/trajectories.err; echo "traj c4 rc=$?"
