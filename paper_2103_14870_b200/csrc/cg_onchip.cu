@@ -17,16 +17,17 @@
 // two rows' solver state plus their loads in flight fit 168 per thread, where one row per thread at 768 threads
 // (80 registers) spills.
 //
-// Symmetric SpMV without reading a block twice from L2: block (i, c) of row i with column j contributes B v_j to row
-// i and t = B^T v_i to row j. Row i's thread computes the direct product; the transposed one travels to row j's
-// thread by one of three routes, decided identically by producer and consumer from (i, j, c):
-//   shuffle  slot 0 (offset +1), j = i + 1 in the same warp: t moves one lane up (shfl), inside the SpMV phase;
-//   smem     slots 1, 2 and j in the same CTA: t goes through the CTA's t buffer, computed inside the SpMV phase;
-//   remote   everything else: t = B^T m_i is computed by the owner at the END of the previous iteration, as soon as
-//            its new m_i exists (the pipelined recurrences know m one iteration ahead), and published through a
-//            double-buffered global array before the grid barrier -- so no extra barrier.
-// Per row and iteration the L2 then carries the slot words, the m gathers of the upper columns, the remote t
-// (written and read) and m itself (~0.45 KB instead of ~1.3 KB).
+// Symmetric SpMV without reading a block twice from L2: block (i, b) of row i with column j = i + off[b] contributes
+// B v_j to row i and t = B^T v_i to row j. Row i's thread computes the direct product; the transposed one reaches row
+// j by one of three routes, decided identically on both sides from (b, lane, CTA range):
+//   shuffle  slot 0 (offset +1), j = i + 1 in the same warp: t moves one lane up (shfl);
+//   on chip  slots 0..2 with both rows in the CTA: row j's thread computes t itself from row i's shared-memory block
+//            and the CTA's shared copy of the gathered vector (the m-cache, written with the global copy);
+//   remote   everything else (slots 3..6, CTA edges): t = B^T m_i is computed by the owner at the END of the previous
+//            iteration, as soon as its new m_i exists (the pipelined recurrences know m one iteration ahead), and
+//            published through double-buffered global planes before the grid barrier -- so no extra barrier.
+// Per row and iteration the L2 then carries the gathers of slots 3..6, the remote t (written and read) and m itself
+// (~0.3 KB instead of ~1.3 KB).
 //
 // The recurrences, decisions and deterministic reductions are k_pcg_pipe's (Ghysels & Vanroose pipelined PCG; one
 // grid barrier per iteration; decisions mapped one to one onto the reference's). The row sum is the lower
@@ -53,10 +54,9 @@ constexpr int kTmCols = 84;              // TMEM columns per row: a warp's two r
 constexpr int kTmSlot3 = 12;             // diagonal (6 doubles) at columns 0..11, slot b >= 3 at 12 + 18 (b - 3)
 constexpr int kMaxGridOc = 1024;         // CTA partial slots per value (as cg_sell.cu)
 constexpr size_t kBlkDoubles = 27 * (size_t)kRows;  // slots 0..2, [b][entry][local row]
-constexpr size_t kTbDoubles = 6 * (size_t)(kRows + 1);  // t of slots 1, 2 for same-CTA targets, [b-1][component][row];
-                                                          // local row kRows is a zero entry
+constexpr size_t kMDoubles = 3 * (size_t)kRows;     // the CTA's rows of the gathered vector, [component][local row]
 constexpr size_t kDDoubles = 3 * (size_t)kRows;     // D^-1, [component][local row]
-constexpr size_t kOcSmem = (kBlkDoubles + kTbDoubles + kDDoubles) * sizeof(double);
+constexpr size_t kOcSmem = (kBlkDoubles + kMDoubles + kDDoubles) * sizeof(double);
 
 struct OcArgs {
   CgLaunch a;
@@ -76,6 +76,10 @@ __device__ __forceinline__ unsigned long long gtimer_oc() {
 }
 // diagnostics (GF_CG_TRACE, tools/cg_trace_oc.py): CTA 0 stamps 5 points of every iteration; at iteration 10 every CTA
 // stamps the end of its SpMV (after a CTA barrier)
+#define OC_SUB(point)                                                                         \
+  do {                                                                                        \
+    if (a.trace && sub_on && tid == 0 && blockIdx.x == 0 && h == 0) a.trace[4100 + (point)] = gtimer_oc(); \
+  } while (0)
 #define OC_STAMP(k, point)                                                   \
   do {                                                                       \
     if (a.trace && tid == 0 && blockIdx.x == 0 && (k) < 200)                 \
@@ -175,25 +179,24 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
   const CgLaunch& a = oa.a;
   extern __shared__ double s_dyn[];
   double* const s_blk = s_dyn;                          // [b][q][local row]
-  double* const s_tb = s_dyn + kBlkDoubles;             // [b-1][component][local row + 1 zero entry]
-  double* const s_d = s_dyn + kBlkDoubles + kTbDoubles;  // D^-1 [component][local row]
+  double* const s_m = s_dyn + kBlkDoubles;              // the gathered vector of the CTA's rows [component][row]
+  double* const s_d = s_dyn + kBlkDoubles + kMDoubles;  // D^-1 [component][local row]
   __shared__ uint32_t s_taddr;
   __shared__ double s_acc[kW][4];
   __shared__ double s_w[kW][4];
-  __shared__ double s_t0[kRows / 32 + 1][3];  // slot 0's t from slice s's lane 31 to slice s+1's lane 0; [0] zero
-  __shared__ double s_x1[3][kT];              // x of each thread's second row (the register budget)
+  __shared__ double s_x1[3][kT];  // x of each thread's second row (the register budget)
+  __shared__ double s_p1[3][kT];  // p of each thread's second row
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, G = (int)gridDim.x;
   const int cs0 = __ldg(a.cta_first + blockIdx.x), cs1 = __ldg(a.cta_first + blockIdx.x + 1);
   const int r0 = cs0 * 32, r1 = cs1 * 32;  // this CTA's rows (rows >= nrows are never referenced)
-  const int nrows = a.nrows, npad = oa.npad, ZP = nrows;  // ZP: the zero entry of every plane
+  const int nrows = a.nrows, npad = oa.npad, ZP = nrows;  // ZP: the zero entry of every global plane
   const bool shuf = oa.shuf != 0;
 
   if (w == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_addr(&s_taddr)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
-  for (int k = tid; k < 6; k += kT) s_tb[(k / 3 * 3 + k % 3) * (kRows + 1) + kRows] = 0.0;
-  if (tid < 3) s_t0[0][tid] = 0.0;
+  for (int k = tid; k < (int)kMDoubles; k += kT) s_m[k] = 0.0;  // rows the CTA does not have stay zero
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -243,17 +246,20 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
   auto lo = [&](int h, int b) -> bool { return (pm[h] >> (8 + b)) & 1u; };
   auto Dv = [&](int h, int k) -> double { return s_d[k * kRows + li[h]]; };
   double* const tg0 = oa.tg;
-  auto smem_block = [&](int h, int b, double (&B)[9]) {
-#pragma unroll
-    for (int q = 0; q < 9; ++q) B[q] = s_blk[(b * 9 + q) * kRows + li[h]];
-  };
   auto tmem_block = [&](int h, int b, double (&B)[9]) { tm_ld9(tmh[h] + kTmSlot3 + 18 * (b - 3), B); };
-  // routes, fixed by the slot b: slot 0 with a +1 offset is the next lane (shuffle) or, from lane 31, the next
-  // slice's lane 0 through s_t0 when that row is in the CTA; slots 1, 2 go through the t buffer when the other row is
-  // in the CTA; everything else is remote (the global t planes, produced at the end of the previous iteration)
+  // routes of the transposed products, fixed by the slot b: slots 0..2 whose other row is in the CTA are computed
+  // by the CONSUMER from the producer's shared-memory block and the CTA's copy of the gathered vector (slot 0 in
+  // lanes 1..31: the previous lane's product, shuffled); everything else is remote -- the global t planes, written by
+  // the producer at the end of the previous iteration
   auto up_remote = [&](int h, int b) -> bool {
-    if (b <= 2) return up(h, b) && ((b == 0 && !shuf) || row[h] + oa.off[b] >= r1);
+    if (b <= 2) return up(h, b) && row[h] + oa.off[b] >= r1;
     return live[h];  // slots 3..6: always (absent slots store zeros that no row reads)
+  };
+  auto lo_remote = [&](int h, int b) -> bool { return lo(h, b) && (b >= 3 || row[h] - oa.off[b] < r0); };
+  // the CTA's copy of the vector the next SpMV gathers (written with the global one; read after the grid barrier)
+  auto put_m = [&](int h, const double (&v)[3]) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s_m[k * kRows + li[h]] = v[k];
   };
 
   // remote transposed products of v (row h's value) for the NEXT SpMV, published before the grid barrier: slots
@@ -269,7 +275,8 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
       double B[9];
       if (b <= 2) {
         if (!__any_sync(0xffffffffu, rem)) continue;
-        smem_block(h, b, B);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) B[q] = s_blk[(b * 9 + q) * kRows + li[h]];
       } else {
         tmem_block(h, b, B);
       }
@@ -282,10 +289,11 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
   };
 
   // n = A v for both rows: v their own values, vg the published vector (zero at row ZP), par the parity of the
-  // remote t of v. Straight-line code: absent slots hold zero blocks and gather the zero entry, a lower product not
-  // taken by a route reads the zero entry of its source, so every row does the same work without tests. One
-  // accumulator per row in a fixed order; loads go out in rounds of three 24-byte items per row, the two rows'
-  // rounds interleaved.
+  // remote t of v; the CTA's rows of v are also in s_m. One accumulator per row in a fixed order: the diagonal, then
+  // the on-chip products (slots 0..2 direct and, for rows of the CTA, transposed) while the first loads fly, then the
+  // remote lower products and the direct products of slots 3..6 as their loads arrive. Loads go out in rounds of at
+  // most four 24-byte items, one row at a time (the register budget).
+  bool sub_on = false;
   auto spmv = [&](const double* vg, const double (&v)[kRpt][3], int par, double (&n)[kRpt][3]) {
 #pragma unroll
     for (int h = 0; h < kRpt; ++h) {
@@ -297,13 +305,11 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
     par = launder(par);
     const double* const tgb = tg0 + (size_t)par * 21 * npad;
     auto lower_t = [&](int h, int b, double (&t)[3]) {  // remote lower product of slot b (zero entry otherwise)
-      const int i = row[h] - oa.off[b];
-      const bool rem = lo(h, b) && (b >= 3 || (b == 0 && !shuf) || i < r0);
-      const int src = rem ? i : ZP;
+      const int i = lo_remote(h, b) ? row[h] - oa.off[b] : ZP;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) t[k] = __ldcg(tgb + (b * 3 + k) * npad + src);
+      for (int k = 0; k < 3; ++k) t[k] = __ldcg(tgb + (b * 3 + k) * npad + i);
     };
-    auto gather = [&](int h, int b, double (&g)[3]) {  // v at slot b's column (the zero entry when absent)
+    auto gather = [&](int h, int b, double (&g)[3]) {  // v at slot b's column from global (zero entry if not taken)
       const int j = up(h, b) ? row[h] + oa.off[b] : ZP;
 #pragma unroll
       for (int k = 0; k < 3; ++k) g[k] = __ldca(vg + k * npad + j);
@@ -312,90 +318,103 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
 #pragma unroll
       for (int k = 0; k < 3; ++k) n[h][k] += t[k];
     };
-    auto slot12 = [&](int h, int b, const double (&g)[3]) {  // shared-memory slot: direct product, own t buffer entry
-      double B[9], t[3];
-      smem_block(h, b, B);
-      mv_add(B, g, n[h]);
-      mtv(B, v[h], t);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) s_tb[((b - 1) * 3 + k) * (kRows + 1) + li[h]] = t[k];
-    };
     auto slot_tm = [&](int h, int b, const double (&g)[3]) {
       double B[9];
       tmem_block(h, b, B);
       mv_add(B, g, n[h]);
     };
-    // one row at a time (the two rows' rounds interleaved keep twice the loads in flight per thread and spill more
-    // of the solver state: measured 11.9 vs 11.5 us per iteration at c3)
-    auto row_rounds = [&](int h) {
-      double Lr[4][3];
-      lower_t(h, 6, Lr[0]);
-      lower_t(h, 5, Lr[1]);
-      gather(h, 1, Lr[2]);
+#pragma unroll
+    for (int h = 0; h < kRpt; ++h) {
+      double L[4][3];
+      OC_SUB(0);
+      // round 1: the remote lower products of slots 6..4 (and of slots 0..2 at CTA edges)
+      lower_t(h, 6, L[0]);
+      lower_t(h, 5, L[1]);
+      lower_t(h, 4, L[2]);
+      const double(&x)[3] = v[h];
       {
         double d[6];
         tm_ld6(tmh[h], d);
-        const double(&x)[3] = v[h];
         n[h][0] = __fma_rn(d[2], x[2], __fma_rn(d[1], x[1], d[0] * x[0]));
         n[h][1] = __fma_rn(d[4], x[2], __fma_rn(d[3], x[1], d[1] * x[0]));
         n[h][2] = __fma_rn(d[5], x[2], __fma_rn(d[4], x[1], d[2] * x[0]));
-        const bool sh = shuf && lane < 31;
+      }
+      // slots 0..2 on chip. Slot 0: the next row is the next lane (shuffle); lane 31 reads the next slice's row from
+      // s_m (or global at the CTA's end); its transposed product reaches lanes 1..31 by shuffle
+      {
         double vj[3], B[9], t1[3], tr[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) vj[k] = __shfl_down_sync(0xffffffffu, x[k], 1);
-        if (!sh) gather(h, 0, vj);
-        smem_block(h, 0, B);
+        if (!(shuf && lane < 31)) {
+          const int j = row[h] + oa.off[0];
+          const bool in = up(h, 0) && j < r1;
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            vj[k] = in ? s_m[k * kRows + li[h] + oa.off[0]] : __ldca(vg + k * npad + (up(h, 0) ? j : ZP));
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) B[q] = s_blk[q * kRows + li[h]];
         mv_add(B, vj, n[h]);
         mtv(B, x, t1);
 #pragma unroll
         for (int k = 0; k < 3; ++k) tr[k] = __shfl_up_sync(0xffffffffu, t1[k], 1);
-        const bool take = shuf && lane > 0 && lo(h, 0);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) n[h][k] += take ? tr[k] : 0.0;
-        if (shuf && lane == 31)
-#pragma unroll
-          for (int k = 0; k < 3; ++k) s_t0[(li[h] >> 5) + 1][k] = t1[k];
+        if (shuf && lane > 0 && lo(h, 0)) add3(h, tr);
       }
-      add3(h, Lr[0]);
-      add3(h, Lr[1]);
-      slot12(h, 1, Lr[2]);
-      lower_t(h, 4, Lr[0]);
-      lower_t(h, 3, Lr[1]);
-      gather(h, 2, Lr[2]);
-      add3(h, Lr[0]);
-      add3(h, Lr[1]);
-      slot12(h, 2, Lr[2]);
-      gather(h, 3, Lr[0]);
-      gather(h, 4, Lr[1]);
-      lower_t(h, 2, Lr[2]);
-      lower_t(h, 0, Lr[3]);
-      slot_tm(h, 3, Lr[0]);
-      slot_tm(h, 4, Lr[1]);
-      add3(h, Lr[2]);
-      add3(h, Lr[3]);
-      gather(h, 5, Lr[0]);
-      gather(h, 6, Lr[1]);
-      lower_t(h, 1, Lr[2]);
-      slot_tm(h, 5, Lr[0]);
-      slot_tm(h, 6, Lr[1]);
-      add3(h, Lr[2]);
-    };
 #pragma unroll
-    for (int h = 0; h < kRpt; ++h) row_rounds(h);
-    __syncthreads();  // the CTA's t buffers are complete
-    // same-CTA lower products: slot 0 from the previous slice's lane 31, slots 2, 1 from the t buffer
+      for (int b = 1; b <= 2; ++b) {  // direct products of slots 1, 2
+        const int j = row[h] + oa.off[b];
+        const bool in = j < r1;
+        double g[3], B[9];
 #pragma unroll
-    for (int h = 0; h < kRpt; ++h) {
-      const int t0 = (shuf && lane == 0 && lo(h, 0) && row[h] - 1 >= r0) ? (li[h] >> 5) : 0;  // 0: zero entry
+        for (int k = 0; k < 3; ++k)
+          g[k] = in ? s_m[k * kRows + li[h] + oa.off[b]] : __ldca(vg + k * npad + (up(h, b) ? j : ZP));
 #pragma unroll
-      for (int k = 0; k < 3; ++k) n[h][k] += s_t0[t0][k];
+        for (int q = 0; q < 9; ++q) B[q] = s_blk[(b * 9 + q) * kRows + li[h]];
+        mv_add(B, g, n[h]);
+      }
+      // transposed products of the CTA's rows: slot 0 for lane 0 (the previous slice's lane 31; without a +1
+      // offset every lane), slots 1, 2
 #pragma unroll
-      for (int b = 2; b >= 1; --b) {
+      for (int b = 0; b <= 2; ++b) {
         const int i = row[h] - oa.off[b];
-        const int src = (lo(h, b) && i >= r0) ? li[h] - oa.off[b] : kRows;  // kRows: the zero entry
+        const bool take = lo(h, b) && i >= r0 && !(b == 0 && shuf && lane > 0);
+        if (take) {
+          const int src = li[h] - oa.off[b];
+          double B[9], mi[3], t[3];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) n[h][q] += s_tb[((b - 1) * 3 + q) * (kRows + 1) + src];
+          for (int q = 0; q < 9; ++q) B[q] = s_blk[(b * 9 + q) * kRows + src];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) mi[k] = s_m[k * kRows + src];
+          mtv(B, mi, t);
+          add3(h, t);
+        }
       }
+      OC_SUB(1);
+      add3(h, L[0]);
+      add3(h, L[1]);
+      add3(h, L[2]);
+      OC_SUB(2);
+      // round 2: slot 3's remote lower product, the columns of slots 3, 4, and the CTA-edge remote lower products
+      lower_t(h, 3, L[0]);
+      gather(h, 3, L[1]);
+      gather(h, 4, L[2]);
+      double E[3][3];
+      lower_t(h, 2, E[0]);
+      lower_t(h, 1, E[1]);
+      lower_t(h, 0, E[2]);
+      add3(h, L[0]);
+      slot_tm(h, 3, L[1]);
+      slot_tm(h, 4, L[2]);
+      add3(h, E[0]);
+      add3(h, E[1]);
+      add3(h, E[2]);
+      OC_SUB(3);
+      // round 3: the columns of slots 5, 6
+      gather(h, 5, L[0]);
+      gather(h, 6, L[1]);
+      slot_tm(h, 5, L[0]);
+      slot_tm(h, 6, L[1]);
+      OC_SUB(4);
     }
   };
 
@@ -437,7 +456,10 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       X[h][k] = live[h] ? a.x[3 * (size_t)row[h] + k] : 0.0;
-      if (h == 1) s_x1[k][tid] = X[h][k];
+      if (h == 1) {
+        s_x1[k][tid] = X[h][k];
+        s_p1[k][tid] = 0.0;
+      }
       R[h][k] = Wv[h][k] = P[h][k] = S[h][k] = Z[h][k] = 0.0;
     }
   int tpar = 0;
@@ -458,11 +480,13 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
       if (live[h])
 #pragma unroll
         for (int k = 0; k < 3; ++k) gm1[k * npad + row[h]] = X[h][k];
+      put_m(h, X[h]);
       produce(h, X[h], tpar);
     }
     grid.sync();
     spmv(gm1, X, tpar, acc);
     tpar ^= 1;
+    __syncthreads();  // every warp's SpMV has read s_m before it is rewritten
   }
   double bb = 0.0, U[kRpt][3];
 #pragma unroll
@@ -476,6 +500,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
       if (live[h]) gm0[k * npad + row[h]] = U[h][k];
       bb = __fma_rn(bi, bi, bb);
     }
+    put_m(h, U[h]);
     produce(h, U[h], tpar);
   }
   bb = lane_sum_oc(bb);
@@ -498,6 +523,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
     // setup 2: w = A u, m = D^-1 w (gathered by iteration 0), partials gamma_0, delta_0, r.r
     spmv(gm0, U, tpar, acc);
     tpar ^= 1;
+    __syncthreads();  // every warp's SpMV has read s_m before it is rewritten
     double v3[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int h = 0; h < kRpt; ++h) {
@@ -507,6 +533,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
         Wv[h][k] = acc[h][k];
         M[k] = Dv(h, k) * acc[h][k];
         if (live[h]) gm1[k * npad + row[h]] = M[k];
+        s_m[k * kRows + li[h]] = M[k];
         v3[0] = __fma_rn(R[h][k], U[h][k], v3[0]);
         v3[1] = __fma_rn(acc[h][k], U[h][k], v3[1]);
         v3[2] = __fma_rn(R[h][k], R[h][k], v3[2]);
@@ -531,7 +558,9 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
         for (int h = 0; h < kRpt; ++h)
 #pragma unroll
           for (int k = 0; k < 3; ++k) m[h][k] = Dv(h, k) * Wv[h][k];
+        sub_on = it == 10;
         spmv(cur ? gm1 : gm0, m, tpar, n3);
+        sub_on = false;
         tpar ^= 1;
       }
       OC_STAMP(it, 1);
@@ -574,14 +603,20 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
           const double dk = Dv(h, k);
           Z[h][k] = __fma_rn(beta, Z[h][k], n3[h][k]);      // z = A q = n + beta z
           S[h][k] = __fma_rn(beta, S[h][k], Wv[h][k]);      // s = A p = w + beta s
-          P[h][k] = __fma_rn(beta, P[h][k], dk * R[h][k]);  // p = u + beta p, u = D^-1 r
-          if (h == 0) X[h][k] = __fma_rn(alpha, P[h][k], X[h][k]);
-          else s_x1[k][tid] = __fma_rn(alpha, P[h][k], s_x1[k][tid]);
+          double pk;  // p = u + beta p, u = D^-1 r
+          if (h == 0) {
+            pk = P[h][k] = __fma_rn(beta, P[h][k], dk * R[h][k]);
+            X[h][k] = __fma_rn(alpha, pk, X[h][k]);
+          } else {
+            pk = s_p1[k][tid] = __fma_rn(beta, s_p1[k][tid], dk * R[h][k]);
+            s_x1[k][tid] = __fma_rn(alpha, pk, s_x1[k][tid]);
+          }
           R[h][k] = __fma_rn(-alpha, S[h][k], R[h][k]);
           const double uk = dk * R[h][k];
           Wv[h][k] = __fma_rn(-alpha, Z[h][k], Wv[h][k]);   // w -= alpha z
           M2[h][k] = dk * Wv[h][k];
           if (live[h]) gnext[k * npad + row[h]] = M2[h][k];
+          s_m[k * kRows + li[h]] = M2[h][k];
           v[0] = __fma_rn(R[h][k], uk, v[0]);
           v[1] = __fma_rn(Wv[h][k], uk, v[1]);
           v[2] = __fma_rn(R[h][k], R[h][k], v[2]);

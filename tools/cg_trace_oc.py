@@ -29,3 +29,7 @@ print("publish-end at iteration 10 (from the first SpMV end): min %.2f median %.
     list(np.argsort(p)[-6:])))
 print("CTAs", nb, "| SpMV-end spread at iteration 10: %.2f us (median %.2f)" % ((e.max() - e.min()) / 1e3,
                                                                              (np.median(e) - e.min()) / 1e3))
+sub = buf[4100:4105].astype(np.float64)
+if sub[0] > 0:
+    print("SpMV of CTA 0 warp 0 row 0 at iteration 10 (us from its start): on-chip part %.2f, round-1 loads consumed %.2f,"
+          " round 2 %.2f, round 3 %.2f" % tuple((sub[1:] - sub[0]) / 1e3))

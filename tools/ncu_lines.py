@@ -1,6 +1,7 @@
 """Per-source-line warp-stall samples of one kernel from an ncu --set full capture (--import-source on), mapped
 through nvdisasm line info of the object the kernel was built from (this container; the capture comes back from the
-GPU box):   python tools/ncu_lines.py REPORT.ncu-rep OBJECT.o SOURCE.cu [N]"""
+GPU box):   python tools/ncu_lines.py REPORT.ncu-rep OBJECT.o SOURCE.cu [N] [MANGLED_SUBSTRING]
+(the substring picks the kernel's section when the object holds several kernels, e.g. k_assembleILi0ELb0E)"""
 import csv
 import os
 import re
@@ -13,6 +14,7 @@ from collections import defaultdict
 def main():
     rep, obj, src = sys.argv[1:4]
     n = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+    fn = sys.argv[5] if len(sys.argv) > 5 else ""
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
@@ -27,8 +29,12 @@ def main():
         cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
         sass = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], stdout=subprocess.PIPE,
                               stderr=subprocess.DEVNULL, text=True).stdout
-    line, off2line = None, {}
+    line, off2line, inside = None, {}, not fn
     for l in sass.splitlines():
+        if l.startswith(".text."):
+            inside = not fn or fn in l
+        if not inside:
+            continue
         m = re.search(r"line (\d+)", l)
         if m:
             line = int(m.group(1))
