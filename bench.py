@@ -220,10 +220,10 @@ def pcg_models(info):
     survey = 12 * 9 * info["node_blocks"] + 4 * (3 * N + 1) + 56 * 3 * N  # SURVEY §8(d) B_CG (scalar CSR)
     if info.get("pcg_solver_name") == "onchip":
         # k_pcg_onchip: the matrix is loaded ONCE per solve into TMEM + shared memory; per iteration only the column
-        # gathers of slots 1..6 (slot 0 is the next lane's), the remote transposed products of slots 3..6 (written
-        # and read) and m leave the chip -- 24 B each (cg_onchip.cu)
+        # gathers and the remote transposed products (written and read) of slots 3..6 and m leave the chip -- 24 B
+        # each; slots 0..2 of the CTA's rows use the shuffle and the shared m-cache (cg_onchip.cu)
         sb = info["oc_slot_blocks"]
-        it = 24 * sum(sb[1:]) + 48 * sum(sb[3:]) + 24 * N
+        it = 72 * sum(sb[3:]) + 24 * N
         once = 72 * info["upper_block_slots"]
         return dict(l2_bytes_per_iter=it, hbm_bytes_per_iter=it, bytes_per_solve=once, working_set_bytes=it,
                     survey_bytes_per_iter=survey,

@@ -30,8 +30,8 @@
 // (~0.3 KB instead of ~1.3 KB).
 //
 // The recurrences, decisions and deterministic reductions are k_pcg_pipe's (Ghysels & Vanroose pipelined PCG; one
-// grid barrier per iteration; decisions mapped one to one onto the reference's). The row sum is the lower
-// contributions in slot (column) order plus the upper ones in ordinal order: fixed, so the solve is bit-reproducible.
+// grid barrier per iteration; decisions mapped one to one onto the reference's). Every row sums its contributions in
+// one fixed order and the reductions use fixed trees, so the solve is bit-reproducible.
 #include <cooperative_groups.h>
 
 #include <algorithm>

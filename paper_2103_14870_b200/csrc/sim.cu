@@ -1147,12 +1147,11 @@ gf_step_stats Simulation::dynamic_step() {
   // next to it.
   double cg_bytes_per_iter = 72.0 * ((double)pat_.cols.size() + mesh_.nn) / 2.0 + 4.0 * 32.0 * (double)sell_slots_ +
                              (cg_ndyn_ ? 312.0 : 48.0) * mesh_.nn;
-  if (cg_.onchip) {  // the matrix stays on chip: per iteration the column gathers of slots 1..6, the remote t of
-                     // slots 3..6 (written and read) and m (bench.py pcg_models; the one matrix load is not counted)
-    double g = 0.0, t = 0.0;
-    for (int b = 1; b < 7; ++b) g += (double)oc_slot_blocks_[b];
+  if (cg_.onchip) {  // the matrix stays on chip: per iteration the column gathers and the remote t (written and read)
+                     // of slots 3..6, and m (bench.py pcg_models); the matrix load once per solve is added below
+    double t = 0.0;
     for (int b = 3; b < 7; ++b) t += (double)oc_slot_blocks_[b];
-    cg_bytes_per_iter = 24.0 * g + 48.0 * t + 24.0 * mesh_.nn;
+    cg_bytes_per_iter = 72.0 * t + 24.0 * mesh_.nn;
   }
   // k_pcg_onchip loads the matrix (upper blocks incl. slice padding) once per solve
   const double cg_bytes_per_solve = cg_.onchip ? 72.0 * 32.0 * (double)usp_[d_.nslices] : 0.0;
