@@ -218,7 +218,7 @@ def pcg_models(info):
     N = info["nodes"]
     dyn = info["pcg_dynamic_units"] > 0
     survey = 12 * 9 * info["node_blocks"] + 4 * (3 * N + 1) + 56 * 3 * N  # SURVEY §8(d) B_CG (scalar CSR)
-    if info.get("pcg_solver_name") == "onchip":
+    if info.get("pcg_solver_name") in ("onchip", "onchip-cluster"):
         # k_pcg_onchip: the matrix is loaded ONCE per solve into TMEM + shared memory; per iteration only the column
         # gathers and the remote transposed products (written and read) of slots 3..6 and m leave the chip -- 24 B
         # each; slots 0..2 of the CTA's rows use the shuffle and the shared m-cache (cg_onchip.cu)
@@ -228,7 +228,8 @@ def pcg_models(info):
         return dict(l2_bytes_per_iter=it, hbm_bytes_per_iter=it, bytes_per_solve=once, working_set_bytes=it,
                     survey_bytes_per_iter=survey,
                     format_bytes_per_iter=72 * info["upper_blocks"] + 4 * info["spmv_slots"] + 48 * N,
-                    solver_state="matrix and solver state on chip (TMEM + shared memory + registers)")
+                    solver_state=("matrix and solver state on chip (TMEM + shared memory + registers)"
+                                  + (", one thread-block cluster" if info["pcg_solver_name"] == "onchip-cluster" else "")))
     vec = (312 if dyn else 48) * N
     l2 = 72 * info["node_blocks"] + 4 * info["spmv_slots"] + vec
     hbm = 72 * info["upper_blocks"] + 4 * info["spmv_slots"] + vec

@@ -174,8 +174,16 @@ __device__ __forceinline__ void mtv(const double (&B)[9], const double (&v)[3], 
   for (int c = 0; c < 3; ++c) t[c] = __fma_rn(B[6 + c], v[2], __fma_rn(B[3 + c], v[1], B[c] * v[0]));
 }
 
+// kCluster: the whole solve in ONE thread-block cluster (small matrices, <= 16 x 24 slices): the hardware cluster
+// barrier replaces the grid barrier, the CTA partials travel through distributed shared memory and the gathered
+// vector is read through L2 (the cluster barrier orders memory at cluster scope; it does not invalidate L1)
+template <bool kCluster>
 __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
-  cgx::grid_group grid = cgx::this_grid();
+  auto gsync = [] {
+    if constexpr (kCluster) cgx::this_cluster().sync();
+    else cgx::this_grid().sync();
+  };
+  __shared__ double s_part[2][4];  // kCluster: this CTA's published partials (read by the cluster through DSMEM)
   const CgLaunch& a = oa.a;
   extern __shared__ double s_dyn[];
   double* const s_blk = s_dyn;                          // [b][q][local row]
@@ -265,6 +273,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
   // remote transposed products of v (row h's value) for the NEXT SpMV, published before the grid barrier: slots
   // 3..6 every row (absent slots hold zero blocks), slots 0..2 at CTA edges only
   auto produce = [&](int h, const double (&v)[3], int par) {
+    if (!__any_sync(0xffffffffu, live[h])) return;
     row[h] = launder(row[h]);
     li[h] = launder(li[h]);
     tmh[h] = launder(tmh[h]);
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
     auto gather = [&](int h, int b, double (&g)[3]) {  // v at slot b's column from global (zero entry if not taken)
       const int j = up(h, b) ? row[h] + oa.off[b] : ZP;
 #pragma unroll
-      for (int k = 0; k < 3; ++k) g[k] = __ldca(vg + k * npad + j);
+      for (int k = 0; k < 3; ++k) g[k] = kCluster ? __ldcg(vg + k * npad + j) : __ldca(vg + k * npad + j);
     };
     auto add3 = [&](int h, const double (&t)[3]) {
 #pragma unroll
@@ -325,6 +334,11 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
     };
 #pragma unroll
     for (int h = 0; h < kRpt; ++h) {
+      if (!__any_sync(0xffffffffu, live[h])) {  // a warp without this slice (CTAs of fewer than 24 slices)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) n[h][k] = 0.0;
+        continue;
+      }
       double L[4][3];
       OC_SUB(0);
       // round 1: the remote lower products of slots 6..4 (and of slots 0..2 at CTA edges)
@@ -350,7 +364,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
           const bool in = up(h, 0) && j < r1;
 #pragma unroll
           for (int k = 0; k < 3; ++k)
-            vj[k] = in ? s_m[k * kRows + li[h] + oa.off[0]] : __ldca(vg + k * npad + (up(h, 0) ? j : ZP));
+            vj[k] = in ? s_m[k * kRows + li[h] + oa.off[0]] : __ldcg(vg + k * npad + (up(h, 0) ? j : ZP));
         }
 #pragma unroll
         for (int q = 0; q < 9; ++q) B[q] = s_blk[q * kRows + li[h]];
@@ -367,7 +381,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
         double g[3], B[9];
 #pragma unroll
         for (int k = 0; k < 3; ++k)
-          g[k] = in ? s_m[k * kRows + li[h] + oa.off[b]] : __ldca(vg + k * npad + (up(h, b) ? j : ZP));
+          g[k] = in ? s_m[k * kRows + li[h] + oa.off[b]] : __ldcg(vg + k * npad + (up(h, b) ? j : ZP));
 #pragma unroll
         for (int q = 0; q < 9; ++q) B[q] = s_blk[(b * 9 + q) * kRows + li[h]];
         mv_add(B, g, n[h]);
@@ -425,7 +439,8 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
     if (tid < nv) {
       double x = 0.0;
       for (int k = 0; k < kW; ++k) x += s_acc[k][tid];
-      oa.cta_part[((size_t)parity * 4 + tid) * kMaxGridOc + blockIdx.x] = x;
+      if constexpr (kCluster) s_part[parity][tid] = x;
+      else oa.cta_part[((size_t)parity * 4 + tid) * kMaxGridOc + blockIdx.x] = x;
     }
   };
   // the published CTA partials (thread k < G holds CTA k's), loaded before an SpMV and reduced after it
@@ -435,7 +450,10 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
     for (int k = tid; k < G; k += kT)
 #pragma unroll
       for (int q = 0; q < 3; ++q)
-        if (q < nv) pb[q] += __ldcg(oa.cta_part + ((size_t)parity * 4 + q) * kMaxGridOc + k);
+        if (q < nv) {
+          if constexpr (kCluster) pb[q] += *cgx::this_cluster().map_shared_rank(&s_part[parity][q], k);
+          else pb[q] += __ldcg(oa.cta_part + ((size_t)parity * 4 + q) * kMaxGridOc + k);
+        }
   };
   auto totals = [&](const double (&pb)[3], double (&out)[3]) {  // fixed lane and warp trees, identical everywhere
 #pragma unroll
@@ -483,7 +501,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
       put_m(h, X[h]);
       produce(h, X[h], tpar);
     }
-    grid.sync();
+    gsync();
     spmv(gm1, X, tpar, acc);
     tpar ^= 1;
     __syncthreads();  // every warp's SpMV has read s_m before it is rewritten
@@ -505,7 +523,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
   }
   bb = lane_sum_oc(bb);
   publish(&bb, 1, 0);
-  grid.sync();
+  gsync();
   double tot[3], pb0[3];
   load_parts(0, 1, pb0);
   totals(pb0, tot);
@@ -544,7 +562,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
     for (int q = 0; q < 3; ++q) v3[q] = lane_sum_oc(v3[q]);
     __syncthreads();  // s_acc reuse
     publish(v3, 3, 1);
-    grid.sync();
+    gsync();
     int pp = 1, cur = 1;
     double gam_prev = 1.0, alpha_prev = 1.0;
     for (int it = 0;; ++it) {
@@ -633,7 +651,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
       if (a.trace && it == 10 && tid == 0) a.trace[2000 + blockIdx.x] = gtimer_oc();
       pp ^= 1;
       cur ^= 1;
-      grid.sync();
+      gsync();
     }
 #pragma unroll
     for (int h = 0; h < kRpt; ++h)
@@ -642,7 +660,9 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
         for (int k = 0; k < 3; ++k) a.x[3 * (size_t)row[h] + k] = h == 0 ? X[h][k] : s_x1[k][tid];
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  // no CTA of a cluster may exit while another can still read its shared memory (the last partial reads)
+  if constexpr (kCluster) cgx::this_cluster().sync();
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(s_taddr));
   if (blockIdx.x == 0 && tid == 0) {
@@ -659,17 +679,44 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
 int pcg_onchip_grid() {
   static int g = -1;
   if (g < 0) {
-    cudaFuncSetAttribute((const void*)k_pcg_onchip, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOcSmem);
+    cudaFuncSetAttribute((const void*)k_pcg_onchip<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOcSmem);
+    cudaFuncSetAttribute((const void*)k_pcg_onchip<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOcSmem);
+    cudaFuncSetAttribute((const void*)k_pcg_onchip<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     int dev = 0, sms = 0, q = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_onchip, kT, kOcSmem) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_onchip<false>, kT, kOcSmem) != cudaSuccess) {
       cudaGetLastError();
       q = 0;
     }
     g = q >= 1 ? std::min(kMaxGridOc, sms) : 0;
   }
   return g;
+}
+// the largest cluster k_pcg_onchip<true> can be launched with (0: clusters unavailable)
+int pcg_onchip_max_cluster() {
+  static int cached = -1;
+  if (cached < 0) {
+    pcg_onchip_grid();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16, 1, 1);
+    cfg.blockDim = dim3(kT, 1, 1);
+    cfg.dynamicSmemBytes = kOcSmem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 16;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxPotentialClusterSize(&n, (const void*)k_pcg_onchip<true>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    cached = std::min(n, 16);
+  }
+  return cached;
 }
 int pcg_onchip_warps_per_cta() { return kRows / 32; }  // slices per CTA (two per warp)
 int pcg_onchip_max_upper() { return 8; }
@@ -681,9 +728,29 @@ void launch_pcg_onchip(const CgLaunch& a, double* part, double* tg, double* gm, 
                        const int32_t off[7], cudaStream_t s) {
   OcArgs oa{a, part, tg, gm, meta, pcg_onchip_npad(a.nslices), off[0] == 1, {}};
   for (int b = 0; b < 7; ++b) oa.off[b] = off[b];
-  void* args[] = {&oa};
   pcg_onchip_grid();
-  const cudaError_t err = cudaLaunchCooperativeKernel((const void*)k_pcg_onchip, a.grid, kT, args, kOcSmem, s);
+  if (a.cluster) {  // one thread-block cluster of a.grid CTAs
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.grid, 1, 1);
+    cfg.blockDim = dim3(kT, 1, 1);
+    cfg.dynamicSmemBytes = kOcSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = a.grid;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t err = cudaLaunchKernelEx(&cfg, k_pcg_onchip<true>, oa);
+    if (err != cudaSuccess) {
+      cudaGetLastError();
+      throw std::runtime_error(std::string("on-chip cluster CG launch failed: ") + cudaGetErrorString(err));
+    }
+    return;
+  }
+  void* args[] = {&oa};
+  const cudaError_t err = cudaLaunchCooperativeKernel((const void*)k_pcg_onchip<false>, a.grid, kT, args, kOcSmem, s);
   if (err != cudaSuccess) {
     cudaGetLastError();
     throw std::runtime_error(std::string("on-chip CG launch failed: ") + cudaGetErrorString(err));

@@ -215,6 +215,7 @@ void launch_spmv_sym(const CgLaunch& a, const double* xin, double* y, cudaStream
 // ---- cg_onchip.cu (the pipelined solve with the matrix on chip: at most 7 distinct positive column offsets (rows
 // of <= 8 upper blocks), <= 24 slices per CTA, exactly symmetric diagonal blocks) ----
 int pcg_onchip_grid();  // co-resident CTAs (0: not launchable on this device)
+int pcg_onchip_max_cluster();  // largest launchable cluster of the on-chip solver (0: none)
 int pcg_onchip_warps_per_cta();
 int pcg_onchip_max_upper();
 int pcg_onchip_npad(int nslices);

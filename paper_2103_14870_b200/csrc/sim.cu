@@ -557,18 +557,37 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     const int Gfull = dyn ? pcg_dyn_grid() : pcg_sell_grid(), W = dyn ? pcg_dyn_warps_per_cta() : pcg_sell_warps_per_cta();
     // CTAs of the cooperative solve: all co-resident ones by default; GF_CG_GRID=<n> asks for fewer (cheaper grid
     // barriers for small matrices), never fewer than one slice per warp needs
-    int G = Gfull;
+    int G = Gfull, want = 0;
     if (const char* e = std::getenv("GF_CG_GRID")) {
-      const int want = std::atoi(e);
+      want = std::atoi(e);
       if (want > 0) G = std::min(Gfull, std::max(want, (ns + W - 1) / W));
     }
     cg_.pipelined = pcg_pipelined_default();
+    // the matrix on chip (cg_onchip.cu) when the pattern has at most 7 distinct positive column offsets (the box
+    // meshes: +1, +nx, +nx+1, +nx ny, ...) and its slices fit one CTA per SM (GF_CG_ONCHIP=0 disables)
+    std::vector<int32_t> offs;
+    for (int32_t i = 0; i < nn && offs.size() <= 7; ++i)
+      for (int32_t q = pat_.row_ptr[i]; q < pat_.row_ptr[i + 1]; ++q) {
+        const int32_t d = pat_.cols[q] - i;
+        if (d > 0 && std::find(offs.begin(), offs.end(), d) == offs.end()) offs.push_back(d);
+      }
+    const char* oe = std::getenv("GF_CG_ONCHIP");
+    const bool onchip_ok = !(oe && std::atoi(oe) == 0) && cg_.pipelined && !dyn && offs.size() <= 7 &&
+                           pcg_onchip_grid() >= G && W == pcg_onchip_warps_per_cta();
     // small matrices (c1): the whole pipelined solve in one thread-block cluster -- hardware cluster barriers and
-    // DSMEM partial exchange instead of grid barriers through global memory (GF_CG_CLUSTER=0 disables)
+    // DSMEM partial exchange instead of grid barriers through global memory (GF_CG_CLUSTER=0 disables); the on-chip
+    // solver's cluster instance when it applies, else k_pcg_pipe's
     const char* ce = std::getenv("GF_CG_CLUSTER");
-    const int cmax = (ce && std::atoi(ce) == 0) || !cg_.pipelined || dyn ? 0 : pcg_max_cluster();
+    const bool cluster_ok = !(ce && std::atoi(ce) == 0) && cg_.pipelined && !dyn;
+    const int cmax_oc = cluster_ok && onchip_ok ? pcg_onchip_max_cluster() : 0;
+    const int cmax = cluster_ok ? pcg_max_cluster() : 0;
     int Weff = W;
-    if (cmax > 0 && ns <= cmax * W) {
+    if (cmax_oc > 0 && ns <= cmax_oc * W) {
+      G = std::min(cmax_oc, ns);  // one CTA per slice up to the cluster size: more SMs, shorter latency chains
+      if (want > 0) G = std::min(G, std::max(want, (ns + W - 1) / W));
+      cg_.cluster = 1;
+      cg_.onchip = 1;
+    } else if (cmax > 0 && ns <= cmax * W) {
       G = cmax;
       cg_.cluster = 1;
       // warps to spare: up to 4 warps share a slice's SpMV (shorter latency chains)
@@ -577,6 +596,8 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
       while (split > 1 && ns > cmax * (W / split)) --split;
       cg_.split = split;
       Weff = W / split;
+    } else if (onchip_ok) {
+      cg_.onchip = 1;
     }
     cg_.grid = G;
     const int64_t gw = (int64_t)G * Weff;
@@ -610,18 +631,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     d_slice_part_ = (double*)zeros(8 * pcg_sell_part_doubles(cg_ndyn_));
     d_ctr_ = (unsigned long long*)zeros(64);
     cg_.cta_first = (const int32_t*)up(first.data(), 4 * first.size());
-    // the matrix on chip (cg_onchip.cu) when the pattern has at most 7 distinct positive column offsets (the box
-    // meshes: +1, +nx, +nx+1, +nx ny, ...) and the slices fit one warp each on a grid of one CTA per SM (c2, c3;
-    // GF_CG_ONCHIP=0 disables)
-    std::vector<int32_t> offs;
-    for (int32_t i = 0; i < nn && offs.size() <= 7; ++i)
-      for (int32_t q = pat_.row_ptr[i]; q < pat_.row_ptr[i + 1]; ++q) {
-        const int32_t d = pat_.cols[q] - i;
-        if (d > 0 && std::find(offs.begin(), offs.end(), d) == offs.end()) offs.push_back(d);
-      }
-    const char* oe = std::getenv("GF_CG_ONCHIP");
-    if (!(oe && std::atoi(oe) == 0) && cg_.pipelined && !dyn && !cg_.cluster && offs.size() <= 7 &&
-        pcg_onchip_grid() >= G && W == pcg_onchip_warps_per_cta()) {
+    if (cg_.onchip) {  // per-row slot masks over the sorted offsets
       std::sort(offs.begin(), offs.end());
       for (size_t b = 0; b < offs.size(); ++b) oc_off_[b] = offs[b];
       auto bit = [&](int32_t d) { return (int)(std::lower_bound(offs.begin(), offs.end(), d) - offs.begin()); };
@@ -636,7 +646,6 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
           else if (j < i) meta[i] |= 1u << (8 + bit(i - j));
         }
       d_oc_meta_ = (uint32_t*)up(meta.data(), sizeof(uint32_t) * meta.size());
-      cg_.onchip = 1;
       d_tg_ = (double*)zeros(8 * pcg_onchip_t_doubles(ns));
       d_ocm_ = (double*)zeros(8 * pcg_onchip_m_doubles(ns));
     }
@@ -665,7 +674,7 @@ gf_sim_info Simulation::info() const {
   o.nl_slots = mat_.r_d <= 0.0 ? 0 : d_.nl_tpl ? 32 * nl_tpl_slots_ : nl_ell_slots_;
   o.nl_layout = nonlocal_layout();
   o.pcg_dynamic_units = cg_ndyn_;
-  o.pcg_solver = cg_ndyn_ > 0 ? 4 : cg_.onchip ? 3 : !cg_.pipelined ? 0 : cg_.cluster ? 2 : 1;
+  o.pcg_solver = cg_ndyn_ > 0 ? 4 : cg_.onchip ? (cg_.cluster ? 5 : 3) : !cg_.pipelined ? 0 : cg_.cluster ? 2 : 1;
   for (int b = 0; b < 7; ++b) {
     o.oc_slot_blocks[b] = cg_.onchip ? oc_slot_blocks_[b] : 0;
     o.oc_offsets[b] = cg_.onchip ? oc_off_[b] : 0;

@@ -358,14 +358,14 @@ def test_step_metrics_match_oracle(model):
 
 # ---------------------------------------------------------------- the production PCG (k_pcg_sell) on given systems
 def _solver_env(monkeypatch, solver):
-    """cluster: k_pcg_pipe in one thread-block cluster; onchip: k_pcg_onchip (matrix in TMEM + shared memory);
-    grid: k_pcg_pipe on the cooperative grid; two-barrier: k_pcg_sell"""
-    monkeypatch.setenv("GF_CG_CLUSTER", "1" if solver == "cluster" else "0")
+    """onchip-cluster / onchip: k_pcg_onchip (matrix in TMEM + shared memory) in one thread-block cluster / on the
+    cooperative grid; cluster / grid: k_pcg_pipe likewise; two-barrier: k_pcg_sell"""
+    monkeypatch.setenv("GF_CG_CLUSTER", "1" if solver in ("cluster", "onchip-cluster") else "0")
     monkeypatch.setenv("GF_CG_PIPE", "0" if solver == "two-barrier" else "1")
-    monkeypatch.setenv("GF_CG_ONCHIP", "1" if solver == "onchip" else "0")
+    monkeypatch.setenv("GF_CG_ONCHIP", "1" if solver in ("onchip", "onchip-cluster") else "0")
 
 
-SOLVERS = ["cluster", "onchip", "grid", "two-barrier"]
+SOLVERS = ["onchip-cluster", "cluster", "onchip", "grid", "two-barrier"]
 
 
 @pytest.fixture(params=SOLVERS)
@@ -457,16 +457,18 @@ def test_production_pcg_matches_oracle_on_the_step_system(pcg_mode):
         prev = an
 
 
+@pytest.mark.parametrize("solver", ["onchip", "onchip-cluster"])
 @pytest.mark.parametrize("grid,cells", [("1", (5, 4, 6)), ("2", (8, 8, 8)), ("4", (14, 14, 14))])
-def test_onchip_pcg_many_slices_per_cta(grid, cells, monkeypatch):
+def test_onchip_pcg_many_slices_per_cta(grid, cells, solver, monkeypatch):
     """k_pcg_onchip with few CTAs (GF_CG_GRID), so that every CTA owns many slices and both rows of its threads: the
-    shared-memory routes of the transposed products (slot 0 across slices, slots 1/2 through the t buffer) and the
-    second row per thread all run; same solution as the oracle's cg_solve within 1e-9, iterations within 2"""
-    _solver_env(monkeypatch, "onchip")
+    on-chip routes of the transposed products (slot 0 across slices, slots 0..2 from the producer's shared-memory
+    block and the m-cache) and the second row per thread all run; same solution as the oracle's cg_solve within
+    1e-9, iterations within 2"""
+    _solver_env(monkeypatch, solver)
     monkeypatch.setenv("GF_CG_GRID", grid)
     s = cf.scaled("c2", cells)
     gs, os_, gm, om = pair(s)
-    assert gs.info()["pcg_solver_name"] == "onchip"
+    assert gs.info()["pcg_solver_name"] == solver
     rp, cols, _ = om.pattern()
     rows = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
     rng = np.random.default_rng(73)
@@ -614,7 +616,7 @@ def run_pair(s, steps, resync_tol=1e-6):
     return worst, resyncs, broken
 
 
-@pytest.mark.parametrize("solver", ["cluster", "onchip", "grid"])
+@pytest.mark.parametrize("solver", ["onchip-cluster", "cluster", "onchip", "grid"])
 def test_trajectory_c1_scaled(solver, monkeypatch):
     """small matrix: the pipelined PCG inside one thread-block cluster (default), with the matrix on chip, and on the
     cooperative grid"""
