@@ -19,7 +19,32 @@
 namespace gfb {
 namespace {
 
-constexpr int kWarps = 4;
+// asynchronous global -> shared copies (no registers while in flight): the epilogue's operands and the contribution
+// lists are requested at the row's start and land while the element phase computes
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// a column's epilogue operands staged in shared memory (EpiCol) and the row's (EpiRow, per dof a < 3)
+struct EpiCol {
+  double vj[3], fvj[3];
+  int32_t bcj, cu;
+};
+struct EpiRow {
+  double v, fext, fcoll, fv;
+};
+
+#ifndef GF_ASM_WARPS
+#define GF_ASM_WARPS 2  // warps per CTA (4: 0.378 ms at c3, 2: 0.372, 1: 0.380)
+#endif
+constexpr int kWarps = GF_ASM_WARPS;
 constexpr int kMaxValence = 32;  // tets per node handled by one warp (validated at setup)
 constexpr int kMaxDeg = 32;      // column blocks per node row (validated at setup)
 constexpr int kBlkStride = 32 * 27 + 9;  // per warp: 27 doubles per lane + the zero block of padding items
@@ -321,7 +346,8 @@ __device__ __forceinline__ double warp_reduce_scatter(double (&v)[N], int lane) 
 // diagonal; kv and corr accumulate
 template <int kMode>
 __device__ __forceinline__ void finish_column(const DevData& d, const StepCoeffs& sc, int i, int row0, int c, int j,
-                                              const double Kin[9], bool fixed_i, double kv[3], double corr[3]) {
+                                              const double Kin[9], bool fixed_i, double kv[3], double corr[3],
+                                              const EpiCol* pre = nullptr, double mass_i = -1.0) {
   // the diagonal block is symmetric up to rounding ((c2 a_r) a_c vs (c2 a_c) a_r): its upper triangle is mirrored so
   // that the stored block is exactly symmetric (the on-chip solver, cg_onchip.cu, keeps 6 of its 9 values)
   double K[9];
@@ -334,7 +360,7 @@ __device__ __forceinline__ void finish_column(const DevData& d, const StepCoeffs
   }
   // destination: the upper block in SELL-32 (entry r at out[32 r]); lower blocks of the symmetric format are
   // not stored (row j writes (j,i) = (i,j)^T)
-  const int cu = __ldg(d.uslot + row0 + c);
+  const int cu = pre ? pre->cu : __ldg(d.uslot + row0 + c);
   double* out = cu >= 0 ? d.bval + sell_addr(d.usp, i, cu, 0) : nullptr;
   constexpr int ostride = 32;
   if (kMode == kAssembleRawK) {
@@ -345,14 +371,14 @@ __device__ __forceinline__ void finish_column(const DevData& d, const StepCoeffs
   }
   double vj[3];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) vj[a] = d.v[3 * (size_t)j + a];
+  for (int a = 0; a < 3; ++a) vj[a] = pre ? pre->vj[a] : d.v[3 * (size_t)j + a];
 #pragma unroll
   for (int a = 0; a < 3; ++a) kv[a] += K[3 * a] * vj[0] + K[3 * a + 1] * vj[1] + K[3 * a + 2] * vj[2];
   double A[9];
 #pragma unroll
   for (int r = 0; r < 9; ++r) A[r] = sc.kscale * K[r];
   if (j == i) {
-    const double md = sc.mscale * __ldg(d.mass + i);
+    const double md = sc.mscale * (pre ? mass_i : __ldg(d.mass + i));
     A[0] += md;
     A[4] += md;
     A[8] += md;
@@ -360,10 +386,10 @@ __device__ __forceinline__ void finish_column(const DevData& d, const StepCoeffs
   if (fixed_i) {  // project_dirichlet: fixed row zeroed, unit diagonal
 #pragma unroll
     for (int r = 0; r < 9; ++r) A[r] = (j == i && r % 4 == 0) ? 1.0 : 0.0;
-  } else if (__ldg(d.node_bc + j) >= 0) {  // fixed column: move A_ij * dv_j to the rhs, zero it
+  } else if ((pre ? pre->bcj : __ldg(d.node_bc + j)) >= 0) {  // fixed column: move A_ij * dv_j to the rhs, zero it
     double fj[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) fj[a] = sc.fixed_zero ? 0.0 : d.fv[3 * (size_t)j + a];
+    for (int a = 0; a < 3; ++a) fj[a] = sc.fixed_zero ? 0.0 : pre ? pre->fvj[a] : d.fv[3 * (size_t)j + a];
 #pragma unroll
     for (int a = 0; a < 3; ++a) corr[a] += A[3 * a] * fj[0] + A[3 * a + 1] * fj[1] + A[3 * a + 2] * fj[2];
 #pragma unroll
@@ -384,23 +410,25 @@ __device__ __forceinline__ void finish_column(const DevData& d, const StepCoeffs
 // row i's rhs / CG initial guess / force output (lanes 0..2), after the kv and corr warp sums
 template <int kMode>
 __device__ __forceinline__ void finish_row(const DevData& d, const StepCoeffs& sc, int i, int lane, double fsum,
-                                           bool fixed_i, double kva, double corra) {
+                                           bool fixed_i, double kva, double corra, const EpiRow* pre = nullptr,
+                                           double mass_i = -1.0) {
   if (lane >= 3) return;
   const int a = lane;
   const size_t dof = 3 * (size_t)i + a;
   if (d.fint_out) d.fint_out[dof] = fsum;
   if (kMode == kAssembleSystem) {
     if (fixed_i) {
-      const double fv = sc.fixed_zero ? 0.0 : d.fv[dof];
+      const double fv = sc.fixed_zero ? 0.0 : pre ? pre->fv : d.fv[dof];
       d.rhs[dof] = fv;
       d.x[dof] = fv;
     } else {
-      const double mv = __ldg(d.mass + i) * d.v[dof];
-      const double fe = sc.use_ext ? d.fext[dof] + d.fcoll[dof] : 0.0;
+      const double mi = pre ? mass_i : __ldg(d.mass + i);
+      const double mv = mi * (pre ? pre->v : d.v[dof]);
+      const double fe = sc.use_ext ? (pre ? pre->fext + pre->fcoll : d.fext[dof] + d.fcoll[dof]) : 0.0;
       double r = sc.rhs_fint_scale * (fe + fsum);
       r -= sc.rhs_mv_scale * mv;
       r -= sc.rhs_kv_scale * kva;
-      if (sc.mdv) r -= __ldg(d.mass + i) * sc.mdv[dof];
+      if (sc.mdv) r -= mi * sc.mdv[dof];
       r -= corra;
       d.rhs[dof] = r;
       d.x[dof] = 0.0;
@@ -418,7 +446,7 @@ __device__ __forceinline__ void finish_row(const DevData& d, const StepCoeffs& s
 #define GF_ASM_FUSED_ENERGY 1  // the tet energies of the assembled state as a by-product of the force pass
 #endif
 #ifndef GF_ASM_MINB
-#define GF_ASM_MINB 4
+#define GF_ASM_MINB (16 / GF_ASM_WARPS)  // 16 warps per SM (123 registers)
 #endif
 template <int kMode, bool kEdge>
 __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d, MatDev m, StepCoeffs sc) {
@@ -438,9 +466,43 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
   double dg[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   constexpr bool kFusedEnergy = kMode == kAssembleSystem && !kEdge && GF_ASM_FUSED_ENERGY;  // edge form: k_tet_edge
   double psi = 0.0;
+  // the incidence (issued first), then the epilogue's operands and the contribution lists requested as asynchronous
+  // copies into shared memory: they land while the element phase computes (the header is their only dependence)
+  const int e = lane < np ? __ldg(d.nt_tet + p0 + lane) : 0;
+  const int4 t = lane < np ? __ldg(d.nt_nodes + p0 + lane) : make_int4(0, 0, 0, 0);  // not tets[e]
+  __shared__ EpiCol s_epi[kBlocks ? kWarps : 1][32];
+  __shared__ EpiRow s_erow[kWarps][3];
+  __shared__ double s_mass[kWarps];
+  const int jc = (kBlocks && lane < deg) ? __ldg(d.bcol + row0 + lane) : -1;
+  int mx4 = 0;
+  if (kBlocks) {
+    const int ib0 = __ldg(d.contrib_ptr + i), nitems = __ldg(d.contrib_ptr + i + 1) - ib0;
+    mx4 = nitems / (4 * deg);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(d.contrib_item + ib0);
+    uint32_t* s_item4 = reinterpret_cast<uint32_t*>(&s_item[w][0]);
+    for (int k = lane; k < nitems / 4; k += 32) cp_async4(s_item4 + k, src + k);
+    if (lane < deg) {
+      EpiCol& E = s_epi[w][lane];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        cp_async8(&E.vj[a], d.v + 3 * (size_t)jc + a);
+        cp_async8(&E.fvj[a], d.fv + 3 * (size_t)jc + a);
+      }
+      cp_async4(&E.bcj, d.node_bc + jc);
+      cp_async4(&E.cu, d.uslot + row0 + lane);
+    }
+  }
+  if (kMode == kAssembleSystem && lane < 3) {
+    const size_t dof = 3 * (size_t)i + lane;
+    EpiRow& R = s_erow[w][lane];
+    cp_async8(&R.v, d.v + dof);
+    cp_async8(&R.fext, d.fext + dof);
+    cp_async8(&R.fcoll, d.fcoll + dof);
+    cp_async8(&R.fv, d.fv + dof);
+  }
+  if (lane == 0) cp_async8(&s_mass[w], d.mass + i);
+  cp_async_commit();
   if (lane < np) {
-    const int e = __ldg(d.nt_tet + p0 + lane);
-    const int4 t = __ldg(d.nt_nodes + p0 + lane);  // not tets[e]: no dependence on e
     const int li = (t.x == i) ? 0 : (t.y == i) ? 1 : (t.z == i) ? 2 : 3;
     double* blk = kBlocks ? &s_blk[w][27 * lane] : nullptr;
     lane_element<kEdge, kBlocks>(d, m, e, t, li, f, blk, dg, kFusedEnergy ? &psi : nullptr);
@@ -459,19 +521,16 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
 
   const bool fixed_i = __ldg(d.node_bc + i) >= 0;
   double kv[3] = {0.0, 0.0, 0.0}, corr[3] = {0.0, 0.0, 0.0};
+  cp_async_wait_all();
+  const double mass_i = s_mass[w];
   if (kBlocks) {
-    const int jc = lane < deg ? __ldg(d.bcol + row0 + lane) : -1;
     const int cdiag = __ffs(__ballot_sync(0xffffffffu, jc == i)) - 1;
     const double dsum = __shfl_sync(0xffffffffu, rsum, 2 * (lane < 9 ? 3 + lane : 3));  // lane q < 9: entry q
-    // the row's padded contribution lists (mx <= 16 items per column) staged in shared memory, so
-    // the reduction below touches only shared memory with a uniform trip count
-    // lists padded to whole 4-item words by the host: staged and read 32 bits (4 items) at a time, so an output's
-    // block loads issue together (the sum stays sequential in item order)
-    const int ib0 = __ldg(d.contrib_ptr + i), nitems = __ldg(d.contrib_ptr + i + 1) - ib0;
-    const int mx4 = nitems / (4 * deg);
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(d.contrib_item + ib0);
-    uint32_t* s_item4 = reinterpret_cast<uint32_t*>(&s_item[w][0]);
-    for (int k = lane; k < nitems / 4; k += 32) s_item4[k] = __ldg(src + k);
+    // the row's padded contribution lists (mx <= 16 items per column), staged in shared memory above, so the
+    // reduction below touches only shared memory with a uniform trip count; lists padded to whole 4-item words by
+    // the host and read 32 bits (4 items) at a time, so an output's block loads issue together (the sum stays
+    // sequential in item order)
+    const uint32_t* s_item4 = reinterpret_cast<const uint32_t*>(&s_item[w][0]);
     if (lane < 9) s_blk[w][32 * 27 + lane] = 0.0;  // the zero block padding items point at
     __syncwarp();
     // off-diagonal outputs (column c != cdiag, entry q), 9 (deg - 1) of them spread over the lanes
@@ -499,7 +558,7 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
       double K[9];
 #pragma unroll
       for (int r = 0; r < 9; ++r) K[r] = s_row[w][9 * c + r];
-      finish_column<kMode>(d, sc, i, row0, c, jc, K, fixed_i, kv, corr);
+      finish_column<kMode>(d, sc, i, row0, c, jc, K, fixed_i, kv, corr, &s_epi[w][c], mass_i);
     }
   }
   double kva = 0.0, corra = 0.0;
@@ -509,7 +568,7 @@ __global__ void __launch_bounds__(32 * kWarps, GF_ASM_MINB) k_assemble(DevData d
     kva = __shfl_sync(0xffffffffu, ksum, 4 * (lane < 3 ? lane : 0));
     corra = __shfl_sync(0xffffffffu, ksum, 4 * (lane < 3 ? 3 + lane : 3));
   }
-  finish_row<kMode>(d, sc, i, lane, fsum, fixed_i, kva, corra);
+  finish_row<kMode>(d, sc, i, lane, fsum, fixed_i, kva, corra, lane < 3 ? &s_erow[w][lane] : nullptr, mass_i);
 }
 
 
