@@ -166,6 +166,16 @@ def ncu_traffic(workload, kernel):
         return None
 
 
+def ncu_limiters(workload, kernel):
+    """the committed ncu summary of `kernel` on `workload` (tools/ncu_summary.py): unit throughput fractions,
+    occupancy, issue activity and top stall reasons -- what bounds the kernel, next to its byte-model fraction."""
+    p = os.path.join(ROOT, "profiles", "ncu_limiters.json")
+    try:
+        return (json.load(open(p)).get(workload) or {}).get(kernel)
+    except (OSError, ValueError, AttributeError):
+        return None
+
+
 # ---------------------------------------------------------------- CPU baseline (oracle)
 def run_cpu(s, steps, budget_s, single_thread=False, warmup=1):
     """Times the CPU oracle (reference's algorithm + OpenMP layout) on a bounded sample of the workload: `warmup`
@@ -448,6 +458,9 @@ def main():
         roofline["kernels"][k] = {"launches": v["launches"], "avg_ms": v["total_ms"] / max(1, v["launches"]),
                                   "share": v["total_ms"] / ms_b, "GBps": gbps,
                                   "hbm_frac": gbps / peak if gbps else None, "traffic": ncu_traffic(s.name, k)}
+        lim = ncu_limiters(s.name, k)
+        if lim:
+            roofline["kernels"][k]["ncu"] = lim
     # whole-step roofline in the metric's own terms (BASELINE metric "% of HBM roofline"): algorithmic bytes per step
     # (B_F + B_D + B_int of SURVEY §8(d) and the PCG's format bytes per iteration x measured iterations) over the
     # measured step time; the SURVEY scalar-CSR PCG model is reported alongside (it overstates the format's bytes)
