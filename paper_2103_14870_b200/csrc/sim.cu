@@ -587,6 +587,7 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
       if (want > 0) G = std::min(G, std::max(want, (ns + W - 1) / W));
       cg_.cluster = 1;
       cg_.onchip = 1;
+      cg_.split = 1;  // k_pcg_pipe's cluster instance on this layout when a caller's matrix falls back (solve_system)
     } else if (cmax > 0 && ns <= cmax * W) {
       G = cmax;
       cg_.cluster = 1;

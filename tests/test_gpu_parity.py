@@ -411,6 +411,24 @@ def test_production_pcg_zero_rhs(pcg_mode):  # sparse.cpp:145-150: b = 0 -> x = 
     assert np.all(x == 0.0) and np.all(xo == 0.0)
 
 
+def test_production_pcg_asymmetric_diagonal_falls_back(pcg_mode):
+    """a caller's matrix whose diagonal blocks are not exactly symmetric cannot use k_pcg_onchip (it keeps their upper
+    triangle): solve_system takes k_pcg_pipe on the same layout and still matches the oracle's cg_solve"""
+    gs, _, om, rp, cols, rows = _pcg_setup(pcg_mode)
+    n = len(rp) - 1
+    rng = np.random.default_rng(74)
+    d = 2.0 + rng.uniform(0, 1, n)
+    vals = np.where(rows == cols, d[rows], 0.0)
+    skew = (rows // 3 == cols // 3) & (rows != cols)  # a tiny asymmetric coupling inside each diagonal block
+    vals = np.where(skew, 1e-3 * np.where(rows < cols, 1.0, -0.5), vals)
+    b = rng.uniform(-1, 1, n)
+    x, r = gs.solve_system(vals, b, tol=1e-12, max_iters=200)
+    xo, ro = _oracle_cg(rp, cols, vals, b, np.zeros(n), 1e-12, 200)
+    assert r["converged"] == ro["converged"] and abs(r["iterations"] - ro["iterations"]) <= 2
+    assert np.abs(x - xo).max() <= 1e-9 * np.abs(xo).max()
+    assert gs.info()["pcg_solver_name"] == pcg_mode  # the simulation's own solver is unchanged afterwards
+
+
 def test_production_pcg_negative_curvature(pcg_mode):  # test_sparse.cpp:74-84 / sparse.cpp:160-168 on k_pcg_sell
     gs, _, om, rp, cols, rows = _pcg_setup(pcg_mode)
     n = len(rp) - 1
