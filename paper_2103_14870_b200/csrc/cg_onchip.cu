@@ -719,7 +719,6 @@ int pcg_onchip_max_cluster() {
   return cached;
 }
 int pcg_onchip_warps_per_cta() { return kRows / 32; }  // slices per CTA (two per warp)
-int pcg_onchip_max_upper() { return 8; }
 int pcg_onchip_npad(int nslices) { return nslices * 32 + 32; }  // row nrows <= npad - 1 is the zero entry
 size_t pcg_onchip_t_doubles(int nslices) { return 2 * 21 * (size_t)pcg_onchip_npad(nslices); }
 size_t pcg_onchip_m_doubles(int nslices) { return 2 * 3 * (size_t)pcg_onchip_npad(nslices); }

@@ -217,7 +217,6 @@ void launch_spmv_sym(const CgLaunch& a, const double* xin, double* y, cudaStream
 int pcg_onchip_grid();  // co-resident CTAs (0: not launchable on this device)
 int pcg_onchip_max_cluster();  // largest launchable cluster of the on-chip solver (0: none)
 int pcg_onchip_warps_per_cta();
-int pcg_onchip_max_upper();
 int pcg_onchip_npad(int nslices);
 size_t pcg_onchip_t_doubles(int nslices);  // the remote transposed-product buffers (zero-initialized)
 size_t pcg_onchip_m_doubles(int nslices);  // the gathered vector's two buffers (zero-initialized)
