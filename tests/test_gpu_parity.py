@@ -679,6 +679,24 @@ def test_damage_pass_bit_exact_c3_full_size():
 
 
 @pytest.mark.slow
+def test_dynamic_steps_c3_full_size_onchip_pcg():
+    """Headline config at full size, three dynamic steps from the rest state with the production solver
+    (k_pcg_onchip: the 622,080-tet system held in TMEM + shared memory over 148 CTAs): labels exact, positions within
+    1e-6, CG iterations within 2 per step."""
+    s = cf.get("c3")
+    gs, os_, gm, om = pair(s)
+    assert gs.info()["pcg_solver_name"] == "onchip"
+    scale = np.abs(om.arrays()["rest"]).max()
+    for _ in range(3):
+        ro = os_.dynamic_step()
+        rg = gs.dynamic_step()
+        assert abs(rg.cg_iterations - ro.cg_iterations) <= 2
+        ost, gst = os_.get_state(), gs.state()
+        assert np.array_equal(gst.edge_damage, ost["zeta"])
+        assert np.abs(gst.displacements - ost["u"]).max() / scale < TRAJ_TOL
+
+
+@pytest.mark.slow
 def test_large_matrix_dynamic_pcg_tail_matches_oracle():
     """c4 physics (impact on a halfspace collider) on 52^3 cells: 148,877 nodes = 4,653 slices, more than one
     slice per PCG warp, so the solver runs its dynamic-tail instance (cg_sell.cu k_pcg_sell<true>)."""
