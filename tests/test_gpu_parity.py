@@ -872,6 +872,34 @@ def test_huge_radius_single_and_tetgen_meshes():
     assert same_bits_or_zero(sg.state().element_chi, so.get_state()["chi"])
 
 
+@pytest.mark.parametrize("solver", SOLVERS)
+def test_dynamic_steps_tiny_unstructured_mesh(solver, monkeypatch):
+    """two tets (offsets +1, +2, +3: k_pcg_onchip takes it, without the box meshes' structure) and the icosphere fan
+    (many column offsets: the on-chip solver declines it) -- dynamic steps equal the oracle's"""
+    _solver_env(monkeypatch, solver)
+    meshes = [([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 1, 1]], [[0, 1, 2, 3], [1, 2, 3, 4]]), _icosphere_fan()]
+    mat = (1e6, 0.3, 1000, 1e9, 0.0, g.STABLE_NEO_HOOKEAN)
+    for k, (nodes, tets) in enumerate(meshes):
+        nodes = np.asarray(nodes, np.float64) * (0.01 if k == 0 else 1.0)
+        gm, om = g.make_mesh(nodes, tets), o.Mesh.create(nodes, tets)
+        sg = g.Simulation(gm, g.MaterialParams.from_youngs(*mat), g.SolverConfig(dt=1e-3))
+        so = o.Sim(om, o.material_from_youngs(*mat), o.solver_config(dt=1e-3))
+        n = len(nodes)
+        u = np.random.default_rng(40 + k).uniform(-1e-3, 1e-3, (n, 3)) * np.abs(nodes).max()
+        sg.set_state(displacements=u)
+        so.set_state(u=u)
+        name = sg.info()["pcg_solver_name"]
+        if k == 0:
+            assert name == solver or (solver == "grid" and name == "grid"), name
+        else:
+            assert not name.startswith("onchip"), name
+        scale = np.abs(nodes).max()
+        for _ in range(3):
+            a, b = so.dynamic_step(), sg.dynamic_step()
+            assert abs(a.cg_iterations - b.cg_iterations) <= 2
+            assert np.abs(sg.state().displacements - so.get_state()["u"]).max() / scale < TRAJ_TOL
+
+
 # ---------------------------------------------------------------- quasi-static Newton (solver.cpp:138-217)
 def _pull_pair(cells=(6, 3, 3), sigma=3e3, model=g.STVK, disp=0.002, cfg=None):
     om_tmp = o.Mesh.make_box((0.2, 0.1, 0.1), cells)
