@@ -4,15 +4,16 @@
 //
 // Why: k_pcg_pipe (cg_sell.cu) streams every block of the full matrix from L2 each iteration (an upper block for its
 // row, the same block transposed for its column's row): ~1.3 KB per node row and iteration at c3, which the L2 -> SM
-// bandwidth (64 B/clk/SM measured) turns into ~8 of its ~15 us per iteration. On chip, per SM (one CTA, 768 threads,
-// one node row per thread, CTAs own 32-row slices as in k_pcg_pipe):
+// bandwidth (64 B/clk/SM measured) turns into ~8 of its ~15 us per iteration. On chip, per SM (one CTA owning up to
+// 24 slices of 32 rows, as in k_pcg_pipe):
 // The pattern must have at most 7 distinct positive column offsets off[0..6] (the box meshes' Freudenthal rows: +1,
 // +nx, +nx+1, +nx ny, +nx ny+1, +nx ny+nx, +nx ny+nx+1); a row's upper block at offset off[b] lives in SLOT b (absent
 // slots hold zero blocks), so a block's column, its transposed partner's slot and every route below are fixed by b:
 //   TMEM (512 columns x 128 lanes; 3 warps share a lane quadrant, 84 columns per row): the diagonal block (symmetric:
 //        6 values -- the assembly writes exactly symmetric diagonal blocks) and slots 3..6 (9 values each);
 //        tcgen05.ld reads 425 B/clk/SM (measured, tools/tmem_bw.cu), 3.3x shared memory;
-//   shared memory: slots 0..2 ([slot][entry][row]), D^-1, and a t buffer (below).
+//   shared memory: slots 0..2 ([slot][entry][row]) -- readable by every thread of the CTA --, the m-cache (below)
+//        and D^-1.
 // 384 threads own two rows each (768 rows = 24 slices per CTA, slices cs0 + w and cs0 + w + 12): the registers of
 // two rows' solver state plus their loads in flight fit 168 per thread, where one row per thread at 768 threads
 // (80 registers) spills.
