@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < 3; ++q) out[q] = lane_sum_oc(lane < kW ? s_w[lane][q] : 0.0);
-    __syncthreads();
+    // no trailing barrier: s_w is next written by the following totals(), which a publish() barrier precedes
   };
 
   // solver state of the two rows in registers (D^-1 in shared memory)
