@@ -565,7 +565,9 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
     publish(v3, 3, 1);
     gsync();
     int pp = 1, cur = 1;
-    double gam_prev = 1.0, alpha_prev = 1.0;
+    // reciprocals of the previous iteration's gamma and gamma * alpha, formed off the critical path: beta and p.Ap
+    // then cost multiplies, and the only division left between the reduction and the update is alpha's
+    double inv_g = 1.0, inv_ga = 1.0;
     for (int it = 0;; ++it) {
       OC_STAMP(it, 0);
       double pb[3], red[3];
@@ -601,8 +603,8 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
         converged = relres <= a.tol;
         break;
       }
-      const double beta = it > 0 ? gam / gam_prev : 0.0;
-      const double pap = it > 0 ? del - beta * gam / alpha_prev : del;  // = p.Ap
+      const double beta = it > 0 ? gam * inv_g : 0.0;                              // gamma / gamma_prev
+      const double pap = it > 0 ? __fma_rn(-(gam * inv_ga), gam, del) : del;      // = p.Ap = delta - beta gamma / alpha_prev
       if (pap <= 0.0) {  // sparse.cpp:160-168
         negcurv = pap < 0.0;
         iterations = it;
@@ -610,8 +612,8 @@ __global__ void __launch_bounds__(kT, 1) k_pcg_onchip(OcArgs oa) {
         break;
       }
       const double alpha = gam / pap;
-      gam_prev = gam;
-      alpha_prev = alpha;
+      inv_g = 1.0 / gam;
+      inv_ga = 1.0 / (gam * alpha);
       double v[3] = {0.0, 0.0, 0.0};
       double* const gnext = cur ? gm0 : gm1;
       double M2[kRpt][3];
