@@ -226,7 +226,8 @@ def pcg_models(info):
     hbm: the same with every STORED block once (72 B x upper_blocks): the format's minimum if nothing stays cached;
     working set: what must stay L2-resident for the solve to run from L2."""
     N = info["nodes"]
-    dyn = info["pcg_dynamic_units"] > 0
+    big = info.get("pcg_solver_name") == "large-matrix-rr"  # k_pcg_big: x += alpha p deferred (288 B per node)
+    dyn = info["pcg_dynamic_units"] > 0 or big
     survey = 12 * 9 * info["node_blocks"] + 4 * (3 * N + 1) + 56 * 3 * N  # SURVEY §8(d) B_CG (scalar CSR)
     if info.get("pcg_solver_name") in ("onchip", "onchip-cluster"):
         # k_pcg_onchip: the matrix is loaded ONCE per solve into TMEM + shared memory; per iteration only the column
@@ -240,7 +241,7 @@ def pcg_models(info):
                     format_bytes_per_iter=72 * info["upper_blocks"] + 4 * info["spmv_slots"] + 48 * N,
                     solver_state=("matrix and solver state on chip (TMEM + shared memory + registers)"
                                   + (", one thread-block cluster" if info["pcg_solver_name"] == "onchip-cluster" else "")))
-    vec = (312 if dyn else 48) * N
+    vec = (288 if big else 312 if dyn else 48) * N
     l2 = 72 * info["node_blocks"] + 4 * info["spmv_slots"] + vec
     hbm = 72 * info["upper_blocks"] + 4 * info["spmv_slots"] + vec
     ws = 72 * info["upper_block_slots"] + 4 * info["spmv_slots"] + (144 if dyn else 24) * N

@@ -280,7 +280,8 @@ typedef struct {
                                  [1] non-local table (grid-binned build), [2] device layout + uploads, [3] ctor total */
   int32_t pcg_solver;         /* production PCG instance: 0 k_pcg_sell (two barriers), 1 k_pcg_pipe (grid), 2 k_pcg_pipe
                                  (one cluster), 3 k_pcg_onchip (matrix in TMEM + shared memory), 4 k_pcg_sell large-matrix,
-                                 5 k_pcg_onchip in one cluster */
+                                 5 k_pcg_onchip in one cluster, 6 k_pcg_big (large matrices: round-robin static
+                                 slices, one partial per CTA, x += alpha p deferred into the next SpMV phase) */
   int32_t _pad0;
   int64_t oc_slot_blocks[7];  /* k_pcg_onchip: upper off-diagonal blocks per slot (column offset oc_offsets[b]) */
   int32_t oc_offsets[7];      /* k_pcg_onchip: the pattern's positive column offsets (0 when not used) */

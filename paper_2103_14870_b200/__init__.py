@@ -95,7 +95,7 @@ class _CgResult(C.Structure):
                 ("_pad", C.c_int32), ("relative_residual", C.c_double)]
 
 
-PCG_SOLVERS = ("two-barrier", "grid", "cluster", "onchip", "large-matrix", "onchip-cluster")  # gf_sim_info.pcg_solver
+PCG_SOLVERS = ("two-barrier", "grid", "cluster", "onchip", "large-matrix", "onchip-cluster", "large-matrix-rr")  # gf_sim_info.pcg_solver
 
 
 class _SimInfo(C.Structure):

@@ -633,6 +633,206 @@ __global__ void __launch_bounds__(kDyn ? kDynThreads : kThreads) k_pcg_sell(Sell
   }
 }
 
+// Large-matrix instance (HBM-streaming, c4): k_pcg_sell<true>'s recurrences with
+//  * round-robin static work: warp w of CTA b takes slices b W + w, b W + w + G W, ... -- the grid sweeps the matrix
+//    in slice order (a block's transposed re-read, one z-plane of slices later, still finds it in L2) without the
+//    ticket atomics, and every CTA publishes ONE partial per value: the reduction after each barrier reads G values
+//    instead of one per dynamic unit (~25k at c4);
+//  * x += alpha p deferred into the next phase A, which reads p_k anyway to form p_{k+1}: phase B then reads only q,
+//    r and D^-1 and writes r and z (the same fma, applied one phase later: bit-identical x), and an exit after a
+//    phase B applies the pending update in one final pass. Per node and iteration 288 instead of 312 vector bytes.
+template <int NV, class Body>
+__device__ __forceinline__ void rr_run(int ns, double* const (&cta)[NV], Body&& body) {
+  __shared__ double s_acc[kDynWarps][4];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int stride = (int)gridDim.x * kDynWarps;
+  double sv[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) sv[q] = 0.0;
+  for (int u = (int)blockIdx.x * kDynWarps + w; u < ns; u += stride) {
+    double v[NV];
+    body(u, v);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) sv[q] += v[q];
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) s_acc[w][q] = sv[q];
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double x = 0.0;
+    for (int k = 0; k < kDynWarps; ++k) x += s_acc[k][threadIdx.x];
+    cta[threadIdx.x][blockIdx.x] = x;
+  }
+}
+
+__global__ void __launch_bounds__(kDynThreads) k_pcg_big(SellArgs sa) {
+  constexpr int W = kDynWarps;
+  cg::grid_group grid = cg::this_grid();
+  const CgLaunch& a = sa.a;
+  const int ns = a.nslices, nrows = a.nrows, lane = threadIdx.x & 31;
+  const int G = (int)gridDim.x;
+  double* const p = a.p0;
+  int parity = 0;
+  auto ptrs = [&](auto& c) {
+    for (int q = 0; q < (int)(sizeof(c) / sizeof(c[0])); ++q) c[q] = sa.cta_part + ((size_t)parity * 4 + q) * kMaxGrid;
+  };
+  // setup (sparse.cpp:145-157): r = b - A x, z = D^-1 r, p = z; partials b.b, r.z, r.r
+  double tot3[3];
+  {
+    double* c3[3];
+    ptrs(c3);
+    rr_run<3>(ns, c3, [&](int sl, double (&v)[3]) {
+      double acc[3];
+      const int row = sl * 32 + lane;
+      if (a.x0_identity) {  // A x0 = x0 (see CgLaunch::x0_identity): no SpMV
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] = row < nrows ? a.x[3 * (size_t)row + c] : 0.0;
+      } else {
+        slice_spmv_sym_g<GatherX, GF_SELL_GROUP_DYN>(a, sl, GatherX{a.x}, acc);
+      }
+      double bb = 0.0, rz = 0.0, rr = 0.0;
+      if (row < nrows) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const size_t dof = 3 * (size_t)row + c;
+          const double bi = a.b[dof];
+          const double ri = bi - acc[c];
+          const double zi = __ldg(a.dinv + dof) * ri;
+          a.r[dof] = ri;
+          a.z[dof] = zi;
+          p[dof] = zi;
+          bb = __fma_rn(bi, bi, bb);
+          rz = __fma_rn(ri, zi, rz);
+          rr = __fma_rn(ri, ri, rr);
+        }
+      }
+      v[0] = lane_sum(bb);
+      v[1] = lane_sum(rz);
+      v[2] = lane_sum(rr);
+    });
+    grid.sync();
+    sum_phase<false, 3, W>(c3, c3, G, 0, tot3);
+    parity ^= 1;
+  }
+  const double bnorm = sqrt(tot3[0]);
+  double rz = tot3[1], rr = tot3[2];
+  int iterations = 0, converged = 0, negcurv = 0;
+  double relres = 0.0;
+  if (bnorm == 0.0) {  // sparse.cpp:145-150
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * (size_t)nrows; i += (size_t)gridDim.x * blockDim.x)
+      a.x[i] = 0.0;
+    converged = 1;
+  } else {
+    double beta = 0.0, alpha_prev = 0.0;
+    bool done = false, pending = false;  // pending: x lacks alpha_prev p (applied by the next phase A or at the end)
+    for (int it = 0; it < a.max_iters; ++it) {
+      const bool fused = it > 0;
+      SELL_STAMP(it, 0);
+      // ---- phase A: q = A p via A p_{k+1} = A z_{k+1} + beta A p_k (only z gathered); x += alpha_k p_k on the way
+      double* cA[1];
+      ptrs(cA);
+      rr_run<1>(ns, cA, [&](int sl, double (&v)[1]) {
+        double acc[3];
+        slice_spmv_sym_g<GatherZ, GF_SELL_GROUP_DYN>(a, sl, GatherZ{a.z}, acc);
+        const int row = sl * 32 + lane;
+        double pq = 0.0;
+        if (row < nrows) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const size_t dof = 3 * (size_t)row + c;
+            const double zi = ldv(a.z + dof);  // gathered by this warp's diagonal slot: an L1 hit
+            double pr = zi, qr = acc[c];
+            if (fused) {
+              const double po = ldv(p + dof);
+              a.x[dof] = __fma_rn(alpha_prev, po, __ldcg(a.x + dof));
+              pr = __fma_rn(beta, po, zi);
+              qr = __fma_rn(beta, ldv(a.Ap + dof), acc[c]);
+            }
+            p[dof] = pr;
+            a.Ap[dof] = qr;
+            pq = __fma_rn(pr, qr, pq);
+          }
+        }
+        v[0] = lane_sum(pq);
+      });
+      pending = false;
+      SELL_STAMP(it, 1);
+      SELL_BLOCK_STAMP(it, 3000);
+      SELL_BLOCK_STAMP_AT(it, 20, 4000);
+      double pap[1];
+      grid.sync();
+      SELL_STAMP(it, 5);
+      sum_phase<false, 1, W>(cA, cA, G, 0, pap);
+      parity ^= 1;
+      SELL_STAMP(it, 2);
+      if (pap[0] <= 0.0) {  // sparse.cpp:160-168
+        negcurv = pap[0] < 0.0;
+        iterations = it;
+        relres = sqrt(rr) / bnorm;
+        converged = relres <= a.tol;
+        done = true;
+        break;
+      }
+      const double alpha = rz / pap[0];
+      // ---- phase B: r -= alpha q, z = D^-1 r (coalesced over the slice's 96 dofs)
+      double* cB[2];
+      ptrs(cB);
+      rr_run<2>(ns, cB, [&](int sl, double (&v)[2]) {
+        double r2 = 0.0, rzp = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const size_t dof = (size_t)sl * 96 + c * 32 + lane;
+          if (dof < 3 * (size_t)nrows) {
+            const double ri = __fma_rn(-alpha, __ldcg(a.Ap + dof), __ldcg(a.r + dof));
+            a.r[dof] = ri;
+            const double zi = __ldg(a.dinv + dof) * ri;
+            a.z[dof] = zi;
+            r2 = __fma_rn(ri, ri, r2);
+            rzp = __fma_rn(ri, zi, rzp);
+          }
+        }
+        v[0] = lane_sum(r2);
+        v[1] = lane_sum(rzp);
+      });
+      alpha_prev = alpha;
+      pending = true;
+      SELL_STAMP(it, 3);
+      SELL_BLOCK_STAMP(it, 2000);
+      double red2[2];
+      grid.sync();
+      SELL_STAMP(it, 6);
+      sum_phase<false, 2, W>(cB, cB, G, 0, red2);
+      parity ^= 1;
+      SELL_STAMP(it, 4);
+      rr = red2[0];
+      iterations = it + 1;
+      const double rnorm = sqrt(rr);
+      if (rnorm / bnorm <= a.tol) {  // sparse.cpp:172-178
+        relres = rnorm / bnorm;
+        converged = 1;
+        done = true;
+        break;
+      }
+      beta = red2[1] / rz;
+      rz = red2[1];
+    }
+    if (!done) {
+      relres = sqrt(rr) / bnorm;
+      converged = relres <= a.tol;
+    }
+    if (pending)  // the last phase B's step: p_k was written before the last two barriers
+      for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * (size_t)nrows; i += (size_t)gridDim.x * blockDim.x)
+        a.x[i] = __fma_rn(alpha_prev, __ldcg(p + i), __ldcg(a.x + i));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.out[0] = iterations;
+    a.out[1] = converged;
+    a.out[2] = negcurv;
+    a.out[3] = relres;
+  }
+}
+
 // Pipelined PCG (Ghysels & Vanroose 2014, preconditioned pipelined CG) for matrices of at most one slice per warp:
 // ONE grid barrier per iteration. The recurrences carry s = A p, q = D^-1 s and z = A q next to x, r, u = D^-1 r and
 // w = A u, so the only SpMV of an iteration is n = A m with m = D^-1 w -- and m is known at the END of the previous
@@ -952,6 +1152,8 @@ int pcg_sell_grid() {
     int q = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_sell<true>, kDynThreads, 0);
     g_dyn_per = q;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_big, kDynThreads, 0);
+    g_dyn_per = std::min(g_dyn_per, q);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_sell<false>, kThreads, kSellSmem);
     per = std::min(per, q);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, k_pcg_pipe<false>, kThreads, kPipeSmem);
@@ -1031,7 +1233,9 @@ void launch_pcg_sell(const CgLaunch& a, double* part, int ndyn, unsigned long lo
     }
     return;
   }
-  const void* fn = pipe ? (const void*)k_pcg_pipe<false> : ndyn > 0 ? (const void*)k_pcg_sell<true> : (const void*)k_pcg_sell<false>;
+  const void* fn = pipe ? (const void*)k_pcg_pipe<false>
+                  : ndyn > 0 ? (a.big ? (const void*)k_pcg_big : (const void*)k_pcg_sell<true>)
+                             : (const void*)k_pcg_sell<false>;
   const size_t smem = pipe ? kPipeSmem : ndyn > 0 ? 0 : kSellSmem;
   const int grid = a.grid > 0 ? a.grid : ndyn > 0 ? pcg_dyn_grid() : pcg_sell_grid();
   const cudaError_t err = cudaLaunchCooperativeKernel(fn, grid, ndyn > 0 ? kDynThreads : kThreads, args, smem, s);

@@ -199,6 +199,7 @@ struct CgLaunch {
   int32_t cluster;    // cg_sell.cu: 1 = the pipelined solve runs in ONE thread-block cluster of `grid` CTAs
   int32_t split;      // cg_sell.cu (cluster): warps sharing one slice's SpMV (1, 2, 3 or 4)
   int32_t onchip;     // cg_onchip.cu: 1 = the pipelined solve with the matrix held in TMEM + shared memory
+  int32_t big;        // cg_sell.cu: 1 = the large-matrix instance k_pcg_big (round-robin static work, deferred x)
 };
 int cg_csr_grid();
 void launch_pcg_csr(const CgLaunch& a, cudaStream_t s);  // scalar CSR (gf_cg_solve_csr)

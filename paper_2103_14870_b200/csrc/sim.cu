@@ -553,7 +553,10 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     const int ns = d_.nslices;
     // a matrix of at most one slice per resident warp keeps the solver state on chip (k_pcg_pipe / k_pcg_sell<false>);
     // a larger one runs the large-matrix instance with its own block size (k_pcg_sell<true>)
-    const bool dyn = ns > pcg_sell_grid() * pcg_sell_warps_per_cta();
+    // GF_CG_BIG=2 forces the large-matrix instance k_pcg_big on any matrix (tests); GF_CG_BIG=0 keeps k_pcg_sell<true>
+    const char* be = std::getenv("GF_CG_BIG");
+    const int big_env = be ? std::atoi(be) : 1;
+    const bool dyn = ns > pcg_sell_grid() * pcg_sell_warps_per_cta() || big_env == 2;
     const int Gfull = dyn ? pcg_dyn_grid() : pcg_sell_grid(), W = dyn ? pcg_dyn_warps_per_cta() : pcg_sell_warps_per_cta();
     // CTAs of the cooperative solve: all co-resident ones by default; GF_CG_GRID=<n> asks for fewer (cheaper grid
     // barriers for small matrices), never fewer than one slice per warp needs
@@ -600,6 +603,9 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     } else if (onchip_ok) {
       cg_.onchip = 1;
     }
+    // large matrices: k_pcg_big (round-robin static slices, one partial per CTA, x deferred; GF_CG_BIG=0: the
+    // ticketed k_pcg_sell<true>)
+    if (dyn) cg_.big = big_env != 0;
     cg_.grid = G;
     const int64_t gw = (int64_t)G * Weff;
     double frac = 0.0;  // measured at c4 (28k slices): all-dynamic tail 22.5 ms, 50 % static 23.0, 80 % 26.2
@@ -675,7 +681,7 @@ gf_sim_info Simulation::info() const {
   o.nl_slots = mat_.r_d <= 0.0 ? 0 : d_.nl_tpl ? 32 * nl_tpl_slots_ : nl_ell_slots_;
   o.nl_layout = nonlocal_layout();
   o.pcg_dynamic_units = cg_ndyn_;
-  o.pcg_solver = cg_ndyn_ > 0 ? 4 : cg_.onchip ? (cg_.cluster ? 5 : 3) : !cg_.pipelined ? 0 : cg_.cluster ? 2 : 1;
+  o.pcg_solver = cg_.big ? 6 : cg_ndyn_ > 0 ? 4 : cg_.onchip ? (cg_.cluster ? 5 : 3) : !cg_.pipelined ? 0 : cg_.cluster ? 2 : 1;
   for (int b = 0; b < 7; ++b) {
     o.oc_slot_blocks[b] = cg_.onchip ? oc_slot_blocks_[b] : 0;
     o.oc_offsets[b] = cg_.onchip ? oc_off_[b] : 0;

@@ -359,13 +359,15 @@ def test_step_metrics_match_oracle(model):
 # ---------------------------------------------------------------- the production PCG (k_pcg_sell) on given systems
 def _solver_env(monkeypatch, solver):
     """onchip-cluster / onchip: k_pcg_onchip (matrix in TMEM + shared memory) in one thread-block cluster / on the
-    cooperative grid; cluster / grid: k_pcg_pipe likewise; two-barrier: k_pcg_sell"""
+    cooperative grid; cluster / grid: k_pcg_pipe likewise; two-barrier: k_pcg_sell; large-matrix-rr: k_pcg_big (the
+    large-matrix instance, forced on these small systems)"""
+    monkeypatch.setenv("GF_CG_BIG", "2" if solver == "large-matrix-rr" else "1")
     monkeypatch.setenv("GF_CG_CLUSTER", "1" if solver in ("cluster", "onchip-cluster") else "0")
     monkeypatch.setenv("GF_CG_PIPE", "0" if solver == "two-barrier" else "1")
     monkeypatch.setenv("GF_CG_ONCHIP", "1" if solver in ("onchip", "onchip-cluster") else "0")
 
 
-SOLVERS = ["onchip-cluster", "cluster", "onchip", "grid", "two-barrier"]
+SOLVERS = ["onchip-cluster", "cluster", "onchip", "grid", "two-barrier", "large-matrix-rr"]
 
 
 @pytest.fixture(params=SOLVERS)
@@ -697,12 +699,16 @@ def test_dynamic_steps_c3_full_size_onchip_pcg():
 
 
 @pytest.mark.slow
-def test_large_matrix_dynamic_pcg_tail_matches_oracle():
+@pytest.mark.parametrize("big", ["1", "0"])
+def test_large_matrix_dynamic_pcg_tail_matches_oracle(big, monkeypatch):
     """c4 physics (impact on a halfspace collider) on 52^3 cells: 148,877 nodes = 4,653 slices, more than one
-    slice per PCG warp, so the solver runs its dynamic-tail instance (cg_sell.cu k_pcg_sell<true>)."""
+    slice per PCG warp, so the solver runs its large-matrix instance (cg_sell.cu k_pcg_big, or with GF_CG_BIG=0 the
+    ticketed k_pcg_sell<true>)."""
+    monkeypatch.setenv("GF_CG_BIG", big)
     s = cf.scaled("c4", (52, 52, 52))
     gs, os_, gm, om = pair(s)
     assert (gm.num_nodes() + 31) // 32 > 148 * 24
+    assert gs.info()["pcg_solver_name"] == ("large-matrix-rr" if big == "1" else "large-matrix")
     scale = np.abs(om.arrays()["rest"]).max()
     for _ in range(2):
         a = os_.dynamic_step()
