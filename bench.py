@@ -331,7 +331,7 @@ def sub_record(g, cf, name, steps, warmup, hbm_peak, l2_roof, e2e=False, env=Non
     pcg = kt.get("pcg", {"total_ms": 0.0})
     rec = {"workload": s.name, "tets": T, "value": T * steps / (ms / 1e3), "unit": UNIT, "steps": steps,
            "warmup": warmup, "ms_per_step": ms / steps, "cg_iterations_per_step": iters / steps,
-           "newly_broken_in_region": newly, "nonlocal_layout": {0: "local", 1: "general sliced-ELL", 2: "template"}[info["nl_layout"]],
+           "newly_broken_in_region": newly, "nonlocal_layout": {0: "local", 1: "general sliced-ELL", 2: "per-tet template", 3: "cell template"}[info["nl_layout"]],
            "setup_s": dict(info["setup_s"], wall_incl_mesh=setup_wall),
            "pcg": pcg_roofline(pcg_models(info), iters, pcg["total_ms"], l2_roof, hbm_peak, steps),
            "step_hbm_GBps": sum(v["bytes"] for v in kt.values()) / ms / 1e6}

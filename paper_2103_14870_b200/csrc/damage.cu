@@ -45,6 +45,12 @@ __device__ __forceinline__ void scatter_max(const DevData& d, const int te[6], c
   for (int k = 0; k < 6; ++k) atomicMax(d.scr_key + te[k], dkey(scr[k]));
 }
 
+#ifndef GF_NC_WARPS
+#define GF_NC_WARPS 4  // cell-template warps per CTA (each with its own weight ring)
+#endif
+#ifndef GF_NC_MINB
+#define GF_NC_MINB 3
+#endif
 #ifndef GF_TS_MINB
 #define GF_TS_MINB 3  // 3 x 256 threads per SM (80 registers): measured faster than 2 at c3 and c4
 #endif
@@ -65,6 +71,12 @@ __global__ void __launch_bounds__(kTpb, GF_TS_MINB) k_tet_stress(DevData d, MatD
     const size_t pos = (size_t)(e % 6) * d.nl_ncell + e / 6;
 #pragma unroll
     for (int p = 0; p < 3; ++p) s2[(size_t)p * d.nt + pos] = make_double2(c6[2 * p], c6[2 * p + 1]);
+    if (d.nl_tpl == 2) {  // a non-finite component (exponent all ones) sends the gather kernel down its exact path
+      int fin = 0x7ff00000;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) fin = min(fin, ~__double2hiint(c6[k]) & 0x7ff00000);
+      if (fin == 0) *d.nl_flag = 1;
+    }
   } else {
 #pragma unroll
     for (int k = 0; k < 6; ++k) d.sigc[6 * (size_t)e + k] = c6[k];
@@ -211,6 +223,186 @@ __global__ void __launch_bounds__(kNlTpb, (GF_NL_MINB * 256) / kNlTpb) k_nonloca
   screen_tet(d, e, avg);
 }
 
+// ---- cell template (DevData::nl_tpl == 2): one thread owns the six tets of a cell ---------------------------
+// A warp covers 32 consecutive cells; its slots are the union over lanes AND residues of the neighbour offsets
+// D = o - 6 q in ascending order, so each of a thread's six sums still runs in table order. One gathered sigma
+// record (48 B per lane) now feeds up to six sums instead of one: the L1 wavefronts per (tet, neighbour) fall
+// ~4x, which was the limiter of the per-residue template. The weights -- one 32-lane vector per (slot, residue)
+// present in the slot's mask, stored in exactly the order the warp consumes them -- are the kernel's only DRAM
+// stream: each warp pulls its own stream through a shared-memory ring with cp.async.bulk + mbarrier (kNcStages
+// copies of kNcVec vectors in flight per warp, independent of register pressure).
+constexpr int kNcWarps = GF_NC_WARPS;
+#ifndef GF_NC_SKIP
+#define GF_NC_SKIP 0
+#endif
+#ifndef GF_NC_VEC
+#define GF_NC_VEC 8
+#endif
+#ifndef GF_NC_STAGES
+#define GF_NC_STAGES 4
+#endif
+constexpr int kNcVec = GF_NC_VEC;  // weight vectors (256 B each) per bulk copy (sim.cu pads each stream to 16)
+constexpr int kNcStages = GF_NC_STAGES;  // ring depth in copies (4 x 2 KB = 8 KB per warp)
+constexpr uint32_t kNcCopyBytes = kNcVec * 256;
+constexpr uint32_t kNcRingBytes = kNcStages * kNcCopyBytes;
+static_assert((kNcRingBytes & (kNcRingBytes - 1)) == 0, "ring size must be a power of two");
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void nc_copy(uint32_t dst, const double* src, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kNcCopyBytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(kNcCopyBytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void nc_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tNC_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra NC_DONE;\n\tbra NC_WAIT;\n\tNC_DONE:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// a += w * s where w != 0, as a predicated multiply and add (mul.rn + add.rn: no contraction, the oracle's two
+// roundings); the compiler turns the equivalent C++ `if` over six components into a divergent branch per residue
+__device__ __forceinline__ void nc_add(double& a, int nz, double w, double s) {
+  asm("{\n\t.reg .pred p;\n\t.reg .f64 t;\n\tsetp.ne.s32 p, %1, 0;\n\tmul.rn.f64 t, %2, %3;\n\t@p add.rn.f64 %0, %0, t;\n\t}"
+      : "+d"(a)
+      : "r"(nz), "d"(w), "d"(s));
+}
+__device__ __forceinline__ void nc_accumulate(double (&a)[6], double w, double2 s01, double2 s23, double2 s45) {
+  const int nz = (__double2hiint(w) << 1) | __double2loint(w);  // w != 0.0 (true for NaN too, like the C++ test)
+  nc_add(a[0], nz, w, s01.x);
+  nc_add(a[1], nz, w, s01.y);
+  nc_add(a[2], nz, w, s23.x);
+  nc_add(a[3], nz, w, s23.y);
+  nc_add(a[4], nz, w, s45.x);
+  nc_add(a[5], nz, w, s45.y);
+}
+
+// EXACT = false: the sums add w * sigma for every lane, a zero weight included -- bit-identical to skipping it while
+// every gathered sigma is finite (avg + (+-0) = avg, and avg is never -0). k_tet_stress raises *nl_flag when it
+// writes a non-finite sigma component; the launch pairs this kernel with its EXACT = true twin (selects keep avg
+// where w = 0, whatever was gathered), and each returns at once unless the flag picks it.
+template <int G, bool EXACT>  // G residues per thread: the warp owns residues [g G, g G + G) of its 32 cells
+__global__ void __launch_bounds__(32 * kNcWarps, G == 6 ? GF_NC_MINB : G == 3 ? GF_NC_MINB + 1 : GF_NC_MINB + 2)
+    k_nonlocal_cell(DevData d) {
+  if ((*d.nl_flag != 0) != EXACT) return;
+  __shared__ __align__(128) double ring[kNcWarps][kNcRingBytes / 8];
+  __shared__ __align__(8) unsigned long long bars[kNcWarps][kNcStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wid = blockIdx.x * kNcWarps + warp;
+  if (wid >= d.nl_nwarps) return;  // warps are independent: no CTA-wide barrier below
+  const int4 info = __ldg(d.nl_warp + wid), next = __ldg(d.nl_warp + wid + 1);
+  const int s0 = info.z, s1 = next.z;
+  const int ncopies = (next.w - info.w) / kNcVec;
+  const double* wsrc = d.nl_tw + (size_t)info.w * 32;
+  const uint32_t ring0 = smem_addr(&ring[warp][0]), bar0 = smem_addr(&bars[warp][0]);
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < kNcStages; ++c) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * c));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int c = 0; c < kNcStages - 2; ++c)
+      if (c < ncopies) nc_copy(ring0 + c * kNcCopyBytes, wsrc + (size_t)c * kNcVec * 32, bar0 + 8 * c);
+  }
+  __syncwarp();
+  const double2* s2 = reinterpret_cast<const double2*>(d.sigc);
+  const int plane = d.nt, last = d.nt - 1;
+  const int2* slots = d.nl_cslot;
+  double avg[G][6];
+#pragma unroll
+  for (int t = 0; t < G; ++t)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) avg[t][k] = 0.0;
+  const uint32_t lane_base = ring0 + (uint32_t)(lane * 8);
+  uint32_t off = 0;  // byte offset of the next weight vector in the warp's stream
+  int cready = -1;   // last copy waited for
+  // Software pipeline over slots, three sigma buffers deep: in the step of slot j the record of slot j + 3 is
+  // requested (one uniform 8-byte load), the gathers of slot j + 2 are issued from the record requested one step
+  // earlier, and slot j (gathered two steps earlier) is consumed. Indices past the end repeat the last slot
+  // (harmless loads). A lane whose neighbour does not exist (mesh boundary, short last range) gathers a clamped
+  // position: its weight is 0.
+  auto record = [&](int j) { return __ldg(slots + min(j, s1 - 1)); };
+  auto gather = [&](int2 rec, double2& a, double2& b, double2& c) {
+    const int p = min(max(rec.x + lane, 0), last);
+    a = __ldg(s2 + p), b = __ldg(s2 + plane + p), c = __ldg(s2 + 2 * plane + p);
+  };
+  auto consume = [&](int mask, const double2& s01, const double2& s23, const double2& s45) {
+    // the slot's <= G (< kNcVec) vectors lie in copies cl - 1 and cl: on first touching copy cl, the stage of copy
+    // cl - 2 is free (fully consumed; never used for cl < 2) and takes copy cl + kNcStages - 2
+    const int cl = (int)((off + 256u * (uint32_t)__popc(mask) - 256u) / kNcCopyBytes);
+    if (cl > cready) {
+      cready = cl;
+      __syncwarp();
+      const int cn = cl + kNcStages - 2;
+      if (lane == 0 && cn < ncopies) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        nc_copy(ring0 + (cn % kNcStages) * kNcCopyBytes, wsrc + (size_t)cn * kNcVec * 32, bar0 + 8 * (cn % kNcStages));
+      }
+      nc_wait(bar0 + 8 * (cl % kNcStages), (uint32_t)((cl / kNcStages) & 1));
+    }
+    // weights first, without branches (an absent (slot, residue) has no vector and reads as 0, like a lane that
+    // lacks this neighbour), so the shared-memory latency is paid once per slot
+    double w[G];
+#pragma unroll
+    for (int t = 0; t < G; ++t) {
+      const bool has = (mask >> t) & 1;
+      w[t] = 0.0;
+      if (has) asm volatile("ld.shared.f64 %0, [%1];" : "=d"(w[t]) : "r"(lane_base + (off & (kNcRingBytes - 1))));
+      off += has ? 256u : 0u;
+    }
+#pragma unroll
+    for (int t = 0; t < G; ++t) {
+#if GF_NC_SKIP
+      if (!((mask >> t) & 1)) continue;  // warp-uniform
+#endif
+      if (EXACT) {
+        nc_accumulate(avg[t], w[t], s01, s23, s45);
+      } else {
+        avg[t][0] = avg[t][0] + w[t] * s01.x;
+        avg[t][1] = avg[t][1] + w[t] * s01.y;
+        avg[t][2] = avg[t][2] + w[t] * s23.x;
+        avg[t][3] = avg[t][3] + w[t] * s23.y;
+        avg[t][4] = avg[t][4] + w[t] * s45.x;
+        avg[t][5] = avg[t][5] + w[t] * s45.y;
+      }
+    }
+  };
+  double2 a01, a23, a45, b01, b23, b45, c01, c23, c45;
+  int2 rec = record(s0);
+  int ma = rec.y, mb, mc;
+  gather(rec, a01, a23, a45);
+  rec = record(s0 + 1);
+  mb = rec.y;
+  gather(rec, b01, b23, b45);
+  rec = record(s0 + 2);
+  for (int j = s0; j < s1; j += 3) {
+    int2 nrec = record(j + 3);
+    mc = rec.y;
+    gather(rec, c01, c23, c45);
+    consume(ma, a01, a23, a45);
+    if (j + 1 >= s1) break;
+    rec = record(j + 4);
+    ma = nrec.y;
+    gather(nrec, a01, a23, a45);
+    consume(mb, b01, b23, b45);
+    if (j + 2 >= s1) break;
+    nrec = record(j + 5);
+    mb = rec.y;
+    gather(rec, b01, b23, b45);
+    consume(mc, c01, c23, c45);
+    rec = nrec;
+  }
+  if (lane >= (info.y & 255)) return;
+#pragma unroll
+  for (int t = 0; t < G; ++t) {
+    const int e = 6 * (info.x + lane) + (info.y >> 8) * G + t;
+    if (!d.deg[e]) screen_tet(d, e, avg[t]);
+  }
+}
+
 __global__ void __launch_bounds__(kTpb) k_relabel(DevData d, double thres, int relabel, int keep_values) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   bool broke = false;
@@ -219,6 +411,7 @@ __global__ void __launch_bounds__(kTpb) k_relabel(DevData d, double thres, int r
     const double s = (key == kKeyNegInf) ? 0.0 : dkey_inv(key);
     if (keep_values) d.screening[i] = s;
     d.scr_key[i] = kKeyNegInf;
+    if (i == 0 && d.nl_tpl == 2) *d.nl_flag = 0;  // this pass's gathers are done (stream order)
     if (relabel && !d.zeta[i] && s >= thres) {
       d.zeta[i] = 1;
       broke = true;
@@ -301,7 +494,21 @@ void launch_tet_stress(const DevData& d, const MatDev& m, bool local_screen, cud
   k_tet_stress<<<nblk(d.nt), kTpb, 0, s>>>(d, m, local_screen ? 1 : 0);
 }
 void launch_nonlocal(const DevData& d, cudaStream_t s) {
-  if (d.nl_tpl) k_nonlocal_tpl<<<(int)((32 * (int64_t)d.nl_nwarps + kNlTpb - 1) / kNlTpb), kNlTpb, 0, s>>>(d);
+  if (d.nl_tpl == 2) {
+    const int grid = (d.nl_nwarps + kNcWarps - 1) / kNcWarps;
+    switch (d.nl_group) {
+#define GF_NC_LAUNCH(G)                                             \
+  k_nonlocal_cell<G, false><<<grid, 32 * kNcWarps, 0, s>>>(d); \
+  k_nonlocal_cell<G, true><<<grid, 32 * kNcWarps, 0, s>>>(d);  \
+  break
+      case 6: GF_NC_LAUNCH(6);
+      case 3: GF_NC_LAUNCH(3);
+      case 2: GF_NC_LAUNCH(2);
+      default: GF_NC_LAUNCH(1);
+#undef GF_NC_LAUNCH
+    }
+  }
+  else if (d.nl_tpl) k_nonlocal_tpl<<<(int)((32 * (int64_t)d.nl_nwarps + kNlTpb - 1) / kNlTpb), kNlTpb, 0, s>>>(d);
   else k_nonlocal<<<nblk(d.nt), kTpb, 0, s>>>(d);
 }
 void launch_relabel(const DevData& d, double thres, bool relabel, bool keep_values, cudaStream_t s) {

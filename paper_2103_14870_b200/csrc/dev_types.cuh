@@ -107,6 +107,16 @@ struct DevData {
   const int4* nl_warp;      // {t, q0, nlanes, first slot}; slot range ends at the next warp's first slot
   const int32_t* nl_spos;   // per slot
   const double* nl_tw;      // per (slot, lane)
+  // cell template (nl_tpl = 2, the default structured layout): a warp holds G x 32 tets -- residues
+  // [g G, g G + G) of 32 consecutive cells, one cell per lane (G = nl_group divides 6). Its slots are the union
+  // over lanes and its residues of the neighbour offsets D = o - 6 q in ascending order (each tet still visits its
+  // neighbours in table order); nl_cslot[slot] = {sigma-plane position of lane 0's neighbour, mask of the warp's
+  // residues (bit t: residue g G + t) with a weight in this slot}; nl_tw then holds one 32-lane weight vector per
+  // set mask bit, in slot-then-residue order, each warp's stream padded to a multiple of 8 vectors;
+  // nl_warp = {q0, nlanes | g << 8, first slot, first weight vector}.
+  const int2* nl_cslot;
+  int32_t nl_group;
+  int32_t* nl_flag;         // != 0: sigma_c holds a non-finite component (set by k_tet_stress, cleared by k_relabel)
   // state
   double* u;                // 3nn
   double* v;                // 3nn

@@ -160,6 +160,104 @@ bool Simulation::build_template_layout(const NonlocalTable& tb, Up&& up) {
   return true;
 }
 
+// Cell template (DevData::nl_tpl == 2, dev_types.cuh): the same shift-invariance test and budget as the per-residue
+// template -- a (slot, residue) pair here is exactly one slot of that layout -- but one thread owns a cell's six
+// tets, so a gathered sigma record feeds up to six sums.
+template <class Up>
+bool Simulation::build_cell_layout(const NonlocalTable& tb, int G, Up&& up) {
+  const int32_t nt = mesh_.nt;
+  if (nt % 6 != 0 || G < 1 || 6 % G != 0) return false;
+  const int32_t nc = nt / 6;
+  int64_t ell_steps = 0;
+  for (int32_t sl = 0; sl < (nt + 31) / 32; ++sl) {
+    int64_t mx = 0;
+    for (int32_t e = 32 * sl; e < std::min(nt, 32 * sl + 32); ++e) mx = std::max(mx, tb.ptr[e + 1] - tb.ptr[e]);
+    ell_steps += mx;
+  }
+  const int64_t budget = ell_steps + ell_steps * 3 / 10;
+  constexpr int kVec = 16;  // a multiple of damage.cu's kNcVec (weight vectors per bulk copy)
+  const int ngroups = 6 / G;
+  const int32_t nw = ((nc + 31) / 32) * ngroups;  // warps: the groups of one 32-cell range are consecutive
+  std::vector<int4> warps(nw + 1);
+  // pass 1 (parallel): per warp the sorted (offset, residue mask) list
+  std::vector<std::vector<int2>> lists(nw);
+  std::vector<int64_t> nvec(nw + 1, 0);
+#pragma omp parallel
+  {
+    std::vector<int64_t> keys;
+#pragma omp for schedule(dynamic, 16)
+    for (int32_t r = 0; r < nw; ++r) {
+      const int32_t q0 = 32 * (r / ngroups), n = std::min<int32_t>(32, nc - q0), g = r % ngroups;
+      keys.clear();
+      for (int k = 0; k < n; ++k)
+        for (int t = 0; t < G; ++t) {
+          const int64_t e = 6 * (int64_t)(q0 + k) + g * G + t;
+          for (int64_t q = tb.ptr[e]; q < tb.ptr[e + 1]; ++q)
+            keys.push_back(((int64_t)(tb.ids[q] - 6 * (int64_t)(q0 + k)) + (int64_t(1) << 40)) * 8 + t);
+        }
+      std::sort(keys.begin(), keys.end());
+      keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+      std::vector<int2>& L = lists[r];
+      for (int64_t key : keys) {
+        const int32_t D = (int32_t)((key >> 3) - (int64_t(1) << 40)), t = (int32_t)(key & 7);
+        if (L.empty() || L.back().x != D) L.push_back(make_int2(D, 0));
+        L.back().y |= 1 << t;
+      }
+      nvec[r + 1] = ((int64_t)keys.size() + kVec - 1) / kVec * kVec;
+    }
+  }
+  int64_t nslots = 0, pairs = 0;
+  for (int32_t r = 0; r < nw; ++r) {
+    const int32_t q0 = 32 * (r / ngroups);
+    warps[r] = make_int4(q0, std::min<int32_t>(32, nc - q0) | ((r % ngroups) << 8), (int32_t)nslots, (int32_t)nvec[r]);
+    nslots += (int64_t)lists[r].size();
+    for (const int2& s : lists[r]) pairs += __builtin_popcount((unsigned)s.y);
+    nvec[r + 1] += nvec[r];
+    if (nvec[r + 1] > INT32_MAX || nslots > INT32_MAX) return false;
+  }
+  if (pairs > budget) return false;
+  warps[nw] = make_int4(0, 0, (int32_t)nslots, (int32_t)nvec[nw]);
+  std::vector<int2> cslot((size_t)nslots);
+  std::vector<double> tw(32 * (size_t)nvec[nw], 0.0);
+  auto fdiv = [](int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int32_t r = 0; r < nw; ++r) {
+    const int32_t q0 = warps[r].x, n = warps[r].y & 255, g = warps[r].y >> 8;
+    const std::vector<int2>& L = lists[r];
+    std::vector<int32_t> first(L.size());  // first weight vector of each slot (relative to the warp's stream)
+    int32_t acc = 0;
+    for (size_t j = 0; j < L.size(); ++j) {
+      first[j] = acc;
+      acc += __builtin_popcount((unsigned)L[j].y);
+      const int64_t o0 = 6 * (int64_t)q0 + L[j].x;  // lane 0's neighbour (lane k: + 6 k, i.e. plane position + k)
+      cslot[(size_t)warps[r].z + j] = make_int2((int32_t)((o0 - 6 * fdiv(o0, 6)) * nc + fdiv(o0, 6)), L[j].y);
+    }
+    for (int k = 0; k < n; ++k)
+      for (int t = 0; t < G; ++t) {
+        const int64_t e = 6 * (int64_t)(q0 + k) + g * G + t;
+        size_t j = 0;
+        for (int64_t q = tb.ptr[e]; q < tb.ptr[e + 1]; ++q) {
+          const int32_t D = (int32_t)(tb.ids[q] - 6 * (int64_t)(q0 + k));
+          while (L[j].x != D) ++j;  // both ascend
+          const int32_t vec = first[j] + __builtin_popcount((unsigned)L[j].y & ((1u << t) - 1u));
+          tw[32 * ((size_t)warps[r].w + vec) + k] = tb.w[q];
+        }
+      }
+  }
+  d_.nl_tpl = 2;
+  d_.nl_group = G;
+  d_.nl_flag = (int32_t*)dalloc(4);
+  GF_CUDA(cudaMemsetAsync(d_.nl_flag, 0, 4, stream_));
+  d_.nl_nwarps = nw;
+  d_.nl_ncell = nc;
+  d_.nl_warp = (const int4*)up(warps.data(), sizeof(int4) * warps.size());
+  d_.nl_cslot = (const int2*)up(cslot.data(), sizeof(int2) * cslot.size());
+  d_.nl_tw = (const double*)up(tw.data(), 8 * tw.size());
+  nl_tpl_slots_ = nvec[nw];
+  GF_CUDA(cudaStreamSynchronize(stream_));  // host staging goes out of scope
+  return true;
+}
+
 Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_solver_config& cfg,
                        const gf_boundary_condition* bcs, int32_t n_bcs, const gf_collider* cols, int32_t n_cols)
     : mesh_(mesh), mat_(mat), cfg_(cfg) {
@@ -411,8 +509,10 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
     const NonlocalTable tb = make_nonlocal_table(mesh_, mat.r_d);
     setup_s_[1] = secs(t_phase);
     nl_entries_ = (int64_t)tb.ids.size();
-    const char* nl_env = std::getenv("GF_NL_LAYOUT");  // "general" forces the sliced-ELL table
-    if (!(nl_env && std::string(nl_env) == "general") && build_template_layout(tb, up)) {
+    // GF_NL_LAYOUT: "general" forces the sliced-ELL table, "tet" the per-residue template (one tet per thread)
+    const std::string nl_env = std::getenv("GF_NL_LAYOUT") ? std::getenv("GF_NL_LAYOUT") : "";
+    const int nl_group = std::getenv("GF_NL_GROUP") ? std::atoi(std::getenv("GF_NL_GROUP")) : 3;
+    if (nl_env != "general" && (nl_env == "tet" ? build_template_layout(tb, up) : build_cell_layout(tb, nl_group, up))) {
       GF_CUDA(cudaStreamSynchronize(stream_));
     } else {
     const int32_t ns = (nt + 31) / 32;

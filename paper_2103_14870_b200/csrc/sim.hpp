@@ -46,7 +46,7 @@ class Simulation {
   gf_step_stats dynamic_step();
   gf_step_stats quasi_static_step(double t_load);
   double newton_tolerance() const { return newton_tol_; }
-  int32_t nonlocal_layout() const { return mat_.r_d <= 0.0 ? 0 : d_.nl_tpl ? 2 : 1; }
+  int32_t nonlocal_layout() const { return mat_.r_d <= 0.0 ? 0 : d_.nl_tpl == 2 ? 3 : d_.nl_tpl ? 2 : 1; }
   std::vector<int32_t> damage_pass();
   // Simulation::viz (solver.hpp:83-84): the render companion, created on first use (catching up on the edges
   // already broken); from then on every damage pass with newly broken edges feeds it (solver.cpp:94)
@@ -113,6 +113,8 @@ class Simulation {
   void check_edge_fallback();
   template <class Up>
   bool build_template_layout(const NonlocalTable& tb, Up&& up);
+  template <class Up>
+  bool build_cell_layout(const NonlocalTable& tb, int G, Up&& up);
 
   static constexpr bool kEdgeFormDefault = false;
   bool edge_form_ = false;

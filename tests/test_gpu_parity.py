@@ -1024,18 +1024,19 @@ def test_full_newton_one_iteration_equals_the_semi_implicit_step():
 
 
 # ---------------------------------------------------------------- non-local table layouts
-@pytest.mark.parametrize("layout", ["template", "general"])
-@pytest.mark.parametrize("cells,rd_h", [((8, 8, 7), 2.0), ((7, 5, 9), 1.5), ((6, 9, 5), 3.1)])
+@pytest.mark.parametrize("layout", ["cell", "template", "general"])
+@pytest.mark.parametrize("cells,rd_h", [((8, 8, 7), 2.0), ((7, 5, 9), 1.5), ((6, 9, 5), 3.1), ((33, 3, 2), 1.2)])
 def test_nonlocal_layouts_bit_exact(layout, cells, rd_h, monkeypatch):
-    """Both device layouts of the non-local table give the oracle's screening values, labels and chi bit for
-    bit, including ragged template warps (cells not a multiple of 32) and other radii."""
-    if layout == "general":
-        monkeypatch.setenv("GF_NL_LAYOUT", "general")
+    """Every device layout of the non-local table (cell template: six tets per thread, weights streamed through a
+    shared-memory ring; per-residue template; general sliced ELL) gives the oracle's screening values, labels and
+    chi bit for bit, including ragged template warps (cells not a multiple of 32) and other radii."""
+    if layout != "cell":
+        monkeypatch.setenv("GF_NL_LAYOUT", {"general": "general", "template": "tet"}[layout])
     s = cf.scaled("c3", cells)
     s.r_d = rd_h * cf.H
     rng = np.random.default_rng(41)
     gs, os_, gm, om = pair(s, rng, disp=0.3, damage=0.2, chi_random=True)
-    assert gs.nonlocal_layout() == (2 if layout == "template" else 1)
+    assert gs.nonlocal_layout() == {"cell": 3, "template": 2, "general": 1}[layout]
     st = os_.get_state()
     sig = om.per_tet_cauchy(os_.mat, st["u"])
     assert same_bits_or_zero(gs.eval_cauchy(), sig)
@@ -1044,6 +1045,41 @@ def test_nonlocal_layouts_bit_exact(layout, cells, rd_h, monkeypatch):
     assert np.array_equal(deg, ref_deg) and same_bits_or_zero(scr, ref_scr) and same_bits_or_zero(sf, ref_sf)
     assert np.array_equal(gs.damage_pass(), os_.damage_pass())
     assert same_bits_or_zero(gs.state().element_chi, os_.get_state()["chi"])
+
+
+@pytest.mark.gpu
+def test_nonlocal_cell_layout_exact_with_non_finite_stress(monkeypatch):
+    """A node flung out to 1e200 m overflows the Cauchy stress of its tets. The cell template then runs its exact twin (zero
+    weights leave a sum untouched whatever was gathered): screening values, labels and chi equal those of the
+    per-tet template and of the general table bit for bit, NaNs included, and the finite ones equal the oracle's."""
+    s = cf.scaled("c3", (8, 8, 7))
+    out = {}
+    for layout, env in (("cell", None), ("template", "tet"), ("general", "general")):
+        if env:
+            monkeypatch.setenv("GF_NL_LAYOUT", env)
+        rng = np.random.default_rng(43)
+        gs, os_, gm, om = pair(s, rng, disp=0.2, damage=0.1)
+        st = os_.get_state()
+        tets, X = om.arrays()["tets"], om.arrays()["rest"]
+        u = st["u"].copy()
+        e = len(tets) // 2 + 1
+        u[tets[e][0]] = 1e200
+        os_.set_state(u=u, v=st["v"], zeta=st["zeta"], chi=st["chi"])
+        gs.set_state(u, st["v"], st["zeta"], st["chi"])
+        assert gs.nonlocal_layout() == {"cell": 3, "template": 2, "general": 1}[layout]
+        sig = gs.eval_cauchy()
+        assert not np.isfinite(sig[e]).all()
+        scr, sf, deg = gs.eval_screening()
+        newly = gs.damage_pass()
+        out[layout] = (bits(scr), bits(sf), deg, newly, bits(gs.state().element_chi))
+        if layout == "cell":
+            ref_scr, _, ref_deg = om.nonlocal_screen(u, om.per_tet_cauchy(os_.mat, u), s.r_d)
+            fin = np.isfinite(ref_scr) & np.isfinite(scr)
+            assert np.array_equal(deg, ref_deg) and fin.sum() > 0.5 * fin.size
+            assert np.array_equal(bits(scr[fin]), bits(ref_scr[fin]))
+    for layout in ("template", "general"):
+        for a, b in zip(out["cell"], out[layout]):
+            assert np.array_equal(a, b), layout
 
 
 def test_nonlocal_layout_falls_back_for_unstructured_meshes():
