@@ -283,14 +283,11 @@ __device__ __forceinline__ void nc_accumulate(double (&a)[6], double w, double2 
 
 // EXACT = false: the sums add w * sigma for every lane, a zero weight included -- bit-identical to skipping it while
 // every gathered sigma is finite (avg + (+-0) = avg, and avg is never -0). k_tet_stress raises *nl_flag when it
-// writes a non-finite sigma component; the launch pairs this kernel with its EXACT = true twin (selects keep avg
-// where w = 0, whatever was gathered), and each returns at once unless the flag picks it.
+// writes a non-finite sigma component; that sends the kernel down its EXACT = true twin (selects keep avg
+// where w = 0, whatever was gathered); the kernel takes the twin the flag picks (one warp-uniform branch).
 template <int G, bool EXACT>  // G residues per thread: the warp owns residues [g G, g G + G) of its 32 cells
-__global__ void __launch_bounds__(32 * kNcWarps, G == 6 ? GF_NC_MINB : G == 3 ? GF_NC_MINB + 1 : GF_NC_MINB + 2)
-    k_nonlocal_cell(DevData d) {
-  if ((*d.nl_flag != 0) != EXACT) return;
-  __shared__ __align__(128) double ring[kNcWarps][kNcRingBytes / 8];
-  __shared__ __align__(8) unsigned long long bars[kNcWarps][kNcStages];
+__device__ __forceinline__ void nonlocal_cell_warp(const DevData& d, double (*ring)[kNcRingBytes / 8],
+                                                   unsigned long long (*bars)[kNcStages]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wid = blockIdx.x * kNcWarps + warp;
   if (wid >= d.nl_nwarps) return;  // warps are independent: no CTA-wide barrier below
@@ -403,6 +400,15 @@ __global__ void __launch_bounds__(32 * kNcWarps, G == 6 ? GF_NC_MINB : G == 3 ? 
   }
 }
 
+template <int G>
+__global__ void __launch_bounds__(32 * kNcWarps, G == 6 ? GF_NC_MINB : G == 3 ? GF_NC_MINB + 1 : GF_NC_MINB + 2)
+    k_nonlocal_cell(DevData d) {
+  __shared__ __align__(128) double ring[kNcWarps][kNcRingBytes / 8];
+  __shared__ __align__(8) unsigned long long bars[kNcWarps][kNcStages];
+  if (*d.nl_flag != 0) nonlocal_cell_warp<G, true>(d, ring, bars);
+  else nonlocal_cell_warp<G, false>(d, ring, bars);
+}
+
 __global__ void __launch_bounds__(kTpb) k_relabel(DevData d, double thres, int relabel, int keep_values) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   bool broke = false;
@@ -497,15 +503,10 @@ void launch_nonlocal(const DevData& d, cudaStream_t s) {
   if (d.nl_tpl == 2) {
     const int grid = (d.nl_nwarps + kNcWarps - 1) / kNcWarps;
     switch (d.nl_group) {
-#define GF_NC_LAUNCH(G)                                             \
-  k_nonlocal_cell<G, false><<<grid, 32 * kNcWarps, 0, s>>>(d); \
-  k_nonlocal_cell<G, true><<<grid, 32 * kNcWarps, 0, s>>>(d);  \
-  break
-      case 6: GF_NC_LAUNCH(6);
-      case 3: GF_NC_LAUNCH(3);
-      case 2: GF_NC_LAUNCH(2);
-      default: GF_NC_LAUNCH(1);
-#undef GF_NC_LAUNCH
+      case 6: k_nonlocal_cell<6><<<grid, 32 * kNcWarps, 0, s>>>(d); break;
+      case 3: k_nonlocal_cell<3><<<grid, 32 * kNcWarps, 0, s>>>(d); break;
+      case 2: k_nonlocal_cell<2><<<grid, 32 * kNcWarps, 0, s>>>(d); break;
+      default: k_nonlocal_cell<1><<<grid, 32 * kNcWarps, 0, s>>>(d); break;
     }
   }
   else if (d.nl_tpl) k_nonlocal_tpl<<<(int)((32 * (int64_t)d.nl_nwarps + kNlTpb - 1) / kNlTpb), kNlTpb, 0, s>>>(d);

@@ -11,7 +11,7 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $o/bench_ref
 timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-sub > $o/plain.json 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $o/launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-sub > $o/ncu_launches.log 2>&1; echo "launches rc=$?"
-for k in k_pcg_onchip k_nonlocal_tpl k_assemble; do
+for k in k_pcg_onchip k_nonlocal_cell k_assemble; do
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 \
     -o $o/ncu_$k -f python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-sub > $o/ncu_$k.log 2>&1; echo "ncu $k rc=$?"
 done
