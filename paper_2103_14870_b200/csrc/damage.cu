@@ -321,7 +321,7 @@ __device__ __forceinline__ void nonlocal_cell_warp(const DevData& d, double (*ri
   // earlier, and slot j (gathered two steps earlier) is consumed. Indices past the end repeat the last slot
   // (harmless loads). A lane whose neighbour does not exist (mesh boundary, short last range) gathers a clamped
   // position: its weight is 0.
-  auto record = [&](int j) { return __ldg(slots + min(j, s1 - 1)); };
+  auto record = [&](int j) { return __ldg(slots + max(min(j, s1 - 1), s0)); };  // (one pad record ends the array)
   auto gather = [&](int2 rec, double2& a, double2& b, double2& c) {
     const int p = min(max(rec.x + lane, 0), last);
     a = __ldg(s2 + p), b = __ldg(s2 + plane + p), c = __ldg(s2 + 2 * plane + p);

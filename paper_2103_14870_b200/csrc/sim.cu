@@ -217,7 +217,7 @@ bool Simulation::build_cell_layout(const NonlocalTable& tb, int G, Up&& up) {
   }
   if (pairs > budget) return false;
   warps[nw] = make_int4(0, 0, (int32_t)nslots, (int32_t)nvec[nw]);
-  std::vector<int2> cslot((size_t)nslots);
+  std::vector<int2> cslot((size_t)nslots + 1, make_int2(0, 0));  // + one pad record (a warp without slots reads it)
   std::vector<double> tw(32 * (size_t)nvec[nw], 0.0);
   auto fdiv = [](int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
 #pragma omp parallel for schedule(dynamic, 16)
