@@ -1024,19 +1024,22 @@ def test_full_newton_one_iteration_equals_the_semi_implicit_step():
 
 
 # ---------------------------------------------------------------- non-local table layouts
-@pytest.mark.parametrize("layout", ["cell", "template", "general"])
+@pytest.mark.parametrize("layout", ["cell", "cell6", "cell2", "cell1", "template", "general"])
 @pytest.mark.parametrize("cells,rd_h", [((8, 8, 7), 2.0), ((7, 5, 9), 1.5), ((6, 9, 5), 3.1), ((33, 3, 2), 1.2)])
 def test_nonlocal_layouts_bit_exact(layout, cells, rd_h, monkeypatch):
     """Every device layout of the non-local table (cell template: six tets per thread, weights streamed through a
     shared-memory ring; per-residue template; general sliced ELL) gives the oracle's screening values, labels and
     chi bit for bit, including ragged template warps (cells not a multiple of 32) and other radii."""
-    if layout != "cell":
+    if layout.startswith("cell"):
+        if layout != "cell":
+            monkeypatch.setenv("GF_NL_GROUP", layout[4:])  # residues per thread (default 3)
+    else:
         monkeypatch.setenv("GF_NL_LAYOUT", {"general": "general", "template": "tet"}[layout])
     s = cf.scaled("c3", cells)
     s.r_d = rd_h * cf.H
     rng = np.random.default_rng(41)
     gs, os_, gm, om = pair(s, rng, disp=0.3, damage=0.2, chi_random=True)
-    assert gs.nonlocal_layout() == {"cell": 3, "template": 2, "general": 1}[layout]
+    assert gs.nonlocal_layout() == {"cell": 3, "template": 2, "general": 1}[layout.rstrip("621")]
     st = os_.get_state()
     sig = om.per_tet_cauchy(os_.mat, st["u"])
     assert same_bits_or_zero(gs.eval_cauchy(), sig)
