@@ -232,6 +232,9 @@ __global__ void __launch_bounds__(kNlTpb, (GF_NL_MINB * 256) / kNlTpb) k_nonloca
 // stream: each warp pulls its own stream through a shared-memory ring with cp.async.bulk + mbarrier (kNcStages
 // copies of kNcVec vectors in flight per warp, independent of register pressure).
 constexpr int kNcWarps = GF_NC_WARPS;
+#ifndef GF_NC_DEPTH
+#define GF_NC_DEPTH 3  // sigma gather buffers (register pipeline depth)
+#endif
 #ifndef GF_NC_SKIP
 #define GF_NC_SKIP 0
 #endif
@@ -367,6 +370,24 @@ __device__ __forceinline__ void nonlocal_cell_warp(const DevData& d, double (*ri
       }
     }
   };
+#if GF_NC_DEPTH == 2
+  double2 a01, a23, a45, b01, b23, b45;
+  int2 rec = record(s0);
+  int ma = rec.y, mb;
+  gather(rec, a01, a23, a45);
+  rec = record(s0 + 1);
+  for (int j = s0; j < s1; j += 2) {  // two buffers: the gathers of slot j + 1 fly while slot j is summed
+    int2 nrec = record(j + 2);
+    mb = rec.y;
+    gather(rec, b01, b23, b45);
+    consume(ma, a01, a23, a45);
+    if (j + 1 >= s1) break;
+    rec = record(j + 3);
+    ma = nrec.y;
+    gather(nrec, a01, a23, a45);
+    consume(mb, b01, b23, b45);
+  }
+#else
   double2 a01, a23, a45, b01, b23, b45, c01, c23, c45;
   int2 rec = record(s0);
   int ma = rec.y, mb, mc;
@@ -392,6 +413,7 @@ __device__ __forceinline__ void nonlocal_cell_warp(const DevData& d, double (*ri
     consume(mc, c01, c23, c45);
     rec = nrec;
   }
+#endif
   if (lane >= (info.y & 255)) return;
 #pragma unroll
   for (int t = 0; t < G; ++t) {
@@ -503,7 +525,9 @@ void launch_nonlocal(const DevData& d, cudaStream_t s) {
   if (d.nl_tpl == 2) {
     const int grid = (d.nl_nwarps + kNcWarps - 1) / kNcWarps;
     switch (d.nl_group) {
+#if GF_NC_VEC >= 8  // a slot's <= G vectors must be fewer than one copy's
       case 6: k_nonlocal_cell<6><<<grid, 32 * kNcWarps, 0, s>>>(d); break;
+#endif
       case 3: k_nonlocal_cell<3><<<grid, 32 * kNcWarps, 0, s>>>(d); break;
       case 2: k_nonlocal_cell<2><<<grid, 32 * kNcWarps, 0, s>>>(d); break;
       default: k_nonlocal_cell<1><<<grid, 32 * kNcWarps, 0, s>>>(d); break;
