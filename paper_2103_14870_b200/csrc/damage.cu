@@ -232,6 +232,12 @@ __global__ void __launch_bounds__(kNlTpb, (GF_NL_MINB * 256) / kNlTpb) k_nonloca
 // stream: each warp pulls its own stream through a shared-memory ring with cp.async.bulk + mbarrier (kNcStages
 // copies of kNcVec vectors in flight per warp, independent of register pressure).
 constexpr int kNcWarps = GF_NC_WARPS;
+#ifndef GF_NC_RING
+#define GF_NC_RING 1  // weights through the cp.async.bulk shared-memory ring (0: straight into registers + L2 prefetch)
+#endif
+#ifndef GF_NC_AHEAD
+#define GF_NC_AHEAD 2
+#endif
 #ifndef GF_NC_DEPTH
 #define GF_NC_DEPTH 3  // sigma gather buffers (register pipeline depth)
 #endif
@@ -422,13 +428,127 @@ __device__ __forceinline__ void nonlocal_cell_warp(const DevData& d, double (*ri
   }
 }
 
+// Ring-free variant (GF_NC_RING=0): the weights are loaded straight into registers (coalesced streaming loads, issued
+// with the slot's gathers, GF_NC_DEPTH - 1 slots ahead of their use) and the DRAM latency is taken by L2 prefetches
+// that run kNcAhead 4-KB chunks ahead of the loads (one prefetch instruction per chunk: each lane one 128-byte
+// line). No shared memory, no mbarrier bookkeeping.
+constexpr int kNcAhead = GF_NC_AHEAD;
+template <int G, bool EXACT>
+__device__ __forceinline__ void nonlocal_cell_direct(const DevData& d) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wid = blockIdx.x * kNcWarps + warp;
+  if (wid >= d.nl_nwarps) return;
+  const int4 info = __ldg(d.nl_warp + wid), next = __ldg(d.nl_warp + wid + 1);
+  const int s0 = info.z, s1 = next.z;
+  const double* wp = d.nl_tw + (size_t)info.w * 32 + lane;  // this lane's entry of the next weight vector
+  const char* const pf0 = reinterpret_cast<const char*>(d.nl_tw + (size_t)info.w * 32) + 128 * lane;
+  const char* const pfend = reinterpret_cast<const char*>(d.nl_tw + (size_t)__ldg(&d.nl_warp[d.nl_nwarps].w) * 32);
+  auto prefetch = [&](int chunk) {
+    const char* p = pf0 + ((size_t)chunk << 12);
+    if (p < pfend) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  };
+#pragma unroll
+  for (int c = 0; c <= kNcAhead; ++c) prefetch(c);
+  const double2* s2 = reinterpret_cast<const double2*>(d.sigc);
+  const int plane = d.nt, last = d.nt - 1;
+  const int2* slots = d.nl_cslot;
+  double avg[G][6];
+#pragma unroll
+  for (int t = 0; t < G; ++t)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) avg[t][k] = 0.0;
+  uint32_t off = 0;  // bytes of the warp's weight stream requested so far
+  int cdone = 0;     // chunks up to cdone + kNcAhead are prefetched
+  auto record = [&](int j) { return __ldg(slots + max(min(j, s1 - 1), s0)); };
+  // the gathers of a slot and its weights (an absent (slot, residue) has no vector and reads as 0)
+  auto fetch = [&](int2 rec, bool live, double2& a, double2& b, double2& c, double (&w)[G]) {
+    const int p = min(max(rec.x + lane, 0), last);
+    a = __ldg(s2 + p), b = __ldg(s2 + plane + p), c = __ldg(s2 + 2 * plane + p);
+    const int mask = live ? rec.y : 0;  // slots past the end are repeated for their (unused) gathers only
+#pragma unroll
+    for (int t = 0; t < G; ++t) {
+      const bool has = (mask >> t) & 1;
+      w[t] = 0.0;
+      if (has) w[t] = __ldcs(wp);
+      wp += has ? 32 : 0;
+    }
+    off += 256u * (uint32_t)__popc(mask);
+    const int c4 = (int)(off >> 12);
+    if (c4 > cdone) {
+      cdone = c4;
+      prefetch(c4 + kNcAhead);
+    }
+  };
+  auto consume = [&](const double (&w)[G], const double2& s01, const double2& s23, const double2& s45) {
+#pragma unroll
+    for (int t = 0; t < G; ++t) {
+      if (EXACT) {
+        nc_accumulate(avg[t], w[t], s01, s23, s45);
+      } else {
+        avg[t][0] = avg[t][0] + w[t] * s01.x;
+        avg[t][1] = avg[t][1] + w[t] * s01.y;
+        avg[t][2] = avg[t][2] + w[t] * s23.x;
+        avg[t][3] = avg[t][3] + w[t] * s23.y;
+        avg[t][4] = avg[t][4] + w[t] * s45.x;
+        avg[t][5] = avg[t][5] + w[t] * s45.y;
+      }
+    }
+  };
+#if GF_NC_DEPTH == 2
+  double2 a01, a23, a45, b01, b23, b45;
+  double wa[G], wb[G];
+  fetch(record(s0), true, a01, a23, a45, wa);
+  int2 rec = record(s0 + 1);
+  for (int j = s0; j < s1; j += 2) {
+    int2 nrec = record(j + 2);
+    fetch(rec, j + 1 < s1, b01, b23, b45, wb);
+    consume(wa, a01, a23, a45);
+    if (j + 1 >= s1) break;
+    rec = record(j + 3);
+    fetch(nrec, j + 2 < s1, a01, a23, a45, wa);
+    consume(wb, b01, b23, b45);
+  }
+#else
+  double2 a01, a23, a45, b01, b23, b45, c01, c23, c45;
+  double wa[G], wb[G], wc[G];
+  fetch(record(s0), true, a01, a23, a45, wa);
+  fetch(record(s0 + 1), s0 + 1 < s1, b01, b23, b45, wb);
+  int2 rec = record(s0 + 2);
+  for (int j = s0; j < s1; j += 3) {
+    int2 nrec = record(j + 3);
+    fetch(rec, j + 2 < s1, c01, c23, c45, wc);
+    consume(wa, a01, a23, a45);
+    if (j + 1 >= s1) break;
+    rec = record(j + 4);
+    fetch(nrec, j + 3 < s1, a01, a23, a45, wa);
+    consume(wb, b01, b23, b45);
+    if (j + 2 >= s1) break;
+    nrec = record(j + 5);
+    fetch(rec, j + 4 < s1, b01, b23, b45, wb);
+    consume(wc, c01, c23, c45);
+    rec = nrec;
+  }
+#endif
+  if (lane >= (info.y & 255)) return;
+#pragma unroll
+  for (int t = 0; t < G; ++t) {
+    const int e = 6 * (info.x + lane) + (info.y >> 8) * G + t;
+    if (!d.deg[e]) screen_tet(d, e, avg[t]);
+  }
+}
+
 template <int G>
 __global__ void __launch_bounds__(32 * kNcWarps, G == 6 ? GF_NC_MINB : G == 3 ? GF_NC_MINB + 1 : GF_NC_MINB + 2)
     k_nonlocal_cell(DevData d) {
+#if GF_NC_RING
   __shared__ __align__(128) double ring[kNcWarps][kNcRingBytes / 8];
   __shared__ __align__(8) unsigned long long bars[kNcWarps][kNcStages];
   if (*d.nl_flag != 0) nonlocal_cell_warp<G, true>(d, ring, bars);
   else nonlocal_cell_warp<G, false>(d, ring, bars);
+#else
+  if (*d.nl_flag != 0) nonlocal_cell_direct<G, true>(d);
+  else nonlocal_cell_direct<G, false>(d);
+#endif
 }
 
 __global__ void __launch_bounds__(kTpb) k_relabel(DevData d, double thres, int relabel, int keep_values) {
