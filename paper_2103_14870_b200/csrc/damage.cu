@@ -232,6 +232,9 @@ __global__ void __launch_bounds__(kNlTpb, (GF_NL_MINB * 256) / kNlTpb) k_nonloca
 // stream: each warp pulls its own stream through a shared-memory ring with cp.async.bulk + mbarrier (kNcStages
 // copies of kNcVec vectors in flight per warp, independent of register pressure).
 constexpr int kNcWarps = GF_NC_WARPS;
+#ifndef GF_NC_WPIPE
+#define GF_NC_WPIPE 1  // weights one slot ahead of the sums in registers
+#endif
 #ifndef GF_NC_RING
 #define GF_NC_RING 1  // weights through the cp.async.bulk shared-memory ring (0: straight into registers + L2 prefetch)
 #endif
@@ -240,9 +243,6 @@ constexpr int kNcWarps = GF_NC_WARPS;
 #endif
 #ifndef GF_NC_DEPTH
 #define GF_NC_DEPTH 3  // sigma gather buffers (register pipeline depth)
-#endif
-#ifndef GF_NC_SKIP
-#define GF_NC_SKIP 0
 #endif
 #ifndef GF_NC_VEC
 #define GF_NC_VEC 8
@@ -335,11 +335,13 @@ __device__ __forceinline__ void nonlocal_cell_warp(const DevData& d, double (*ri
     const int p = min(max(rec.x + lane, 0), last);
     a = __ldg(s2 + p), b = __ldg(s2 + plane + p), c = __ldg(s2 + 2 * plane + p);
   };
-  auto consume = [&](int mask, const double2& s01, const double2& s23, const double2& s45) {
+  // the weights of a slot from the ring into registers, without branches over the residues (an absent (slot,
+  // residue) has no vector and reads as 0, like a lane that lacks this neighbour)
+  auto loadw = [&](int mask, double (&w)[G]) {
     // the slot's <= G (< kNcVec) vectors lie in copies cl - 1 and cl: on first touching copy cl, the stage of copy
     // cl - 2 is free (fully consumed; never used for cl < 2) and takes copy cl + kNcStages - 2
     const int cl = (int)((off + 256u * (uint32_t)__popc(mask) - 256u) / kNcCopyBytes);
-    if (cl > cready) {
+    if (mask != 0 && cl > cready) {
       cready = cl;
       __syncwarp();
       const int cn = cl + kNcStages - 2;
@@ -349,9 +351,6 @@ __device__ __forceinline__ void nonlocal_cell_warp(const DevData& d, double (*ri
       }
       nc_wait(bar0 + 8 * (cl % kNcStages), (uint32_t)((cl / kNcStages) & 1));
     }
-    // weights first, without branches (an absent (slot, residue) has no vector and reads as 0, like a lane that
-    // lacks this neighbour), so the shared-memory latency is paid once per slot
-    double w[G];
 #pragma unroll
     for (int t = 0; t < G; ++t) {
       const bool has = (mask >> t) & 1;
@@ -359,11 +358,10 @@ __device__ __forceinline__ void nonlocal_cell_warp(const DevData& d, double (*ri
       if (has) asm volatile("ld.shared.f64 %0, [%1];" : "=d"(w[t]) : "r"(lane_base + (off & (kNcRingBytes - 1))));
       off += has ? 256u : 0u;
     }
+  };
+  auto sums = [&](const double (&w)[G], const double2& s01, const double2& s23, const double2& s45) {
 #pragma unroll
     for (int t = 0; t < G; ++t) {
-#if GF_NC_SKIP
-      if (!((mask >> t) & 1)) continue;  // warp-uniform
-#endif
       if (EXACT) {
         nc_accumulate(avg[t], w[t], s01, s23, s45);
       } else {
@@ -375,6 +373,45 @@ __device__ __forceinline__ void nonlocal_cell_warp(const DevData& d, double (*ri
         avg[t][5] = avg[t][5] + w[t] * s45.y;
       }
     }
+  };
+#if GF_NC_WPIPE
+  // the weights run one slot ahead of the sums in registers: the shared-memory loads of slot j + 1 are issued before
+  // the sums of slot j (mask 0 past the end: no loads, no ring progress)
+  double2 a01, a23, a45, b01, b23, b45, c01, c23, c45;
+  double wa[G], wb[G], wc[G];
+  int2 rec = record(s0);
+  int mb, mc;
+  gather(rec, a01, a23, a45);
+  loadw(rec.y, wa);
+  rec = record(s0 + 1);
+  mb = s0 + 1 < s1 ? rec.y : 0;
+  gather(rec, b01, b23, b45);
+  rec = record(s0 + 2);
+  for (int j = s0; j < s1; j += 3) {
+    int2 nrec = record(j + 3);
+    mc = j + 2 < s1 ? rec.y : 0;
+    gather(rec, c01, c23, c45);
+    loadw(mb, wb);
+    sums(wa, a01, a23, a45);
+    if (j + 1 >= s1) break;
+    rec = record(j + 4);
+    const int ma = j + 3 < s1 ? nrec.y : 0;
+    gather(nrec, a01, a23, a45);
+    loadw(mc, wc);
+    sums(wb, b01, b23, b45);
+    if (j + 2 >= s1) break;
+    nrec = record(j + 5);
+    mb = j + 4 < s1 ? rec.y : 0;
+    gather(rec, b01, b23, b45);
+    loadw(ma, wa);
+    sums(wc, c01, c23, c45);
+    rec = nrec;
+  }
+#else
+  auto consume = [&](int mask, const double2& s01, const double2& s23, const double2& s45) {
+    double w[G];
+    loadw(mask, w);
+    sums(w, s01, s23, s45);
   };
 #if GF_NC_DEPTH == 2
   double2 a01, a23, a45, b01, b23, b45;
@@ -420,6 +457,7 @@ __device__ __forceinline__ void nonlocal_cell_warp(const DevData& d, double (*ri
     rec = nrec;
   }
 #endif
+#endif  // GF_NC_WPIPE
   if (lane >= (info.y & 255)) return;
 #pragma unroll
   for (int t = 0; t < G; ++t) {
