@@ -8,7 +8,9 @@
 //                (fracture.cpp:74), degenerate flag; for r_d = 0 also the screened value T*(0 + 1*sigma_c)
 //                reduced straight into the per-edge max (fracture.cpp:80-87) by an order-free atomic max.
 //  k_nonlocal    thread/tet (r_d > 0): avg = sum_w w*sigma_c[o] in table order (fracture.cpp:75-76),
-//                screened = T*avg (fracture.cpp:77), atomic max into the edges.
+//                screened = T*avg (fracture.cpp:77), atomic max into the edges. k_nonlocal_cell (several tets of a
+//                cell per thread, weights through a cp.async.bulk ring) and k_nonlocal_tpl are its structured-mesh
+//                forms: the same sums in the same order.
 //  k_relabel     thread/edge: decode the max (-inf -> 0, fracture.cpp:88-89), signed >= threshold relabel
 //                of intact edges (update_damage, fracture.cpp:93-104), warp-ballot + one atomic per warp
 //                compaction of the newly-broken ids (ascending order restored on read-back), key reset.
@@ -223,14 +225,16 @@ __global__ void __launch_bounds__(kNlTpb, (GF_NL_MINB * 256) / kNlTpb) k_nonloca
   screen_tet(d, e, avg);
 }
 
-// ---- cell template (DevData::nl_tpl == 2): one thread owns the six tets of a cell ---------------------------
-// A warp covers 32 consecutive cells; its slots are the union over lanes AND residues of the neighbour offsets
-// D = o - 6 q in ascending order, so each of a thread's six sums still runs in table order. One gathered sigma
-// record (48 B per lane) now feeds up to six sums instead of one: the L1 wavefronts per (tet, neighbour) fall
-// ~4x, which was the limiter of the per-residue template. The weights -- one 32-lane vector per (slot, residue)
-// present in the slot's mask, stored in exactly the order the warp consumes them -- are the kernel's only DRAM
-// stream: each warp pulls its own stream through a shared-memory ring with cp.async.bulk + mbarrier (kNcStages
-// copies of kNcVec vectors in flight per warp, independent of register pressure).
+// ---- cell template (DevData::nl_tpl == 2): one thread owns G tets of a cell (G = 3 by default) ---------------
+// A warp covers G residues of 32 consecutive cells; its slots are the union over lanes AND its residues of the
+// neighbour offsets D = o - 6 q in ascending order, so each of a thread's G sums still runs in table order. One
+// gathered sigma record (48 B per lane, three coalesced 512-byte reads per warp) feeds up to G sums instead of one:
+// the L1 wavefronts per (tet, neighbour) fall ~2.3x at G = 3 -- they were the limiter of the per-tet template. The
+// weights -- one 32-lane vector per (slot, residue) present in the slot's mask, stored in exactly the order the
+// warp consumes them -- are the kernel's only DRAM stream: each warp pulls its own stream through a shared-memory
+// ring with cp.async.bulk + mbarrier (kNcStages copies of kNcVec vectors, two in flight beyond the one being
+// consumed), so the stream depends neither on registers nor on the warp's scoreboard. Measured design steps and
+// rejected variants: DESIGN.md §7.
 constexpr int kNcWarps = GF_NC_WARPS;
 #ifndef GF_NC_WPIPE
 #define GF_NC_WPIPE 1  // weights one slot ahead of the sums in registers
