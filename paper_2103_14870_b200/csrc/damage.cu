@@ -95,8 +95,10 @@ __global__ void __launch_bounds__(kTpb, GF_TS_MINB) k_tet_stress(DevData d, MatD
   constexpr int le[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
-    te[k] = __ldg(d.tet_edges + 6 * (size_t)e + k);
-    const double rl = __ldg(d.rest_len + te[k]);
+    // std::max(1.0, rest length) is 1.0 for every edge unless some rest length exceeds 1 (flag set at setup): the
+    // scattered rest-length gathers -- and, with the non-local table, the edge ids -- are then not needed here
+    te[k] = (local_screen || d.rest_len_gt1) ? __ldg(d.tet_edges + 6 * (size_t)e + k) : 0;
+    const double rl = d.rest_len_gt1 ? __ldg(d.rest_len + te[k]) : 0.0;
     const double dx = x[le[k][1]][0] - x[le[k][0]][0];
     const double dy = x[le[k][1]][1] - x[le[k][0]][1];
     const double dz = x[le[k][1]][2] - x[le[k][0]][2];

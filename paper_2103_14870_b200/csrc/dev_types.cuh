@@ -59,6 +59,7 @@ struct DevData {
   const double2* bv;        // 5nt: per tet B^-1 row-major (9 doubles) then V -- one 80-byte record, 5 x 16-byte loads
   const int32_t* tet_edges; // 6nt AoS
   const double* rest_len;   // ne
+  int32_t rest_len_gt1;     // some rest length exceeds 1.0: build_T's degeneracy bound 1e-14 max(1, L) needs L
   const int32_t* et_ptr;    // ne+1 (edge -> tets, ascending)
   const int32_t* et_ids;
   const double* mass;       // nn (lumped node mass; all three dofs equal)

@@ -375,6 +375,8 @@ Simulation::Simulation(const HostMesh& mesh, const gf_material& mat, const gf_so
   }
   d_.tet_edges = (const int32_t*)up(mesh_.tet_edges.data(), 4 * mesh_.tet_edges.size());
   d_.rest_len = (const double*)up(mesh_.rest_len.data(), 8 * mesh_.rest_len.size());
+  d_.rest_len_gt1 = 0;
+  for (double L : mesh_.rest_len) d_.rest_len_gt1 |= (1.0 < L) ? 1 : 0;
   d_.et_ptr = (const int32_t*)up(mesh_.et_ptr.data(), 4 * mesh_.et_ptr.size());
   d_.et_ids = (const int32_t*)up(mesh_.et_ids.data(), 4 * mesh_.et_ids.size());
   d_.mass = (const double*)up(mass_.data(), 8 * mass_.size());

@@ -88,6 +88,29 @@ def test_degenerate_tets_flagged_identically():
     assert np.array_equal(got[2], ref[2]) and same_bits_or_zero(got[0], ref[0])
 
 
+@pytest.mark.parametrize("rd_cells", [0.0, 1.5])
+def test_degenerate_bound_scales_with_rest_lengths_above_one(rd_cells):
+    """build_T's degeneracy bound is 1e-14 max(1, rest length) (fracture.cpp:16-28): on a mesh in tens of metres an
+    edge squeezed to 5e-14 m is degenerate although it is longer than 1e-14 -- the kernels take the rest-length
+    gathers they skip when no rest length exceeds 1 (every BASELINE config)."""
+    size, cells = (30.0, 30.0, 30.0), (3, 3, 3)
+    r_d = rd_cells * 10.0
+    gm = g.make_box_mesh(size, cells)
+    gs = g.Simulation(gm, g.MaterialParams.from_youngs(1e6, 0.3, 1000.0, 10.0, r_d), g.SolverConfig(dt=1e-3))
+    om = o.Mesh.make_box(size, cells)
+    mat = o.material_from_youngs(1e6, 0.3, 1000.0, 10.0, r_d)
+    X = om.arrays()["rest"]
+    u = np.random.default_rng(9).uniform(-0.05, 0.05, X.shape)
+    u[5] = (X[6] + u[6]) - X[5] + np.array([5e-14, 0.0, 0.0])  # edge (5, 6): ~5e-14 m long, rest length 10 m
+    gs.set_state(u)
+    assert gs.nonlocal_layout() == (3 if r_d > 0 else 0)
+    sig = om.per_tet_cauchy(mat, u)
+    ref_scr, ref_sf, ref_deg = om.nonlocal_screen(u, sig, r_d)
+    scr, sf, deg = gs.eval_screening()
+    assert 0 < ref_deg.sum() < len(ref_deg)
+    assert np.array_equal(deg, ref_deg) and same_bits_or_zero(sf, ref_sf) and same_bits_or_zero(scr, ref_scr)
+
+
 @pytest.mark.parametrize("s", SMALL, ids=lambda s: s.name)
 @pytest.mark.parametrize("damage", [0.0, 0.1, 0.5])
 def test_damage_pass_bit_exact(s, damage):
